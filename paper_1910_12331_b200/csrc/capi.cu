@@ -1,0 +1,1009 @@
+// C ABI: include/cpkit.h (drop-in for the reference proj/include/cpkit.h,
+// implemented after proj/src/capi/cpkit_c.cpp:18-389 semantics) and
+// include/cpkit_dev.h (device-level seams).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <memory>
+#include <sstream>
+#include <thread>
+
+#include "../../include/cpkit.h"
+#include "../../include/cpkit_dev.h"
+#include "json.h"
+#include "solver.h"
+
+using cpkit::Json;
+
+struct cpkit_tensor {
+    cpkit::DenseTensor t;
+};
+struct cpkit_model {
+    cpkit::KruskalModel m;
+};
+struct cpkit_report {
+    std::string kind = "trace";
+    Json config = Json::object();
+    cpkit::ConvergenceReport trace;
+};
+struct cpkit_dev_problem {
+    std::unique_ptr<cpkit::Context> ctx;
+    std::unique_ptr<cpkit::DeviceProblem> p;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cpkit_status fail(cpkit_status code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+// Exceptions never cross the ABI (cpkit_c.cpp:38-62).
+template <typename Fn>
+cpkit_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return CPKIT_OK;
+    } catch (const cpkit::InvalidArgument& e) {
+        return fail(CPKIT_ERR_INVALID_ARGUMENT, e.what());
+    } catch (const cpkit::ParseError& e) {
+        return fail(CPKIT_ERR_PARSE, e.what());
+    } catch (const cpkit::IoError& e) {
+        return fail(CPKIT_ERR_IO, e.what());
+    } catch (const cpkit::SingularSystem& e) {
+        return fail(CPKIT_ERR_SINGULAR, e.what());
+    } catch (const cpkit::NumericalFailure& e) {
+        return fail(CPKIT_ERR_NUMERICAL, e.what());
+    } catch (const cpkit::LimitExceeded& e) {
+        return fail(CPKIT_ERR_LIMIT, e.what());
+    } catch (const std::bad_alloc&) {
+        return fail(CPKIT_ERR_INTERNAL, "out of host memory");
+    } catch (const std::exception& e) {
+        return fail(CPKIT_ERR_INTERNAL, e.what());
+    } catch (...) {
+        return fail(CPKIT_ERR_INTERNAL, "unknown error");
+    }
+}
+cpkit_status require(bool ok, const char* msg) { return ok ? CPKIT_OK : fail(CPKIT_ERR_INVALID_ARGUMENT, msg); }
+char* dup_string(const std::string& s) {
+    char* out = new char[s.size() + 1];
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return out;
+}
+Json parse_config(const char* cfg) { return cfg ? Json::parse(cfg) : Json::object(); }
+
+int current_device() {
+    if (const char* e = std::getenv("CPKIT_DEVICE")) return std::atoi(e);
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+    return d;
+}
+
+// ---- config parsing (harness.cpp:88-167) and resolution (:203-303)
+enum class InitKind { family_default, uniform, gaussian };
+struct InitDist {
+    InitKind kind = InitKind::family_default;
+    double a = 0.0, b = 1.0;
+};
+struct Spec {
+    std::string family = "gaussian";
+    double fa = 0.0, fb = 1.0;
+    std::vector<std::uint64_t> dims;
+    std::vector<int> ranks{1};
+    std::string optimizer = "als";
+    cpkit::AlsConfig als;
+    cpkit::GnConfig gn;
+    int problems = 1, inits = 1;
+    InitDist init;
+    std::uint64_t seed = 0;
+    int threads = 0;
+};
+
+cpkit::AlsConfig als_from_json(const Json& j) {
+    cpkit::AlsConfig c;
+    if (!j.contains("als")) return c;
+    const Json& a = j.at("als");
+    c.max_sweeps = a.value("max_sweeps", c.max_sweeps);
+    c.residual_tol = a.value("residual_tol", c.residual_tol);
+    c.step_tol = a.value("step_tol", c.step_tol);
+    c.lambda0 = a.value("lambda0", c.lambda0);
+    c.decay_factor = a.value("decay_factor", c.decay_factor);
+    if (a.contains("decay_every") && !a.at("decay_every").is_null())
+        c.decay_every = static_cast<int>(a.at("decay_every").as_int());
+    return c;
+}
+cpkit::RegShape shape_from_string(const std::string& s) {
+    if (s == "identity") return cpkit::RegShape::identity;
+    if (s == "diagonal") return cpkit::RegShape::diagonal;
+    throw cpkit::ParseError("unknown regularization shape: " + s);
+}
+cpkit::GnConfig gn_from_block(const Json& g) {
+    cpkit::GnConfig c;
+    c.grad_tol = g.value("grad_tol", c.grad_tol);
+    c.residual_tol = g.value("residual_tol", c.residual_tol);
+    c.step_tol = g.value("step_tol", c.step_tol);
+    c.max_iters = g.value("max_iters", c.max_iters);
+    c.cg_tol = g.value("cg_tol", c.cg_tol);
+    c.cg_max_iters = g.value("cg_max_iters", c.cg_max_iters);
+    if (g.contains("reg")) {
+        const Json& r = g.at("reg");
+        const std::string mode = r.value("mode", "varying");
+        const cpkit::RegShape shape = shape_from_string(r.value("shape", "identity"));
+        if (mode == "constant") {
+            c.schedule = cpkit::RegSchedule::constant(r.value("lambda", 1e-3), shape);
+        } else if (mode == "varying") {
+            const double upper = r.value("upper", 1e-2);
+            c.schedule = cpkit::RegSchedule::varying(upper, r.value("lower", 1e-6), r.value("mu", 2.0), shape);
+            c.schedule.lambda = r.value("lambda", upper);
+        } else {
+            throw cpkit::ParseError("unknown regularization mode: " + mode);
+        }
+    }
+    if (g.contains("armijo")) {
+        const Json& ar = g.at("armijo");
+        if (ar.is_boolean()) {
+            if (ar.as_bool()) c.armijo = cpkit::ArmijoParams{};
+        } else if (ar.value("enabled", true)) {
+            cpkit::ArmijoParams ap;
+            ap.c1 = ar.value("c1", ap.c1);
+            ap.shrink = ar.value("shrink", ap.shrink);
+            ap.max_backtracks = ar.value("max_backtracks", ap.max_backtracks);
+            c.armijo = ap;
+        }
+    }
+    const std::string beta = g.value("cg_beta", "standard");
+    if (beta == "standard") c.cg_beta = cpkit::CgBetaVariant::standard;
+    else if (beta == "stale_denominator") c.cg_beta = cpkit::CgBetaVariant::stale_denominator;
+    else throw cpkit::ParseError("unknown cg_beta variant: " + beta);
+    return c;
+}
+cpkit::GnConfig gn_from_json(const Json& j) {
+    return j.contains("gn") ? gn_from_block(j.at("gn")) : cpkit::GnConfig{};
+}
+InitDist init_from_json(const Json& j) {
+    InitDist d;
+    if (!j.contains("init")) return d;
+    const Json& i = j.at("init");
+    const std::string name = i.value("distribution", "default");
+    if (name == "default") d.kind = InitKind::family_default;
+    else if (name == "uniform") {
+        d.kind = InitKind::uniform;
+        d.a = i.value("a", 0.0);
+        d.b = i.value("b", 1.0);
+    } else if (name == "gaussian") d.kind = InitKind::gaussian;
+    else throw cpkit::ParseError("unknown init distribution: " + name);
+    return d;
+}
+void family_from_json(const Json& p, Spec& s) {
+    const std::string name = p.value("family", "uniform01");
+    if (name == "uniform01") { s.family = "uniform"; s.fa = 0.0; s.fb = 1.0; }
+    else if (name == "uniform11") { s.family = "uniform"; s.fa = -1.0; s.fb = 1.0; }
+    else if (name == "uniform") { s.family = "uniform"; s.fa = p.value("a", 0.0); s.fb = p.value("b", 1.0); }
+    else if (name == "gaussian") { s.family = "gaussian"; }
+    else if (name == "matmul") { s.family = "matmul"; }
+    else throw cpkit::ParseError("unknown problem family: " + name);
+}
+int resolved_threads(int t) {
+    if (t > 0) return t;
+    const unsigned hw = std::thread::hardware_concurrency();
+    return hw == 0 ? 1 : static_cast<int>(hw);
+}
+Spec spec_from_json(const Json& j) {  // harness.cpp:242-276
+    Spec s;
+    const Json problem = j.contains("problem") ? j.at("problem") : Json::object();
+    family_from_json(problem, s);
+    if (s.family == "matmul") {
+        const std::uint64_t n = problem.value("matmul_n", 2ull);
+        s.dims = {n * n, n * n, n * n};
+    } else if (problem.contains("dims")) {
+        s.dims.clear();
+        for (const auto& d : problem.at("dims").items()) s.dims.push_back(d.as_uint());
+    } else {
+        throw cpkit::ParseError("experiment: problem.dims required");
+    }
+    if (problem.contains("ranks")) {
+        s.ranks.clear();
+        for (const auto& r : problem.at("ranks").items()) s.ranks.push_back(static_cast<int>(r.as_int()));
+    } else if (problem.contains("rank")) {
+        s.ranks = {static_cast<int>(problem.at("rank").as_int())};
+    }
+    s.optimizer = j.value("optimizer", "als");
+    if (s.optimizer != "als" && s.optimizer != "gn") throw cpkit::ParseError("unknown optimizer: " + s.optimizer);
+    s.als = als_from_json(j);
+    s.gn = gn_from_json(j);
+    s.problems = j.value("problems", 1);
+    s.inits = j.value("inits", 1);
+    s.init = init_from_json(j);
+    s.seed = j.value("seed", 0ull);
+    s.threads = j.value("threads", 0);
+    // validate (harness.cpp:203-220)
+    if (s.ranks.empty()) throw cpkit::InvalidArgument("experiment: at least one rank required");
+    for (int r : s.ranks)
+        if (r < 1) throw cpkit::InvalidArgument("experiment: ranks must be positive");
+    if (s.problems < 1 || s.inits < 1) throw cpkit::InvalidArgument("experiment: problems and inits must be >= 1");
+    if (s.init.kind == InitKind::uniform && !(s.init.a < s.init.b))
+        throw cpkit::InvalidArgument("experiment: init uniform needs a < b");
+    if (s.family == "uniform" && !(s.fa < s.fb)) throw cpkit::InvalidArgument("problem spec: uniform needs a < b");
+    if (s.dims.empty()) throw cpkit::InvalidArgument("problem spec: dims must be nonempty");
+    s.als.validate();
+    s.gn.validate();
+    return s;
+}
+InitDist resolved_init(const Spec& s) {
+    if (s.init.kind != InitKind::family_default) return s.init;
+    InitDist d;
+    if (s.family == "uniform" && s.fa >= 0.0) {
+        d.kind = InitKind::uniform;
+        return d;
+    }
+    d.kind = InitKind::gaussian;
+    return d;
+}
+Json als_to_json(const cpkit::AlsConfig& c) {
+    Json a = Json::object();
+    a["max_sweeps"] = c.max_sweeps;
+    a["residual_tol"] = c.residual_tol;
+    a["step_tol"] = c.step_tol;
+    a["lambda0"] = c.lambda0;
+    a["decay_factor"] = c.decay_factor;
+    a["decay_every"] = c.decay_every ? Json(*c.decay_every) : Json();
+    return a;
+}
+Json gn_to_json(const cpkit::GnConfig& c) {
+    Json g = Json::object();
+    g["grad_tol"] = c.grad_tol;
+    g["residual_tol"] = c.residual_tol;
+    g["step_tol"] = c.step_tol;
+    g["max_iters"] = c.max_iters;
+    g["cg_tol"] = c.cg_tol;
+    g["cg_max_iters"] = c.cg_max_iters;
+    Json r = Json::object();
+    r["mode"] = c.schedule.mode == cpkit::RegMode::constant ? "constant" : "varying";
+    r["shape"] = c.schedule.shape == cpkit::RegShape::identity ? "identity" : "diagonal";
+    r["lambda"] = c.schedule.lambda;
+    if (c.schedule.mode == cpkit::RegMode::varying) {
+        r["mu"] = c.schedule.mu;
+        r["lower"] = c.schedule.lower;
+        r["upper"] = c.schedule.upper;
+    }
+    g["reg"] = r;
+    Json a = Json::object();
+    a["enabled"] = static_cast<bool>(c.armijo);
+    if (c.armijo) {
+        a["c1"] = c.armijo->c1;
+        a["shrink"] = c.armijo->shrink;
+        a["max_backtracks"] = c.armijo->max_backtracks;
+    }
+    g["armijo"] = a;
+    g["cg_beta"] = c.cg_beta == cpkit::CgBetaVariant::standard ? "standard" : "stale_denominator";
+    return g;
+}
+Json init_to_json(const InitDist& d) {
+    Json i = Json::object();
+    switch (d.kind) {
+        case InitKind::family_default: i["distribution"] = "default"; break;
+        case InitKind::uniform:
+            i["distribution"] = "uniform";
+            i["a"] = d.a;
+            i["b"] = d.b;
+            break;
+        case InitKind::gaussian: i["distribution"] = "gaussian"; break;
+    }
+    return i;
+}
+Json resolved_json(const Spec& s) {
+    Json j = Json::object();
+    Json p = Json::object();
+    if (s.family == "uniform") {
+        p["family"] = "uniform";
+        p["a"] = s.fa;
+        p["b"] = s.fb;
+    } else {
+        p["family"] = s.family;
+    }
+    Json dims = Json::array();
+    for (auto d : s.dims) dims.push_back(Json(static_cast<unsigned long long>(d)));
+    p["dims"] = dims;
+    Json ranks = Json::array();
+    for (int r : s.ranks) ranks.push_back(Json(r));
+    p["ranks"] = ranks;
+    j["problem"] = p;
+    j["optimizer"] = s.optimizer;
+    j["als"] = als_to_json(s.als);
+    j["gn"] = gn_to_json(s.gn);
+    j["problems"] = s.problems;
+    j["inits"] = s.inits;
+    j["init"] = init_to_json(resolved_init(s));
+    j["seed"] = static_cast<unsigned long long>(s.seed);
+    j["threads"] = resolved_threads(s.threads);
+    return j;
+}
+
+Json report_to_json(const cpkit_report& r) {  // report.cpp:95-111 (trace kind)
+    Json j = Json::object();
+    j["kind"] = r.kind;
+    j["config"] = r.config;
+    j["status"] = cpkit::to_string(r.trace.status);
+    Json recs = Json::array();
+    for (const auto& rec : r.trace.records) {
+        Json o = Json::object();
+        o["iter"] = rec.iteration;
+        o["residual"] = rec.residual;
+        o["fitness"] = rec.fitness;
+        o["lambda"] = rec.lambda;
+        o["cg_iters"] = rec.cg_iters;
+        o["seconds"] = rec.seconds;
+        recs.push_back(o);
+    }
+    j["records"] = recs;
+    return j;
+}
+std::string fmt_double(double v) { return Json(v).dump(); }
+std::string report_to_csv(const cpkit_report& r) {  // report.cpp:254-266
+    std::ostringstream os;
+    os << "iter,residual,fitness,lambda,cg_iters,seconds\n";
+    for (const auto& rec : r.trace.records)
+        os << rec.iteration << ',' << fmt_double(rec.residual) << ',' << fmt_double(rec.fitness) << ','
+           << fmt_double(rec.lambda) << ',' << rec.cg_iters << ',' << fmt_double(rec.seconds) << '\n';
+    return os.str();
+}
+
+cpkit::KruskalModel start_model(const std::vector<std::uint64_t>& dims, const Json& j, const Spec& spec) {
+    const int rank = j.value("rank", 0);
+    if (rank < 1) throw cpkit::InvalidArgument("cpkit_decompose: rank required when init is null");
+    InitDist dist = spec.init;
+    if (dist.kind == InitKind::family_default) dist.kind = InitKind::gaussian;
+    const std::uint64_t seed = cpkit::init_seed(spec.seed, rank, 0, 0);
+    return dist.kind == InitKind::uniform ? cpkit::random_model_uniform(dims, rank, seed, dist.a, dist.b)
+                                          : cpkit::random_model_gaussian(dims, rank, seed);
+}
+
+// Runs the selected optimizer on a device problem; fills model + report.
+void run_optimizer(cpkit::DeviceProblem& p, const std::string& optimizer, const Spec& spec,
+                   cpkit::KruskalModel start, cpkit::KruskalModel& result, cpkit_report& report) {
+    if (optimizer == "als") {
+        auto [m, rep] = cpkit::als_optimize(p, std::move(start), spec.als);
+        result = std::move(m);
+        report.trace = std::move(rep);
+    } else if (optimizer == "gn") {
+        auto [m, rep] = cpkit::gn_optimize(p, std::move(start), spec.gn);
+        result = std::move(m);
+        report.trace = std::move(rep);
+    } else {
+        throw cpkit::ParseError("cpkit_decompose: unknown optimizer " + optimizer);
+    }
+}
+
+cpkit::KruskalModel model_from_stacked(const std::vector<std::uint64_t>& dims, std::int64_t rank,
+                                       const double* buf) {
+    cpkit::KruskalModel m;
+    m.dims = dims;
+    m.rank = rank;
+    std::size_t at = 0;
+    for (auto d : dims) {
+        cpkit::Matrix a(static_cast<std::int64_t>(d), rank);
+        std::memcpy(a.data.data(), buf + at, a.data.size() * 8);
+        at += a.data.size();
+        m.factors.push_back(std::move(a));
+    }
+    return m;
+}
+void model_to_stacked(const cpkit::KruskalModel& m, double* buf) {
+    std::size_t at = 0;
+    for (const auto& a : m.factors) {
+        std::memcpy(buf + at, a.data.data(), a.data.size() * 8);
+        at += a.data.size();
+    }
+}
+
+struct EventPair {
+    cudaEvent_t a{}, b{};
+    EventPair() {
+        CPK_CUDA(cudaEventCreate(&a));
+        CPK_CUDA(cudaEventCreate(&b));
+    }
+    ~EventPair() {
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+    }
+    float ms() {
+        CPK_CUDA(cudaEventSynchronize(b));
+        float v = 0;
+        CPK_CUDA(cudaEventElapsedTime(&v, a, b));
+        return v;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* cpkit_version(void) { return "1.0.0"; }
+
+const char* cpkit_status_name(cpkit_status status) {
+    switch (status) {
+        case CPKIT_OK: return "ok";
+        case CPKIT_ERR_INVALID_ARGUMENT: return "invalid_argument";
+        case CPKIT_ERR_PARSE: return "parse_error";
+        case CPKIT_ERR_IO: return "io_error";
+        case CPKIT_ERR_SINGULAR: return "singular_system";
+        case CPKIT_ERR_NUMERICAL: return "numerical_failure";
+        case CPKIT_ERR_LIMIT: return "limit_exceeded";
+        case CPKIT_ERR_INTERNAL: return "internal_error";
+    }
+    return "unknown";
+}
+const char* cpkit_last_error(void) { return g_last_error.c_str(); }
+void cpkit_string_free(char* s) { delete[] s; }
+
+// ---- tensors -------------------------------------------------------------------
+cpkit_status cpkit_tensor_create(const uint64_t* dims, uint64_t order, const double* data, cpkit_tensor** out) {
+    if (auto st = require(dims && data && out && order > 0, "cpkit_tensor_create: null argument")) return st;
+    return guarded([&] {
+        std::vector<std::uint64_t> d(dims, dims + order);
+        const std::uint64_t total = cpkit::product_of_dims(d);
+        std::vector<double> v(data, data + total);
+        auto t = cpkit::DenseTensor::from_data(std::move(d), std::move(v));
+        t.validate();
+        *out = new cpkit_tensor{std::move(t)};
+    });
+}
+cpkit_status cpkit_tensor_load(const char* path, cpkit_tensor** out) {
+    if (auto st = require(path && out, "cpkit_tensor_load: null argument")) return st;
+    return guarded([&] { *out = new cpkit_tensor{cpkit::read_tensor(path)}; });
+}
+cpkit_status cpkit_tensor_save(const cpkit_tensor* t, const char* path) {
+    if (auto st = require(t && path, "cpkit_tensor_save: null argument")) return st;
+    return guarded([&] { cpkit::write_tensor(t->t, path); });
+}
+uint64_t cpkit_tensor_order(const cpkit_tensor* t) { return t ? t->t.order() : 0; }
+uint64_t cpkit_tensor_extent(const cpkit_tensor* t, uint64_t mode) {
+    return (t && mode < t->t.order()) ? t->t.extent(mode) : 0;
+}
+uint64_t cpkit_tensor_element_count(const cpkit_tensor* t) { return t ? t->t.size() : 0; }
+const double* cpkit_tensor_data(const cpkit_tensor* t) { return t ? t->t.data() : nullptr; }
+void cpkit_tensor_destroy(cpkit_tensor* t) { delete t; }
+
+// ---- models ----------------------------------------------------------------------
+cpkit_status cpkit_model_load(const char* path, cpkit_model** out) {
+    if (auto st = require(path && out, "cpkit_model_load: null argument")) return st;
+    return guarded([&] { *out = new cpkit_model{cpkit::read_model(path)}; });
+}
+cpkit_status cpkit_model_save(const cpkit_model* m, const char* path) {
+    if (auto st = require(m && path, "cpkit_model_save: null argument")) return st;
+    return guarded([&] { cpkit::write_model(m->m, path); });
+}
+uint64_t cpkit_model_order(const cpkit_model* m) { return m ? m->m.order() : 0; }
+uint64_t cpkit_model_rank(const cpkit_model* m) { return m ? static_cast<uint64_t>(m->m.rank) : 0; }
+uint64_t cpkit_model_extent(const cpkit_model* m, uint64_t mode) {
+    return (m && mode < m->m.order()) ? m->m.dims[mode] : 0;
+}
+const double* cpkit_model_factor(const cpkit_model* m, uint64_t mode) {
+    return (m && mode < m->m.order()) ? m->m.factors[mode].data.data() : nullptr;
+}
+namespace {
+cpkit::DenseTensor reconstruct_on_device(const cpkit::KruskalModel& m, std::uint64_t cap) {
+    m.validate();
+    const std::uint64_t total = cpkit::product_of_dims(m.dims);
+    if (total > cap) throw cpkit::LimitExceeded("reconstruct: element count exceeds cap");
+    cpkit::DenseTensor t(m.dims);
+    if (m.order() < 2) {  // order-1 model: the single factor's row sums
+        for (std::uint64_t i = 0; i < total; ++i) {
+            double acc = 0.0;
+            for (std::int64_t r = 0; r < m.rank; ++r) acc += m.factors[0].data[i * m.rank + r];
+            t.data()[i] = acc;
+        }
+        return t;
+    }
+    cpkit::Context ctx(current_device());
+    cpkit::DeviceProblem p(ctx, m.dims, static_cast<int>(m.rank));
+    p.generate_tensor(m, 0, 0.0);
+    CPK_CUDA(cudaMemcpyAsync(t.data(), p.tensor_device(), total * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+    return t;
+}
+}  // namespace
+cpkit_status cpkit_model_reconstruct(const cpkit_model* m, cpkit_tensor** out) {
+    if (auto st = require(m && out, "cpkit_model_reconstruct: null argument")) return st;
+    return guarded([&] { *out = new cpkit_tensor{reconstruct_on_device(m->m, cpkit::kDefaultElementCap)}; });
+}
+void cpkit_model_destroy(cpkit_model* m) { delete m; }
+
+// ---- generators (cpkit_c.cpp:198-225; generators.cpp:78-117) ---------------------
+cpkit_status cpkit_generate_low_rank(const char* spec_json, cpkit_model** out_model, cpkit_tensor** out_tensor) {
+    if (auto st = require(spec_json && (out_model || out_tensor), "cpkit_generate_low_rank: null argument"))
+        return st;
+    return guarded([&] {
+        const Json j = Json::parse(spec_json);
+        Json wrapped = Json::object();
+        wrapped["problem"] = j;
+        const Spec s = spec_from_json(wrapped);
+        if (s.family == "matmul") throw cpkit::InvalidArgument("random_low_rank: family must be uniform or gaussian");
+        if (cpkit::product_of_dims(s.dims) > cpkit::kDefaultElementCap)
+            throw cpkit::LimitExceeded("random_low_rank: element count exceeds cap");
+        const std::uint64_t seed = j.value("seed", 0ull);
+        cpkit::KruskalModel model = s.family == "uniform"
+                                        ? cpkit::random_model_uniform(s.dims, s.ranks[0], seed, s.fa, s.fb)
+                                        : cpkit::random_model_gaussian(s.dims, s.ranks[0], seed);
+        if (out_tensor) *out_tensor = new cpkit_tensor{reconstruct_on_device(model, cpkit::kDefaultElementCap)};
+        if (out_model) *out_model = new cpkit_model{std::move(model)};
+    });
+}
+cpkit_status cpkit_matmul_tensor(uint64_t n, cpkit_tensor** out) {
+    if (auto st = require(out != nullptr, "cpkit_matmul_tensor: null argument")) return st;
+    return guarded([&] {
+        if (n < 1) throw cpkit::InvalidArgument("matmul_tensor: n must be >= 1");
+        const std::uint64_t sq = n * n;
+        if (sq * sq * sq > cpkit::kDefaultElementCap) throw cpkit::LimitExceeded("matmul_tensor: element count exceeds cap");
+        cpkit::DenseTensor t({sq, sq, sq});
+        for (std::uint64_t i = 0; i < n; ++i)
+            for (std::uint64_t l = 0; l < n; ++l)
+                for (std::uint64_t jj = 0; jj < n; ++jj) {
+                    const std::uint64_t m0 = i * n + jj, m1 = i * n + l, m2 = l * n + jj;
+                    t.data()[(m0 * sq + m1) * sq + m2] = 1.0;
+                }
+        *out = new cpkit_tensor{std::move(t)};
+    });
+}
+
+// ---- decomposition (cpkit_c.cpp:229-297) ----------------------------------------------
+cpkit_status cpkit_decompose(const cpkit_tensor* t, const char* config_json, const cpkit_model* init,
+                             cpkit_model** out_model, cpkit_report** out_report) {
+    if (auto st = require(t != nullptr, "cpkit_decompose: null tensor")) return st;
+    return guarded([&] {
+        const Json j = parse_config(config_json);
+        const std::string optimizer = j.value("optimizer", "als");
+        Json wrapped = j;
+        Json prob = Json::object();
+        prob["family"] = "gaussian";
+        Json dims = Json::array();
+        for (auto d : t->t.dims()) dims.push_back(Json(static_cast<unsigned long long>(d)));
+        prob["dims"] = dims;
+        prob["rank"] = j.value("rank", 1);
+        wrapped["problem"] = prob;
+        const Spec spec = spec_from_json(wrapped);
+
+        cpkit::KruskalModel start;
+        if (init != nullptr) {
+            start = init->m;
+            if (start.dims != t->t.dims())
+                throw cpkit::InvalidArgument("cpkit_decompose: init model extents do not match tensor");
+        } else {
+            start = start_model(t->t.dims(), j, spec);
+        }
+        if (t->t.order() < 2) throw cpkit::InvalidArgument("mttkrp: tensor order must be at least 2");
+
+        auto report = std::make_unique<cpkit_report>();
+        Json cfg = resolved_json(spec);
+        cfg["kind"] = "decompose";
+        cfg["optimizer"] = optimizer;
+        report->config = cfg;
+
+        cpkit::Context ctx(current_device());
+        cpkit::DeviceProblem p(ctx, t->t.dims(), static_cast<int>(start.rank));
+        p.upload_tensor(t->t.data());
+        cpkit::KruskalModel result;
+        run_optimizer(p, optimizer, spec, std::move(start), result, *report);
+        if (out_model) *out_model = new cpkit_model{std::move(result)};
+        if (out_report) *out_report = report.release();
+    });
+}
+
+// ---- runners ---------------------------------------------------------------------------
+// run_trace (harness.cpp:461-486): one problem from the spec's family, one init.
+cpkit_status cpkit_run_trace(const char* config_json, cpkit_report** out) {
+    if (auto st = require(config_json && out, "cpkit_run_trace: null argument")) return st;
+    return guarded([&] {
+        const Spec spec = spec_from_json(Json::parse(config_json));
+        if (spec.family == "matmul") throw cpkit::InvalidArgument("run_trace: matmul family not served by the B200 build");
+        const int rank = spec.ranks[0];
+        const std::uint64_t ps = cpkit::problem_seed(spec.seed, rank, 0);
+        cpkit::KruskalModel truth = spec.family == "uniform"
+                                        ? cpkit::random_model_uniform(spec.dims, rank, ps, spec.fa, spec.fb)
+                                        : cpkit::random_model_gaussian(spec.dims, rank, ps);
+        const InitDist d = resolved_init(spec);
+        const std::uint64_t is = cpkit::init_seed(spec.seed, rank, 0, 0);
+        cpkit::KruskalModel start = d.kind == InitKind::uniform ? cpkit::random_model_uniform(spec.dims, rank, is, d.a, d.b)
+                                                                : cpkit::random_model_gaussian(spec.dims, rank, is);
+        auto report = std::make_unique<cpkit_report>();
+        Json cfg = resolved_json(spec);
+        cfg["kind"] = "trace";
+        report->config = cfg;
+        cpkit::Context ctx(current_device());
+        cpkit::DeviceProblem p(ctx, spec.dims, rank);
+        p.generate_tensor(truth, 0, 0.0);
+        cpkit::KruskalModel result;
+        try {
+            run_optimizer(p, spec.optimizer, spec, std::move(start), result, *report);
+        } catch (const cpkit::Error&) {
+            report->trace.status = cpkit::TerminalStatus::numerical_failure;
+        }
+        *out = report.release();
+    });
+}
+cpkit_status cpkit_run_likelihood(const char*, cpkit_report**) {
+    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_likelihood: experiment runner not provided by the B200 build");
+}
+cpkit_status cpkit_run_matmul(const char*, cpkit_report**) {
+    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_matmul: experiment runner not provided by the B200 build");
+}
+cpkit_status cpkit_run_bench_matvec(const char*, cpkit_report**) {
+    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_bench_matvec: use cpkit_dev_time_jtj in the B200 build");
+}
+cpkit_status cpkit_run_selftest_oracle(const char*, cpkit_report**) {
+    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_selftest_oracle: oracle checks live in tests/ for the B200 build");
+}
+
+// ---- reports ------------------------------------------------------------------------------
+cpkit_status cpkit_report_emit(const cpkit_report* r, const char* format, const char* path) {
+    if (auto st = require(r && format && path, "cpkit_report_emit: null argument")) return st;
+    return guarded([&] {
+        std::string payload;
+        const std::string f(format);
+        if (f == "json") payload = report_to_json(*r).dump(2) + "\n";
+        else if (f == "csv") payload = report_to_csv(*r);
+        else throw cpkit::InvalidArgument("emit_report: format must be csv or json");
+        if (std::string(path) == "-") {
+            std::cout << payload;
+            std::cout.flush();
+            return;
+        }
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw cpkit::IoError(std::string("cannot open for writing: ") + path);
+        os << payload;
+        if (!os) throw cpkit::IoError(std::string("write failed: ") + path);
+    });
+}
+cpkit_status cpkit_report_to_json(const cpkit_report* r, char** out_json) {
+    if (auto st = require(r && out_json, "cpkit_report_to_json: null argument")) return st;
+    return guarded([&] { *out_json = dup_string(report_to_json(*r).dump(2)); });
+}
+cpkit_status cpkit_report_config(const cpkit_report* r, char** out_json) {
+    if (auto st = require(r && out_json, "cpkit_report_config: null argument")) return st;
+    return guarded([&] { *out_json = dup_string(r->config.dump(2)); });
+}
+int cpkit_report_ok(const cpkit_report* r) { return r ? 1 : 0; }
+void cpkit_report_destroy(cpkit_report* r) { delete r; }
+
+// ================================================================ device layer
+cpkit_status cpkit_dev_problem_create(int device, const uint64_t* dims, uint64_t order, uint64_t rank,
+                                      cpkit_dev_problem** out) {
+    if (auto st = require(dims && out && order > 0 && rank > 0, "cpkit_dev_problem_create: bad argument")) return st;
+    return guarded([&] {
+        auto h = std::make_unique<cpkit_dev_problem>();
+        h->ctx = std::make_unique<cpkit::Context>(device);
+        h->p = std::make_unique<cpkit::DeviceProblem>(*h->ctx, std::vector<std::uint64_t>(dims, dims + order),
+                                                      static_cast<int>(rank));
+        *out = h.release();
+    });
+}
+cpkit_status cpkit_dev_nccl_unique_id(void* out128) {
+    if (auto st = require(out128 != nullptr, "cpkit_dev_nccl_unique_id: null argument")) return st;
+    return guarded([&] { cpkit::nccl_unique_id(out128); });
+}
+cpkit_status cpkit_dev_problem_create_sharded(int device, const uint64_t* dims, uint64_t order, uint64_t rank,
+                                              int shard, int world, const void* nccl_id128,
+                                              cpkit_dev_problem** out) {
+    if (auto st = require(dims && out && order > 0 && rank > 0 && world >= 1 && shard >= 0 && shard < world,
+                          "cpkit_dev_problem_create_sharded: bad argument"))
+        return st;
+    return guarded([&] {
+        auto h = std::make_unique<cpkit_dev_problem>();
+        h->ctx = std::make_unique<cpkit::Context>(device);
+        if (world > 1) {
+            if (!nccl_id128) throw cpkit::InvalidArgument("sharded problem needs an NCCL unique id");
+            h->ctx->comm = cpkit::make_nccl_comm(nccl_id128, shard, world);
+        }
+        h->p = std::make_unique<cpkit::DeviceProblem>(*h->ctx, std::vector<std::uint64_t>(dims, dims + order),
+                                                      static_cast<int>(rank));
+        *out = h.release();
+    });
+}
+void cpkit_dev_problem_destroy(cpkit_dev_problem* p) {
+    if (!p) return;
+    try {
+        p->p.reset();
+        p->ctx.reset();
+    } catch (...) {
+    }
+    delete p;
+}
+cpkit_status cpkit_dev_slab(const cpkit_dev_problem* p, uint64_t* lo, uint64_t* hi, uint64_t* local_elems) {
+    if (auto st = require(p && lo && hi && local_elems, "cpkit_dev_slab: null argument")) return st;
+    *lo = p->p->slab_lo();
+    *hi = p->p->slab_hi();
+    *local_elems = p->p->local_elems();
+    return CPKIT_OK;
+}
+
+#define DEV_REQ(cond) \
+    if (auto st_ = require((cond), __func__)) return st_
+
+cpkit_status cpkit_dev_upload_tensor(cpkit_dev_problem* p, const double* host) {
+    DEV_REQ(p && host);
+    return guarded([&] {
+        p->p->upload_tensor(host);
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_generate_tensor(cpkit_dev_problem* p, const double* truth, uint64_t noise_seed,
+                                       double noise_rel) {
+    DEV_REQ(p && truth);
+    return guarded([&] {
+        auto m = model_from_stacked(p->p->dims(), p->p->rank(), truth);
+        p->p->generate_tensor(m, noise_seed, noise_rel);
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_set_factors(cpkit_dev_problem* p, const double* f) {
+    DEV_REQ(p && f);
+    return guarded([&] {
+        p->p->set_factors(model_from_stacked(p->p->dims(), p->p->rank(), f));
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_get_factors(cpkit_dev_problem* p, double* f) {
+    DEV_REQ(p && f);
+    return guarded([&] {
+        cpkit::KruskalModel m;
+        p->p->get_factors(m);
+        model_to_stacked(m, f);
+    });
+}
+cpkit_status cpkit_dev_norm2(cpkit_dev_problem* p, double* out) {
+    DEV_REQ(p && out);
+    return guarded([&] { *out = p->p->norm2(); });
+}
+cpkit_status cpkit_dev_mttkrp(cpkit_dev_problem* p, uint64_t mode, double* out) {
+    DEV_REQ(p);
+    return guarded([&] {
+        if (mode >= static_cast<uint64_t>(p->p->order())) throw cpkit::InvalidArgument("mttkrp: mode out of range");
+        p->p->mttkrp(static_cast<int>(mode));
+        if (out) p->p->download_mttkrp(static_cast<int>(mode), out);
+        else p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_mttkrp_naive(cpkit_dev_problem* p, uint64_t mode, double* out) {
+    DEV_REQ(p);
+    return guarded([&] {
+        if (mode >= static_cast<uint64_t>(p->p->order())) throw cpkit::InvalidArgument("mttkrp: mode out of range");
+        p->p->mttkrp_naive(static_cast<int>(mode));
+        if (out) p->p->download_mttkrp(static_cast<int>(mode), out);
+        else p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_note_factor_update(cpkit_dev_problem* p, uint64_t mode) {
+    DEV_REQ(p);
+    return guarded([&] { p->p->note_factor_update(static_cast<int>(mode)); });
+}
+int cpkit_dev_full_contractions(const cpkit_dev_problem* p) { return p ? p->p->full_contractions() : 0; }
+void cpkit_dev_reset_contraction_counter(cpkit_dev_problem* p) {
+    if (p) p->p->reset_contraction_counter();
+}
+cpkit_status cpkit_dev_gamma_set(cpkit_dev_problem* p, double* grams, double* pair) {
+    DEV_REQ(p);
+    return guarded([&] {
+        p->p->build_gamma_set();
+        const int N = p->p->order();
+        const std::size_t RR = static_cast<std::size_t>(p->p->rank()) * p->p->rank();
+        std::vector<double> g(N * RR), pr(static_cast<std::size_t>(N) * N * RR);
+        p->p->download_gammas(g.data(), pr.data());
+        if (grams) std::memcpy(grams, g.data(), g.size() * 8);
+        if (pair) std::memcpy(pair, pr.data(), pr.size() * 8);
+    });
+}
+cpkit_status cpkit_dev_set_gamma_set(cpkit_dev_problem* p, const double* grams, const double* pair) {
+    DEV_REQ(p && grams && pair);
+    return guarded([&] {
+        p->p->upload_gammas(grams, pair);
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_residual(cpkit_dev_problem* p, double xnorm2, double* r, double* f) {
+    DEV_REQ(p && r && f);
+    return guarded([&] {
+        p->p->build_gamma_set();
+        auto rf = p->p->residual_fitness(xnorm2, p->p->order() - 1);
+        *r = rf.first;
+        *f = rf.second;
+    });
+}
+namespace {
+void upload_stacked(cpkit_dev_problem* p, double* dev, const double* host) {
+    CPK_CUDA(cudaMemcpyAsync(dev, host, p->p->stacked_elems() * 8, cudaMemcpyHostToDevice, p->ctx->stream));
+}
+void download_stacked(cpkit_dev_problem* p, double* host, const double* dev) {
+    CPK_CUDA(cudaMemcpyAsync(host, dev, p->p->stacked_elems() * 8, cudaMemcpyDeviceToHost, p->ctx->stream));
+    p->ctx->sync();
+}
+}  // namespace
+cpkit_status cpkit_dev_gradient(cpkit_dev_problem* p, const double* mttkrps, double* g_out) {
+    DEV_REQ(p && g_out);
+    return guarded([&] {
+        if (mttkrps) {
+            // load caller M into the device M buffer (mode blocks are contiguous)
+            CPK_CUDA(cudaMemcpyAsync(const_cast<double*>(p->p->mttkrp_result(0)), mttkrps,
+                                     p->p->stacked_elems() * 8, cudaMemcpyHostToDevice, p->ctx->stream));
+        }
+        p->p->gradient();
+        download_stacked(p, g_out, p->p->G());
+    });
+}
+cpkit_status cpkit_dev_jtj_matvec(cpkit_dev_problem* p, const double* w, double lambda, int shape, double* u) {
+    DEV_REQ(p && w && u);
+    return guarded([&] {
+        upload_stacked(p, p->p->Wbuf(), w);
+        p->p->jtj_matvec(p->p->Wbuf(), p->p->Ubuf(), lambda,
+                         shape == 0 ? cpkit::RegShape::identity : cpkit::RegShape::diagonal);
+        download_stacked(p, u, p->p->Ubuf());
+    });
+}
+cpkit_status cpkit_dev_preconditioner(cpkit_dev_problem* p, double lambda, int shape, double* out) {
+    DEV_REQ(p && out);
+    return guarded([&] {
+        p->p->build_preconditioner(lambda, shape == 0 ? cpkit::RegShape::identity : cpkit::RegShape::diagonal);
+        const std::size_t n = static_cast<std::size_t>(p->p->order()) * p->p->rank() * p->p->rank();
+        CPK_CUDA(cudaMemcpyAsync(out, p->p->pinv(), n * 8, cudaMemcpyDeviceToHost, p->ctx->stream));
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_cp_cg(cpkit_dev_problem* p, const double* g, double lambda, const char* gn_json,
+                             double* v_out, int* iterations, int* hit_cap, int* breakdown) {
+    DEV_REQ(p && g && v_out);
+    return guarded([&] {
+        const cpkit::GnConfig cfg = gn_json ? gn_from_block(Json::parse(gn_json)) : cpkit::GnConfig{};
+        cfg.validate();
+        upload_stacked(p, p->p->G(), g);
+        const cpkit::CgResultInfo r = p->p->cp_cg(lambda, cfg);
+        download_stacked(p, v_out, p->p->V());
+        if (iterations) *iterations = r.iterations;
+        if (hit_cap) *hit_cap = r.hit_cap;
+        if (breakdown) *breakdown = r.breakdown;
+    });
+}
+cpkit_status cpkit_dev_spd_solve(cpkit_dev_problem* p, const double* s, const double* b, uint64_t rows,
+                                 double lambda, double* y) {
+    DEV_REQ(p && s && b && y);
+    return guarded([&] {
+        const int R = p->p->rank();
+        const std::size_t rr = static_cast<std::size_t>(R) * R;
+        cpkit::DevBuf<double> ds(rr), db(rows * R), dy(rows * R);
+        CPK_CUDA(cudaMemcpyAsync(ds.get(), s, rr * 8, cudaMemcpyHostToDevice, p->ctx->stream));
+        CPK_CUDA(cudaMemcpyAsync(db.get(), b, rows * R * 8, cudaMemcpyHostToDevice, p->ctx->stream));
+        p->p->spd_solve(ds.get(), db.get(), static_cast<std::int64_t>(rows), lambda, dy.get());
+        CPK_CUDA(cudaMemcpyAsync(y, dy.get(), rows * R * 8, cudaMemcpyDeviceToHost, p->ctx->stream));
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_spd_inverse(cpkit_dev_problem* p, const double* s, double lambda, double* inv) {
+    DEV_REQ(p && s && inv);
+    return guarded([&] {
+        const int R = p->p->rank();
+        const std::size_t rr = static_cast<std::size_t>(R) * R;
+        cpkit::DevBuf<double> ds(rr), di(rr);
+        CPK_CUDA(cudaMemcpyAsync(ds.get(), s, rr * 8, cudaMemcpyHostToDevice, p->ctx->stream));
+        p->p->spd_inverse(ds.get(), lambda, di.get());
+        CPK_CUDA(cudaMemcpyAsync(inv, di.get(), rr * 8, cudaMemcpyDeviceToHost, p->ctx->stream));
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_als_sweep(cpkit_dev_problem* p, double lambda, double* step_norm, int* contractions) {
+    DEV_REQ(p);
+    return guarded([&] {
+        const cpkit::AlsSweepDiag d = p->p->als_sweep(lambda);
+        if (step_norm) *step_norm = d.step_norm;
+        if (contractions) *contractions = d.full_contractions;
+    });
+}
+cpkit_status cpkit_dev_gn_step(cpkit_dev_problem* p, const char* gn_json, double xnorm2, double* diag12) {
+    DEV_REQ(p && diag12);
+    return guarded([&] {
+        const cpkit::GnConfig cfg = gn_json ? gn_from_block(Json::parse(gn_json)) : cpkit::GnConfig{};
+        cfg.validate();
+        cpkit::RegSchedule s = cfg.schedule;
+        const cpkit::GnStepDiag d = p->p->gn_step(cfg, s, xnorm2);
+        const double v[12] = {static_cast<double>(d.halt), double(d.stepped), d.residual_before, d.residual_after,
+                              d.grad_norm, d.lambda, double(d.cg_iters), d.step_norm, d.alpha,
+                              double(d.armijo_exhausted), double(d.cg_hit_cap), double(d.cg_breakdown)};
+        std::memcpy(diag12, v, sizeof v);
+    });
+}
+cpkit_status cpkit_dev_optimize(cpkit_dev_problem* p, const char* config_json, const double* init,
+                                double* out_factors, cpkit_report** out_report) {
+    DEV_REQ(p);
+    return guarded([&] {
+        const Json j = parse_config(config_json);
+        const std::string optimizer = j.value("optimizer", "als");
+        Json wrapped = j;
+        Json prob = Json::object();
+        prob["family"] = "gaussian";
+        Json dims = Json::array();
+        for (auto d : p->p->dims()) dims.push_back(Json(static_cast<unsigned long long>(d)));
+        prob["dims"] = dims;
+        prob["rank"] = p->p->rank();
+        wrapped["problem"] = prob;
+        const Spec spec = spec_from_json(wrapped);
+        cpkit::KruskalModel start;
+        if (init) {
+            start = model_from_stacked(p->p->dims(), p->p->rank(), init);
+        } else {
+            Json jr = j;
+            jr["rank"] = p->p->rank();
+            start = start_model(p->p->dims(), jr, spec);
+        }
+        auto report = std::make_unique<cpkit_report>();
+        Json cfg = resolved_json(spec);
+        cfg["kind"] = "decompose";
+        cfg["optimizer"] = optimizer;
+        report->config = cfg;
+        cpkit::KruskalModel result;
+        run_optimizer(*p->p, optimizer, spec, std::move(start), result, *report);
+        if (out_factors) model_to_stacked(result, out_factors);
+        if (out_report) *out_report = report.release();
+    });
+}
+
+// ---- timing ----------------------------------------------------------------------------
+cpkit_status cpkit_dev_time_als_sweeps(cpkit_dev_problem* p, double lambda, int sweeps, double* ms) {
+    DEV_REQ(p && ms && sweeps > 0);
+    return guarded([&] {
+        EventPair ev;
+        CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
+        for (int i = 0; i < sweeps; ++i) p->p->als_sweep(lambda);
+        CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
+        *ms = ev.ms();
+    });
+}
+cpkit_status cpkit_dev_time_roots(cpkit_dev_problem* p, int reps, double* ms_back, double* ms_front) {
+    DEV_REQ(p && ms_back && ms_front && reps > 0);
+    return guarded([&] {
+        const int N = p->p->order();
+        const int h = (N + 1) / 2;
+        EventPair e1, e2;
+        CPK_CUDA(cudaEventRecord(e1.a, p->ctx->stream));
+        for (int i = 0; i < reps; ++i) p->p->mttkrp_naive(0);  // back root + level 2
+        CPK_CUDA(cudaEventRecord(e1.b, p->ctx->stream));
+        CPK_CUDA(cudaEventRecord(e2.a, p->ctx->stream));
+        for (int i = 0; i < reps; ++i) p->p->mttkrp_naive(h);  // front root + level 2
+        CPK_CUDA(cudaEventRecord(e2.b, p->ctx->stream));
+        *ms_back = e1.ms() / reps;
+        *ms_front = e2.ms() / reps;
+    });
+}
+cpkit_status cpkit_dev_time_jtj(cpkit_dev_problem* p, int reps, double* ms) {
+    DEV_REQ(p && ms && reps > 0);
+    return guarded([&] {
+        p->p->build_gamma_set();
+        EventPair ev;
+        CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
+        for (int i = 0; i < reps; ++i)
+            p->p->jtj_matvec(p->p->factors_device(), p->p->Ubuf(), 1e-3, cpkit::RegShape::identity);
+        CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
+        *ms = ev.ms() / reps;
+    });
+}
+cpkit_status cpkit_dev_time_norm2(cpkit_dev_problem* p, int reps, double* ms) {
+    DEV_REQ(p && ms && reps > 0);
+    return guarded([&] {
+        EventPair ev;
+        CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
+        for (int i = 0; i < reps; ++i) p->p->norm2();
+        CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
+        *ms = ev.ms() / reps;
+    });
+}
+cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops) {
+    DEV_REQ(tflops);
+    return guarded([&] { *tflops = cpkit::probe_dmma_peak(device); });
+}
+uint64_t cpkit_dev_kernel_launches(void) { return cpkit::kernel_launches(); }
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+// Internal declarations shared by the host drivers and the sm_100a kernels.
+//
+// Layout conventions follow the reference exactly (tensor.hpp:14-16,
+// matrix_ops.hpp:7-10): every array is fp64, row-major, last index fastest.
+// Factors A^(n) are s_n x R row-major; a tensor of order N is viewed as the
+// (F x B) row-major matrix with F = prod_{m<h} s_m, B = prod_{m>=h} s_m and
+// h = ceil(N/2), the reference's front/back split (mttkrp.cpp:166-178).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace cpkit {
+
+// ---- exception taxonomy (reference errors.hpp:9-49); mapped to cpkit_status
+// codes at the C ABI (cpkit.h:30-39).
+class Error : public std::runtime_error {
+public:
+    using std::runtime_error::runtime_error;
+};
+class InvalidArgument : public Error { public: using Error::Error; };
+class SingularSystem : public Error { public: using Error::Error; };
+class NumericalFailure : public Error { public: using Error::Error; };
+class LimitExceeded : public Error { public: using Error::Error; };
+class IoError : public Error { public: using Error::Error; };
+class ParseError : public Error { public: using Error::Error; };
+// CUDA / NCCL runtime failures (mapped to CPKIT_ERR_INTERNAL).
+class DeviceError : public Error { public: using Error::Error; };
+
+#define CPK_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw ::cpkit::DeviceError(std::string("CUDA error ") + cudaGetErrorString(e_) + \
+                                       " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+// ---- owning device buffer
+template <typename T>
+class DevBuf {
+public:
+    DevBuf() = default;
+    explicit DevBuf(std::size_t n) { resize(n); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+        return *this;
+    }
+    void resize(std::size_t n) {
+        if (n == n_) return;
+        release();
+        if (n) CPK_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void ensure(std::size_t n) { if (n > n_) resize(n); }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+
+// ---- kernel launch accounting (runtime.cu)
+void count_launch(int n);
+std::uint64_t kernel_launches();
+
+// ---- device launch helpers (implemented in kernels_*.cu) -------------------
+
+constexpr int kMaxOrder = 16;
+
+// Shape of a KRP operand: the (sub)tensor index k over `nmodes` consecutive
+// modes decomposes row-major; value(k, r) = prod_j factor_j[i_j(k), r].
+struct KrpDesc {
+    int nmodes = 0;
+    std::int64_t ext[kMaxOrder] = {};      // extents, slowest first
+    const double* fac[kMaxOrder] = {};     // factor pointers (s_j x R row-major)
+};
+
+// MTTKRP root contractions (kernels_mttkrp.cu).
+//   back root:  P_F[F x R] = X[F x B] * KRP_B        (NN, TMA-staged X rows)
+//   front root: P_B[B x R] = X[F x B]^T * KRP_F      (TN, split-K)
+void launch_root_back(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kb,
+                      double* pf, cudaStream_t st);
+void launch_root_front(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kf,
+                       double* pb, double* splitk_ws, std::size_t splitk_ws_elems, cudaStream_t st);
+std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R);
+
+// Second dimension-tree level: P over kept modes (ext[0..k), R) reduced to the
+// single kept mode `keep`, weighting by the other kept modes' factor rows.
+void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, double* out,
+                        double* ws, std::size_t ws_elems, cudaStream_t st);
+std::size_t reduce_kept_workspace_elems(const KrpDesc& kept, int keep, int R);
+
+// Small dense kernels (kernels_small.cu).
+void launch_norm2(const double* x, std::uint64_t n, double* partials, int nparts, double* out,
+                  cudaStream_t st);
+int norm2_parts(std::uint64_t n);
+// grams of modes [lo, hi): factor n at base + offs[n] (device arrays), rows[n]
+void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
+                  int hi, int R, double* grams, cudaStream_t st);
+// pair[(n*order+p)] = Hadamard over grams m not in {n,p} ascending (kruskal.cpp:42-65)
+void launch_gamma_pairs(const double* grams, int order, int R, double* pair, cudaStream_t st);
+// gamma_one = Hadamard over grams m != n (als.cpp:34-37)
+void launch_gamma_excl(const double* grams, int order, int R, int n, double* out, cudaStream_t st);
+// scal[0..] <- residual pieces; writes r,f into out2 (kruskal.cpp:94-118)
+void launch_residual(const double* m_last, const double* a_last, std::int64_t rows, const double* grams,
+                     int order, int R, const double* xnorm2, double* partials, double* out2,
+                     cudaStream_t st);
+// G_n = A_n * Gamma(n,n) - M_n  (gauss_newton.cpp:81-94)
+void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
+                     double* g, cudaStream_t st);
+// out = sum_n scale*||X_n||_F (per-block Frobenius norms, summed in block order)
+void launch_block_norm_sum(const double* x, const std::int64_t* offsets, int nblocks,
+                           double* partials, double* out, double scale, cudaStream_t st);
+// y += alpha * x ; writes finite flag
+void launch_axpy(double* y, const double* x, double alpha, std::uint64_t n, cudaStream_t st);
+// out = ||a - b||_F accumulated into *acc (adds); deterministic per call
+void launch_diff_norm_add(const double* a, const double* b, std::uint64_t n, double* partials,
+                          double* acc, cudaStream_t st);
+void launch_dot(const double* a, const double* b, std::uint64_t n, double* partials, double* out,
+                cudaStream_t st);
+// out = a + alpha * x
+void launch_axpby(double* out, const double* a, double alpha, const double* x, std::uint64_t n,
+                  cudaStream_t st);
+void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st);
+// Dense evaluation of a Kruskal model + keyed-RNG noise (generators / reconstruct)
+void launch_reconstruct(const KrpDesc& all, int R, double* out, std::uint64_t offset, std::uint64_t n,
+                        cudaStream_t st);
+void launch_gaussian_fill(std::uint64_t seed, std::uint64_t stream, double* out, std::uint64_t n,
+                          std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
+                          cudaStream_t st);
+void launch_scaled_add(double* y, const double* x, const double* scale_num, const double* scale_den,
+                       double factor, std::uint64_t n, cudaStream_t st);
+
+// Cholesky-based SPD kernels (kernels_chol.cu); status: 0 ok, 1 ok after jitter, 2 singular
+// factor count matrices (contiguous R x R); lambda is a host value; mode 0:
+// S + lambda I, mode 1: diag(S) *= (1 + lambda). Packed lower L per matrix.
+void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode,
+                       double* l_out, int* status, cudaStream_t st);
+void launch_chol_solve_rows(const double* l, int R, const double* b, std::int64_t rows, double* y,
+                            cudaStream_t st);
+void launch_chol_inverse_batch(const double* l, int count, int R, double* inv, double* tmp,
+                               cudaStream_t st);
+
+// Persistent CG (kernels_cg.cu)
+struct CgParams {
+    int order = 0;
+    int R = 0;
+    std::int64_t rows[kMaxOrder] = {};
+    std::int64_t off[kMaxOrder + 1] = {};  // block offsets (elements) in stacked s x R buffers
+    const double* A = nullptr;     // stacked factors
+    const double* pair = nullptr;  // order*order*R*R gamma blocks
+    const double* pinv = nullptr;  // order*R*R preconditioner inverses
+    const double* G = nullptr;     // gradient
+    double* V = nullptr;
+    double* Rr[2] = {nullptr, nullptr};
+    double* W[2] = {nullptr, nullptr};
+    double* Z = nullptr;
+    double* Q = nullptr;
+    double* Bp = nullptr;          // order*R*R
+    double* slots = nullptr;       // per-task partial sums
+    int nslots = 0;
+    unsigned int* barrier = nullptr;
+    double lambda = 0.0;
+    int shape = 0;                 // 0 identity, 1 diagonal
+    int beta_variant = 0;          // 0 standard, 1 stale denominator
+    double cg_tol = 1e-3;
+    int cap = 0;
+    int* result = nullptr;         // [iters, hit_cap, breakdown, nonfinite, final_buffer]
+};
+void run_cg(const CgParams& p, int grid, cudaStream_t st);
+int cg_max_grid(int device);
+std::size_t cg_slots_needed(const CgParams& p);
+// U = J^T J W + lambda Reg(W) (same task code as the CG phases)
+void launch_jtj_matvec(const CgParams& p, const double* w, double* u, cudaStream_t st);
+
+// FP64 DMMA issue-rate probe (TFLOP/s), used as the measured roofline peak.
+double probe_dmma_peak(int device);
+
+}  // namespace cpkit

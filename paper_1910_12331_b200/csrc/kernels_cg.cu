@@ -1,0 +1,525 @@
+// Preconditioned implicit CG for (J^T J + lambda Reg) vec(V) = -vec(G)
+// as ONE persistent cooperative kernel (sm_100a, fp64).
+//
+// Reference: cp_cg (gauss_newton.cpp:279-349), hessian_matvec (:96-136),
+// build_preconditioner (:190-207), norm_sum/dot_sum (:246-258).
+//
+// The reference calls N^2 small Eigen GEMMs per matvec and recomputes
+// A_p^T W_p for every (n, p) pair. Here one CG iteration is three grid-wide
+// phases of 32x32 DMMA tile tasks separated by a software grid barrier:
+//   A: W' = Z + beta W (ping-pong, written once) and B_p = A_p^T W'_p
+//      (split over rows into partial slabs)                     O(R^2 sum s)
+//   B: Q_n = [W'_n | A_n] [Gamma(n,n) ; D_n^T] + lambda Reg(W'_n)
+//      with D_n = sum_{p!=n} Gamma(n,p) o B_p folded into the operand
+//      load, plus per-task partials of <W', Q>                  O(2 R^2 sum s)
+//   C: alpha = rz / <W,Q>; V += alpha W'; R' = R - alpha Q (ping-pong);
+//      Z = R' Pinv_n; partials of <R', Z> and ||R'_n||^2       O(R^2 sum s)
+// Every scalar (alpha, beta, the stop test sum_n ||R_n||_F <= tol sum_n ||G_n||_F,
+// the cap, breakdown !(wq > 0), the non-finite check) is recomputed by every
+// CTA from the same partial slots in the same order, so all CTAs take the
+// same branch with no host round trip. Results are bitwise reproducible.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.h"
+
+namespace cpkit {
+
+namespace {
+
+constexpr int kT = 32;        // task tile edge
+constexpr int kKC = 16;       // k chunk
+constexpr int kThreads = 256;  // 8 warps: 2 (m16) x 4 (n8)
+constexpr int kAS = kKC + 4;  // A smem row stride (doubles): conflict-free a-fragments
+constexpr int kBS = kT + 8;   // B smem row stride
+
+__device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
+        "{%4,%5,%6,%7,%8,%9,%10,%11},{%12,%13,%14,%15},{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+          "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+struct Smem {
+    double As[2][kT * kAS];
+    double Bs[2][kKC * kBS];
+    double red[kThreads / 32 * 4];
+    double bcast[8];
+};
+
+// C[32x32] tile = sum_{k<K} LA(row, k) * LB(k, col); rows/cols are tile-local.
+// Each of the 8 warps owns a 16x8 sub-tile; acc[4] holds (g, 2t..2t+1),
+// (g+8, 2t..2t+1). Operands are staged through double-buffered smem with the
+// next chunk prefetched into registers while the current one is multiplied.
+template <typename LA, typename LB>
+__device__ __forceinline__ void tile_gemm(Smem& sm, int K, LA la, LB lb, double acc[4]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 2) * 16, wn = (warp & 3) * 8;
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+    const int nch = (K + kKC - 1) / kKC;
+    // element assignment: A chunk 32x16 = 512 -> 2 per thread; B chunk 16x32 -> 2
+    const int ar0 = tid >> 4, ac0 = tid & 15;            // rows 0..15
+    const int ar1 = ar0 + 16;                            // rows 16..31
+    const int bk0 = tid >> 5, bc0 = tid & 31;            // k 0..7
+    const int bk1 = bk0 + 8;                             // k 8..15
+    double pa0, pa1, pb0, pb1;
+    auto fetch = [&](int c) {
+        const int k0 = c * kKC;
+        pa0 = (k0 + ac0 < K) ? la(ar0, k0 + ac0) : 0.0;
+        pa1 = (k0 + ac0 < K) ? la(ar1, k0 + ac0) : 0.0;
+        pb0 = (k0 + bk0 < K) ? lb(k0 + bk0, bc0) : 0.0;
+        pb1 = (k0 + bk1 < K) ? lb(k0 + bk1, bc0) : 0.0;
+    };
+    auto stash = [&](int buf) {
+        sm.As[buf][ar0 * kAS + ac0] = pa0;
+        sm.As[buf][ar1 * kAS + ac0] = pa1;
+        sm.Bs[buf][bk0 * kBS + bc0] = pb0;
+        sm.Bs[buf][bk1 * kBS + bc0] = pb1;
+    };
+    if (nch > 0) {
+        fetch(0);
+        stash(0);
+    }
+    __syncthreads();
+    for (int c = 0; c < nch; ++c) {
+        const int buf = c & 1;
+        if (c + 1 < nch) fetch(c + 1);
+        double a[8], b[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = sm.As[buf][(wm + g + 8 * (i & 1)) * kAS + t + 4 * (i >> 1)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = sm.Bs[buf][(t + 4 * i) * kBS + wn + g];
+        dmma16816(acc, a, b);
+        if (c + 1 < nch) stash(buf ^ 1);
+        __syncthreads();
+    }
+}
+
+// Fixed-order CTA reduction of one value per thread; returns to all threads.
+__device__ double cta_sum(Smem& sm, double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sm.red[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < kThreads / 32; ++i) s += sm.red[i];
+    __syncthreads();
+    return s;
+}
+
+__device__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vb = bar;
+        const unsigned int gen = vb[1];
+        __threadfence();
+        const unsigned int arrived = atomicAdd(&bar[0], 1u);
+        if (arrived == nblocks - 1) {
+            atomicExch(&bar[0], 0u);
+            __threadfence();
+            atomicAdd(&bar[1], 1u);
+        } else {
+            for (unsigned long long spin = 0; vb[1] == gen; ++spin) {
+                __nanosleep(20);
+                if (spin > (1ull << 28)) __trap();  // never hang the GPU on a lost arrival
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct Layout {
+    int order, R, tr;            // tr = tiles along R
+    int ksplit;                  // phase A row splits
+    int tasksA, tasksBC;
+    int rowtiles[kMaxOrder];     // tiles along s_n
+    int taskoff[kMaxOrder + 1];  // phase B/C task offsets per mode
+};
+
+__device__ __forceinline__ void decode_bc(const Layout& L, int task, int& n, int& rt, int& ct) {
+    n = 0;
+    while (task >= L.taskoff[n + 1]) ++n;
+    const int local = task - L.taskoff[n];
+    rt = local / L.tr;
+    ct = local % L.tr;
+}
+
+struct Dev {
+    CgParams p;
+    Layout L;
+    int mode;  // 0 = full CG, 1 = single matvec (W given in W[0], result in Q)
+};
+
+// slot regions (doubles): [0, tasksB) wq partials; then rz, nrm, fin per task C
+__device__ __forceinline__ double* slot_wq(const Dev& d) { return d.p.slots; }
+__device__ __forceinline__ double* slot_rz(const Dev& d) { return d.p.slots + d.L.tasksBC; }
+__device__ __forceinline__ double* slot_nrm(const Dev& d) { return d.p.slots + 2 * d.L.tasksBC; }
+__device__ __forceinline__ double* slot_fin(const Dev& d) { return d.p.slots + 3 * d.L.tasksBC; }
+__device__ __forceinline__ double* bpart(const Dev& d) { return d.p.slots + 4 * d.L.tasksBC; }
+
+// ---- phase A: W' = Z + beta W_old (first: W' = Z; matvec: W' = W_in), B_p partials
+__device__ void phase_a(const Dev& d, Smem& sm, const double* Wold, double* Wnew, double beta,
+                        bool first) {
+    const CgParams& p = d.p;
+    const Layout& L = d.L;
+    const int R = L.R;
+    for (int task = blockIdx.x; task < L.tasksA; task += gridDim.x) {
+        int rem = task;
+        const int ks = rem % L.ksplit; rem /= L.ksplit;
+        const int zt = rem % L.tr; rem /= L.tr;
+        const int rt = rem % L.tr; rem /= L.tr;
+        const int pm = rem;
+        const long long s = p.rows[pm];
+        const long long per = (s + L.ksplit - 1) / L.ksplit;
+        const long long k0 = ks * per, k1 = min(s, k0 + per);
+        const int K = static_cast<int>(max(0LL, k1 - k0));
+        const double* A = p.A + p.off[pm];
+        const double* Z = p.Z + p.off[pm];
+        const double* Wo = Wold + p.off[pm];
+        double* Wn = Wnew + p.off[pm];
+        const int r0 = rt * kT, z0 = zt * kT;
+        const bool writer = (rt == 0) && d.mode == 0;
+        auto la = [&](int row, int k) -> double {
+            const int r = r0 + row;
+            return r < R ? A[(k0 + k) * R + r] : 0.0;
+        };
+        auto lb = [&](int k, int col) -> double {
+            const int z = z0 + col;
+            if (z >= R) return 0.0;
+            const long long e = (k0 + k) * R + z;
+            if (d.mode == 1) return Wo[e];
+            const double v = first ? Z[e] : Z[e] + beta * Wo[e];
+            if (writer) Wn[e] = v;
+            return v;
+        };
+        double acc[4];
+        tile_gemm(sm, K, la, lb, acc);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int g = lane >> 2, t = lane & 3;
+        double* out = bpart(d) + (static_cast<long long>(ks) * L.order + pm) * R * R;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int r = r0 + (warp >> 2) * 16 + g + 8 * h;
+                const int z = z0 + (warp & 3) * 8 + 2 * t + c;
+                if (r < R && z < R) out[r * R + z] = acc[2 * h + c];
+            }
+    }
+}
+
+// ---- phase B: Q_n = [W'|A_n][Gnn; D^T] + lambda Reg(W'); wq partials
+__device__ void phase_b(const Dev& d, Smem& sm, const double* Wn_all, double* Qout) {
+    const CgParams& p = d.p;
+    const Layout& L = d.L;
+    const int R = L.R;
+    const long long RR = static_cast<long long>(R) * R;
+    for (int task = blockIdx.x; task < L.tasksBC; task += gridDim.x) {
+        int n, rt, ct;
+        decode_bc(L, task, n, rt, ct);
+        const long long s = p.rows[n];
+        const long long row0 = static_cast<long long>(rt) * kT;
+        const int c0 = ct * kT;
+        const double* W = Wn_all + p.off[n];
+        const double* A = p.A + p.off[n];
+        const double* Gnn = p.pair + (n * L.order + n) * RR;
+        auto la = [&](int row, int kk) -> double {
+            const long long i = row0 + row;
+            if (i >= s) return 0.0;
+            return kk < R ? W[i * R + kk] : A[i * R + (kk - R)];
+        };
+        auto lb = [&](int kk, int col) -> double {
+            const int r = c0 + col;
+            if (r >= R) return 0.0;
+            if (kk < R) return Gnn[kk * R + r];
+            const int z = kk - R;
+            double dsum = 0.0;
+            for (int q = 0; q < L.order; ++q) {
+                if (q == n) continue;
+                double b = 0.0;
+                for (int ks = 0; ks < L.ksplit; ++ks)
+                    b += bpart(d)[(static_cast<long long>(ks) * L.order + q) * RR + r * R + z];
+                dsum += p.pair[(n * L.order + q) * RR + r * R + z] * b;
+            }
+            return dsum;
+        };
+        double acc[4];
+        tile_gemm(sm, 2 * R, la, lb, acc);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int g = lane >> 2, t = lane & 3;
+        double part = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
+                const int r = c0 + (warp & 3) * 8 + 2 * t + c;
+                if (i < s && r < R) {
+                    const double w = W[i * R + r];
+                    const double reg = (p.shape == 0) ? p.lambda * w : w * (p.lambda * Gnn[r * R + r]);
+                    const double q = acc[2 * h + c] + reg;
+                    Qout[p.off[n] + i * R + r] = q;
+                    part += w * q;
+                }
+            }
+        const double tot = cta_sum(sm, part);
+        if (threadIdx.x == 0 && d.mode == 0) slot_wq(d)[task] = tot;
+    }
+}
+
+// ---- phase C: V += alpha W'; R' = R - alpha Q (init: R' = -G); Z = R' Pinv
+__device__ void phase_c(const Dev& d, Smem& sm, const double* Wn_all, const double* Rold_all,
+                        double* Rnew_all, double alpha, bool init) {
+    const CgParams& p = d.p;
+    const Layout& L = d.L;
+    const int R = L.R;
+    const long long RR = static_cast<long long>(R) * R;
+    for (int task = blockIdx.x; task < L.tasksBC; task += gridDim.x) {
+        int n, rt, ct;
+        decode_bc(L, task, n, rt, ct);
+        const long long s = p.rows[n];
+        const long long row0 = static_cast<long long>(rt) * kT;
+        const int c0 = ct * kT;
+        const long long off = p.off[n];
+        const double* Pinv = p.pinv + n * RR;
+        auto rnew = [&](long long e) -> double {
+            return init ? -p.G[e] : Rold_all[e] - alpha * p.Q[e];
+        };
+        auto la = [&](int row, int z) -> double {
+            const long long i = row0 + row;
+            return i < s ? rnew(off + i * R + z) : 0.0;
+        };
+        auto lb = [&](int z, int col) -> double {
+            const int r = c0 + col;
+            return r < R ? Pinv[z * R + r] : 0.0;
+        };
+        double acc[4];
+        tile_gemm(sm, R, la, lb, acc);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int g = lane >> 2, t = lane & 3;
+        double rz = 0.0, nrm = 0.0, bad = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
+                const int r = c0 + (warp & 3) * 8 + 2 * t + c;
+                if (i < s && r < R) {
+                    const long long e = off + i * R + r;
+                    const double rv = rnew(e);
+                    const double zv = acc[2 * h + c];
+                    double v;
+                    if (init) {
+                        v = 0.0;
+                    } else {
+                        v = p.V[e] + alpha * Wn_all[e];
+                    }
+                    p.V[e] = v;
+                    Rnew_all[e] = rv;
+                    p.Z[e] = zv;
+                    rz += rv * zv;
+                    nrm += rv * rv;
+                    if (!isfinite(v) || !isfinite(rv)) bad = 1.0;
+                }
+            }
+        const double trz = cta_sum(sm, rz);
+        const double tnrm = cta_sum(sm, nrm);
+        const double tbad = cta_sum(sm, bad);
+        if (threadIdx.x == 0) {
+            slot_rz(d)[task] = trz;
+            slot_nrm(d)[task] = tnrm;
+            slot_fin(d)[task] = tbad;
+        }
+    }
+}
+
+// Broadcast helpers: thread 0 sums slots in task order.
+__device__ double sum_slots(Smem& sm, const double* slots, int n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < n; ++i) s += reinterpret_cast<const volatile double*>(slots)[i];
+        sm.bcast[0] = s;
+    }
+    __syncthreads();
+    const double v = sm.bcast[0];
+    __syncthreads();
+    return v;
+}
+__device__ double norm_sum_slots(const Dev& d, Smem& sm) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const volatile double* nr = slot_nrm(d);
+        double total = 0.0;
+        for (int n = 0; n < d.L.order; ++n) {
+            double sq = 0.0;
+            for (int i = d.L.taskoff[n]; i < d.L.taskoff[n + 1]; ++i) sq += nr[i];
+            total += sqrt(sq);
+        }
+        sm.bcast[1] = total;
+    }
+    __syncthreads();
+    const double v = sm.bcast[1];
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) cg_kernel(Dev d) {
+    __shared__ Smem sm;
+    const CgParams& p = d.p;
+    const unsigned nb = gridDim.x;
+    if (d.mode == 1) {
+        // U = H W: W in W[0]; B_p from W then Q
+        phase_a(d, sm, p.W[0], p.W[1], 0.0, false);
+        grid_barrier(p.barrier, nb);
+        phase_b(d, sm, p.W[0], p.Q);
+        return;
+    }
+    // init: R = -G, Z = R Pinv, V = 0
+    phase_c(d, sm, p.W[0], p.Rr[0], p.Rr[1], 0.0, true);
+    grid_barrier(p.barrier, nb);
+    int rc = 1;  // current residual buffer
+    int wc = 0;  // current direction buffer (W_old)
+    int it = 0;
+    double rz = 0.0, wq = 0.0;
+    bool first = true;
+    const double gnorm = norm_sum_slots(d, sm);  // ||R|| = ||G|| at init
+    const double target = p.cg_tol * gnorm;
+    int hit_cap = 0, breakdown = 0, nonfinite = 0;
+    for (;;) {
+        const double rz_new = sum_slots(sm, slot_rz(d), d.L.tasksBC);
+        const double nsum = norm_sum_slots(d, sm);
+        double beta = 0.0;
+        if (!first) {
+            const double bad = sum_slots(sm, slot_fin(d), d.L.tasksBC);
+            if (bad != 0.0) {
+                nonfinite = 1;
+                break;
+            }
+            beta = (p.beta_variant == 0) ? rz_new / rz : rz_new / wq;
+        }
+        rz = rz_new;
+        if (!(nsum > target)) break;
+        if (it >= p.cap) {
+            hit_cap = 1;
+            break;
+        }
+        phase_a(d, sm, p.W[wc], p.W[wc ^ 1], beta, first);
+        wc ^= 1;
+        grid_barrier(p.barrier, nb);
+        phase_b(d, sm, p.W[wc], p.Q);
+        grid_barrier(p.barrier, nb);
+        wq = sum_slots(sm, slot_wq(d), d.L.tasksBC);
+        if (!(wq > 0.0)) {
+            breakdown = 1;
+            break;
+        }
+        const double alpha = rz / wq;
+        phase_c(d, sm, p.W[wc], p.Rr[rc], p.Rr[rc ^ 1], alpha, false);
+        rc ^= 1;
+        grid_barrier(p.barrier, nb);
+        ++it;
+        first = false;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.result[0] = it;
+        p.result[1] = hit_cap;
+        p.result[2] = breakdown;
+        p.result[3] = nonfinite;
+        p.result[4] = rc;
+    }
+}
+
+Layout make_layout(const CgParams& p, int grid) {
+    Layout L{};
+    L.order = p.order;
+    L.R = p.R;
+    L.tr = (p.R + kT - 1) / kT;
+    int off = 0;
+    long long smax = 1;
+    for (int n = 0; n < p.order; ++n) {
+        L.rowtiles[n] = static_cast<int>((p.rows[n] + kT - 1) / kT);
+        L.taskoff[n] = off;
+        off += L.rowtiles[n] * L.tr;
+        smax = std::max<long long>(smax, p.rows[n]);
+    }
+    L.taskoff[p.order] = off;
+    L.tasksBC = off;
+    const int base = p.order * L.tr * L.tr;
+    int ks = std::max(1, (grid + base - 1) / base);
+    ks = static_cast<int>(std::min<long long>(ks, std::max<long long>(1, smax / 32)));
+    L.ksplit = ks;
+    L.tasksA = base * ks;
+    return L;
+}
+
+int occupancy_grid(int device) {
+    int sms = 0, per = 0;
+    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, 0));
+    return sms * std::max(1, per);
+}
+
+void launch_coop(const Dev& d, int grid, cudaStream_t st) {
+    Dev dd = d;
+    void* args[] = {&dd};
+    CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_kernel), dim3(grid),
+                                         dim3(kThreads), args, 0, st));
+    count_launch(1);
+}
+
+}  // namespace
+
+int cg_max_grid(int device) {
+    int sms = 0;
+    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    return std::min(occupancy_grid(device), sms);
+}
+
+std::size_t cg_slots_needed(const CgParams& p) {
+    const Layout L = make_layout(p, 148);
+    // generous: ksplit may grow with grid, bound it by the rows/32 cap
+    long long smax = 1;
+    for (int n = 0; n < p.order; ++n) smax = std::max<long long>(smax, p.rows[n]);
+    const long long ksmax = std::max<long long>(1, smax / 32);
+    return static_cast<std::size_t>(4 * L.tasksBC) +
+           static_cast<std::size_t>(ksmax) * p.order * p.R * p.R;
+}
+
+void run_cg(const CgParams& p, int grid, cudaStream_t st) {
+    Dev d{};
+    d.p = p;
+    d.mode = 0;
+    // no point in more CTAs than the widest phase has tasks
+    const Layout L0 = make_layout(p, grid);
+    grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
+    d.L = make_layout(p, grid);
+    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, 2 * sizeof(unsigned int), st));
+    launch_coop(d, grid, st);
+}
+
+void launch_jtj_matvec(const CgParams& p, const double* w, double* u, cudaStream_t st) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    Dev d{};
+    d.p = p;
+    d.p.W[0] = const_cast<double*>(w);
+    d.p.Q = u;
+    d.mode = 1;
+    int grid = cg_max_grid(dev);
+    const Layout L0 = make_layout(p, grid);
+    grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
+    d.L = make_layout(p, grid);
+    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, 2 * sizeof(unsigned int), st));
+    launch_coop(d, grid, st);
+}
+
+}  // namespace cpkit

@@ -1,0 +1,578 @@
+// MTTKRP dimension-tree kernels for sm_100a (fp64).
+//
+// Reference: mttkrp.cpp:160-189 computes M^(n) by contracting the tensor with
+// the "back" factors (modes >= h) when n < h, else with the "front" factors,
+// caching the root partial, then contracting the remaining kept modes
+// (:118-126, :63-75). The reference's root step is a mode-at-a-time Eigen GEMM
+// over a full tensor copy (:46-62, :79-87).
+//
+// B200 design: the root contraction is ONE fused GEMM against the
+// Khatri-Rao product of all contracted factors, generated tile-by-tile in
+// shared memory and never materialised:
+//   back root   P_F[F x R] = X[F x B]   * KRP_B[B x R]   (kernel TRANS=false)
+//   front root  P_B[B x R] = X[F x B]^T * KRP_F[F x R]   (kernel TRANS=true, split-K)
+// X tiles are staged by TMA (cp.async.bulk.tensor, 128B swizzle) into a
+// multi-stage mbarrier pipeline; the math is FP64 DMMA (mma.sync m16n8k16,
+// SASS DMMA.8x8x4; tcgen05 has no f64 kind on sm_100a). Each warp owns a
+// 16-row strip of the CTA tile and all NT n8-tiles of the rank columns.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include "common.h"
+
+namespace cpkit {
+
+namespace {
+
+constexpr int kBK = 32;  // k-depth of one pipeline stage (two 16-double swizzle atoms)
+
+// ---------------------------------------------------------------- TMA plumbing
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    if (!fn) throw DeviceError("cuTensorMapEncodeTiled entry point unavailable");
+    return fn;
+}
+
+// 2-D fp64 map over a row-major (outer x inner) matrix; box = 16 doubles
+// (128 B, the swizzle atom) along inner by box_outer rows.
+CUtensorMap make_map(const double* base, std::uint64_t inner, std::uint64_t outer,
+                     std::uint32_t box_outer) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * sizeof(double)};
+    cuuint32_t box[2] = {16, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+    return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned phase) {
+    // bounded spin: a lost TMA transaction traps instead of hanging the GPU
+    for (unsigned long long spin = 0;; ++spin) {
+        unsigned ok;
+        asm volatile(
+            "{\n.reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+        if (ok) return;
+        if (spin > (1ull << 26)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, std::uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
+        "{%4,%5,%6,%7,%8,%9,%10,%11},{%12,%13,%14,%15},{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+          "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+// Byte offset of element (row, col) inside a 128B-swizzled atom of 16 doubles
+// per row (the layout TMA SWIZZLE_128B produces; 1024-B aligned atom base).
+__device__ __forceinline__ int swz(int row, int col) {
+    return row * 128 + ((((col >> 1) ^ row) & 7) << 4) + ((col & 1) << 3);
+}
+
+// Row padding for the KRP operand so the B-fragment loads are conflict-free:
+// rows are read either as t+4i (NN) or 2t+c+8h (TN, permuted k-slots).
+template <bool TRANS>
+__host__ __device__ constexpr int krp_stride(int bn) {
+    const int want = TRANS ? 4 : 8;
+    int s = bn;
+    while (s % 16 != want) ++s;
+    return s;
+}
+
+// k-slot -> physical smem row inside a 16-deep k step (TN only): makes the
+// transposed A-fragment reads hit 8 distinct 16B chunks per half-warp.
+__device__ __forceinline__ int kperm(int s) { return 2 * (s & 3) + ((s >> 2) & 1) + 8 * (s >> 3); }
+
+struct KrpDev {
+    int nmodes;
+    long long ext[kMaxOrder];
+    const double* fac[kMaxOrder];
+};
+
+// Fill one BK x BN tile of the Khatri-Rao operand:
+// Bs[p][n] = prod_j fac_j[i_j(k0+p), n0+n]  (0 outside [0,K) x [0,R)).
+template <int BNS>
+__device__ __forceinline__ void gen_krp_tile(double* bs, const KrpDev& kd, long long k0, long long K,
+                                             int n0, int R, int bn) {
+    const int nthr = blockDim.x;
+    const int tpr = 8;  // threads per row
+    for (int row = threadIdx.x / tpr; row < kBK; row += nthr / tpr) {
+        const long long k = k0 + row;
+        double* dst = bs + row * BNS;
+        const int lane8 = threadIdx.x % tpr;
+        if (k >= K) {
+            for (int n = lane8; n < bn; n += tpr) dst[n] = 0.0;
+            continue;
+        }
+        const double* rowp[kMaxOrder];
+        long long rem = k;
+        for (int j = kd.nmodes - 1; j >= 0; --j) {
+            const long long e = kd.ext[j];
+            const long long i = rem % e;
+            rem /= e;
+            rowp[j] = kd.fac[j] + i * R;
+        }
+        for (int n = lane8; n < bn; n += tpr) {
+            const int col = n0 + n;
+            double v = 0.0;
+            if (col < R) {
+                v = rowp[0][col];
+                for (int j = 1; j < kd.nmodes; ++j) v *= rowp[j][col];
+            }
+            dst[n] = v;
+        }
+    }
+}
+
+// Manual (non-TMA) X tile load producing the same swizzled layout; used when
+// the row stride is not 16-byte aligned (odd inner extent).
+template <bool TRANS>
+__device__ void load_x_manual(char* xs, const double* x, long long rows_total, long long cols_total,
+                              long long r0, long long c0, int box_rows, int nboxes) {
+    // NN: boxes along columns (k); box b covers cols c0+16b.., rows r0..r0+box_rows
+    // TN: boxes along columns (m); rows are k. Same addressing either way.
+    const int per_box = box_rows * 16;
+    const int total = per_box * nboxes;
+    for (int e = threadIdx.x; e < total; e += blockDim.x) {
+        const int b = e / per_box;
+        const int w = e % per_box;
+        const int row = w / 16, col = w % 16;
+        const long long gr = r0 + row, gc = c0 + 16LL * b + col;
+        double v = 0.0;
+        if (gr < rows_total && gc < cols_total) v = x[gr * cols_total + gc];
+        *reinterpret_cast<double*>(xs + b * box_rows * 128 + swz(row, col)) = v;
+    }
+}
+
+// ---------------------------------------------------------------- root GEMM
+// TRANS=false: C[m][n] = sum_k X[m][k] KRP[k][n]   (X is M x K, row stride K)
+// TRANS=true:  C[m][n] = sum_k X[k][m] KRP[k][n]   (X is K x M, row stride M)
+// grid: (n_tiles, m_tiles, splits); block: 32 * (BM/16) threads.
+template <int NT, bool TRANS>
+__global__ void __launch_bounds__(256, 1)
+root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ x,
+                 int use_tma, long long M, long long K, int R, int BM, int stages, KrpDev kd,
+                 long long k_per_split, double* __restrict__ out, long long out_split_stride) {
+    constexpr int BN = 8 * NT;
+    constexpr int BNS = krp_stride<TRANS>(BN);
+    extern __shared__ __align__(1024) char smem_raw[];
+    char* smem = reinterpret_cast<char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+    const int x_bytes = BM * kBK * 8;
+    const int b_bytes = kBK * BNS * 8;
+    char* xs_base = smem;
+    double* bs_base = reinterpret_cast<double*>(smem + stages * x_bytes);
+    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + stages * (x_bytes + b_bytes));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int n0 = blockIdx.x * BN;
+    const long long m0 = static_cast<long long>(blockIdx.y) * BM;
+    const long long kbeg = static_cast<long long>(blockIdx.z) * k_per_split;
+    const long long kend = min(K, kbeg + k_per_split);
+    const int nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
+    const int bn = min(BN, R - n0);
+
+    // NN: 2 boxes of (16 k) x BM rows.  TN: BM/16 boxes of (16 m) x BK rows.
+    const int nboxes = TRANS ? BM / 16 : kBK / 16;
+    const int box_rows = TRANS ? kBK : BM;
+    const unsigned stage_tx = static_cast<unsigned>(x_bytes);
+
+    if (threadIdx.x == 0 && use_tma) {
+        for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int kt, int s) {
+        const long long kk = kbeg + static_cast<long long>(kt) * kBK;
+        char* xs = xs_base + s * x_bytes;
+        if (use_tma) {
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(&bars[s], stage_tx);
+                for (int b = 0; b < nboxes; ++b) {
+                    if (TRANS)
+                        tma_load_2d(&xmap, &bars[s], xs + b * box_rows * 128,
+                                    static_cast<int>(m0 + 16 * b), static_cast<int>(kk));
+                    else
+                        tma_load_2d(&xmap, &bars[s], xs + b * box_rows * 128,
+                                    static_cast<int>(kk + 16 * b), static_cast<int>(m0));
+                }
+            }
+        } else {
+            if (TRANS)
+                load_x_manual<TRANS>(xs, x, K, M, kk, m0, box_rows, nboxes);
+            else
+                load_x_manual<TRANS>(xs, x, M, K, m0, kk, box_rows, nboxes);
+        }
+        gen_krp_tile<BNS>(bs_base + s * (kBK * BNS), kd, kk, kend, n0, R, bn);
+    };
+
+    double acc[NT][4];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+    const int pre = min(stages, nk);
+    for (int s = 0; s < pre; ++s) issue(s, s);
+    __syncthreads();
+
+    const int wm = warp * 16;  // warp's row strip inside the CTA tile
+    for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % stages;
+        if (use_tma) mbar_wait(&bars[s], (kt / stages) & 1);
+        const char* xs = xs_base + s * x_bytes;
+        const double* bs = bs_base + s * (kBK * BNS);
+#pragma unroll
+        for (int ks = 0; ks < kBK / 16; ++ks) {
+            double a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int mrow = wm + g + 8 * (i & 1);
+                if (!TRANS) {
+                    // X[m][k]: box ks holds k in [16ks,16ks+16), rows m
+                    const int kc = t + 4 * (i >> 1);
+                    a[i] = *reinterpret_cast<const double*>(xs + ks * BM * 128 + swz(mrow, kc));
+                } else {
+                    // X[k][m]: box (mrow/16) holds m cols; rows are k (permuted slots)
+                    const int krow = ks * 16 + kperm(t + 4 * (i >> 1));
+                    const int box = mrow >> 4;
+                    a[i] = *reinterpret_cast<const double*>(xs + box * kBK * 128 +
+                                                            swz(krow, mrow & 15));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < NT; ++j) {
+                double b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int krow = TRANS ? ks * 16 + kperm(t + 4 * i) : ks * 16 + t + 4 * i;
+                    b[i] = bs[krow * BNS + j * 8 + g];
+                }
+                dmma16816(acc[j], a, b);
+            }
+        }
+        __syncthreads();
+        if (kt + stages < nk) {
+            if (use_tma) fence_proxy_async();
+            issue(kt + stages, s);
+        }
+    }
+
+    // epilogue: rows m0+wm+g(+8), cols n0+8j+2t(+1)
+    double* o = out + blockIdx.z * out_split_stride;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+        const int col = n0 + 8 * j + 2 * t;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const long long row = m0 + wm + g + 8 * h;
+            if (row < M) {
+                if (col < R) o[row * R + col] = acc[j][2 * h];
+                if (col + 1 < R) o[row * R + col + 1] = acc[j][2 * h + 1];
+            }
+        }
+    }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, long long n,
+                                     double* __restrict__ out) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int k = 0; k < splits; ++k) s += ws[k * n + i];  // fixed order: deterministic
+        out[i] = s;
+    }
+}
+
+KrpDev to_dev(const KrpDesc& d) {
+    KrpDev k{};
+    k.nmodes = d.nmodes;
+    for (int i = 0; i < d.nmodes; ++i) {
+        k.ext[i] = d.ext[i];
+        k.fac[i] = d.fac[i];
+    }
+    return k;
+}
+
+int num_sms() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        CPK_CUDA(cudaGetDevice(&dev));
+        CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return sms;
+}
+
+// Rank tiling: n8 tiles per CTA (instantiated set) and number of column tiles.
+constexpr int kNtChoices[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16};
+void pick_nt(int R, int& nt, int& ntiles) {
+    ntiles = (R + 127) / 128;
+    const int need = (R + 8 * ntiles - 1) / (8 * ntiles);
+    nt = 16;
+    for (int c : kNtChoices)
+        if (c >= need) {
+            nt = c;
+            break;
+        }
+}
+
+// Rows per CTA: 16 x warps, warps in [4,8], minimising padded rows.
+int pick_bm(long long M) {
+    int best_w = 8;
+    long long best_waste = -1;
+    for (int w = 8; w >= 4; --w) {
+        const long long bm = 16LL * w;
+        const long long waste = ((M + bm - 1) / bm) * bm - M;
+        if (best_waste < 0 || waste < best_waste) {
+            best_waste = waste;
+            best_w = w;
+        }
+    }
+    return 16 * best_w;
+}
+
+template <bool TRANS>
+void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, const CUtensorMap& map,
+              const double* x, int use_tma, long long M, long long K, int R, int BM, int stages,
+              const KrpDev& kd, long long kps, double* out, long long oss) {
+#define CPK_CASE(NTV)                                                                         \
+    case NTV: {                                                                               \
+        auto fn = root_gemm_kernel<NTV, TRANS>;                                               \
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                                      static_cast<int>(smem)));                               \
+        fn<<<grid, block, smem, st>>>(map, x, use_tma, M, K, R, BM, stages, kd, kps, out, oss); ::cpkit::count_launch(1); \
+        break;                                                                                \
+    }
+    switch (nt) {
+        CPK_CASE(1) CPK_CASE(2) CPK_CASE(3) CPK_CASE(4) CPK_CASE(5) CPK_CASE(6) CPK_CASE(7)
+        CPK_CASE(8) CPK_CASE(10) CPK_CASE(12) CPK_CASE(13) CPK_CASE(16)
+        default: throw DeviceError("unsupported rank tile");
+    }
+#undef CPK_CASE
+    CPK_CUDA(cudaGetLastError());
+}
+
+std::size_t smem_bytes(int BM, int nt, bool trans, int stages) {
+    const int bns = trans ? krp_stride<true>(8 * nt) : krp_stride<false>(8 * nt);
+    return static_cast<std::size_t>(stages) * (BM * kBK * 8 + kBK * bns * 8) + stages * 8 + 1024;
+}
+
+int pick_stages(int BM, int nt, bool trans) {
+    for (int s = 4; s >= 2; --s)
+        if (smem_bytes(BM, nt, trans, s) <= 220 * 1024) return s;
+    return 2;
+}
+
+bool tma_ok(const double* x, long long inner) {
+    return (inner % 2 == 0) && (reinterpret_cast<std::uintptr_t>(x) % 16 == 0) &&
+           inner < (1LL << 31);
+}
+
+struct FrontPlan {
+    int nt, ntiles, BM, mtiles, splits;
+    long long kps;
+};
+FrontPlan plan_front(long long F, long long B, int R) {
+    FrontPlan p{};
+    pick_nt(R, p.nt, p.ntiles);
+    p.BM = pick_bm(B);
+    p.mtiles = static_cast<int>((B + p.BM - 1) / p.BM);
+    const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
+    const long long target = 2LL * num_sms();
+    const long long kchunks = (F + kBK - 1) / kBK;
+    long long splits = std::max<long long>(1, (target + base - 1) / base);
+    splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
+    p.kps = ((kchunks + splits - 1) / splits) * kBK;
+    p.splits = static_cast<int>((F + p.kps - 1) / p.kps);
+    return p;
+}
+
+}  // namespace
+
+void launch_root_back(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kb,
+                      double* pf, cudaStream_t st) {
+    int nt, ntiles;
+    pick_nt(R, nt, ntiles);
+    const int BM = pick_bm(F);
+    const int stages = pick_stages(BM, nt, false);
+    const bool tma = tma_ok(x, B) && F < (1LL << 31);
+    CUtensorMap map{};
+    if (tma) map = make_map(x, B, F, BM);
+    dim3 grid(ntiles, static_cast<unsigned>((F + BM - 1) / BM), 1);
+    if (grid.y > 65535) throw LimitExceeded("root_back: too many row tiles");
+    dispatch<false>(nt, grid, dim3(2 * BM), smem_bytes(BM, nt, false, stages), st, map, x, tma, F, B,
+                    R, BM, stages, to_dev(kb), B, pf, 0);
+}
+
+std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R) {
+    const FrontPlan p = plan_front(F, B, R);
+    return p.splits > 1 ? static_cast<std::size_t>(p.splits) * B * R : 0;
+}
+
+void launch_root_front(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kf,
+                       double* pb, double* ws, std::size_t ws_elems, cudaStream_t st) {
+    const FrontPlan p = plan_front(F, B, R);
+    const int stages = pick_stages(p.BM, p.nt, true);
+    const bool tma = tma_ok(x, B) && F < (1LL << 31);
+    CUtensorMap map{};
+    if (tma) map = make_map(x, B, F, kBK);
+    dim3 grid(p.ntiles, p.mtiles, p.splits);
+    double* out = pb;
+    long long oss = 0;
+    if (p.splits > 1) {
+        if (ws_elems < static_cast<std::size_t>(p.splits) * B * R)
+            throw DeviceError("root_front: split-K workspace too small");
+        out = ws;
+        oss = B * R;
+    }
+    dispatch<true>(p.nt, grid, dim3(2 * p.BM), smem_bytes(p.BM, p.nt, true, stages), st, map, x, tma,
+                   B, F, R, p.BM, stages, to_dev(kf), p.kps, out, oss);
+    if (p.splits > 1) {
+        const long long n = B * static_cast<long long>(R);
+        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, pb); ::cpkit::count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+    }
+}
+
+// ---------------------------------------------------------------- second level
+// out[i, r] = sum over all other kept indices of P[idx, r] * prod_{l != keep} A_l[idx_l, r]
+// (the descending mode-at-a-time contraction of mttkrp.cpp:118-126/:63-75,
+// done in one pass). P is [outer][s_keep][inner][R]. One CTA per (i, split);
+// threads stride over r; each CTA sums its (outer x inner) range in order.
+namespace {
+__global__ void reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep, int R,
+                                   long long outer, long long sk, long long inner, int splits,
+                                   double* __restrict__ out, long long out_split_stride) {
+    const long long i = blockIdx.x;
+    const int split = blockIdx.y;
+    const long long total = outer * inner;
+    const long long per = (total + splits - 1) / splits;
+    const long long lo = split * per, hi = min(total, lo + per);
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double acc = 0.0;
+        for (long long q = lo; q < hi; ++q) {
+            const long long o = q / inner, in = q % inner;
+            const double* src = p + ((o * sk + i) * inner + in) * R;
+            // weight = prod over kept modes l != keep (decompose o and in)
+            double w = 1.0;
+            long long rem = in;
+            for (int l = kd.nmodes - 1; l > keep; --l) {
+                const long long e = kd.ext[l];
+                w *= kd.fac[l][(rem % e) * R + r];
+                rem /= e;
+            }
+            rem = o;
+            for (int l = keep - 1; l >= 0; --l) {
+                const long long e = kd.ext[l];
+                w *= kd.fac[l][(rem % e) * R + r];
+                rem /= e;
+            }
+            acc += src[r] * w;
+        }
+        out[split * out_split_stride + i * R + r] = acc;
+    }
+}
+}  // namespace
+
+namespace {
+int reduce_splits(const KrpDesc& kept, int keep) {
+    long long sk = kept.ext[keep];
+    long long total = 1;
+    for (int l = 0; l < kept.nmodes; ++l)
+        if (l != keep) total *= kept.ext[l];
+    const long long target = 2LL * num_sms();
+    long long s = std::max<long long>(1, (target + sk - 1) / sk);
+    s = std::min<long long>(s, std::max<long long>(1, total / 8));
+    return static_cast<int>(s);
+}
+}  // namespace
+
+std::size_t reduce_kept_workspace_elems(const KrpDesc& kept, int keep, int R) {
+    const int s = reduce_splits(kept, keep);
+    return s > 1 ? static_cast<std::size_t>(s) * kept.ext[keep] * R : 0;
+}
+
+void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, double* out,
+                        double* ws, std::size_t ws_elems, cudaStream_t st) {
+    long long outer = 1, inner = 1;
+    for (int l = 0; l < keep; ++l) outer *= kept.ext[l];
+    for (int l = keep + 1; l < kept.nmodes; ++l) inner *= kept.ext[l];
+    const long long sk = kept.ext[keep];
+    const int splits = reduce_splits(kept, keep);
+    const int threads = R >= 128 ? 128 : ((R + 31) / 32) * 32;
+    double* dst = out;
+    if (splits > 1) {
+        if (ws_elems < static_cast<std::size_t>(splits) * sk * R)
+            throw DeviceError("reduce_kept: workspace too small");
+        dst = ws;
+    }
+    dim3 grid(static_cast<unsigned>(sk), splits);
+    reduce_kept_kernel<<<grid, threads, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits,
+                                                 dst, sk * R); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+    if (splits > 1) {
+        const long long n = sk * R;
+        splitk_reduce_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 1024)), 256, 0,
+                               st>>>(ws, splits, n, out); ::cpkit::count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+    }
+}
+
+}  // namespace cpkit

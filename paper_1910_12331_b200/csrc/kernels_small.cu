@@ -1,0 +1,432 @@
+// Bandwidth/latency-bound kernels of the GN/ALS path (sm_100a, fp64).
+// All reductions are two-pass with a fixed grid and a fixed combine order,
+// so every result is bitwise reproducible run to run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "common.h"
+
+namespace cpkit {
+
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kRedBlocksMax = 592;  // 4 x 148 SMs
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+// Block sum in a fixed order; result valid in thread 0.
+__device__ double block_sum(double v) {
+    __shared__ double sh[32];
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    double r = 0.0;
+    if (w == 0) {
+        r = l < nw ? sh[l] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;
+}
+
+// ---- ||X||^2 (tensor.cpp:61-67), HBM-streaming with 16-byte loads
+__global__ void norm2_partial_kernel(const double* __restrict__ x, unsigned long long n,
+                                     double* __restrict__ partials) {
+    double acc = 0.0;
+    const unsigned long long stride = static_cast<unsigned long long>(gridDim.x) * blockDim.x;
+    const unsigned long long n2 = n / 2;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n2; i += stride) {
+        const double2 v = __ldcs(x2 + i);
+        acc += v.x * v.x;
+        acc += v.y * v.y;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) acc += x[n - 1] * x[n - 1];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void sum_partials_kernel(const double* __restrict__ partials, int n, double* out,
+                                    double scale) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partials[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) *out = s * scale;
+}
+
+// ---- Gram S = A^T A with exact symmetry (matrix_ops.cpp:30-34).
+// One thread per (r <= z) entry, sequential sum over rows; modes [lo, hi).
+__global__ void grams_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
+                             const long long* __restrict__ rows, int lo, int R,
+                             double* __restrict__ grams) {
+    const int n = lo + blockIdx.y;
+    const double* a = base + offs[n];
+    const long long s = rows[n];
+    double* out = grams + static_cast<long long>(n) * R * R;
+    const int tri = R * (R + 1) / 2;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tri; e += gridDim.x * blockDim.x) {
+        // map e -> (r, z) with r <= z, row-major over the upper triangle
+        int r = 0, rem = e;
+        while (rem >= R - r) {
+            rem -= R - r;
+            ++r;
+        }
+        const int z = r + rem;
+        double acc = 0.0;
+        for (long long i = 0; i < s; ++i) acc += a[i * R + r] * a[i * R + z];
+        out[r * R + z] = acc;
+        out[z * R + r] = acc;
+    }
+}
+
+// Gamma(n,p) = Ones o S^(m) for ascending m not in {n,p}; computed for p >= n
+// and mirrored, so bitwise symmetric (kruskal.cpp:42-65).
+__global__ void gamma_pairs_kernel(const double* __restrict__ grams, int order, int R,
+                                   double* __restrict__ pair) {
+    const int n = blockIdx.y / order, p = blockIdx.y % order;
+    if (p < n) return;
+    const long long rr = static_cast<long long>(R) * R;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < rr;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double g = 1.0;
+        for (int m = 0; m < order; ++m) {
+            if (m == n || m == p) continue;
+            g *= grams[m * rr + e];
+        }
+        pair[(n * order + p) * rr + e] = g;
+        if (p != n) pair[(p * order + n) * rr + e] = g;
+    }
+}
+__global__ void gamma_excl_kernel(const double* __restrict__ grams, int order, int R, int n,
+                                  double* __restrict__ out) {
+    const long long rr = static_cast<long long>(R) * R;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < rr;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        double g = 1.0;
+        for (int m = 0; m < order; ++m)
+            if (m != n) g *= grams[m * rr + e];
+        out[e] = g;
+    }
+}
+
+// Residual (kruskal.cpp:94-118): partial cross term <M, A> per block plus
+// the model norm sum_rz prod_m S^(m)_rz; finalised by one block.
+__global__ void residual_partial_kernel(const double* __restrict__ m, const double* __restrict__ a,
+                                        long long n, const double* __restrict__ grams, int order,
+                                        int R, double* __restrict__ partials) {
+    // blocks [0, gridDim.x-1): cross term; last block: model norm
+    if (blockIdx.x + 1 < gridDim.x) {
+        double acc = 0.0;
+        const long long stride = static_cast<long long>(gridDim.x - 1) * blockDim.x;
+        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+             i += stride)
+            acc += m[i] * a[i];
+        const double s = block_sum(acc);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    } else {
+        const long long rr = static_cast<long long>(R) * R;
+        double acc = 0.0;
+        for (long long e = threadIdx.x; e < rr; e += blockDim.x) {
+            double g = 1.0;
+            for (int q = 0; q < order; ++q) g *= grams[q * rr + e];
+            acc += g;
+        }
+        const double s = block_sum(acc);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    }
+}
+__global__ void residual_final_kernel(const double* __restrict__ partials, int nparts,
+                                      const double* __restrict__ xnorm2, double* __restrict__ out) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nparts - 1; i += blockDim.x) acc += partials[i];
+    const double cross = block_sum(acc);
+    if (threadIdx.x == 0) {
+        const double model = partials[nparts - 1];
+        const double x2 = *xnorm2;
+        double res2 = x2 - 2.0 * cross + model;
+        if (res2 < 0.0) res2 = 0.0;
+        const double r = sqrt(res2 / x2);
+        out[0] = r;
+        out[1] = 1.0 - r;
+    }
+}
+
+// G = A * Gamma - M   (s x R) (R x R)
+__global__ void gradient_kernel(const double* __restrict__ a, const double* __restrict__ gnn,
+                                const double* __restrict__ m, long long rows, int R,
+                                double* __restrict__ g) {
+    const long long total = rows * R;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = e / R;
+        const int r = static_cast<int>(e % R);
+        double acc = 0.0;
+        for (int z = 0; z < R; ++z) acc += a[i * R + z] * gnn[z * R + r];
+        g[e] = acc - m[e];
+    }
+}
+
+// Sum over blocks of ||block||_F (gauss_newton.cpp:246-250 norm_sum): partial
+// sums of squares per (block, chunk); final kernel does sqrt per block in order.
+__global__ void block_sq_partial_kernel(const double* __restrict__ x,
+                                        const long long* __restrict__ off, int nblocks, int chunks,
+                                        double* __restrict__ partials) {
+    const int b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    const long long lo = off[b], hi = off[b + 1];
+    double acc = 0.0;
+    for (long long i = lo + c * static_cast<long long>(blockDim.x) + threadIdx.x; i < hi;
+         i += static_cast<long long>(chunks) * blockDim.x)
+        acc += x[i] * x[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void block_norm_final_kernel(const double* __restrict__ partials, int nblocks, int chunks,
+                                        double* out, double scale) {
+    if (threadIdx.x != 0) return;
+    double total = 0.0;
+    for (int b = 0; b < nblocks; ++b) {
+        double sq = 0.0;
+        for (int c = 0; c < chunks; ++c) sq += partials[b * chunks + c];
+        total += scale * sqrt(sq);
+    }
+    *out = total;
+}
+
+__global__ void axpy_kernel(double* __restrict__ y, const double* __restrict__ x, double alpha,
+                            unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        y[i] += alpha * x[i];
+}
+__global__ void diff_sq_partial_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                       unsigned long long n, double* __restrict__ partials) {
+    double acc = 0.0;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const double d = a[i] - b[i];
+        acc += d * d;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void sqrt_add_kernel(const double* __restrict__ partials, int n, double* acc) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += partials[i];
+    const double s = block_sum(v);
+    if (threadIdx.x == 0) *acc += sqrt(s);
+}
+__global__ void dot_partial_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                   unsigned long long n, double* __restrict__ partials) {
+    double acc = 0.0;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        acc += a[i] * b[i];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+__global__ void axpby_kernel(double* __restrict__ out, const double* __restrict__ a, double alpha,
+                             const double* __restrict__ x, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        out[i] = a[i] + alpha * x[i];
+}
+__global__ void all_finite_kernel(const double* __restrict__ x, unsigned long long n, int* flag) {
+    bool bad = false;
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        bad |= !isfinite(x[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 0);
+}
+
+// ---- generators (kruskal.cpp:67-92 reconstruct; rng.hpp keyed gaussian)
+struct KrpDevS {
+    int nmodes;
+    long long ext[kMaxOrder];
+    const double* fac[kMaxOrder];
+};
+__global__ void reconstruct_kernel(KrpDevS kd, int R, double* __restrict__ out,
+                                   unsigned long long offset, unsigned long long n) {
+    for (unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         e < n; e += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        unsigned long long f = offset + e;
+        long long idx[kMaxOrder];
+        for (int m = kd.nmodes - 1; m >= 0; --m) {
+            idx[m] = static_cast<long long>(f % kd.ext[m]);
+            f /= kd.ext[m];
+        }
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) {
+            double prod = 1.0;
+            for (int m = 0; m < kd.nmodes; ++m) prod = __dmul_rn(prod, kd.fac[m][idx[m] * R + r]);
+            acc = __dadd_rn(acc, prod);
+        }
+        out[e] = acc;
+    }
+}
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ unsigned long long derive(unsigned long long h, unsigned long long v) {
+    return mix64(h ^ (v * 0xD6E8FEB86659FD93ull + 0xA0761D6478BD642Full));
+}
+// Noise entry e of a (possibly last-mode-sharded) slab uses the keyed index of
+// its GLOBAL flat position so the noise is independent of the GPU count.
+__global__ void gaussian_fill_kernel(unsigned long long seed, unsigned long long stream,
+                                     double* __restrict__ out, unsigned long long n,
+                                     unsigned long long slab, unsigned long long s_last,
+                                     unsigned long long slab_lo) {
+    const unsigned long long base = derive(mix64(seed), stream);
+    for (unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         e < n; e += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const unsigned long long gidx = (e / slab) * s_last + slab_lo + (e % slab);
+        const unsigned long long h = derive(base, gidx);
+        const double u1 = static_cast<double>((derive(h, 1) >> 11) + 1) * 0x1.0p-53;
+        const double u2 = static_cast<double>(derive(h, 2) >> 11) * 0x1.0p-53;
+        out[e] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+    }
+}
+__global__ void scaled_add_kernel(double* __restrict__ y, const double* __restrict__ x,
+                                  const double* num, const double* den, double factor,
+                                  unsigned long long n) {
+    const double s = factor * sqrt(*num) / sqrt(*den);
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
+         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+        y[i] += s * x[i];
+}
+
+int grid_for(unsigned long long n, int threads, int cap = kRedBlocksMax) {
+    const unsigned long long b = (n + threads - 1) / threads;
+    return static_cast<int>(std::max<unsigned long long>(1, std::min<unsigned long long>(b, cap)));
+}
+
+}  // namespace
+
+int norm2_parts(std::uint64_t n) { return grid_for(std::max<std::uint64_t>(1, n / 2), kRedThreads); }
+
+void launch_norm2(const double* x, std::uint64_t n, double* partials, int nparts, double* out,
+                  cudaStream_t st) {
+    if (reinterpret_cast<std::uintptr_t>(x) % 16 != 0) throw DeviceError("norm2: misaligned tensor");
+    norm2_partial_kernel<<<nparts, kRedThreads, 0, st>>>(x, n, partials); ::cpkit::count_launch(1);
+    sum_partials_kernel<<<1, kRedThreads, 0, st>>>(partials, nparts, out, 1.0); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
+                  int hi, int R, double* grams, cudaStream_t st) {
+    const int tri = R * (R + 1) / 2;
+    dim3 grid(std::max(1, std::min((tri + 127) / 128, 256)), hi - lo);
+    grams_kernel<<<grid, 128, 0, st>>>(base, reinterpret_cast<const long long*>(offs),
+                                       reinterpret_cast<const long long*>(rows), lo, R, grams); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_gamma_pairs(const double* grams, int order, int R, double* pair, cudaStream_t st) {
+    const long long rr = static_cast<long long>(R) * R;
+    dim3 grid(static_cast<unsigned>(std::max<long long>(1, std::min<long long>((rr + 255) / 256, 64))),
+              order * order);
+    gamma_pairs_kernel<<<grid, 256, 0, st>>>(grams, order, R, pair); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_gamma_excl(const double* grams, int order, int R, int n, double* out, cudaStream_t st) {
+    const long long rr = static_cast<long long>(R) * R;
+    gamma_excl_kernel<<<static_cast<int>(std::max<long long>(1, std::min<long long>((rr + 255) / 256, 64))),
+                        256, 0, st>>>(grams, order, R, n, out); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_residual(const double* m_last, const double* a_last, std::int64_t rows, const double* grams,
+                     int order, int R, const double* xnorm2, double* partials, double* out2,
+                     cudaStream_t st) {
+    const long long n = rows * static_cast<long long>(R);
+    const int nb = grid_for(n, kRedThreads, 64) + 1;
+    residual_partial_kernel<<<nb, kRedThreads, 0, st>>>(m_last, a_last, n, grams, order, R, partials); ::cpkit::count_launch(1);
+    residual_final_kernel<<<1, kRedThreads, 0, st>>>(partials, nb, xnorm2, out2); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
+                     double* g, cudaStream_t st) {
+    const long long n = rows * static_cast<long long>(R);
+    gradient_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(a, gnn, m, rows, R, g); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_block_norm_sum(const double* x, const std::int64_t* offsets, int nblocks,
+                           double* partials, double* out, double scale, cudaStream_t st) {
+    const int chunks = 16;
+    block_sq_partial_kernel<<<nblocks * chunks, kRedThreads, 0, st>>>(
+        x, reinterpret_cast<const long long*>(offsets), nblocks, chunks, partials); ::cpkit::count_launch(1);
+    block_norm_final_kernel<<<1, 32, 0, st>>>(partials, nblocks, chunks, out, scale); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_axpy(double* y, const double* x, double alpha, std::uint64_t n, cudaStream_t st) {
+    axpy_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(y, x, alpha, n); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_diff_norm_add(const double* a, const double* b, std::uint64_t n, double* partials,
+                          double* acc, cudaStream_t st) {
+    const int nb = grid_for(n, kRedThreads, 128);
+    diff_sq_partial_kernel<<<nb, kRedThreads, 0, st>>>(a, b, n, partials); ::cpkit::count_launch(1);
+    sqrt_add_kernel<<<1, kRedThreads, 0, st>>>(partials, nb, acc); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_dot(const double* a, const double* b, std::uint64_t n, double* partials, double* out,
+                cudaStream_t st) {
+    const int nb = grid_for(n, kRedThreads, 128);
+    dot_partial_kernel<<<nb, kRedThreads, 0, st>>>(a, b, n, partials); ::cpkit::count_launch(1);
+    sum_partials_kernel<<<1, kRedThreads, 0, st>>>(partials, nb, out, 1.0); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_axpby(double* out, const double* a, double alpha, const double* x, std::uint64_t n,
+                  cudaStream_t st) {
+    axpby_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(out, a, alpha, x, n); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st) {
+    all_finite_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(x, n, flag); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_reconstruct(const KrpDesc& all, int R, double* out, std::uint64_t offset, std::uint64_t n,
+                        cudaStream_t st) {
+    KrpDevS kd{};
+    kd.nmodes = all.nmodes;
+    for (int i = 0; i < all.nmodes; ++i) {
+        kd.ext[i] = all.ext[i];
+        kd.fac[i] = all.fac[i];
+    }
+    reconstruct_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(kd, R, out, offset, n); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_gaussian_fill(std::uint64_t seed, std::uint64_t stream, double* out, std::uint64_t n,
+                          std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
+                          cudaStream_t st) {
+    gaussian_fill_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(seed, stream, out, n, slab, s_last,
+                                                                      slab_lo); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+void launch_scaled_add(double* y, const double* x, const double* num, const double* den,
+                       double factor, std::uint64_t n, cudaStream_t st) {
+    scaled_add_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(y, x, num, den, factor, n); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+}  // namespace cpkit

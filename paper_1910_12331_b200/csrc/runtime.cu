@@ -1,0 +1,154 @@
+// Process-level runtime pieces: kernel-launch accounting, the NCCL
+// communicator used for last-mode sharding, and the FP64 DMMA peak probe.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+
+#include "solver.h"
+
+namespace cpkit {
+
+// ---------------------------------------------------------------- launch counter
+namespace {
+std::atomic<std::uint64_t> g_launches{0};
+}
+void count_launch(int n) { g_launches.fetch_add(static_cast<std::uint64_t>(n), std::memory_order_relaxed); }
+std::uint64_t kernel_launches() { return g_launches.load(); }
+
+// ---------------------------------------------------------------- NCCL (dlopen'd)
+// The library links no NCCL at build time; the sharded path resolves the
+// handful of symbols it needs from libnccl.so.2 (torch's copy when torch is
+// already loaded in the process, else the system one).
+namespace {
+using ncclComm_t = void*;
+struct NcclUniqueId {
+    char internal[128];
+};
+enum NcclDataType { kNcclFloat64 = 8 };
+enum NcclRedOp { kNcclSum = 0 };
+struct NcclApi {
+    int (*GetUniqueId)(NcclUniqueId*) = nullptr;
+    int (*CommInitRank)(ncclComm_t*, int, NcclUniqueId, int) = nullptr;
+    int (*CommDestroy)(ncclComm_t) = nullptr;
+    int (*AllReduce)(const void*, void*, std::size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    int (*AllGather)(const void*, void*, std::size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(int) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.GetUniqueId = reinterpret_cast<int (*)(NcclUniqueId*)>(dlsym(h, "ncclGetUniqueId"));
+        api.CommInitRank = reinterpret_cast<int (*)(ncclComm_t*, int, NcclUniqueId, int)>(dlsym(h, "ncclCommInitRank"));
+        api.CommDestroy = reinterpret_cast<int (*)(ncclComm_t)>(dlsym(h, "ncclCommDestroy"));
+        api.AllReduce = reinterpret_cast<int (*)(const void*, void*, std::size_t, int, int, ncclComm_t, cudaStream_t)>(
+            dlsym(h, "ncclAllReduce"));
+        api.AllGather = reinterpret_cast<int (*)(const void*, void*, std::size_t, int, ncclComm_t, cudaStream_t)>(
+            dlsym(h, "ncclAllGather"));
+        api.GetErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    });
+    if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.AllGather)
+        throw DeviceError("NCCL (libnccl.so.2) not available for the sharded path");
+    return api;
+}
+void nccl_check(int rc, const char* what) {
+    if (rc != 0) {
+        const char* msg = nccl().GetErrorString ? nccl().GetErrorString(rc) : "?";
+        throw DeviceError(std::string("NCCL ") + what + " failed: " + msg);
+    }
+}
+
+class NcclComm final : public Comm {
+public:
+    NcclComm(const void* id, int rank, int world) : rank_(rank), world_(world) {
+        NcclUniqueId uid;
+        std::memcpy(uid.internal, id, sizeof uid.internal);
+        nccl_check(nccl().CommInitRank(&comm_, world, uid, rank), "CommInitRank");
+    }
+    ~NcclComm() override {
+        if (comm_ && nccl().CommDestroy) nccl().CommDestroy(comm_);
+    }
+    int rank() const override { return rank_; }
+    int world() const override { return world_; }
+    void allreduce_sum(double* dev, std::size_t count, cudaStream_t st) override {
+        nccl_check(nccl().AllReduce(dev, dev, count, kNcclFloat64, kNcclSum, comm_, st), "AllReduce");
+    }
+    void allgather(const double* in, double* out, std::size_t per, cudaStream_t st) override {
+        nccl_check(nccl().AllGather(in, out, per, kNcclFloat64, comm_, st), "AllGather");
+    }
+
+private:
+    ncclComm_t comm_ = nullptr;
+    int rank_, world_;
+};
+}  // namespace
+
+std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int world) {
+    return std::make_unique<NcclComm>(unique_id, rank, world);
+}
+void nccl_unique_id(void* out128) {
+    NcclUniqueId uid;
+    nccl_check(nccl().GetUniqueId(&uid), "GetUniqueId");
+    std::memcpy(out128, uid.internal, sizeof uid.internal);
+}
+
+// ---------------------------------------------------------------- DMMA peak probe
+namespace {
+__global__ void dmma_probe_kernel(double* out, int iters) {
+    double acc[8][4];
+    double a[8], b[4];
+    for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3 + i;
+    for (int i = 0; i < 4; ++i) b[i] = 1.0 + blockIdx.x * 1e-6;
+    for (int c = 0; c < 8; ++c)
+        for (int j = 0; j < 4; ++j) acc[c][j] = 0.0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            asm volatile(
+                "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
+                "{%4,%5,%6,%7,%8,%9,%10,%11},{%12,%13,%14,%15},{%0,%1,%2,%3};"
+                : "+d"(acc[c][0]), "+d"(acc[c][1]), "+d"(acc[c][2]), "+d"(acc[c][3])
+                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                  "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+    }
+    double s = 0.0;
+    for (int c = 0; c < 8; ++c)
+        for (int j = 0; j < 4; ++j) s += acc[c][j];
+    if (s == 123.456) out[0] = s;
+}
+}  // namespace
+
+double probe_dmma_peak(int device) {
+    CPK_CUDA(cudaSetDevice(device));
+    int sms = 0;
+    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DevBuf<double> out(1);
+    const int blocks = sms * 2, threads = 256, iters = 4000;
+    cudaEvent_t a, b;
+    CPK_CUDA(cudaEventCreate(&a));
+    CPK_CUDA(cudaEventCreate(&b));
+    dmma_probe_kernel<<<blocks, threads>>>(out.get(), iters);  // warm-up
+    count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+    CPK_CUDA(cudaEventRecord(a));
+    for (int r = 0; r < 3; ++r) {
+        dmma_probe_kernel<<<blocks, threads>>>(out.get(), iters);
+        count_launch(1);
+    }
+    CPK_CUDA(cudaEventRecord(b));
+    CPK_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    CPK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    const double flops = 3.0 * blocks * (threads / 32) * static_cast<double>(iters) * 8 * 2.0 * 16 * 8 * 16;
+    return flops / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace cpkit

@@ -1,0 +1,914 @@
+// Host drivers of the GN-CG / ALS hot path over device-resident state.
+//
+// Mirrors the reference's C++ solver API and semantics:
+//   mttkrp + MttkrpWorkspace     mttkrp.cpp:136-189
+//   build_gamma_set / residual   kruskal.cpp:42-65, :94-118
+//   gradient / cp_cg / gn_step / gn_optimize   gauss_newton.cpp:81-494
+//   als_sweep / als_optimize     als.cpp:22-94
+// The host only sees per-iteration scalars (one stream sync per ALS sweep /
+// GN outer iteration, plus one inside cp_cg); every vector lives in HBM.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <limits>
+
+#include "solver.h"
+
+namespace cpkit {
+
+// ================================================================ host types
+double Matrix::norm() const {
+    double s = 0.0;
+    for (double v : data) s += v * v;
+    return std::sqrt(s);
+}
+bool Matrix::all_finite() const {
+    for (double v : data)
+        if (!std::isfinite(v)) return false;
+    return true;
+}
+
+std::uint64_t product_of_dims(const std::vector<std::uint64_t>& dims) {  // tensor.cpp:26-37
+    std::uint64_t n = 1;
+    for (std::uint64_t d : dims) {
+        if (d == 0) throw InvalidArgument("tensor extents must be positive");
+        if (n > std::numeric_limits<std::uint64_t>::max() / d)
+            throw LimitExceeded("tensor element count overflows 64 bits");
+        n *= d;
+    }
+    return n;
+}
+
+DenseTensor::DenseTensor(std::vector<std::uint64_t> dims) : dims_(std::move(dims)) {
+    if (dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
+    data_.assign(product_of_dims(dims_), 0.0);
+}
+DenseTensor DenseTensor::from_data(std::vector<std::uint64_t> dims, std::vector<double> data) {
+    DenseTensor t;
+    t.dims_ = std::move(dims);
+    t.data_ = std::move(data);
+    if (t.dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
+    if (product_of_dims(t.dims_) != t.data_.size())
+        throw InvalidArgument("tensor data length does not match extents");
+    return t;
+}
+void DenseTensor::validate() const {  // tensor.cpp:71-83
+    if (dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
+    if (product_of_dims(dims_) != data_.size())
+        throw InvalidArgument("tensor data length does not match extents");
+    for (double v : data_)
+        if (!std::isfinite(v)) throw InvalidArgument("tensor contains non-finite entries");
+}
+
+void KruskalModel::validate() const {  // kruskal.cpp:27-40
+    if (dims.empty() || rank < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
+    if (factors.size() != dims.size()) throw InvalidArgument("model factor count does not match order");
+    for (std::size_t n = 0; n < dims.size(); ++n) {
+        if (static_cast<std::uint64_t>(factors[n].rows) != dims[n] || factors[n].cols != rank)
+            throw InvalidArgument("model factor shape mismatch");
+        if (!factors[n].all_finite()) throw InvalidArgument("model factor contains non-finite entries");
+    }
+}
+
+namespace {
+void put_u64(std::ostream& os, std::uint64_t v) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    os.write(reinterpret_cast<const char*>(b), 8);
+}
+std::uint64_t get_u64(std::istream& is) {
+    unsigned char b[8] = {};
+    is.read(reinterpret_cast<char*>(b), 8);
+    std::uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(b[i]) << (8 * i);
+    return v;
+}
+void put_f64s(std::ostream& os, const double* d, std::size_t n) {
+    // little-endian host: bytes of each double in order (tensor.cpp:249-253)
+    os.write(reinterpret_cast<const char*>(d), static_cast<std::streamsize>(n * 8));
+}
+void get_f64s(std::istream& is, double* d, std::size_t n) {
+    is.read(reinterpret_cast<char*>(d), static_cast<std::streamsize>(n * 8));
+}
+}  // namespace
+
+void write_tensor(const DenseTensor& t, const std::string& path) {  // tensor.cpp:264-276
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw IoError("cannot open for writing: " + path);
+    os.write("CPKT1", 5);
+    put_u64(os, t.order());
+    for (auto d : t.dims()) put_u64(os, d);
+    put_f64s(os, t.data(), t.size());
+    if (!os) throw IoError("write failed: " + path);
+}
+DenseTensor read_tensor(const std::string& path) {  // tensor.cpp:278-306
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw IoError("cannot open for reading: " + path);
+    char magic[5];
+    is.read(magic, 5);
+    if (!is || std::memcmp(magic, "CPKT1", 5) != 0) throw ParseError("bad tensor magic: " + path);
+    const std::uint64_t order = get_u64(is);
+    if (!is || order == 0 || order > 64) throw ParseError("bad tensor order: " + path);
+    std::vector<std::uint64_t> dims(order);
+    for (auto& d : dims) d = get_u64(is);
+    if (!is) throw ParseError("truncated tensor header: " + path);
+    const std::uint64_t total = product_of_dims(dims);
+    std::vector<double> data(total);
+    get_f64s(is, data.data(), total);
+    if (!is) throw ParseError("truncated tensor data: " + path);
+    DenseTensor t = DenseTensor::from_data(std::move(dims), std::move(data));
+    t.validate();
+    return t;
+}
+void write_model(const KruskalModel& m, const std::string& path) {  // kruskal.cpp:143-161
+    m.validate();
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw IoError("cannot open for writing: " + path);
+    os.write("CPKM1", 5);
+    put_u64(os, m.order());
+    put_u64(os, static_cast<std::uint64_t>(m.rank));
+    for (auto d : m.dims) put_u64(os, d);
+    for (const auto& a : m.factors) put_f64s(os, a.data.data(), a.data.size());
+    if (!os) throw IoError("write failed: " + path);
+}
+KruskalModel read_model(const std::string& path) {  // kruskal.cpp:163-203
+    std::ifstream is(path, std::ios::binary);
+    if (!is) throw IoError("cannot open for reading: " + path);
+    char magic[5];
+    is.read(magic, 5);
+    if (!is || std::memcmp(magic, "CPKM1", 5) != 0) throw ParseError("bad model magic: " + path);
+    const std::uint64_t order = get_u64(is);
+    const std::uint64_t rank = get_u64(is);
+    if (!is || order == 0 || order > 64 || rank == 0) throw ParseError("bad model header: " + path);
+    KruskalModel m;
+    m.rank = static_cast<std::int64_t>(rank);
+    m.dims.resize(order);
+    for (auto& d : m.dims) d = get_u64(is);
+    if (!is) throw ParseError("truncated model header: " + path);
+    for (auto d : m.dims) {
+        Matrix a(static_cast<std::int64_t>(d), m.rank);
+        get_f64s(is, a.data.data(), a.data.size());
+        m.factors.push_back(std::move(a));
+    }
+    if (!is) throw ParseError("truncated model data: " + path);
+    m.validate();
+    return m;
+}
+
+// ================================================================ configs
+RegSchedule RegSchedule::constant(double lambda, RegShape shape) {
+    RegSchedule s;
+    s.mode = RegMode::constant;
+    s.shape = shape;
+    s.lambda = lambda;
+    s.validate();
+    return s;
+}
+RegSchedule RegSchedule::varying(double upper, double lower, double mu, RegShape shape) {
+    RegSchedule s;
+    s.mode = RegMode::varying;
+    s.shape = shape;
+    s.lambda = upper;
+    s.mu = mu;
+    s.lower = lower;
+    s.upper = upper;
+    s.direction = Direction::down;
+    s.validate();
+    return s;
+}
+void RegSchedule::validate() const {  // gauss_newton.cpp:33-45
+    if (lambda < 0) throw InvalidArgument("schedule: lambda must be nonnegative");
+    if (mode == RegMode::varying) {
+        if (!(mu > 1.0)) throw InvalidArgument("schedule: mu must exceed 1");
+        if (!(lower > 0.0) || !(lower < upper)) throw InvalidArgument("schedule: need 0 < lower < upper");
+    }
+}
+RegSchedule schedule_next(RegSchedule s) {  // gauss_newton.cpp:47-59
+    if (s.mode == RegMode::constant) return s;
+    if (s.direction == RegSchedule::Direction::down) {
+        s.lambda /= s.mu;
+        if (s.lambda < s.lower) s.direction = RegSchedule::Direction::up;
+    } else {
+        s.lambda *= s.mu;
+        if (s.lambda > s.upper) s.direction = RegSchedule::Direction::down;
+    }
+    return s;
+}
+void GnConfig::validate() const {  // gauss_newton.cpp:61-79
+    schedule.validate();
+    if (grad_tol < 0 || residual_tol < 0 || step_tol < 0) throw InvalidArgument("gn config: negative tolerance");
+    if (max_iters < 0 || cg_max_iters < 0) throw InvalidArgument("gn config: negative iteration cap");
+    if (!(cg_tol > 0)) throw InvalidArgument("gn config: cg_tol must be positive");
+    if (armijo) {
+        if (!(armijo->c1 > 0 && armijo->c1 < 1) || !(armijo->shrink > 0 && armijo->shrink < 1) ||
+            armijo->max_backtracks < 1)
+            throw InvalidArgument("gn config: bad armijo parameters");
+    }
+}
+void AlsConfig::validate() const {  // als.cpp:10-20
+    if (max_sweeps < 0 || residual_tol < 0 || step_tol < 0 || lambda0 < 0)
+        throw InvalidArgument("als config: negative tolerance, cap or lambda");
+    if (decay_factor < 1.0) throw InvalidArgument("als config: decay_factor must be >= 1");
+    if (decay_every && *decay_every < 1) throw InvalidArgument("als config: decay_every must be positive");
+}
+
+const char* to_string(TerminalStatus s) {
+    switch (s) {
+        case TerminalStatus::converged_residual: return "converged_residual";
+        case TerminalStatus::converged_step: return "converged_step";
+        case TerminalStatus::cap_hit: return "cap_hit";
+        case TerminalStatus::numerical_failure: return "numerical_failure";
+    }
+    return "unknown";
+}
+double ConvergenceReport::best_residual() const {
+    double best = 1.0;
+    for (const auto& r : records) best = std::min(best, r.residual);
+    return best;
+}
+
+// ================================================================ rng (rng.hpp:11-46)
+namespace {
+inline std::uint64_t mix64(std::uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+inline std::uint64_t derive(std::uint64_t h, std::uint64_t v) {
+    return mix64(h ^ (v * 0xD6E8FEB86659FD93ull + 0xA0761D6478BD642Full));
+}
+inline std::uint64_t keyed(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, std::uint64_t salt) {
+    return derive(derive(derive(mix64(seed), stream), index), salt);
+}
+inline double to_unit(std::uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
+}  // namespace
+
+double rng_uniform(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, double a, double b) {
+    return a + (b - a) * to_unit(keyed(seed, stream, index, 0));
+}
+double rng_gaussian(std::uint64_t seed, std::uint64_t stream, std::uint64_t index) {
+    const double u1 = static_cast<double>((keyed(seed, stream, index, 1) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = to_unit(keyed(seed, stream, index, 2));
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+}
+std::uint64_t problem_seed(std::uint64_t master, int rank, int problem) {  // harness.cpp:378-383
+    return derive(derive(derive(mix64(master), 0x50524F42ull), static_cast<std::uint64_t>(rank)),
+                  static_cast<std::uint64_t>(problem));
+}
+std::uint64_t init_seed(std::uint64_t master, int rank, int problem, int init) {  // :385-391
+    return derive(derive(derive(derive(mix64(master), 0x494E4954ull), static_cast<std::uint64_t>(rank)),
+                         static_cast<std::uint64_t>(problem)),
+                  static_cast<std::uint64_t>(init));
+}
+namespace {
+template <typename Draw>
+KruskalModel fill_model(const std::vector<std::uint64_t>& dims, std::int64_t rank, Draw&& draw) {
+    if (rank < 1) throw InvalidArgument("random_model: rank must be positive");
+    KruskalModel m;
+    m.dims = dims;
+    m.rank = rank;
+    for (std::size_t n = 0; n < dims.size(); ++n) {
+        Matrix a(static_cast<std::int64_t>(dims[n]), rank);
+        for (std::int64_t i = 0; i < a.rows; ++i)
+            for (std::int64_t r = 0; r < rank; ++r)
+                a.data[static_cast<std::size_t>(i * rank + r)] =
+                    draw(n, static_cast<std::uint64_t>(i) * static_cast<std::uint64_t>(rank) + static_cast<std::uint64_t>(r));
+        m.factors.push_back(std::move(a));
+    }
+    m.validate();
+    return m;
+}
+}  // namespace
+KruskalModel random_model_uniform(const std::vector<std::uint64_t>& dims, std::int64_t rank,
+                                  std::uint64_t seed, double a, double b) {  // generators.cpp:59-68
+    if (!(a < b)) throw InvalidArgument("random_model: uniform needs a < b");
+    return fill_model(dims, rank, [&](std::uint64_t n, std::uint64_t idx) { return rng_uniform(seed, n, idx, a, b); });
+}
+KruskalModel random_model_gaussian(const std::vector<std::uint64_t>& dims, std::int64_t rank,
+                                   std::uint64_t seed) {  // generators.cpp:70-76
+    return fill_model(dims, rank, [&](std::uint64_t n, std::uint64_t idx) { return rng_gaussian(seed, n, idx); });
+}
+
+// ================================================================ context
+Context::Context(int dev) : device(dev) {
+    CPK_CUDA(cudaSetDevice(dev));
+    CPK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+}
+Context::~Context() {
+    comm.reset();
+    if (stream) cudaStreamDestroy(stream);
+}
+void Context::sync() const { CPK_CUDA(cudaStreamSynchronize(stream)); }
+
+void shard_range(std::uint64_t extent, int rank, int world, std::uint64_t* lo, std::uint64_t* hi) {
+    const std::uint64_t base = extent / static_cast<std::uint64_t>(world);
+    const std::uint64_t rem = extent % static_cast<std::uint64_t>(world);
+    const std::uint64_t r = static_cast<std::uint64_t>(rank);
+    *lo = r * base + std::min(r, rem);
+    *hi = *lo + base + (r < rem ? 1 : 0);
+}
+
+// ================================================================ DeviceProblem
+namespace {
+enum Scal { kXnorm = 0, kRes = 1, kFit = 2, kStep = 3, kNormSum = 4, kDot = 5, kNScal = 16 };
+}
+
+DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int rank)
+    : ctx_(ctx), dims_(std::move(dims)), R_(rank) {
+    const int N = order();
+    if (N < 2) throw InvalidArgument("mttkrp: tensor order must be at least 2");
+    if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
+    if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
+    CPK_CUDA(cudaSetDevice(ctx_.device));
+    h_ = (N + 1) / 2;
+    shard_range(dims_[N - 1], ctx_.rank(), ctx_.world(), &slab_lo_, &slab_hi_);
+    if (ctx_.world() > 1 && dims_[N - 1] % static_cast<std::uint64_t>(ctx_.world()) != 0)
+        throw LimitExceeded("sharded runs need the last extent divisible by the GPU count");
+    local_rows_.resize(N);
+    for (int n = 0; n < N; ++n) local_rows_[n] = static_cast<std::int64_t>(dims_[n]);
+    local_rows_[N - 1] = static_cast<std::int64_t>(slab_hi_ - slab_lo_);
+    F_ = 1;
+    Bl_ = 1;
+    for (int n = 0; n < h_; ++n) F_ *= local_rows_[n];
+    for (int n = h_; n < N; ++n) Bl_ *= local_rows_[n];
+    local_elems_ = static_cast<std::uint64_t>(F_) * static_cast<std::uint64_t>(Bl_);
+
+    off_.assign(N + 1, 0);
+    for (int n = 0; n < N; ++n) off_[n + 1] = off_[n] + static_cast<std::int64_t>(dims_[n]) * R_;
+    const std::size_t S = static_cast<std::size_t>(off_[N]);
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+
+    x_.resize(local_elems_);
+    A_.resize(S); Atrial_.resize(S); M_.resize(S); G_.resize(S); V_.resize(S); Z_.resize(S); Q_.resize(S);
+    for (int i = 0; i < 2; ++i) { Rr_[i].resize(S); W_[i].resize(S); }
+    PF_.resize(static_cast<std::size_t>(F_) * R_);
+    PB_.resize(static_cast<std::size_t>(Bl_) * R_);
+    // split-K and second-level workspaces
+    std::size_t ws = root_front_workspace_elems(F_, Bl_, R_);
+    {
+        KrpDesc kf = krp(0, h_, A_.get(), false), kb = krp(h_, N, A_.get(), true);
+        for (int n = 0; n < h_; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kf, n, R_));
+        for (int n = h_; n < N; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kb, n - h_, R_));
+    }
+    ws_.resize(std::max<std::size_t>(ws, 1));
+    grams_.resize(N * RR);
+    pair_.resize(static_cast<std::size_t>(N) * N * RR);
+    gam_.resize(N * RR);
+    pinv_.resize(N * RR);
+    chol_.resize(static_cast<std::size_t>(N) * R_ * (R_ + 1) / 2);
+    chol_tmp_.resize(N * RR);
+    std::int64_t smax = 1;
+    for (auto d : dims_) smax = std::max<std::int64_t>(smax, static_cast<std::int64_t>(d));
+    anew_.resize(static_cast<std::size_t>(smax) * R_);
+    scal_.resize(kNScal);
+    partials_.resize(std::max(4096, norm2_parts(local_elems_) + 8));
+    status_.resize(std::max(N, 1));
+    cgres_.resize(8);
+    flag_.resize(4);
+    barrier_.resize(4);
+    offs_dev_.resize(N + 1);
+    rows_dev_.resize(N);
+    std::vector<std::int64_t> rows(dims_.begin(), dims_.end());
+    CPK_CUDA(cudaMemcpy(offs_dev_.get(), off_.data(), (N + 1) * sizeof(std::int64_t), cudaMemcpyHostToDevice));
+    CPK_CUDA(cudaMemcpy(rows_dev_.get(), rows.data(), N * sizeof(std::int64_t), cudaMemcpyHostToDevice));
+    CPK_CUDA(cudaMemset(scal_.get(), 0, kNScal * sizeof(double)));
+    // CG slots
+    CgParams cp{};
+    cp.order = N;
+    cp.R = R_;
+    for (int n = 0; n < N; ++n) cp.rows[n] = static_cast<std::int64_t>(dims_[n]);
+    slots_.resize(cg_slots_needed(cp));
+}
+
+DeviceProblem::~DeviceProblem() = default;
+
+KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {
+    KrpDesc d{};
+    d.nmodes = hi - lo;
+    const int N = order();
+    for (int m = lo; m < hi; ++m) {
+        const bool last = (m == N - 1);
+        d.ext[m - lo] = (last && local_last) ? local_rows_[m] : static_cast<std::int64_t>(dims_[m]);
+        d.fac[m - lo] = base + off_[m] + ((last && local_last) ? static_cast<std::int64_t>(slab_lo_) * R_ : 0);
+    }
+    return d;
+}
+
+void DeviceProblem::upload_tensor(const double* host_local) {
+    CPK_CUDA(cudaMemcpyAsync(x_.get(), host_local, local_elems_ * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx_.stream));
+    invalidate_all();
+}
+
+// Device-side low-rank (+ noise) generation: the reference's reconstruct
+// order per entry (kruskal.cpp:76-90) with non-fused multiply/add, so the
+// noiseless tensor is bitwise equal to the CPU generator's.
+void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel) {
+    set_factors(truth);
+    const int N = order();
+    KrpDesc all = krp(0, N, A_.get(), true);
+    // global flat offset of the local slab is not contiguous when sharded; generate
+    // slab-local entries through a local descriptor (last factor already offset).
+    launch_reconstruct(all, R_, x_.get(), 0, local_elems_, ctx_.stream);
+    if (noise_rel > 0.0) {
+        // noise E ~ N(0,1) (keyed, stream 0x4E01), scaled to noise_rel * ||X|| / ||E||
+        DevBuf<double> e(local_elems_);
+        launch_gaussian_fill(noise_seed, 0x4E01, e.get(), local_elems_, slab_hi_ - slab_lo_, dims_[N - 1], slab_lo_,
+                             ctx_.stream);
+        const int parts = norm2_parts(local_elems_);
+        launch_norm2(x_.get(), local_elems_, partials_.get(), parts, scal_.get() + 8, ctx_.stream);
+        launch_norm2(e.get(), local_elems_, partials_.get() + parts, parts, scal_.get() + 9, ctx_.stream);
+        if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + 8, 2, ctx_.stream);
+        launch_scaled_add(x_.get(), e.get(), scal_.get() + 8, scal_.get() + 9, noise_rel, local_elems_,
+                          ctx_.stream);
+        ctx_.sync();
+    }
+    invalidate_all();
+}
+
+void DeviceProblem::set_factors(const std::vector<const double*>& host) {
+    for (int n = 0; n < order(); ++n)
+        CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], host[n], (off_[n + 1] - off_[n]) * sizeof(double),
+                                 cudaMemcpyHostToDevice, ctx_.stream));
+    invalidate_all();
+}
+void DeviceProblem::get_factors(std::vector<double*>& host) {
+    for (int n = 0; n < order(); ++n)
+        CPK_CUDA(cudaMemcpyAsync(host[n], A_.get() + off_[n], (off_[n + 1] - off_[n]) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+}
+void DeviceProblem::set_factors(const KruskalModel& m) {
+    if (m.dims != dims_ || m.rank != R_) throw InvalidArgument("model extents/rank do not match the problem");
+    std::vector<const double*> p;
+    for (const auto& a : m.factors) p.push_back(a.data.data());
+    set_factors(p);
+}
+void DeviceProblem::get_factors(KruskalModel& m) {
+    m.dims = dims_;
+    m.rank = R_;
+    m.factors.resize(dims_.size());
+    std::vector<double*> p;
+    for (std::size_t n = 0; n < dims_.size(); ++n) {
+        m.factors[n] = Matrix(static_cast<std::int64_t>(dims_[n]), R_);
+        p.push_back(m.factors[n].data.data());
+    }
+    get_factors(p);
+}
+
+double DeviceProblem::read_scalar(int idx) {
+    double v = 0.0;
+    CPK_CUDA(cudaMemcpyAsync(&v, scal_.get() + idx, sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    return v;
+}
+
+double DeviceProblem::norm2() {
+    launch_norm2(x_.get(), local_elems_, partials_.get(), norm2_parts(local_elems_), scal_.get() + kXnorm,
+                 ctx_.stream);
+    if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + kXnorm, 1, ctx_.stream);
+    return read_scalar(kXnorm);
+}
+
+// ---- dimension tree (mttkrp.cpp:160-189) -----------------------------------
+void DeviceProblem::root_back() {
+    const int N = order();
+    launch_root_back(x_.get(), F_, Bl_, R_, krp(h_, N, A_.get(), true), PF_.get(), ctx_.stream);
+    ++contractions_;
+    pf_valid_ = true;
+}
+void DeviceProblem::root_front() {
+    launch_root_front(x_.get(), F_, Bl_, R_, krp(0, h_, A_.get(), false), PB_.get(), ws_.get(), ws_.size(),
+                      ctx_.stream);
+    ++contractions_;
+    pb_valid_ = true;
+}
+void DeviceProblem::second_level_back(int mode) {
+    double* out = M_.get() + off_[mode];
+    if (h_ == 1) {
+        CPK_CUDA(cudaMemcpyAsync(out, PF_.get(), static_cast<std::size_t>(F_) * R_ * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+    } else {
+        launch_reduce_kept(PF_.get(), krp(0, h_, A_.get(), false), mode, R_, out, ws_.get(), ws_.size(),
+                           ctx_.stream);
+    }
+    if (ctx_.comm) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
+}
+void DeviceProblem::second_level_front(int mode) {
+    const int N = order();
+    const bool last = (mode == N - 1);
+    // rows of the last mode land at their global slab position
+    double* out = M_.get() + off_[mode] + (last ? static_cast<std::int64_t>(slab_lo_) * R_ : 0);
+    if (N - h_ == 1) {
+        CPK_CUDA(cudaMemcpyAsync(out, PB_.get(), static_cast<std::size_t>(Bl_) * R_ * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+    } else {
+        launch_reduce_kept(PB_.get(), krp(h_, N, A_.get(), true), mode - h_, R_, out, ws_.get(), ws_.size(),
+                           ctx_.stream);
+    }
+    if (ctx_.comm) {
+        if (last) {
+            const std::size_t per = static_cast<std::size_t>(slab_hi_ - slab_lo_) * R_;
+            ctx_.comm->allgather(out, M_.get() + off_[mode], per, ctx_.stream);
+        } else {
+            ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
+        }
+    }
+}
+
+void DeviceProblem::mttkrp(int mode) {
+    if (mode < 0 || mode >= order()) throw InvalidArgument("mttkrp: mode out of range");
+    if (mode < h_) {
+        if (!pf_valid_) root_back();
+        second_level_back(mode);
+    } else {
+        if (!pb_valid_) root_front();
+        second_level_front(mode);
+    }
+}
+void DeviceProblem::mttkrp_naive(int mode) {
+    if (mode < 0 || mode >= order()) throw InvalidArgument("mttkrp: mode out of range");
+    const int saved = contractions_;
+    if (mode < h_) {
+        root_back();
+        second_level_back(mode);
+        pf_valid_ = false;
+    } else {
+        root_front();
+        second_level_front(mode);
+        pb_valid_ = false;
+    }
+    contractions_ = saved;  // the uncached overload does not count (mttkrp.cpp:149-158)
+}
+void DeviceProblem::note_factor_update(int mode) {
+    if (mode >= h_) pf_valid_ = false;  // back-root key holds modes >= h
+    else pb_valid_ = false;             // front-root key holds modes < h
+    m_all_valid_ = false;
+}
+void DeviceProblem::invalidate_all() {
+    pf_valid_ = pb_valid_ = false;
+    m_all_valid_ = false;
+}
+void DeviceProblem::download_mttkrp(int mode, double* host) {
+    CPK_CUDA(cudaMemcpyAsync(host, M_.get() + off_[mode], (off_[mode + 1] - off_[mode]) * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+}
+void DeviceProblem::compute_all_mttkrp() {
+    for (int n = 0; n < order(); ++n) mttkrp(n);
+    m_all_valid_ = true;
+}
+
+// ---- Gamma set / residual / gradient --------------------------------------
+void DeviceProblem::grams_all() {
+    launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), 0, order(), R_, grams_.get(), ctx_.stream);
+}
+void DeviceProblem::build_gamma_set() {
+    grams_all();
+    launch_gamma_pairs(grams_.get(), order(), R_, pair_.get(), ctx_.stream);
+}
+void DeviceProblem::download_gammas(double* grams, double* pair) {
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    const int N = order();
+    CPK_CUDA(cudaMemcpyAsync(grams, grams_.get(), N * RR * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(pair, pair_.get(), N * N * RR * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+}
+void DeviceProblem::upload_gammas(const double* grams, const double* pair) {
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    const int N = order();
+    CPK_CUDA(cudaMemcpyAsync(grams_.get(), grams, N * RR * 8, cudaMemcpyHostToDevice, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(pair_.get(), pair, N * N * RR * 8, cudaMemcpyHostToDevice, ctx_.stream));
+}
+std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*last_src*/) {
+    if (!(xnorm2 > 0.0)) throw InvalidArgument("residual_fitness: tensor norm must be positive");
+    const int N = order();
+    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kXnorm, &xnorm2, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
+    launch_residual(M_.get() + off_[N - 1], A_.get() + off_[N - 1], static_cast<std::int64_t>(dims_[N - 1]),
+                    grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
+                    ctx_.stream);
+    double rf[2];
+    CPK_CUDA(cudaMemcpyAsync(rf, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    return {rf[0], rf[1]};
+}
+void DeviceProblem::gradient() {
+    const int N = order();
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    for (int n = 0; n < N; ++n)
+        launch_gradient(A_.get() + off_[n], pair_.get() + (n * N + n) * RR, M_.get() + off_[n],
+                        static_cast<std::int64_t>(dims_[n]), R_, G_.get() + off_[n], ctx_.stream);
+}
+double DeviceProblem::norm_sum(const double* dev_stacked) {
+    launch_block_norm_sum(dev_stacked, offs_dev_.get(), order(), partials_.get(), scal_.get() + kNormSum, 1.0,
+                          ctx_.stream);
+    return read_scalar(kNormSum);
+}
+
+// ---- SPD ---------------------------------------------------------------------
+void DeviceProblem::check_status(int count, const char* what) {
+    std::vector<int> st(count);
+    CPK_CUDA(cudaMemcpyAsync(st.data(), status_.get(), count * sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    for (int s : st)
+        if (s == 2) throw SingularSystem(std::string(what) + ": factorization failed after jitter retry");
+}
+void DeviceProblem::spd_solve(const double* dev_s, const double* dev_b, std::int64_t rows, double lambda,
+                              double* dev_y) {
+    launch_chol_batch(dev_s, 1, R_, &lambda, 0, chol_.get(), status_.get(), ctx_.stream);
+    check_status(1, "spd_solve");
+    launch_chol_solve_rows(chol_.get(), R_, dev_b, rows, dev_y, ctx_.stream);
+}
+void DeviceProblem::spd_inverse(const double* dev_s, double lambda, double* dev_inv) {
+    launch_chol_batch(dev_s, 1, R_, &lambda, 0, chol_.get(), status_.get(), ctx_.stream);
+    check_status(1, "spd_solve");
+    launch_chol_inverse_batch(chol_.get(), 1, R_, dev_inv, chol_tmp_.get(), ctx_.stream);
+}
+// gauss_newton.cpp:190-207: per mode (Gamma(n,n) + lambda Reg)^-1
+void DeviceProblem::build_preconditioner(double lambda, RegShape shape) {
+    if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
+    const int N = order();
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    for (int n = 0; n < N; ++n)
+        CPK_CUDA(cudaMemcpyAsync(gam_.get() + n * RR, pair_.get() + (n * N + n) * RR, RR * 8,
+                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+    launch_chol_batch(gam_.get(), N, R_, &lambda, shape == RegShape::identity ? 0 : 1, chol_.get(),
+                      status_.get(), ctx_.stream);
+    check_status(N, "spd_solve");
+    launch_chol_inverse_batch(chol_.get(), N, R_, pinv_.get(), chol_tmp_.get(), ctx_.stream);
+}
+
+// ---- J^T J v and CG ------------------------------------------------------------
+namespace {
+CgParams base_params(int N, int R, const std::vector<std::uint64_t>& dims, const std::vector<std::int64_t>& off) {
+    CgParams p{};
+    p.order = N;
+    p.R = R;
+    for (int n = 0; n < N; ++n) p.rows[n] = static_cast<std::int64_t>(dims[n]);
+    for (int n = 0; n <= N; ++n) p.off[n] = off[n];
+    return p;
+}
+}  // namespace
+
+void DeviceProblem::jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape) {
+    CgParams p = base_params(order(), R_, dims_, off_);
+    p.A = A_.get();
+    p.pair = pair_.get();
+    p.W[1] = W_[1].get();
+    p.slots = slots_.get();
+    p.barrier = barrier_.get();
+    p.lambda = lambda;
+    p.shape = shape == RegShape::identity ? 0 : 1;
+    launch_jtj_matvec(p, dev_w, dev_u, ctx_.stream);
+}
+
+// gauss_newton.cpp:279-349; G must hold the gradient. Result in V.
+CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
+    const int N = order();
+    const RegShape shape = cfg.schedule.shape;
+    int cap = cfg.cg_max_iters;
+    if (cap <= 0) {  // default_cg_cap (gauss_newton.cpp:267-275)
+        std::uint64_t total = 0;
+        for (auto d : dims_) total += d * static_cast<std::uint64_t>(R_);
+        cap = static_cast<int>(std::min<std::uint64_t>(total, 10ull * static_cast<std::uint64_t>(R_)));
+    }
+    CgResultInfo out;
+    const double gnorm = norm_sum(G_.get());
+    if (gnorm == 0.0) {
+        CPK_CUDA(cudaMemsetAsync(V_.get(), 0, off_[N] * sizeof(double), ctx_.stream));
+        return out;
+    }
+    build_preconditioner(lambda, shape);
+    CgParams p = base_params(N, R_, dims_, off_);
+    p.A = A_.get();
+    p.pair = pair_.get();
+    p.pinv = pinv_.get();
+    p.G = G_.get();
+    p.V = V_.get();
+    p.Rr[0] = Rr_[0].get();
+    p.Rr[1] = Rr_[1].get();
+    p.W[0] = W_[0].get();
+    p.W[1] = W_[1].get();
+    p.Z = Z_.get();
+    p.Q = Q_.get();
+    p.slots = slots_.get();
+    p.barrier = barrier_.get();
+    p.lambda = lambda;
+    p.shape = shape == RegShape::identity ? 0 : 1;
+    p.beta_variant = cfg.cg_beta == CgBetaVariant::standard ? 0 : 1;
+    p.cg_tol = cfg.cg_tol;
+    p.cap = cap;
+    p.result = cgres_.get();
+    run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);
+    int res[5];
+    CPK_CUDA(cudaMemcpyAsync(res, cgres_.get(), sizeof res, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    if (res[3]) throw NumericalFailure("cp_cg: non-finite iterate");
+    out.iterations = res[0];
+    out.hit_cap = res[1] != 0;
+    out.breakdown = res[2] != 0;
+    return out;
+}
+
+// ---- ALS sweep (als.cpp:22-52) ----------------------------------------------------
+AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
+    const int N = order();
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    reset_contraction_counter();
+    int one = 1;
+    CPK_CUDA(cudaMemcpyAsync(flag_.get(), &one, sizeof(int), cudaMemcpyHostToDevice, ctx_.stream));
+    launch_all_finite(A_.get(), off_[N], flag_.get(), ctx_.stream);  // model.validate()
+    double zero = 0.0;
+    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kStep, &zero, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
+    grams_all();
+    for (int n = 0; n < N; ++n) {
+        launch_gamma_excl(grams_.get(), N, R_, n, gam_.get(), ctx_.stream);
+        mttkrp(n);
+        const std::int64_t rows = static_cast<std::int64_t>(dims_[n]);
+        launch_chol_batch(gam_.get(), 1, R_, &lambda, 0, chol_.get(), status_.get() + n, ctx_.stream);
+        launch_chol_solve_rows(chol_.get(), R_, M_.get() + off_[n], rows, anew_.get(), ctx_.stream);
+        launch_diff_norm_add(anew_.get(), A_.get() + off_[n], static_cast<std::uint64_t>(rows) * R_,
+                             partials_.get(), scal_.get() + kStep, ctx_.stream);
+        CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], anew_.get(), rows * R_ * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+        note_factor_update(n);
+        launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), n, n + 1, R_, grams_.get(), ctx_.stream);
+    }
+    (void)RR;
+    AlsSweepDiag diag;
+    std::vector<int> st(N);
+    int fin = 1;
+    CPK_CUDA(cudaMemcpyAsync(st.data(), status_.get(), N * sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(&fin, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(&diag.step_norm, scal_.get() + kStep, sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx_.stream));
+    ctx_.sync();
+    if (!fin) throw InvalidArgument("model factor contains non-finite entries");
+    for (int s : st)
+        if (s == 2) throw SingularSystem("spd_solve: factorization failed after jitter retry");
+    diag.full_contractions = contractions_;
+    return diag;
+}
+
+// ---- GN step (gauss_newton.cpp:360-449) -------------------------------------------
+// B200 change: the post-step residual reuses the next iteration's tree pass
+// (one fused set of two root contractions computes every M^(n) of the new
+// factors; M^(N-1) gives residual_after and the rest is cached for the next
+// step), instead of a third, naive contraction (:442-444).
+GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
+    const int N = order();
+    const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
+    GnStepDiag diag;
+    if (!m_all_valid_) compute_all_mttkrp();
+    build_gamma_set();
+    auto [res, fit] = residual_fitness(xnorm2, N - 1);
+    (void)fit;
+    diag.residual_before = res;
+    diag.residual_after = res;
+    if (res < cfg.residual_tol) {
+        diag.halt = GnStepDiag::Halt::residual;
+        return diag;
+    }
+    gradient();
+    diag.grad_norm = norm_sum(G_.get());
+    if (diag.grad_norm <= cfg.grad_tol) {
+        diag.halt = GnStepDiag::Halt::gradient;
+        return diag;
+    }
+    diag.lambda = schedule.lambda;
+    const CgResultInfo cg = cp_cg(diag.lambda, cfg);
+    diag.cg_iters = cg.iterations;
+    diag.cg_hit_cap = cg.hit_cap;
+    diag.cg_breakdown = cg.breakdown;
+
+    double alpha = 1.0;
+    double residual_after = -1.0;
+    if (cfg.armijo) {
+        const ArmijoParams& ap = *cfg.armijo;
+        const double f0 = 0.5 * res * res * xnorm2;
+        launch_dot(G_.get(), V_.get(), S, partials_.get(), scal_.get() + kDot, ctx_.stream);
+        const double gv = read_scalar(kDot);
+        // keep the pre-step factors in Atrial_; A_ holds the trial point
+        CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), S * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.stream));
+        auto eval_trial = [&](double a) {
+            launch_axpby(A_.get(), Atrial_.get(), a, V_.get(), S, ctx_.stream);
+            invalidate_all();
+            mttkrp_naive(N - 1);
+            grams_all();
+            return residual_fitness(xnorm2, N - 1).first;
+        };
+        bool accepted = false;
+        for (int t = 0; t < ap.max_backtracks; ++t) {
+            const double r_trial = eval_trial(alpha);
+            const double f_trial = 0.5 * r_trial * r_trial * xnorm2;
+            if (f_trial <= f0 + ap.c1 * alpha * gv) {
+                accepted = true;
+                residual_after = r_trial;
+                break;
+            }
+            alpha *= ap.shrink;
+        }
+        if (!accepted) {
+            diag.armijo_exhausted = true;
+            residual_after = eval_trial(alpha);
+        }
+    } else {
+        launch_axpy(A_.get(), V_.get(), 1.0, S, ctx_.stream);
+    }
+    diag.alpha = alpha;
+    launch_block_norm_sum(V_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, alpha,
+                          ctx_.stream);
+    diag.step_norm = read_scalar(kNormSum);
+    invalidate_all();
+    int one = 1, fin = 1;
+    CPK_CUDA(cudaMemcpyAsync(flag_.get(), &one, sizeof(int), cudaMemcpyHostToDevice, ctx_.stream));
+    launch_all_finite(A_.get(), S, flag_.get(), ctx_.stream);
+    CPK_CUDA(cudaMemcpyAsync(&fin, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    if (!fin) throw NumericalFailure("gn_step: non-finite factors after update");
+    if (residual_after < 0.0) {
+        compute_all_mttkrp();
+        grams_all();
+        residual_after = residual_fitness(xnorm2, N - 1).first;
+    }
+    diag.residual_after = residual_after;
+    diag.stepped = true;
+    schedule = schedule_next(schedule);
+    return diag;
+}
+
+// ================================================================ drivers
+std::pair<KruskalModel, ConvergenceReport> als_optimize(DeviceProblem& p, KruskalModel model,
+                                                        const AlsConfig& cfg) {  // als.cpp:54-94
+    cfg.validate();
+    model.validate();
+    p.set_factors(model);
+    const double xnorm2 = p.norm2();
+    if (!(xnorm2 > 0.0)) throw InvalidArgument("als_optimize: tensor norm must be positive");
+    ConvergenceReport report;
+    report.status = TerminalStatus::cap_hit;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int sweep = 1; sweep <= cfg.max_sweeps; ++sweep) {
+        double lambda = cfg.lambda0;
+        if (cfg.decay_every)
+            lambda /= std::pow(cfg.decay_factor, static_cast<double>((sweep - 1) / *cfg.decay_every));
+        AlsSweepDiag diag = p.als_sweep(lambda);
+        auto [res, fit] = p.residual_fitness(xnorm2, p.order() - 1);
+        const double seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        report.records.push_back({sweep, res, fit, lambda, 0, seconds});
+        if (res < cfg.residual_tol) {
+            report.status = TerminalStatus::converged_residual;
+            break;
+        }
+        if (diag.step_norm < cfg.step_tol) {
+            report.status = TerminalStatus::converged_step;
+            break;
+        }
+    }
+    p.get_factors(model);
+    return {std::move(model), std::move(report)};
+}
+
+std::pair<KruskalModel, ConvergenceReport> gn_optimize(DeviceProblem& p, KruskalModel model,
+                                                       const GnConfig& cfg) {  // gauss_newton.cpp:451-494
+    cfg.validate();
+    model.validate();
+    p.set_factors(model);
+    const double xnorm2 = p.norm2();
+    if (!(xnorm2 > 0.0)) throw InvalidArgument("gn_optimize: tensor norm must be positive");
+    ConvergenceReport report;
+    report.status = TerminalStatus::cap_hit;
+    RegSchedule schedule = cfg.schedule;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+        GnStepDiag diag = p.gn_step(cfg, schedule, xnorm2);
+        if (diag.halt == GnStepDiag::Halt::residual) {
+            report.status = TerminalStatus::converged_residual;
+            break;
+        }
+        if (diag.halt == GnStepDiag::Halt::gradient) {
+            report.status = TerminalStatus::converged_step;
+            break;
+        }
+        const double seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        report.records.push_back({iter, diag.residual_after, 1.0 - diag.residual_after, diag.lambda,
+                                  diag.cg_iters, seconds});
+        if (diag.residual_after < cfg.residual_tol) {
+            report.status = TerminalStatus::converged_residual;
+            break;
+        }
+        if (diag.step_norm < cfg.step_tol) {
+            report.status = TerminalStatus::converged_step;
+            break;
+        }
+    }
+    p.get_factors(model);
+    return {std::move(model), std::move(report)};
+}
+
+}  // namespace cpkit

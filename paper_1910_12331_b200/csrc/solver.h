@@ -1,0 +1,283 @@
+// Host-side mirror of the reference solver API (cpkit::DenseTensor,
+// KruskalModel, RegSchedule, GnConfig, AlsConfig, ConvergenceReport and the
+// als_optimize / gn_optimize drivers), re-implemented over device-resident
+// state. Reference headers: tensor.hpp, kruskal.hpp, gauss_newton.hpp,
+// als.hpp, report.hpp, mttkrp.hpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "common.h"
+
+namespace cpkit {
+
+// ---------------------------------------------------------------- host types
+// Row-major fp64 matrix (matrix_ops.hpp:9-10).
+struct Matrix {
+    std::int64_t rows = 0, cols = 0;
+    std::vector<double> data;
+    Matrix() = default;
+    Matrix(std::int64_t r, std::int64_t c) : rows(r), cols(c), data(static_cast<std::size_t>(r * c), 0.0) {}
+    double norm() const;
+    bool all_finite() const;
+};
+
+inline constexpr std::uint64_t kDefaultElementCap = 100'000'000ull;  // tensor.hpp:12
+
+std::uint64_t product_of_dims(const std::vector<std::uint64_t>& dims);
+
+// tensor.hpp:16-48 (host copy; the device copy lives in DeviceProblem)
+class DenseTensor {
+public:
+    DenseTensor() = default;
+    explicit DenseTensor(std::vector<std::uint64_t> dims);
+    static DenseTensor from_data(std::vector<std::uint64_t> dims, std::vector<double> data);
+    std::size_t order() const { return dims_.size(); }
+    std::uint64_t extent(std::size_t m) const { return dims_[m]; }
+    const std::vector<std::uint64_t>& dims() const { return dims_; }
+    std::uint64_t size() const { return data_.size(); }
+    double* data() { return data_.data(); }
+    const double* data() const { return data_.data(); }
+    void validate() const;
+
+private:
+    std::vector<std::uint64_t> dims_;
+    std::vector<double> data_;
+};
+
+// kruskal.hpp:15-26
+struct KruskalModel {
+    std::vector<std::uint64_t> dims;
+    std::int64_t rank = 0;
+    std::vector<Matrix> factors;
+    std::size_t order() const { return dims.size(); }
+    void validate() const;
+};
+
+// CPKT1 / CPKM1 binary formats (tensor.cpp:197-239, kruskal.cpp:143-203)
+void write_tensor(const DenseTensor& t, const std::string& path);
+DenseTensor read_tensor(const std::string& path);
+void write_model(const KruskalModel& m, const std::string& path);
+KruskalModel read_model(const std::string& path);
+
+// ---------------------------------------------------------------- configs
+enum class RegMode { constant, varying };
+enum class RegShape { identity, diagonal };
+struct RegSchedule {  // gauss_newton.hpp:19-34
+    RegMode mode = RegMode::constant;
+    RegShape shape = RegShape::identity;
+    double lambda = 1e-3, mu = 2.0, lower = 1e-6, upper = 1e-2;
+    enum class Direction { down, up };
+    Direction direction = Direction::down;
+    static RegSchedule constant(double lambda, RegShape shape = RegShape::identity);
+    static RegSchedule varying(double upper = 1e-2, double lower = 1e-6, double mu = 2.0,
+                               RegShape shape = RegShape::identity);
+    void validate() const;
+};
+RegSchedule schedule_next(RegSchedule s);  // gauss_newton.cpp:47-59
+
+enum class CgBetaVariant { standard, stale_denominator };
+struct ArmijoParams {
+    double c1 = 1e-4, shrink = 0.5;
+    int max_backtracks = 20;
+};
+struct GnConfig {  // gauss_newton.hpp:50-62
+    double grad_tol = 0.0, residual_tol = 5e-5, step_tol = 1e-7;
+    int max_iters = 500;
+    double cg_tol = 1e-3;
+    int cg_max_iters = 0;
+    RegSchedule schedule = RegSchedule::varying();
+    std::optional<ArmijoParams> armijo;
+    CgBetaVariant cg_beta = CgBetaVariant::standard;
+    void validate() const;
+};
+struct AlsConfig {  // als.hpp:11-22
+    int max_sweeps = 10000;
+    double residual_tol = 5e-5, step_tol = 1e-7, lambda0 = 0.0, decay_factor = 2.0;
+    std::optional<int> decay_every;
+    void validate() const;
+};
+
+// ---------------------------------------------------------------- reports
+enum class TerminalStatus { converged_residual, converged_step, cap_hit, numerical_failure };
+const char* to_string(TerminalStatus s);
+struct TraceRecord {  // report.hpp:21-28
+    int iteration = 0;
+    double residual = 0.0, fitness = 0.0, lambda = 0.0;
+    int cg_iters = 0;
+    double seconds = 0.0;
+};
+struct ConvergenceReport {
+    std::vector<TraceRecord> records;
+    TerminalStatus status = TerminalStatus::cap_hit;
+    double final_residual() const { return records.empty() ? 1.0 : records.back().residual; }
+    double best_residual() const;
+};
+
+struct GnStepDiag {  // gauss_newton.hpp:117-131
+    enum class Halt { none, residual, gradient };
+    Halt halt = Halt::none;
+    bool stepped = false;
+    double residual_before = 1.0, residual_after = 1.0, grad_norm = 0.0, lambda = 0.0;
+    int cg_iters = 0;
+    double step_norm = 0.0, alpha = 1.0;
+    bool armijo_exhausted = false, cg_hit_cap = false, cg_breakdown = false;
+};
+struct AlsSweepDiag {  // als.hpp:24-28 (last-mode MTTKRP stays on device)
+    double step_norm = 0.0;
+    int full_contractions = 0;
+};
+struct CgResultInfo {
+    int iterations = 0;
+    bool hit_cap = false, breakdown = false;
+};
+
+// ---------------------------------------------------------------- device layer
+// Collective hooks for last-mode sharding (NCCL over NVLink when world > 1).
+class Comm {
+public:
+    virtual ~Comm() = default;
+    virtual int rank() const = 0;
+    virtual int world() const = 0;
+    virtual void allreduce_sum(double* dev, std::size_t count, cudaStream_t st) = 0;
+    // gather equal-size row blocks from every rank into dev_out (rank-major)
+    virtual void allgather(const double* dev_in, double* dev_out, std::size_t count_per_rank,
+                           cudaStream_t st) = 0;
+};
+std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int world);
+void nccl_unique_id(void* out128);
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::unique_ptr<Comm> comm;  // null: single GPU
+    explicit Context(int dev);
+    ~Context();
+    int rank() const { return comm ? comm->rank() : 0; }
+    int world() const { return comm ? comm->world() : 1; }
+    void sync() const;
+};
+
+// Slab of the last mode owned by a rank (balanced contiguous split).
+void shard_range(std::uint64_t extent, int rank, int world, std::uint64_t* lo, std::uint64_t* hi);
+
+// Device-resident problem: the (local slab of the) tensor, the replicated
+// factors, the dimension-tree cache (mttkrp.hpp:35-54) and every GN/ALS buffer.
+class DeviceProblem {
+public:
+    // dims: global extents. local_data: the rank's slab (row-major over
+    // dims with the last extent replaced by the slab size); host or device.
+    DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int rank);
+    ~DeviceProblem();
+    void upload_tensor(const double* host_local);          // H2D copy of the local slab
+    void generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel);
+    double* tensor_device() { return x_.get(); }
+    std::uint64_t local_elems() const { return local_elems_; }
+
+    int order() const { return static_cast<int>(dims_.size()); }
+    int rank() const { return R_; }
+    const std::vector<std::uint64_t>& dims() const { return dims_; }
+    std::uint64_t slab_lo() const { return slab_lo_; }
+    std::uint64_t slab_hi() const { return slab_hi_; }
+
+    void set_factors(const std::vector<const double*>& host);  // host s_n x R blocks
+    void get_factors(std::vector<double*>& host);
+    void set_factors(const KruskalModel& m);
+    void get_factors(KruskalModel& m);
+    double* factors_device() { return A_.get(); }
+    std::int64_t factor_offset(int n) const { return off_[n]; }
+
+    // ---- reference seams
+    double norm2();                                   // ||X||^2 (tensor.cpp:61-67)
+    void mttkrp(int mode);                            // tree, into M block (mttkrp.cpp:160-189)
+    void mttkrp_naive(int mode);                      // uncached, same kernels
+    void note_factor_update(int mode);                // mttkrp.cpp:136-145
+    void invalidate_all();
+    int full_contractions() const { return contractions_; }
+    void reset_contraction_counter() { contractions_ = 0; }
+    const double* mttkrp_result(int mode) const { return M_.get() + off_[mode]; }
+    void download_mttkrp(int mode, double* host);
+
+    void build_gamma_set();                           // grams + pairwise (kruskal.cpp:42-65)
+    void download_gammas(double* grams, double* pair);
+    void upload_gammas(const double* grams, const double* pair);
+    std::pair<double, double> residual_fitness(double xnorm2, int last_src);  // kruskal.cpp:94-118
+    void gradient();                                  // G (gauss_newton.cpp:81-94)
+    double norm_sum(const double* dev_stacked);       // sum_n ||block_n||_F
+    void jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape);
+    CgResultInfo cp_cg(double lambda, const GnConfig& cfg);  // V from G (gauss_newton.cpp:279-349)
+    void build_preconditioner(double lambda, RegShape shape);
+    void spd_solve(const double* dev_s, const double* dev_b, std::int64_t rows, double lambda,
+                   double* dev_y);
+    void spd_inverse(const double* dev_s, double lambda, double* dev_inv);
+
+    AlsSweepDiag als_sweep(double lambda);            // als.cpp:22-52
+    GnStepDiag gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);  // :360-449
+
+    // stacked device buffers (N blocks of s_n x R)
+    double* G() { return G_.get(); }
+    double* V() { return V_.get(); }
+    double* Wbuf() { return W_[0].get(); }
+    double* Ubuf() { return Q_.get(); }
+    double* grams() { return grams_.get(); }
+    double* pairs() { return pair_.get(); }
+    double* pinv() { return pinv_.get(); }
+    std::int64_t stacked_elems() const { return off_[dims_.size()]; }
+    Context& ctx() { return ctx_; }
+
+private:
+    Context& ctx_;
+    std::vector<std::uint64_t> dims_;
+    int R_ = 0, h_ = 0;
+    std::uint64_t slab_lo_ = 0, slab_hi_ = 0, local_elems_ = 0;
+    std::int64_t F_ = 0, Bl_ = 0;                    // local matrix view F x B_local
+    std::vector<std::int64_t> off_;                  // stacked offsets (elements)
+    DevBuf<double> x_;
+    DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
+    DevBuf<double> PF_, PB_, ws_;
+    bool pf_valid_ = false, pb_valid_ = false;
+    int contractions_ = 0;
+    DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_;
+    DevBuf<double> scal_, partials_, slots_;
+    DevBuf<int> status_, cgres_, flag_;
+    DevBuf<unsigned int> barrier_;
+    DevBuf<std::int64_t> offs_dev_, rows_dev_;
+    DevBuf<const double*> facptr_dev_;
+    double* Mall_gather_ = nullptr;
+    std::vector<std::int64_t> local_rows_;           // rows of each mode in the LOCAL tensor
+    bool m_all_valid_ = false;                       // all M computed for current factors (GN reuse)
+
+    KrpDesc krp(int lo, int hi, const double* base, bool local_last) const;
+    void root_back();
+    void root_front();
+    void second_level_back(int mode);
+    void second_level_front(int mode);
+    void finish_mode(int mode);  // collectives on M^(mode)
+    void compute_all_mttkrp();
+    void grams_all();
+    void check_status(int count, const char* what);
+    double read_scalar(int idx);
+};
+
+std::pair<KruskalModel, ConvergenceReport> als_optimize(DeviceProblem& p, KruskalModel model,
+                                                        const AlsConfig& cfg);
+std::pair<KruskalModel, ConvergenceReport> gn_optimize(DeviceProblem& p, KruskalModel model,
+                                                       const GnConfig& cfg);
+
+// Generators (generators.cpp:32-117), host side.
+KruskalModel random_model_uniform(const std::vector<std::uint64_t>& dims, std::int64_t rank,
+                                  std::uint64_t seed, double a, double b);
+KruskalModel random_model_gaussian(const std::vector<std::uint64_t>& dims, std::int64_t rank,
+                                   std::uint64_t seed);
+std::uint64_t problem_seed(std::uint64_t master, int rank, int problem);
+std::uint64_t init_seed(std::uint64_t master, int rank, int problem, int init);
+double rng_uniform(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, double a, double b);
+double rng_gaussian(std::uint64_t seed, std::uint64_t stream, std::uint64_t index);
+
+}  // namespace cpkit

@@ -1,0 +1,393 @@
+"""GPU parity: every device kernel/driver of the hot path against the CPU oracle
+on identical seeded inputs, called through the C ABI (libcpkit_b200.so).
+
+Tolerances (north_star): per-kernel outputs within 1e-11 Frobenius-relative
+(test_tensor_core.cpp:30-32 metric); same GN/ALS iteration counts; final
+fitness within 1e-8.
+"""
+import numpy as np
+import pytest
+
+from tests.helpers import gauss_factors, gauss_tensor, mttkrp_unfold, rel_err, vec_rel_err
+
+pytestmark = pytest.mark.gpu
+
+KTOL = 1e-11  # per-kernel Frobenius-relative tolerance
+
+
+@pytest.fixture(scope="module")
+def ck():
+    from paper_1910_12331_b200 import cpkit
+    cpkit.load()
+    return cpkit
+
+
+def make(ck, x, factors):
+    p = ck.DeviceProblem(list(x.shape), factors[0].shape[1])
+    p.upload(x)
+    p.set_factors(factors)
+    return p
+
+
+# ---------------------------------------------------------------- MTTKRP
+TREE_CASES = [
+    ([5, 3], 3), ([3, 4, 2], 3), ([2, 3, 4, 5], 3), ([3, 2, 2, 3, 2], 2),  # odd dims, orders 2-5
+    ([3, 3, 3], 4), ([3, 3, 3, 3], 4), ([3, 3, 3, 3, 3], 4),                # test_tensor_core.cpp:210-231
+    ([50, 50, 50], 5),                                                      # C1 shape
+    ([40, 31, 37], 20), ([17, 19, 23, 11], 7), ([33, 65, 129], 13),
+    ([40, 30, 50], 100),                                                    # R=100 (NT=13 tiles)
+    ([20, 24, 26], 200),                                                    # R=200 (two rank tiles)
+    ([1, 1, 1], 1), ([1, 7, 1], 3),                                         # degenerate extents
+]
+
+
+@pytest.mark.parametrize("dims,rank", TREE_CASES)
+def test_mttkrp_tree_matches_oracle(orc, ck, dims, rank):
+    x = np.random.default_rng(sum(dims) + rank).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 11 + rank)
+    ref, ref_cnt = orc.mttkrp_tree_all(x, f)
+    p = make(ck, x, f)
+    for n in range(len(dims)):
+        got = p.mttkrp(n)
+        assert rel_err(got, ref[n]) < KTOL, (n, rel_err(got, ref[n]))
+    assert p.full_contractions == ref_cnt <= 2
+
+
+@pytest.mark.parametrize("dims,rank", [([3, 4, 2], 3), ([6, 5, 4, 3], 5), ([30, 20, 10], 9)])
+def test_mttkrp_naive_and_unfolding(orc, ck, dims, rank):
+    x = gauss_tensor(orc, dims, 5) if np.prod(dims) < 5000 else \
+        np.random.default_rng(3).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 6)
+    p = make(ck, x, f)
+    for n in range(len(dims)):
+        got = p.mttkrp_naive(n)
+        assert rel_err(got, orc.mttkrp_naive(x, f, n)) < KTOL
+        assert rel_err(got, mttkrp_unfold(x, f, n)) < KTOL
+    assert p.full_contractions == 0  # uncached overload does not count
+
+
+def test_mttkrp_kats(ck):
+    # test_tensor_core.cpp:178-199
+    p = make(ck, np.ones((2, 2, 2)), [np.ones((2, 2))] * 3)
+    assert np.array_equal(p.mttkrp(0), 4 * np.ones((2, 2)))
+    a = np.array([1.0, -2.0, 0.5]); b = np.array([2.0, 1.0, 1.0]); c = np.array([0.5, 3.0, -1.0])
+    x = np.einsum("i,j,k->ijk", a, b, c)
+    p = make(ck, x, [a[:, None], b[:, None], c[:, None]])
+    assert rel_err(p.mttkrp(0), a[:, None] * (b @ b) * (c @ c)) < 1e-12
+
+
+def test_workspace_invalidation(orc, ck):
+    # test_tensor_core.cpp:233-244
+    x = gauss_tensor(orc, [3, 4, 2], 29)
+    f = gauss_factors(orc, [3, 4, 2], 2, 30)
+    p = make(ck, x, f)
+    p.mttkrp(0)
+    f2 = [f[0], f[1], gauss_factors(orc, [2], 2, 31)[0]]
+    p.set_factors(f2)
+    p.note_factor_update(2)
+    assert rel_err(p.mttkrp(0), orc.mttkrp_naive(x, f2, 0)) < KTOL
+
+
+def test_mttkrp_mode_out_of_range(ck):
+    p = make(ck, np.ones((2, 2, 2)), [np.ones((2, 2))] * 3)
+    with pytest.raises(ck.CpkitError) as e:
+        p.mttkrp(3)
+    assert e.value.status == "invalid_argument"
+
+
+# ---------------------------------------------------------------- Gamma / residual / gradient
+@pytest.mark.parametrize("dims,rank", [([3, 2, 4, 2], 3), ([50, 50, 50], 5), ([40, 30, 20], 60)])
+def test_gamma_set(orc, ck, dims, rank):
+    f = gauss_factors(orc, dims, rank, 19)
+    x = np.zeros(dims)
+    p = make(ck, x, f)
+    g, pr = p.gamma_set()
+    rg, rp = orc.gamma_set(f)
+    assert rel_err(g, rg) < KTOL and rel_err(pr, rp) < KTOL
+    for n in range(len(dims)):
+        for q in range(len(dims)):
+            assert np.array_equal(pr[n, q], pr[q, n])  # bitwise symmetric (test_kruskal.cpp:140-149)
+
+
+def test_gamma_kat(ck):
+    a = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    p = make(ck, np.zeros((3, 3, 3)), [a, a, a])
+    g, pr = p.gamma_set()
+    assert np.array_equal(g[0], [[2.0, 1.0], [1.0, 2.0]])
+    assert np.array_equal(pr[0, 0], [[4.0, 1.0], [1.0, 4.0]])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_residual_matches_oracle(orc, ck, seed):
+    rng = np.random.default_rng(seed)
+    order = 3 + seed % 2
+    dims = [int(rng.integers(2, 9)) for _ in range(order)]
+    rank = int(rng.integers(1, 9))
+    m = gauss_factors(orc, dims, rank, 100 + seed)
+    t = gauss_factors(orc, dims, rank, 200 + seed)
+    x = orc.reconstruct(t)
+    xn2 = orc.norm2(x)
+    p = make(ck, x, m)
+    assert abs(p.norm2() - xn2) <= 1e-13 * xn2
+    p.mttkrp(order - 1)
+    r, f = p.residual(xn2)
+    rr, ff = orc.residual(x, m, xn2)
+    assert abs(r - rr) < 1e-10
+    dense = np.linalg.norm(x - orc.reconstruct(m)) / np.linalg.norm(x)
+    assert abs(r - dense) < 1e-10
+
+
+def test_residual_exact_model_floor(orc, ck):
+    f = gauss_factors(orc, [3, 3, 3], 2, 23)
+    x = orc.reconstruct(f)
+    p = make(ck, x, f)
+    p.mttkrp(2)
+    r, fit = p.residual(orc.norm2(x))
+    assert r < 1e-7 and fit > 1 - 1e-7
+
+
+def test_gradient(orc, ck):
+    f = gauss_factors(orc, [6, 5, 4], 3, 7)
+    x = gauss_tensor(orc, [6, 5, 4], 99)
+    p = make(ck, x, f)
+    mk = [orc.mttkrp_naive(x, f, n) for n in range(3)]
+    rg, rp = orc.gamma_set(f)
+    p.gamma_set()
+    g = p.gradient(mk)
+    assert vec_rel_err(g, orc.gradient(f, mk, rg, rp)) < KTOL
+
+
+# ---------------------------------------------------------------- J^T J v
+@pytest.mark.parametrize("dims,rank,lam,shape", [
+    ([3, 3, 3], 2, 0.0, 0), ([3, 2, 4], 3, 0.37, 0), ([3, 3, 3], 2, 0.25, 1),
+    ([5, 4], 3, 0.1, 0), ([3, 4, 2, 5], 2, 1e-3, 0), ([2, 3, 2, 2, 3], 2, 0.5, 1),
+    ([50, 50, 50], 5, 1e-2, 0), ([60, 45, 70], 40, 1e-3, 0), ([100, 100, 100, 100], 50, 1e-4, 1),
+])
+def test_jtj_matvec(orc, ck, dims, rank, lam, shape):
+    f = gauss_factors(orc, dims, rank, 17)
+    w = gauss_factors(orc, dims, rank, 18)
+    p = ck.DeviceProblem(dims, rank)
+    p.set_factors(f)
+    p.gamma_set()
+    g, pr = orc.gamma_set(f)
+    got = p.jtj_matvec(w, lam, shape)
+    ref = orc.hessian_matvec(f, g, pr, w, lam, shape)
+    assert vec_rel_err(got, ref) < KTOL
+
+
+def test_jtj_vs_explicit_and_identity(orc, ck):
+    # test_gauss_newton.cpp:146-195 and acceptance c1
+    rng = np.random.default_rng(17)
+    for trial in range(12):
+        order = 2 + int(rng.integers(0, 3))
+        dims = [2 + int(rng.integers(0, 3)) for _ in range(order)]
+        rank = 1 + int(rng.integers(0, 3))
+        f = gauss_factors(orc, dims, rank, 300 + trial)
+        w = gauss_factors(orc, dims, rank, 600 + trial)
+        p = ck.DeviceProblem(dims, rank)
+        p.set_factors(f)
+        p.gamma_set()
+        u = p.jtj_matvec(w, 0.0)
+        exp = orc.explicit_jtj(f) @ orc.vec_stack(w)
+        assert np.linalg.norm(orc.vec_stack(u) - exp) <= 1e-12 * np.linalg.norm(exp)
+    f = gauss_factors(orc, [3, 3, 3], 2, 11)
+    p = ck.DeviceProblem([3, 3, 3], 2)
+    p.set_factors(f)
+    grams = np.stack([np.eye(2)] * 3)
+    pair = np.zeros((3, 3, 2, 2))
+    for n in range(3):
+        pair[n, n] = np.eye(2)
+    p.set_gamma_set(grams, pair)
+    w = gauss_factors(orc, [3, 3, 3], 2, 12)
+    assert vec_rel_err(p.jtj_matvec(w, 0.0), w) < 1e-14
+
+
+# ---------------------------------------------------------------- SPD / preconditioner
+def test_spd_solve_and_inverse(orc, ck):
+    for R in (2, 5, 33, 100, 200):
+        a = gauss_factors(orc, [R + 7], R, R)[0]
+        s = orc.gram(a)
+        b = gauss_factors(orc, [37], R, R + 1)[0]
+        p = ck.DeviceProblem([3, 3], R)
+        assert rel_err(p.spd_solve(s, b, 1e-3), orc.spd_solve(s, b, 1e-3)) < 1e-10
+        assert rel_err(p.spd_inverse(s, 1e-3), orc.spd_inverse(s, 1e-3)) < 1e-10
+    p = ck.DeviceProblem([3, 3], 2)
+    assert np.allclose(p.spd_solve(2 * np.eye(2), np.eye(2), 0.0), 0.5 * np.eye(2))
+    y = p.spd_solve(np.ones((2, 2)), np.ones((1, 2)), 0.0)  # jitter retry (test_tensor_core.cpp:280-288)
+    assert np.isfinite(y).all()
+    with pytest.raises(ck.CpkitError) as e:
+        p.spd_solve(np.zeros((2, 2)), np.eye(2), 0.0)
+    assert e.value.status == "singular_system"
+
+
+@pytest.mark.parametrize("shape", [0, 1])
+def test_preconditioner(orc, ck, shape):
+    f = gauss_factors(orc, [4, 4, 4], 3, 41)
+    p = make(ck, np.zeros((4, 4, 4)), f)
+    p.gamma_set()
+    g, pr = orc.gamma_set(f)
+    assert rel_err(p.preconditioner(1e-3, shape), orc.preconditioner(g, pr, 1e-3, shape)) < 1e-10
+
+
+# ---------------------------------------------------------------- CG
+@pytest.mark.parametrize("dims,rank,lam,cfg", [
+    ([3, 3, 3], 2, 1e-3, {"cg_tol": 1e-10, "cg_max_iters": 10000}),
+    ([6, 5, 7], 3, 1e-2, {}),
+    ([8, 9, 7, 6], 4, 1e-3, {"cg_beta": "stale_denominator", "cg_max_iters": 50}),
+    ([30, 25, 20], 6, 1e-4, {"reg": {"shape": "diagonal"}}),
+    ([50, 50, 50], 5, 1e-2, {"cg_max_iters": 20}),
+])
+def test_cp_cg_matches_oracle(orc, ck, dims, rank, lam, cfg):
+    f = gauss_factors(orc, dims, rank, 59)
+    x = np.random.default_rng(1).standard_normal(dims)
+    mk = [orc.mttkrp_naive(x, f, n) for n in range(len(dims))]
+    g, pr = orc.gamma_set(f)
+    grad = orc.gradient(f, mk, g, pr)
+    ocfg = orc.GnConfig(cg_tol=cfg.get("cg_tol", 1e-3), cg_max_iters=cfg.get("cg_max_iters", 0),
+                        cg_beta=1 if cfg.get("cg_beta") == "stale_denominator" else 0,
+                        reg_shape=1 if cfg.get("reg", {}).get("shape") == "diagonal" else 0)
+    v_ref, it_ref, cap_ref, bd_ref = orc.cp_cg(f, g, pr, grad, lam, ocfg)
+    p = make(ck, x, f)
+    p.gamma_set()
+    v, it, cap, bd = p.cp_cg(grad, lam, cfg)
+    assert (it, cap, bd) == (it_ref, cap_ref, bd_ref)
+    assert vec_rel_err(v, v_ref) < 1e-9  # iterate after `it` steps (error grows with conditioning)
+
+
+def test_cg_isolated_identity_and_zero_gradient(orc, ck):
+    # test_gauss_newton.cpp:323-346
+    f = gauss_factors(orc, [3, 3, 3], 2, 47)
+    p = make(ck, np.zeros((3, 3, 3)), f)
+    grams = np.stack([np.eye(2)] * 3)
+    pair = np.zeros((3, 3, 2, 2))
+    for n in range(3):
+        pair[n, n] = np.eye(2)
+    p.set_gamma_set(grams, pair)
+    g = gauss_factors(orc, [3, 3, 3], 2, 48)
+    v, it, _, _ = p.cp_cg(g, 0.0, {"cg_tol": 1e-10})
+    assert it == 1
+    for n in range(3):
+        assert np.linalg.norm(v[n] + g[n]) <= 1e-12 * np.linalg.norm(g[n])
+    p.gamma_set()
+    v, it, _, _ = p.cp_cg([np.zeros((3, 2))] * 3, 1e-3)
+    assert it == 0 and all(np.linalg.norm(a) == 0 for a in v)
+
+
+# ---------------------------------------------------------------- GN / ALS drivers
+def test_gn_step_matches_oracle(orc, ck):
+    dims, rank = [12, 10, 9], 4
+    t = orc.random_model(dims, rank, 5)
+    x = orc.reconstruct(t) + 1e-3 * np.random.default_rng(0).standard_normal(dims)
+    init = orc.random_model(dims, rank, 6)
+    xn2 = orc.norm2(x)
+    for cfg, ocfg in [({}, orc.GnConfig()),
+                      ({"armijo": True, "reg": {"mode": "constant", "lambda": 1e-3}},
+                       orc.GnConfig(armijo=1, reg_mode=0, lambda_=1e-3))]:
+        p = make(ck, x, init)
+        d = p.gn_step(cfg, xn2)
+        f_ref, d_ref = orc.gn_step(x, init, ocfg, xn2)
+        for k in ("halt", "stepped", "cg_iters", "alpha", "armijo_exhausted", "cg_hit_cap"):
+            assert d[k] == d_ref[k], (k, d, d_ref)
+        for k in ("residual_before", "residual_after", "grad_norm", "step_norm"):
+            assert abs(d[k] - d_ref[k]) <= 1e-9 * max(1.0, abs(d_ref[k])), (k, d[k], d_ref[k])
+        assert vec_rel_err(p.get_factors(), f_ref) < 1e-9
+
+
+def test_gn_step_kats(orc, ck):
+    # exact-fit halt (test_gauss_newton.cpp:384-407)
+    f = gauss_factors(orc, [3, 3, 3], 2, 67)
+    x = orc.reconstruct(f)
+    p = make(ck, x, f)
+    d = p.gn_step({}, orc.norm2(x))
+    assert d["halt"] == 1 and d["stepped"] == 0
+    # Armijo on the one-entry tensor [8] (test_gauss_newton.cpp:426-467)
+    x = np.array([8.0]).reshape(1, 1, 1)
+    p = make(ck, x, [np.ones((1, 1))] * 3)
+    d = p.gn_step({"residual_tol": 0.0, "reg": {"mode": "constant", "lambda": 1e-3}, "armijo": True},
+                  64.0)
+    assert d["stepped"] == 1 and d["alpha"] < 1.0 and d["armijo_exhausted"] == 0
+    p = make(ck, x, [np.ones((1, 1))] * 3)
+    d = p.gn_step({"residual_tol": 0.0, "reg": {"mode": "constant", "lambda": 1e-3},
+                   "armijo": {"c1": 0.999999, "shrink": 0.5, "max_backtracks": 2}}, 64.0)
+    assert d["armijo_exhausted"] == 1 and d["alpha"] == pytest.approx(0.25)
+
+
+@pytest.mark.parametrize("dims,rank", [([3, 4, 2], 2), ([12, 10, 9], 4), ([8, 7, 6, 5], 3)])
+def test_als_sweep_matches_oracle(orc, ck, dims, rank):
+    t = orc.random_model(dims, rank, 1)
+    x = orc.reconstruct(t)
+    init = orc.random_model(dims, rank, 2)
+    f_ref, step_ref, cnt_ref, _ = orc.als_sweep(x, init, 1e-3)
+    p = make(ck, x, init)
+    step, cnt = p.als_sweep(1e-3)
+    assert cnt == cnt_ref == 2
+    assert abs(step - step_ref) <= 1e-9 * step_ref
+    assert vec_rel_err(p.get_factors(), f_ref) < 1e-10
+
+
+def _c1(orc):
+    """BASELINE config 1: order 3, s=50, R=5, uniform[0,1) truth, exact rank."""
+    dims, rank = [50, 50, 50], 5
+    truth = orc.random_model(dims, rank, orc.problem_seed(0, rank, 0))
+    x = orc.reconstruct(truth)
+    init = orc.random_model(dims, rank, orc.init_seed(0, rank, 0, 0))
+    return dims, rank, x, init
+
+
+def test_c1_gn_trace_matches_oracle(orc, ck):
+    dims, rank, x, init = _c1(orc)
+    _, recs, st = orc.gn_optimize(x, init, orc.GnConfig(cg_max_iters=20))
+    p = ck.DeviceProblem(dims, rank)
+    p.upload(x)
+    got, rep = p.optimize({"optimizer": "gn", "gn": {"cg_max_iters": 20}}, init)
+    j = rep.to_json()
+    assert j["status"] == st
+    assert len(j["records"]) == len(recs)
+    for a, b in zip(j["records"], recs):
+        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"]
+        assert abs(a["residual"] - b["residual"]) < 1e-8
+
+
+def test_c1_als_trace_matches_oracle(orc, ck):
+    dims, rank, x, init = _c1(orc)
+    cfg = orc.AlsConfig(max_sweeps=300)
+    _, recs, st = orc.als_optimize(x, init, cfg)
+    p = ck.DeviceProblem(dims, rank)
+    p.upload(x)
+    got, rep = p.optimize({"optimizer": "als", "als": {"max_sweeps": 300}}, init)
+    j = rep.to_json()
+    assert j["status"] == st and len(j["records"]) == len(recs)
+    assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
+
+
+# ---------------------------------------------------------------- C ABI end to end
+def test_decompose_through_c_abi(orc, ck):
+    # test_capi.cpp:96-126 shape: gaussian [4,4,4] rank 2, GN
+    m, t = ck.generate_low_rank({"family": "gaussian", "dims": [4, 4, 4], "rank": 2, "seed": 3})
+    truth = orc.random_model([4, 4, 4], 2, 3, kind="gaussian")
+    assert np.array_equal(t.numpy(), orc.reconstruct(truth))  # bitwise generator parity
+    model, rep = ck.decompose(t, {"optimizer": "gn", "rank": 2, "seed": 19,
+                                  "gn": {"max_iters": 200, "residual_tol": 5e-5}})
+    assert model.rank == 2
+    js = rep.to_json_text()
+    assert '"kind": "trace"' in js
+    assert rep.config()["optimizer"] == "gn"
+    # oracle run on the same start point (cpkit_c.cpp:256-272: gaussian init, init_seed)
+    init = orc.random_model([4, 4, 4], 2, orc.init_seed(19, 2, 0, 0), kind="gaussian")
+    _, recs, st = orc.gn_optimize(t.numpy(), init, orc.GnConfig(max_iters=200))
+    j = rep.to_json()
+    assert j["status"] == st and len(j["records"]) == len(recs)
+
+
+def test_c_abi_errors(ck):
+    t = ck.Tensor.create(np.zeros((2, 2, 2)))
+    with pytest.raises(ck.CpkitError) as e:
+        ck.decompose(t, {"optimizer": "als", "rank": 1})
+    assert e.value.status == "invalid_argument"  # zero-norm tensor
+    t = ck.Tensor.create(np.ones((2, 2, 2)))
+    with pytest.raises(ck.CpkitError) as e:
+        ck.decompose(t, {"optimizer": "bogus", "rank": 1})
+    assert e.value.status == "parse_error"
+    with pytest.raises(ck.CpkitError) as e:
+        ck.decompose(t, {"optimizer": "gn"})
+    assert e.value.status == "invalid_argument"  # rank required
