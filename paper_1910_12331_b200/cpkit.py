@@ -336,12 +336,14 @@ class DeviceProblem:
         return v.value
 
     def mttkrp(self, mode: int, download: bool = True):
-        out = np.empty((self.dims[mode], self.rank)) if download else None
+        rows = self.dims[mode] if 0 <= mode < len(self.dims) else 1
+        out = np.empty((rows, self.rank)) if download else None
         _chk(load().cpkit_dev_mttkrp(self._h, _u64(mode), _ptr(out)))
         return out
 
     def mttkrp_naive(self, mode: int):
-        out = np.empty((self.dims[mode], self.rank))
+        rows = self.dims[mode] if 0 <= mode < len(self.dims) else 1
+        out = np.empty((rows, self.rank))
         _chk(load().cpkit_dev_mttkrp_naive(self._h, _u64(mode), _ptr(out)))
         return out
 
