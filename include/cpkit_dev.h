@@ -106,15 +106,33 @@ CPKIT_API cpkit_status cpkit_dev_optimize(cpkit_dev_problem* p, const char* conf
 /* `sweeps` back-to-back ALS sweeps at lambda (factors evolve). */
 CPKIT_API cpkit_status cpkit_dev_time_als_sweeps(cpkit_dev_problem* p, double lambda, int sweeps,
                                                  double* ms_total);
-/* reps x (back root, front root) contractions; average ms per launch each. */
+/* reps x (back root, front root) root-GEMM launches; average ms per launch each. */
 CPKIT_API cpkit_status cpkit_dev_time_roots(cpkit_dev_problem* p, int reps, double* ms_back,
                                             double* ms_front);
+/* Per-launch event timing of the dominant kernels inside a caller's timed
+ * region: kinds [0] back-root GEMM, [1] front-root GEMM (+ split-K reduce),
+ * [2] persistent CG solve. enable(1) clears the record. */
+CPKIT_API cpkit_status cpkit_dev_profile(cpkit_dev_problem* p, int enable);
+CPKIT_API cpkit_status cpkit_dev_profile_read(cpkit_dev_problem* p, double* ms3, int* count3);
 /* reps x J^T J v on the current factors; average ms per matvec. */
 CPKIT_API cpkit_status cpkit_dev_time_jtj(cpkit_dev_problem* p, int reps, double* ms);
 /* reps x ||X||^2 streaming pass; average ms. */
 CPKIT_API cpkit_status cpkit_dev_time_norm2(cpkit_dev_problem* p, int reps, double* ms);
 /* FP64 DMMA issue-rate probe on `device`, TFLOP/s (roofline denominator). */
 CPKIT_API cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops);
+/* `steps` gn_step calls (one schedule from the config); total ms and the
+ * inner CG iterations they ran. */
+CPKIT_API cpkit_status cpkit_dev_time_gn_steps(cpkit_dev_problem* p, const char* gn_json, int steps,
+                                               double* ms, int* cg_iters_total);
+/* Seeded inputs: generators.cpp:59-76 factor draws (kind 0 uniform(a,b),
+ * 1 gaussian) and harness.cpp:378-391 seed derivations. */
+CPKIT_API cpkit_status cpkit_dev_random_factors(const uint64_t* dims, uint64_t order, uint64_t rank,
+                                                uint64_t seed, int kind, double a, double b,
+                                                double* out);
+CPKIT_API uint64_t cpkit_dev_problem_seed(uint64_t master, int rank, int problem);
+CPKIT_API uint64_t cpkit_dev_init_seed(uint64_t master, int rank, int problem, int init);
+/* Device tensor slab back to host. */
+CPKIT_API cpkit_status cpkit_dev_download_tensor(cpkit_dev_problem* p, double* host_local);
 /* Number of kernels this library launched since load (for the bench). */
 CPKIT_API uint64_t cpkit_dev_kernel_launches(void);
 

@@ -43,8 +43,11 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_residual", "cpkit_dev_gradient", "cpkit_dev_jtj_matvec",
     "cpkit_dev_preconditioner", "cpkit_dev_cp_cg", "cpkit_dev_spd_solve",
     "cpkit_dev_spd_inverse", "cpkit_dev_als_sweep", "cpkit_dev_gn_step", "cpkit_dev_optimize",
-    "cpkit_dev_time_als_sweeps", "cpkit_dev_time_roots", "cpkit_dev_time_jtj",
+    "cpkit_dev_time_als_sweeps", "cpkit_dev_time_roots", "cpkit_dev_profile",
+    "cpkit_dev_profile_read", "cpkit_dev_time_jtj",
     "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
+    "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
+    "cpkit_dev_init_seed", "cpkit_dev_download_tensor",
 )
 
 
@@ -93,6 +96,10 @@ def load():
     L.cpkit_dev_reset_contraction_counter.restype = None
     L.cpkit_dev_kernel_launches.restype = _u64
     L.cpkit_report_ok.argtypes = [_vp]
+    L.cpkit_dev_problem_seed.restype = _u64
+    L.cpkit_dev_problem_seed.argtypes = [_u64, C.c_int, C.c_int]
+    L.cpkit_dev_init_seed.restype = _u64
+    L.cpkit_dev_init_seed.argtypes = [_u64, C.c_int, C.c_int, C.c_int]
     _lib = L
     return L
 
@@ -445,10 +452,34 @@ class DeviceProblem:
         _chk(load().cpkit_dev_time_roots(self._h, reps, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def profile(self, enable: bool):
+        _chk(load().cpkit_dev_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        ms = (C.c_double * 3)()
+        cnt = (C.c_int * 3)()
+        _chk(load().cpkit_dev_profile_read(self._h, ms, cnt))
+        return list(ms), list(cnt)
+
     def time_jtj(self, reps: int) -> float:
         ms = C.c_double()
         _chk(load().cpkit_dev_time_jtj(self._h, reps, C.byref(ms)))
         return ms.value
+
+    def download(self) -> np.ndarray:
+        lo, hi, n = self.slab()
+        out = np.empty(n)
+        _chk(load().cpkit_dev_download_tensor(self._h, _ptr(out)))
+        return out.reshape(self.dims[:-1] + [hi - lo])
+
+    def download_into(self, out: np.ndarray) -> None:
+        _chk(load().cpkit_dev_download_tensor(self._h, _ptr(out)))
+
+    def time_gn_steps(self, gn: Optional[dict], steps: int):
+        ms, cg = C.c_double(), C.c_int()
+        _chk(load().cpkit_dev_time_gn_steps(self._h, None if gn is None else json.dumps(gn).encode(),
+                                            steps, C.byref(ms), C.byref(cg)))
+        return ms.value, cg.value
 
     def time_norm2(self, reps: int) -> float:
         ms = C.c_double()
@@ -466,6 +497,23 @@ def probe_dmma_peak(device: int = 0) -> float:
     v = C.c_double()
     _chk(load().cpkit_dev_probe_dmma_peak(device, C.byref(v)))
     return v.value
+
+
+def random_factors(dims, rank, seed, kind="uniform", a=0.0, b=1.0):
+    """generators.cpp:59-76 seeded factor draws, computed by the library."""
+    out = np.empty(sum(int(d) for d in dims) * rank)
+    _chk(load().cpkit_dev_random_factors(_dims(dims), _u64(len(dims)), _u64(rank), _u64(seed),
+                                         0 if kind == "uniform" else 1, C.c_double(a),
+                                         C.c_double(b), _ptr(out)))
+    return unstack(out, dims, rank)
+
+
+def problem_seed(master: int, rank: int, problem: int) -> int:
+    return int(load().cpkit_dev_problem_seed(master, rank, problem))
+
+
+def init_seed(master: int, rank: int, problem: int, init: int) -> int:
+    return int(load().cpkit_dev_init_seed(master, rank, problem, init))
 
 
 def kernel_launches() -> int:

@@ -967,16 +967,26 @@ cpkit_status cpkit_dev_time_roots(cpkit_dev_problem* p, int reps, double* ms_bac
     return guarded([&] {
         const int N = p->p->order();
         const int h = (N + 1) / 2;
-        EventPair e1, e2;
-        CPK_CUDA(cudaEventRecord(e1.a, p->ctx->stream));
-        for (int i = 0; i < reps; ++i) p->p->mttkrp_naive(0);  // back root + level 2
-        CPK_CUDA(cudaEventRecord(e1.b, p->ctx->stream));
-        CPK_CUDA(cudaEventRecord(e2.a, p->ctx->stream));
-        for (int i = 0; i < reps; ++i) p->p->mttkrp_naive(h);  // front root + level 2
-        CPK_CUDA(cudaEventRecord(e2.b, p->ctx->stream));
-        *ms_back = e1.ms() / reps;
-        *ms_front = e2.ms() / reps;
+        p->p->profile_enable(true);
+        for (int i = 0; i < reps; ++i) {
+            p->p->mttkrp_naive(0);  // back root (+ level 2, not timed)
+            p->p->mttkrp_naive(h);  // front root (+ level 2, not timed)
+        }
+        double ms[3];
+        int cnt[3];
+        p->p->profile_read(ms, cnt);
+        p->p->profile_enable(false);
+        *ms_back = cnt[0] ? ms[0] / cnt[0] : 0.0;
+        *ms_front = cnt[1] ? ms[1] / cnt[1] : 0.0;
     });
+}
+cpkit_status cpkit_dev_profile(cpkit_dev_problem* p, int enable) {
+    DEV_REQ(p);
+    return guarded([&] { p->p->profile_enable(enable != 0); });
+}
+cpkit_status cpkit_dev_profile_read(cpkit_dev_problem* p, double* ms3, int* count3) {
+    DEV_REQ(p && ms3 && count3);
+    return guarded([&] { p->p->profile_read(ms3, count3); });
 }
 cpkit_status cpkit_dev_time_jtj(cpkit_dev_problem* p, int reps, double* ms) {
     DEV_REQ(p && ms && reps > 0);
@@ -1005,5 +1015,51 @@ cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops) {
     return guarded([&] { *tflops = cpkit::probe_dmma_peak(device); });
 }
 uint64_t cpkit_dev_kernel_launches(void) { return cpkit::kernel_launches(); }
+
+cpkit_status cpkit_dev_random_factors(const uint64_t* dims, uint64_t order, uint64_t rank, uint64_t seed,
+                                      int kind, double a, double b, double* out) {
+    DEV_REQ(dims && out && order > 0 && rank > 0);
+    return guarded([&] {
+        std::vector<std::uint64_t> d(dims, dims + order);
+        const auto m = kind == 0 ? cpkit::random_model_uniform(d, static_cast<std::int64_t>(rank), seed, a, b)
+                                 : cpkit::random_model_gaussian(d, static_cast<std::int64_t>(rank), seed);
+        model_to_stacked(m, out);
+    });
+}
+uint64_t cpkit_dev_problem_seed(uint64_t master, int rank, int problem) {
+    return cpkit::problem_seed(master, rank, problem);
+}
+uint64_t cpkit_dev_init_seed(uint64_t master, int rank, int problem, int init) {
+    return cpkit::init_seed(master, rank, problem, init);
+}
+cpkit_status cpkit_dev_download_tensor(cpkit_dev_problem* p, double* host_local) {
+    DEV_REQ(p && host_local);
+    return guarded([&] {
+        CPK_CUDA(cudaMemcpyAsync(host_local, p->p->tensor_device(), p->p->local_elems() * 8,
+                                 cudaMemcpyDeviceToHost, p->ctx->stream));
+        p->ctx->sync();
+    });
+}
+cpkit_status cpkit_dev_time_gn_steps(cpkit_dev_problem* p, const char* gn_json, int steps, double* ms,
+                                     int* cg_iters_total) {
+    DEV_REQ(p && ms && steps > 0);
+    return guarded([&] {
+        const cpkit::GnConfig cfg = gn_json ? gn_from_block(Json::parse(gn_json)) : cpkit::GnConfig{};
+        cfg.validate();
+        cpkit::RegSchedule s = cfg.schedule;
+        const double xn2 = p->p->norm2();
+        int cg = 0;
+        EventPair ev;
+        CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
+        for (int i = 0; i < steps; ++i) {
+            cpkit::GnStepDiag d = p->p->gn_step(cfg, s, xn2);
+            cg += d.cg_iters;
+            if (!d.stepped) break;
+        }
+        CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
+        *ms = ev.ms();
+        if (cg_iters_total) *cg_iters_total = cg;
+    });
+}
 
 }  // extern "C"

@@ -385,7 +385,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     slots_.resize(cg_slots_needed(cp));
 }
 
-DeviceProblem::~DeviceProblem() = default;
+DeviceProblem::~DeviceProblem() { profile_enable(false); }
 
 KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {
     KrpDesc d{};
@@ -475,16 +475,56 @@ double DeviceProblem::norm2() {
     return read_scalar(kXnorm);
 }
 
+// ---- launch profiling ----------------------------------------------------------
+void DeviceProblem::profile_enable(bool on) {
+    for (auto& e : prof_) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    prof_.clear();
+    profile_ = on;
+}
+void DeviceProblem::prof_begin(int kind) {
+    if (!profile_) return;
+    ProfEvent e{};
+    e.kind = kind;
+    CPK_CUDA(cudaEventCreate(&e.a));
+    CPK_CUDA(cudaEventCreate(&e.b));
+    CPK_CUDA(cudaEventRecord(e.a, ctx_.stream));
+    prof_.push_back(e);
+}
+void DeviceProblem::prof_end() {
+    if (!profile_) return;
+    CPK_CUDA(cudaEventRecord(prof_.back().b, ctx_.stream));
+}
+void DeviceProblem::profile_read(double* ms, int* count) {
+    ctx_.sync();
+    for (int k = 0; k < kProfKinds; ++k) {
+        ms[k] = 0.0;
+        count[k] = 0;
+    }
+    for (auto& e : prof_) {
+        float v = 0.0f;
+        CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
+        ms[e.kind] += v;
+        count[e.kind] += 1;
+    }
+}
+
 // ---- dimension tree (mttkrp.cpp:160-189) -----------------------------------
 void DeviceProblem::root_back() {
     const int N = order();
+    prof_begin(kProfBack);
     launch_root_back(x_.get(), F_, Bl_, R_, krp(h_, N, A_.get(), true), PF_.get(), ctx_.stream);
+    prof_end();
     ++contractions_;
     pf_valid_ = true;
 }
 void DeviceProblem::root_front() {
+    prof_begin(kProfFront);
     launch_root_front(x_.get(), F_, Bl_, R_, krp(0, h_, A_.get(), false), PB_.get(), ws_.get(), ws_.size(),
                       ctx_.stream);
+    prof_end();
     ++contractions_;
     pb_valid_ = true;
 }
@@ -704,7 +744,9 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
     p.cg_tol = cfg.cg_tol;
     p.cap = cap;
     p.result = cgres_.get();
+    prof_begin(kProfCg);
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);
+    prof_end();
     int res[5];
     CPK_CUDA(cudaMemcpyAsync(res, cgres_.get(), sizeof res, cudaMemcpyDeviceToHost, ctx_.stream));
     ctx_.sync();

@@ -231,7 +231,22 @@ public:
     std::int64_t stacked_elems() const { return off_[dims_.size()]; }
     Context& ctx() { return ctx_; }
 
+    // Per-launch CUDA-event timing of the dominant kernels inside a timed region.
+    enum ProfKind { kProfBack = 0, kProfFront = 1, kProfCg = 2, kProfKinds = 3 };
+    void profile_enable(bool on);
+    // total ms and launch count per kind since enable (syncs the stream)
+    void profile_read(double* ms, int* count);
+
 private:
+    struct ProfEvent {
+        cudaEvent_t a, b;
+        int kind;
+    };
+    bool profile_ = false;
+    std::vector<ProfEvent> prof_;
+    void prof_begin(int kind);
+    void prof_end();
+
     Context& ctx_;
     std::vector<std::uint64_t> dims_;
     int R_ = 0, h_ = 0;
