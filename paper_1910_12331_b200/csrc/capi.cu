@@ -506,8 +506,7 @@ cpkit::DenseTensor reconstruct_on_device(const cpkit::KruskalModel& m, std::uint
     cpkit::Context ctx(current_device());
     cpkit::DeviceProblem p(ctx, m.dims, static_cast<int>(m.rank));
     p.generate_tensor(m, 0, 0.0);
-    CPK_CUDA(cudaMemcpyAsync(t.data(), p.tensor_device(), total * 8, cudaMemcpyDeviceToHost, ctx.stream));
-    ctx.sync();
+    p.download_tensor(t.data());
     return t;
 }
 }  // namespace
@@ -1035,9 +1034,7 @@ uint64_t cpkit_dev_init_seed(uint64_t master, int rank, int problem, int init) {
 cpkit_status cpkit_dev_download_tensor(cpkit_dev_problem* p, double* host_local) {
     DEV_REQ(p && host_local);
     return guarded([&] {
-        CPK_CUDA(cudaMemcpyAsync(host_local, p->p->tensor_device(), p->p->local_elems() * 8,
-                                 cudaMemcpyDeviceToHost, p->ctx->stream));
-        p->ctx->sync();
+        p->p->download_tensor(host_local);
     });
 }
 cpkit_status cpkit_dev_time_gn_steps(cpkit_dev_problem* p, const char* gn_json, int steps, double* ms,

@@ -89,14 +89,18 @@ struct KrpDesc {
     const double* fac[kMaxOrder] = {};     // factor pointers (s_j x R row-major)
 };
 
-// MTTKRP root contractions (kernels_mttkrp.cu).
-//   back root:  P_F[F x R] = X[F x B] * KRP_B        (NN, TMA-staged X rows)
+// MTTKRP root contractions (kernels_mttkrp.cu). X is F x B stored with an
+// even row stride Bs >= B (TMA needs 16-byte strides); krp is a K x Rs
+// workspace (krp_workspace_elems) filled with the Khatri-Rao operand.
+//   back root:  P_F[F x R] = X[F x B] * KRP_B        (NN)
 //   front root: P_B[B x R] = X[F x B]^T * KRP_F      (TN, split-K)
-void launch_root_back(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kb,
-                      double* pf, cudaStream_t st);
-void launch_root_front(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kf,
-                       double* pb, double* splitk_ws, std::size_t splitk_ws_elems, cudaStream_t st);
+void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
+                      const KrpDesc& kb, double* krp, double* pf, cudaStream_t st);
+void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
+                       const KrpDesc& kf, double* krp, double* pb, double* splitk_ws,
+                       std::size_t splitk_ws_elems, cudaStream_t st);
 std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R);
+std::size_t krp_workspace_elems(std::int64_t rows, int R);
 
 // Second dimension-tree level: P over kept modes (ext[0..k), R) reduced to the
 // single kept mode `keep`, weighting by the other kept modes' factor rows.

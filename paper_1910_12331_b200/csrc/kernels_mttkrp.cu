@@ -51,19 +51,19 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D fp64 map over a row-major (outer x inner) matrix; box = 16 doubles
-// (128 B, the swizzle atom) along inner by box_outer rows.
-CUtensorMap make_map(const double* base, std::uint64_t inner, std::uint64_t outer,
-                     std::uint32_t box_outer) {
+// 2-D fp64 map over a row-major (outer x inner) matrix with box
+// (box_inner x box_outer); swizzled maps use the 128-B atom (box_inner = 16).
+CUtensorMap make_map(const double* base, std::uint64_t inner, std::uint64_t outer, std::uint32_t box_inner,
+                     std::uint32_t box_outer, bool swizzle) {
     CUtensorMap m;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {inner * sizeof(double)};
-    cuuint32_t box[2] = {16, box_outer};
+    cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(r));
     return m;
 }
@@ -125,8 +125,9 @@ __device__ __forceinline__ int swz(int row, int col) {
     return row * 128 + ((((col >> 1) ^ row) & 7) << 4) + ((col & 1) << 3);
 }
 
-// Row padding for the KRP operand so the B-fragment loads are conflict-free:
-// rows are read either as t+4i (NN) or 2t+c+8h (TN, permuted k-slots).
+// Row stride of the B (KRP) tile in shared memory, in doubles, so the
+// B-fragment loads are conflict-free: rows are read as t+4i (NN, stride = 8
+// mod 16) or as the permuted slots 2t+c+8h (TN, stride = 4 mod 16).
 template <bool TRANS>
 __host__ __device__ constexpr int krp_stride(int bn) {
     const int want = TRANS ? 4 : 8;
@@ -145,185 +146,172 @@ struct KrpDev {
     const double* fac[kMaxOrder];
 };
 
-// Fill one BK x BN tile of the Khatri-Rao operand:
-// Bs[p][n] = prod_j fac_j[i_j(k0+p), n0+n]  (0 outside [0,K) x [0,R)).
-template <int BNS>
-__device__ __forceinline__ void gen_krp_tile(double* bs, const KrpDev& kd, long long k0, long long K,
-                                             int n0, int R, int bn) {
-    const int nthr = blockDim.x;
-    const int tpr = 8;  // threads per row
-    for (int row = threadIdx.x / tpr; row < kBK; row += nthr / tpr) {
-        const long long k = k0 + row;
-        double* dst = bs + row * BNS;
-        const int lane8 = threadIdx.x % tpr;
-        if (k >= K) {
-            for (int n = lane8; n < bn; n += tpr) dst[n] = 0.0;
-            continue;
-        }
-        const double* rowp[kMaxOrder];
-        long long rem = k;
-        for (int j = kd.nmodes - 1; j >= 0; --j) {
-            const long long e = kd.ext[j];
-            const long long i = rem % e;
-            rem /= e;
-            rowp[j] = kd.fac[j] + i * R;
-        }
-        for (int n = lane8; n < bn; n += tpr) {
-            const int col = n0 + n;
-            double v = 0.0;
-            if (col < R) {
-                v = rowp[0][col];
-                for (int j = 1; j < kd.nmodes; ++j) v *= rowp[j][col];
+// KRP[k][r] = prod_j fac_j[i_j(k), r] for k < K, r < R; zero for R <= r < Rs.
+// Streams K x Rs doubles once per contraction (HBM-bound, coalesced writes).
+__global__ void krp_fill_kernel(KrpDev kd, long long K, int R, int Rs, double* __restrict__ out) {
+    const long long total = K * Rs;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long k = e / Rs;
+        const int r = static_cast<int>(e - k * Rs);
+        double v = 0.0;
+        if (r < R) {
+            long long rem = k;
+            v = 1.0;
+            for (int j = kd.nmodes - 1; j >= 0; --j) {
+                const long long ext = kd.ext[j];
+                const long long i = rem % ext;
+                rem /= ext;
+                v *= kd.fac[j][i * R + r];
             }
-            dst[n] = v;
         }
+        out[e] = v;
     }
 }
 
-// Manual (non-TMA) X tile load producing the same swizzled layout; used when
-// the row stride is not 16-byte aligned (odd inner extent).
-template <bool TRANS>
-__device__ void load_x_manual(char* xs, const double* x, long long rows_total, long long cols_total,
-                              long long r0, long long c0, int box_rows, int nboxes) {
-    // NN: boxes along columns (k); box b covers cols c0+16b.., rows r0..r0+box_rows
-    // TN: boxes along columns (m); rows are k. Same addressing either way.
-    const int per_box = box_rows * 16;
-    const int total = per_box * nboxes;
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-        const int b = e / per_box;
-        const int w = e % per_box;
-        const int row = w / 16, col = w % 16;
-        const long long gr = r0 + row, gc = c0 + 16LL * b + col;
-        double v = 0.0;
-        if (gr < rows_total && gc < cols_total) v = x[gr * cols_total + gc];
-        *reinterpret_cast<double*>(xs + b * box_rows * 128 + swz(row, col)) = v;
-    }
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ double lds64(std::uint32_t addr) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
 }
 
 // ---------------------------------------------------------------- root GEMM
-// TRANS=false: C[m][n] = sum_k X[m][k] KRP[k][n]   (X is M x K, row stride K)
-// TRANS=true:  C[m][n] = sum_k X[k][m] KRP[k][n]   (X is K x M, row stride M)
-// grid: (n_tiles, m_tiles, splits); block: 32 * (BM/16) threads.
+// TRANS=false: C[m][n] = sum_k X[m][k] KRP[k][n]   (X is M x K, row stride = xmap)
+// TRANS=true:  C[m][n] = sum_k X[k][m] KRP[k][n]   (X is K x M)
+// Warp-specialised: warps 0..W-1 issue DMMA on 16-row strips of the BM = 16W
+// tile; warp W is the TMA producer (one elected lane) feeding a `stages`-deep
+// ring of (X tile, KRP tile) buffers guarded by full/empty mbarriers.
+// grid: (n_tiles, m_tiles, splits); block: 32 * (W + 1).
 template <int NT, bool TRANS>
-__global__ void __launch_bounds__(256, 1)
-root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const double* __restrict__ x,
-                 int use_tma, long long M, long long K, int R, int BM, int stages, KrpDev kd,
-                 long long k_per_split, double* __restrict__ out, long long out_split_stride) {
+__global__ void __launch_bounds__(288, 1)
+root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                 long long M, long long K, int R, int BM, int stages, long long k_per_split,
+                 double* __restrict__ out, long long out_split_stride) {
     constexpr int BN = 8 * NT;
     constexpr int BNS = krp_stride<TRANS>(BN);
     extern __shared__ __align__(1024) char smem_raw[];
-    char* smem = reinterpret_cast<char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+    const std::uint32_t raw = smem_u32(smem_raw);
+    const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
+    char* const smem = smem_raw + (base - raw);
     const int x_bytes = BM * kBK * 8;
     const int b_bytes = kBK * BNS * 8;
-    char* xs_base = smem;
-    double* bs_base = reinterpret_cast<double*>(smem + stages * x_bytes);
-    std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + stages * (x_bytes + b_bytes));
+    const int stage_bytes = x_bytes + b_bytes;
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + stages * stage_bytes);
+    std::uint64_t* empty = full + stages;
 
+    const int W = BM / 16;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2, t = lane & 3;
     const int n0 = blockIdx.x * BN;
     const long long m0 = static_cast<long long>(blockIdx.y) * BM;
     const long long kbeg = static_cast<long long>(blockIdx.z) * k_per_split;
     const long long kend = min(K, kbeg + k_per_split);
     const int nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
-    const int bn = min(BN, R - n0);
-
-    // NN: 2 boxes of (16 k) x BM rows.  TN: BM/16 boxes of (16 m) x BK rows.
     const int nboxes = TRANS ? BM / 16 : kBK / 16;
     const int box_rows = TRANS ? kBK : BM;
-    const unsigned stage_tx = static_cast<unsigned>(x_bytes);
 
-    if (threadIdx.x == 0 && use_tma) {
-        for (int s = 0; s < stages; ++s) mbar_init(&bars[s], 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], W);
+        }
         fence_barrier_init();
     }
     __syncthreads();
 
-    auto issue = [&](int kt, int s) {
-        const long long kk = kbeg + static_cast<long long>(kt) * kBK;
-        char* xs = xs_base + s * x_bytes;
-        if (use_tma) {
-            if (threadIdx.x == 0) {
-                mbar_expect_tx(&bars[s], stage_tx);
+    if (warp == W) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&xmap)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
+            for (int kt = 0; kt < nk; ++kt) {
+                const int s = kt % stages;
+                if (kt >= stages) mbar_wait(&empty[s], ((kt / stages) - 1) & 1);
+                const int kk = static_cast<int>(kbeg + static_cast<long long>(kt) * kBK);
+                char* xs = smem + s * stage_bytes;
+                mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
                 for (int b = 0; b < nboxes; ++b) {
                     if (TRANS)
-                        tma_load_2d(&xmap, &bars[s], xs + b * box_rows * 128,
-                                    static_cast<int>(m0 + 16 * b), static_cast<int>(kk));
+                        tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(m0 + 16 * b), kk);
                     else
-                        tma_load_2d(&xmap, &bars[s], xs + b * box_rows * 128,
-                                    static_cast<int>(kk + 16 * b), static_cast<int>(m0));
+                        tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, kk + 16 * b, static_cast<int>(m0));
                 }
+                tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, kk);
             }
-        } else {
-            if (TRANS)
-                load_x_manual<TRANS>(xs, x, K, M, kk, m0, box_rows, nboxes);
-            else
-                load_x_manual<TRANS>(xs, x, M, K, m0, kk, box_rows, nboxes);
         }
-        gen_krp_tile<BNS>(bs_base + s * (kBK * BNS), kd, kk, kend, n0, R, bn);
-    };
+        return;
+    }
 
+    // ---------------- DMMA consumers
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp * 16;
     double acc[NT][4];
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
-    const int pre = min(stages, nk);
-    for (int s = 0; s < pre; ++s) issue(s, s);
-    __syncthreads();
+    // per-lane constant parts of the fragment addresses
+    std::uint32_t aoff[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int mrow = wm + g + 8 * (i & 1);
+        if (!TRANS) {
+            aoff[i] = static_cast<std::uint32_t>(swz(mrow, t + 4 * (i >> 1)));
+        } else {
+            const int krow = kperm(t + 4 * (i >> 1));
+            aoff[i] = static_cast<std::uint32_t>((mrow >> 4) * kBK * 128 + swz(krow, mrow & 15));
+        }
+    }
+    std::uint32_t boff[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int krow = TRANS ? kperm(t + 4 * i) : t + 4 * i;
+        boff[i] = static_cast<std::uint32_t>((krow * BNS + g) * 8);
+    }
 
-    const int wm = warp * 16;  // warp's row strip inside the CTA tile
     for (int kt = 0; kt < nk; ++kt) {
         const int s = kt % stages;
-        if (use_tma) mbar_wait(&bars[s], (kt / stages) & 1);
-        const char* xs = xs_base + s * x_bytes;
-        const double* bs = bs_base + s * (kBK * BNS);
+        mbar_wait(&full[s], (kt / stages) & 1);
+        const std::uint32_t xs = base + s * stage_bytes;
+        const std::uint32_t bs = xs + x_bytes;
 #pragma unroll
         for (int ks = 0; ks < kBK / 16; ++ks) {
             double a[8];
+            // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
+            const std::uint32_t abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int mrow = wm + g + 8 * (i & 1);
-                if (!TRANS) {
-                    // X[m][k]: box ks holds k in [16ks,16ks+16), rows m
-                    const int kc = t + 4 * (i >> 1);
-                    a[i] = *reinterpret_cast<const double*>(xs + ks * BM * 128 + swz(mrow, kc));
-                } else {
-                    // X[k][m]: box (mrow/16) holds m cols; rows are k (permuted slots)
-                    const int krow = ks * 16 + kperm(t + 4 * (i >> 1));
-                    const int box = mrow >> 4;
-                    a[i] = *reinterpret_cast<const double*>(xs + box * kBK * 128 +
-                                                            swz(krow, mrow & 15));
-                }
-            }
+            for (int i = 0; i < 8; ++i) a[i] = lds64(abase + aoff[i]);
+            const std::uint32_t bb = bs + ks * 16 * BNS * 8;
 #pragma unroll
             for (int j = 0; j < NT; ++j) {
                 double b[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int krow = TRANS ? ks * 16 + kperm(t + 4 * i) : ks * 16 + t + 4 * i;
-                    b[i] = bs[krow * BNS + j * 8 + g];
-                }
+                for (int i = 0; i < 4; ++i) b[i] = lds64(bb + boff[i] + j * 64);
                 dmma16816(acc[j], a, b);
             }
         }
-        __syncthreads();
-        if (kt + stages < nk) {
-            if (use_tma) fence_proxy_async();
-            issue(kt + stages, s);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 
-    // epilogue: rows m0+wm+g(+8), cols n0+8j+2t(+1)
+    // epilogue: rows m0+wm+g(+8), cols n0+8j+2t(+1); 16-byte stores when aligned
     double* o = out + blockIdx.z * out_split_stride;
+    const bool vec = (R % 2) == 0;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
         const int col = n0 + 8 * j + 2 * t;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const long long row = m0 + wm + g + 8 * h;
-            if (row < M) {
-                if (col < R) o[row * R + col] = acc[j][2 * h];
-                if (col + 1 < R) o[row * R + col + 1] = acc[j][2 * h + 1];
+            if (row < M && col < R) {
+                double* dst = o + row * R + col;
+                if (vec) {
+                    *reinterpret_cast<double2*>(dst) = make_double2(acc[j][2 * h], acc[j][2 * h + 1]);
+                } else {
+                    dst[0] = acc[j][2 * h];
+                    if (col + 1 < R) dst[1] = acc[j][2 * h + 1];
+                }
             }
         }
     }
@@ -388,16 +376,16 @@ int pick_bm(long long M) {
 }
 
 template <bool TRANS>
-void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, const CUtensorMap& map,
-              const double* x, int use_tma, long long M, long long K, int R, int BM, int stages,
-              const KrpDev& kd, long long kps, double* out, long long oss) {
-#define CPK_CASE(NTV)                                                                         \
-    case NTV: {                                                                               \
-        auto fn = root_gemm_kernel<NTV, TRANS>;                                               \
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                                      static_cast<int>(smem)));                               \
-        fn<<<grid, block, smem, st>>>(map, x, use_tma, M, K, R, BM, stages, kd, kps, out, oss); ::cpkit::count_launch(1); \
-        break;                                                                                \
+void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, const CUtensorMap& xmap,
+              const CUtensorMap& kmap, long long M, long long K, int R, int BM, int stages, long long kps,
+              double* out, long long oss) {
+#define CPK_CASE(NTV)                                                                              \
+    case NTV: {                                                                                    \
+        auto fn = root_gemm_kernel<NTV, TRANS>;                                                    \
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
+                                      static_cast<int>(smem)));                                    \
+        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, BM, stages, kps, out, oss);             \
+        break;                                                                                     \
     }
     switch (nt) {
         CPK_CASE(1) CPK_CASE(2) CPK_CASE(3) CPK_CASE(4) CPK_CASE(5) CPK_CASE(6) CPK_CASE(7)
@@ -405,23 +393,20 @@ void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, 
         default: throw DeviceError("unsupported rank tile");
     }
 #undef CPK_CASE
+    count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
 
+int bns_of(int nt, bool trans) { return trans ? krp_stride<true>(8 * nt) : krp_stride<false>(8 * nt); }
+
 std::size_t smem_bytes(int BM, int nt, bool trans, int stages) {
-    const int bns = trans ? krp_stride<true>(8 * nt) : krp_stride<false>(8 * nt);
-    return static_cast<std::size_t>(stages) * (BM * kBK * 8 + kBK * bns * 8) + stages * 8 + 1024;
+    return static_cast<std::size_t>(stages) * (BM * kBK * 8 + kBK * bns_of(nt, trans) * 8) + stages * 16 + 1024;
 }
 
 int pick_stages(int BM, int nt, bool trans) {
-    for (int s = 4; s >= 2; --s)
-        if (smem_bytes(BM, nt, trans, s) <= 220 * 1024) return s;
+    for (int s = 6; s >= 2; --s)
+        if (smem_bytes(BM, nt, trans, s) <= 225 * 1024) return s;
     return 2;
-}
-
-bool tma_ok(const double* x, long long inner) {
-    return (inner % 2 == 0) && (reinterpret_cast<std::uintptr_t>(x) % 16 == 0) &&
-           inner < (1LL << 31);
 }
 
 struct FrontPlan {
@@ -434,30 +419,48 @@ FrontPlan plan_front(long long F, long long B, int R) {
     p.BM = pick_bm(B);
     p.mtiles = static_cast<int>((B + p.BM - 1) / p.BM);
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
-    const long long target = 2LL * num_sms();
+    const long long target = num_sms();
     const long long kchunks = (F + kBK - 1) / kBK;
     long long splits = std::max<long long>(1, (target + base - 1) / base);
     splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
-    p.kps = ((kchunks + splits - 1) / splits) * kBK;
+    p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
     p.splits = static_cast<int>((F + p.kps - 1) / p.kps);
     return p;
 }
 
+// Fill the KRP operand (K x Rs, Rs = R rounded to even) for a contraction.
+void fill_krp(const KrpDesc& kd, long long K, int R, double* krp, cudaStream_t st) {
+    const int Rs = (R + 1) & ~1;
+    const long long total = K * Rs;
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 16LL * num_sms()));
+    krp_fill_kernel<<<blocks, 256, 0, st>>>(to_dev(kd), K, R, Rs, krp);
+    count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
 }  // namespace
 
-void launch_root_back(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kb,
-                      double* pf, cudaStream_t st) {
+std::size_t krp_workspace_elems(std::int64_t rows, int R) {
+    return static_cast<std::size_t>(rows) * ((R + 1) & ~1);
+}
+
+// X is F x Bs row-major (Bs >= B, Bs even: the padded row stride).
+void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
+                      const KrpDesc& kb, double* krp, double* pf, cudaStream_t st) {
     int nt, ntiles;
     pick_nt(R, nt, ntiles);
     const int BM = pick_bm(F);
     const int stages = pick_stages(BM, nt, false);
-    const bool tma = tma_ok(x, B) && F < (1LL << 31);
-    CUtensorMap map{};
-    if (tma) map = make_map(x, B, F, BM);
+    const int Rs = (R + 1) & ~1;
+    fill_krp(kb, B, R, krp, st);
+    const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16,
+                                      static_cast<std::uint32_t>(BM), true);
+    const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(B),
+                                      static_cast<std::uint32_t>(bns_of(nt, false)), kBK, false);
     dim3 grid(ntiles, static_cast<unsigned>((F + BM - 1) / BM), 1);
     if (grid.y > 65535) throw LimitExceeded("root_back: too many row tiles");
-    dispatch<false>(nt, grid, dim3(2 * BM), smem_bytes(BM, nt, false, stages), st, map, x, tma, F, B,
-                    R, BM, stages, to_dev(kb), B, pf, 0);
+    dispatch<false>(nt, grid, dim3(32 * (BM / 16 + 1)), smem_bytes(BM, nt, false, stages), st, xmap, kmap, F, B,
+                    R, BM, stages, B, pf, 0);
 }
 
 std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R) {
@@ -465,13 +468,17 @@ std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R) {
     return p.splits > 1 ? static_cast<std::size_t>(p.splits) * B * R : 0;
 }
 
-void launch_root_front(const double* x, std::int64_t F, std::int64_t B, int R, const KrpDesc& kf,
-                       double* pb, double* ws, std::size_t ws_elems, cudaStream_t st) {
+void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
+                       const KrpDesc& kf, double* krp, double* pb, double* ws, std::size_t ws_elems,
+                       cudaStream_t st) {
     const FrontPlan p = plan_front(F, B, R);
     const int stages = pick_stages(p.BM, p.nt, true);
-    const bool tma = tma_ok(x, B) && F < (1LL << 31);
-    CUtensorMap map{};
-    if (tma) map = make_map(x, B, F, kBK);
+    const int Rs = (R + 1) & ~1;
+    fill_krp(kf, F, R, krp, st);
+    const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16, kBK,
+                                      true);
+    const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
+                                      static_cast<std::uint32_t>(bns_of(p.nt, true)), kBK, false);
     dim3 grid(p.ntiles, p.mtiles, p.splits);
     double* out = pb;
     long long oss = 0;
@@ -481,12 +488,13 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, int R, c
         out = ws;
         oss = B * R;
     }
-    dispatch<true>(p.nt, grid, dim3(2 * p.BM), smem_bytes(p.BM, p.nt, true, stages), st, map, x, tma,
-                   B, F, R, p.BM, stages, to_dev(kf), p.kps, out, oss);
+    dispatch<true>(p.nt, grid, dim3(32 * (p.BM / 16 + 1)), smem_bytes(p.BM, p.nt, true, stages), st, xmap, kmap,
+                   B, F, R, p.BM, stages, p.kps, out, oss);
     if (p.splits > 1) {
         const long long n = B * static_cast<long long>(R);
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
-        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, pb); ::cpkit::count_launch(1);
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, pb);
+        count_launch(1);
         CPK_CUDA(cudaGetLastError());
     }
 }

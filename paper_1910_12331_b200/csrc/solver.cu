@@ -337,13 +337,16 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     for (int n = 0; n < h_; ++n) F_ *= local_rows_[n];
     for (int n = h_; n < N; ++n) Bl_ *= local_rows_[n];
     local_elems_ = static_cast<std::uint64_t>(F_) * static_cast<std::uint64_t>(Bl_);
+    Bs_ = (Bl_ % 2 == 0) ? Bl_ : Bl_ + 1;  // TMA needs 16-byte row strides: pad odd rows once
 
     off_.assign(N + 1, 0);
     for (int n = 0; n < N; ++n) off_[n + 1] = off_[n] + static_cast<std::int64_t>(dims_[n]) * R_;
     const std::size_t S = static_cast<std::size_t>(off_[N]);
     const std::size_t RR = static_cast<std::size_t>(R_) * R_;
 
-    x_.resize(local_elems_);
+    x_.resize(static_cast<std::size_t>(F_) * static_cast<std::size_t>(Bs_));
+    if (Bs_ != Bl_) CPK_CUDA(cudaMemset(x_.get(), 0, x_.size() * sizeof(double)));
+    krp_.resize(krp_workspace_elems(std::max(F_, Bl_), R_));
     A_.resize(S); Atrial_.resize(S); M_.resize(S); G_.resize(S); V_.resize(S); Z_.resize(S); Q_.resize(S);
     for (int i = 0; i < 2; ++i) { Rr_[i].resize(S); W_[i].resize(S); }
     PF_.resize(static_cast<std::size_t>(F_) * R_);
@@ -366,7 +369,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     for (auto d : dims_) smax = std::max<std::int64_t>(smax, static_cast<std::int64_t>(d));
     anew_.resize(static_cast<std::size_t>(smax) * R_);
     scal_.resize(kNScal);
-    partials_.resize(std::max(4096, norm2_parts(local_elems_) + 8));
+    partials_.resize(std::max(4096, 2 * norm2_parts(static_cast<std::uint64_t>(F_) * Bs_) + 8));
     status_.resize(std::max(N, 1));
     cgres_.resize(8);
     flag_.resize(4);
@@ -400,9 +403,22 @@ KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) 
 }
 
 void DeviceProblem::upload_tensor(const double* host_local) {
-    CPK_CUDA(cudaMemcpyAsync(x_.get(), host_local, local_elems_ * sizeof(double), cudaMemcpyHostToDevice,
-                             ctx_.stream));
+    if (Bs_ == Bl_)
+        CPK_CUDA(cudaMemcpyAsync(x_.get(), host_local, local_elems_ * sizeof(double), cudaMemcpyHostToDevice,
+                                 ctx_.stream));
+    else
+        CPK_CUDA(cudaMemcpy2DAsync(x_.get(), Bs_ * sizeof(double), host_local, Bl_ * sizeof(double),
+                                   Bl_ * sizeof(double), F_, cudaMemcpyHostToDevice, ctx_.stream));
     invalidate_all();
+}
+void DeviceProblem::download_tensor(double* host_local) {
+    if (Bs_ == Bl_)
+        CPK_CUDA(cudaMemcpyAsync(host_local, x_.get(), local_elems_ * sizeof(double), cudaMemcpyDeviceToHost,
+                                 ctx_.stream));
+    else
+        CPK_CUDA(cudaMemcpy2DAsync(host_local, Bl_ * sizeof(double), x_.get(), Bs_ * sizeof(double),
+                                   Bl_ * sizeof(double), F_, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
 }
 
 // Device-side low-rank (+ noise) generation: the reference's reconstruct
@@ -414,20 +430,29 @@ void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noi
     KrpDesc all = krp(0, N, A_.get(), true);
     // global flat offset of the local slab is not contiguous when sharded; generate
     // slab-local entries through a local descriptor (last factor already offset).
-    launch_reconstruct(all, R_, x_.get(), 0, local_elems_, ctx_.stream);
+    DevBuf<double> dense;
+    double* xd = x_.get();
+    if (Bs_ != Bl_) {
+        dense.resize(local_elems_);
+        xd = dense.get();
+    }
+    launch_reconstruct(all, R_, xd, 0, local_elems_, ctx_.stream);
     if (noise_rel > 0.0) {
         // noise E ~ N(0,1) (keyed, stream 0x4E01), scaled to noise_rel * ||X|| / ||E||
         DevBuf<double> e(local_elems_);
         launch_gaussian_fill(noise_seed, 0x4E01, e.get(), local_elems_, slab_hi_ - slab_lo_, dims_[N - 1], slab_lo_,
                              ctx_.stream);
         const int parts = norm2_parts(local_elems_);
-        launch_norm2(x_.get(), local_elems_, partials_.get(), parts, scal_.get() + 8, ctx_.stream);
+        launch_norm2(xd, local_elems_, partials_.get(), parts, scal_.get() + 8, ctx_.stream);
         launch_norm2(e.get(), local_elems_, partials_.get() + parts, parts, scal_.get() + 9, ctx_.stream);
         if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + 8, 2, ctx_.stream);
-        launch_scaled_add(x_.get(), e.get(), scal_.get() + 8, scal_.get() + 9, noise_rel, local_elems_,
+        launch_scaled_add(xd, e.get(), scal_.get() + 8, scal_.get() + 9, noise_rel, local_elems_,
                           ctx_.stream);
-        ctx_.sync();
     }
+    if (Bs_ != Bl_)
+        CPK_CUDA(cudaMemcpy2DAsync(x_.get(), Bs_ * sizeof(double), xd, Bl_ * sizeof(double), Bl_ * sizeof(double),
+                                   F_, cudaMemcpyDeviceToDevice, ctx_.stream));
+    ctx_.sync();
     invalidate_all();
 }
 
@@ -469,8 +494,8 @@ double DeviceProblem::read_scalar(int idx) {
 }
 
 double DeviceProblem::norm2() {
-    launch_norm2(x_.get(), local_elems_, partials_.get(), norm2_parts(local_elems_), scal_.get() + kXnorm,
-                 ctx_.stream);
+    const std::uint64_t stored = static_cast<std::uint64_t>(F_) * static_cast<std::uint64_t>(Bs_);  // pad is zero
+    launch_norm2(x_.get(), stored, partials_.get(), norm2_parts(stored), scal_.get() + kXnorm, ctx_.stream);
     if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + kXnorm, 1, ctx_.stream);
     return read_scalar(kXnorm);
 }
@@ -515,15 +540,15 @@ void DeviceProblem::profile_read(double* ms, int* count) {
 void DeviceProblem::root_back() {
     const int N = order();
     prof_begin(kProfBack);
-    launch_root_back(x_.get(), F_, Bl_, R_, krp(h_, N, A_.get(), true), PF_.get(), ctx_.stream);
+    launch_root_back(x_.get(), F_, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get(), ctx_.stream);
     prof_end();
     ++contractions_;
     pf_valid_ = true;
 }
 void DeviceProblem::root_front() {
     prof_begin(kProfFront);
-    launch_root_front(x_.get(), F_, Bl_, R_, krp(0, h_, A_.get(), false), PB_.get(), ws_.get(), ws_.size(),
-                      ctx_.stream);
+    launch_root_front(x_.get(), F_, Bl_, Bs_, R_, krp(0, h_, A_.get(), false), krp_.get(), PB_.get(), ws_.get(),
+                      ws_.size(), ctx_.stream);
     prof_end();
     ++contractions_;
     pb_valid_ = true;

@@ -178,6 +178,7 @@ public:
     void upload_tensor(const double* host_local);          // H2D copy of the local slab
     void generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel);
     double* tensor_device() { return x_.get(); }
+    void download_tensor(double* host_local);
     std::uint64_t local_elems() const { return local_elems_; }
 
     int order() const { return static_cast<int>(dims_.size()); }
@@ -251,11 +252,11 @@ private:
     std::vector<std::uint64_t> dims_;
     int R_ = 0, h_ = 0;
     std::uint64_t slab_lo_ = 0, slab_hi_ = 0, local_elems_ = 0;
-    std::int64_t F_ = 0, Bl_ = 0;                    // local matrix view F x B_local
+    std::int64_t F_ = 0, Bl_ = 0, Bs_ = 0;           // local matrix view F x B_local, row stride Bs
     std::vector<std::int64_t> off_;                  // stacked offsets (elements)
     DevBuf<double> x_;
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
-    DevBuf<double> PF_, PB_, ws_;
+    DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
     int contractions_ = 0;
     DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_;
