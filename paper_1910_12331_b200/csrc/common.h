@@ -112,9 +112,11 @@ std::size_t reduce_kept_workspace_elems(const KrpDesc& kept, int keep, int R);
 void launch_norm2(const double* x, std::uint64_t n, double* partials, int nparts, double* out,
                   cudaStream_t st);
 int norm2_parts(std::uint64_t n);
-// grams of modes [lo, hi): factor n at base + offs[n] (device arrays), rows[n]
+// grams of modes [lo, hi): factor n at base + offs[n] (device arrays), rows[n];
+// ws holds gram_workspace_elems(hi - lo, R, max rows) doubles.
+std::size_t gram_workspace_elems(int nmodes, int R, std::int64_t smax);
 void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
-                  int hi, int R, double* grams, cudaStream_t st);
+                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st);
 // pair[(n*order+p)] = Hadamard over grams m not in {n,p} ascending (kruskal.cpp:42-65)
 void launch_gamma_pairs(const double* grams, int order, int R, double* pair, cudaStream_t st);
 // gamma_one = Hadamard over grams m != n (als.cpp:34-37)

@@ -97,60 +97,93 @@ __global__ void chol_kernel(const double* __restrict__ s_all, int R, double lamb
     if (threadIdx.x == 0) status[mat] = st;
 }
 
-// One warp per rhs row: solve (L L^T) y = b; L packed lower (R(R+1)/2).
-// Lane q owns entries k = q + 32*c, c < kMaxPer.
+// One warp per rhs row: solve (L L^T) y = b; L packed lower (R(R+1)/2),
+// staged once per CTA in shared memory (every row of a CTA uses the same L).
+// Lane q owns entries k = q + 32*c, c < kMaxPer, in registers.
 constexpr int kMaxPer = 16;  // R <= 512
-__global__ void chol_solve_rows_kernel(const double* __restrict__ l, int R,
-                                       const double* __restrict__ b, long long rows,
-                                       double* __restrict__ y, long long l_stride, int nmats,
-                                       long long rows_per_mat) {
-    const int lane = threadIdx.x & 31;
-    const long long row = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
-    if (row >= rows) return;
-    const double* L = l + (nmats > 1 ? (row / rows_per_mat) * l_stride : 0);
-    double v[kMaxPer];
-#pragma unroll
-    for (int c = 0; c < kMaxPer; ++c) {
-        const int k = lane + 32 * c;
-        v[c] = (k < R) ? b[row * R + k] : 0.0;
+constexpr int kSolveWarps = 8;
+template <bool kSmem>
+__global__ void __launch_bounds__(32 * kSolveWarps)
+chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __restrict__ b, long long rows,
+                       double* __restrict__ y, long long l_stride, long long rows_per_mat) {
+    extern __shared__ double lsh[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long mat = blockIdx.y;
+    const double* Lg = l_all + mat * l_stride;
+    const long long np = static_cast<long long>(R) * (R + 1) / 2;
+    if (kSmem) {
+        for (long long e = threadIdx.x; e < np; e += blockDim.x) lsh[e] = Lg[e];
+        __syncthreads();
     }
-    // forward: z_i = v_i / L_ii ; v_k -= L_ki z_i (k > i)
-    for (int i = 0; i < R; ++i) {
-        const int owner = i & 31, ci = i >> 5;
-        double vi = 0.0;
-#pragma unroll
-        for (int c = 0; c < kMaxPer; ++c)
-            if (c == ci) vi = v[c];
-        vi = __shfl_sync(0xffffffffu, vi, owner);
-        const double zi = vi / __ldg(&L[pk(i, i)]);
+    const double* L = kSmem ? lsh : Lg;
+    for (long long local = blockIdx.x * kSolveWarps + warp; local < rows_per_mat;
+         local += static_cast<long long>(gridDim.x) * kSolveWarps) {
+        const long long row = mat * rows_per_mat + local;
+        if (row >= rows) break;
+        double v[kMaxPer];
 #pragma unroll
         for (int c = 0; c < kMaxPer; ++c) {
             const int k = lane + 32 * c;
-            if (k == i) v[c] = zi;
-            else if (k > i && k < R) v[c] -= __ldg(&L[pk(k, i)]) * zi;
+            v[c] = (k < R) ? b[row * R + k] : 0.0;
         }
-    }
-    // backward with L^T: y_i = v_i / L_ii ; v_k -= L_ik y_i (k < i)
-    for (int i = R - 1; i >= 0; --i) {
-        const int owner = i & 31, ci = i >> 5;
-        double vi = 0.0;
+        // forward: z_i = v_i / L_ii ; v_k -= L_ki z_i (k > i)
+        for (int i = 0; i < R; ++i) {
+            const int owner = i & 31, ci = i >> 5;
+            double vi = 0.0;
 #pragma unroll
-        for (int c = 0; c < kMaxPer; ++c)
-            if (c == ci) vi = v[c];
-        vi = __shfl_sync(0xffffffffu, vi, owner);
-        const double yi = vi / __ldg(&L[pk(i, i)]);
+            for (int c = 0; c < kMaxPer; ++c)
+                if (c == ci) vi = v[c];
+            vi = __shfl_sync(0xffffffffu, vi, owner);
+            const double zi = vi / L[pk(i, i)];
+#pragma unroll
+            for (int c = 0; c < kMaxPer; ++c) {
+                const int k = lane + 32 * c;
+                if (k == i) v[c] = zi;
+                else if (k > i && k < R) v[c] -= L[pk(k, i)] * zi;
+            }
+        }
+        // backward with L^T: y_i = v_i / L_ii ; v_k -= L_ik y_i (k < i)
+        for (int i = R - 1; i >= 0; --i) {
+            const int owner = i & 31, ci = i >> 5;
+            double vi = 0.0;
+#pragma unroll
+            for (int c = 0; c < kMaxPer; ++c)
+                if (c == ci) vi = v[c];
+            vi = __shfl_sync(0xffffffffu, vi, owner);
+            const double yi = vi / L[pk(i, i)];
+#pragma unroll
+            for (int c = 0; c < kMaxPer; ++c) {
+                const int k = lane + 32 * c;
+                if (k == i) v[c] = yi;
+                else if (k < i) v[c] -= L[pk(i, k)] * yi;
+            }
+        }
 #pragma unroll
         for (int c = 0; c < kMaxPer; ++c) {
             const int k = lane + 32 * c;
-            if (k == i) v[c] = yi;
-            else if (k < i) v[c] -= __ldg(&L[pk(i, k)]) * yi;
+            if (k < R) y[row * R + k] = v[c];
         }
     }
-#pragma unroll
-    for (int c = 0; c < kMaxPer; ++c) {
-        const int k = lane + 32 * c;
-        if (k < R) y[row * R + k] = v[c];
+}
+
+void solve_rows(const double* l, int R, const double* b, long long rows, double* y, long long l_stride,
+                int nmats, long long rows_per_mat, cudaStream_t st) {
+    const std::size_t np = static_cast<std::size_t>(R) * (R + 1) / 2;
+    const bool smem = np * 8 <= 200 * 1024;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const long long per_mat_ctas = std::max<long long>(
+        1, std::min<long long>((rows_per_mat + kSolveWarps - 1) / kSolveWarps, std::max(1, 2 * sms / nmats)));
+    dim3 grid(static_cast<unsigned>(per_mat_ctas), nmats);
+    if (smem) {
+        CPK_CUDA(cudaFuncSetAttribute(chol_solve_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(np * 8)));
+        chol_solve_rows_kernel<true><<<grid, 32 * kSolveWarps, np * 8, st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+    } else {
+        chol_solve_rows_kernel<false><<<grid, 32 * kSolveWarps, 0, st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
     }
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
 }
 
 __global__ void identity_rows_kernel(double* __restrict__ out, int count, int R) {
@@ -191,10 +224,7 @@ void launch_chol_batch(const double* s, int count, int R, const double* lambda, 
 
 void launch_chol_solve_rows(const double* l, int R, const double* b, std::int64_t rows, double* y,
                             cudaStream_t st) {
-    const long long threads = rows * 32;
-    const int blocks = static_cast<int>((threads + 255) / 256);
-    chol_solve_rows_kernel<<<blocks, 256, 0, st>>>(l, R, b, rows, y, 0, 1, rows); ::cpkit::count_launch(1);
-    CPK_CUDA(cudaGetLastError());
+    solve_rows(l, R, b, rows, y, 0, 1, rows, st);
 }
 
 void launch_chol_inverse_batch(const double* l, int count, int R, double* inv, double* tmp,
@@ -205,8 +235,7 @@ void launch_chol_inverse_batch(const double* l, int count, int R, double* inv, d
     identity_rows_kernel<<<g, 256, 0, st>>>(inv, count, R); ::cpkit::count_launch(1);
     const long long rows = static_cast<long long>(count) * R;
     const long long np = static_cast<long long>(R) * (R + 1) / 2;
-    chol_solve_rows_kernel<<<static_cast<int>((rows * 32 + 255) / 256), 256, 0, st>>>(
-        l, R, inv, rows, tmp, np, count, R); ::cpkit::count_launch(1);
+    solve_rows(l, R, inv, rows, tmp, np, count, R, st);
     symmetrize_kernel<<<g, 256, 0, st>>>(tmp, count, R, inv); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }

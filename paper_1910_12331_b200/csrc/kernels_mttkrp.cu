@@ -403,9 +403,12 @@ std::size_t smem_bytes(int BM, int nt, bool trans, int stages) {
     return static_cast<std::size_t>(stages) * (BM * kBK * 8 + kBK * bns_of(nt, trans) * 8) + stages * 16 + 1024;
 }
 
+// Pipeline depth: as deep as shared memory allows; small CTAs (<= 5 DMMA
+// warps) keep two CTAs resident per SM so >= 10 warps feed the DMMA pipe.
 int pick_stages(int BM, int nt, bool trans) {
+    const std::size_t budget = (BM / 16 <= 5 ? 112 : 225) * 1024;
     for (int s = 6; s >= 2; --s)
-        if (smem_bytes(BM, nt, trans, s) <= 225 * 1024) return s;
+        if (smem_bytes(BM, nt, trans, s) <= budget) return s;
     return 2;
 }
 
@@ -502,52 +505,84 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
 // ---------------------------------------------------------------- second level
 // out[i, r] = sum over all other kept indices of P[idx, r] * prod_{l != keep} A_l[idx_l, r]
 // (the descending mode-at-a-time contraction of mttkrp.cpp:118-126/:63-75,
-// done in one pass). P is [outer][s_keep][inner][R]. One CTA per (i, split);
-// threads stride over r; each CTA sums its (outer x inner) range in order.
+// done in one pass). P is [outer][s_keep][inner][R]. HBM-bound: one CTA per
+// (i, split), threads over (q-lane, r) with 4 independent loads in flight
+// each; q-lanes and splits are combined in a fixed order (deterministic).
 namespace {
-__global__ void reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep, int R,
-                                   long long outer, long long sk, long long inner, int splits,
-                                   double* __restrict__ out, long long out_split_stride) {
+constexpr int kRedT = 256;
+__device__ __forceinline__ double kept_weight(const KrpDev& kd, int keep, long long o, long long in, int r,
+                                              int R) {
+    double w = 1.0;
+    long long rem = in;
+    for (int l = kd.nmodes - 1; l > keep; --l) {
+        const long long e = kd.ext[l];
+        w *= kd.fac[l][(rem % e) * R + r];
+        rem /= e;
+    }
+    rem = o;
+    for (int l = keep - 1; l >= 0; --l) {
+        const long long e = kd.ext[l];
+        w *= kd.fac[l][(rem % e) * R + r];
+        rem /= e;
+    }
+    return w;
+}
+__global__ void __launch_bounds__(kRedT) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
+                                                             int R, long long outer, long long sk, long long inner,
+                                                             int splits, double* __restrict__ out,
+                                                             long long out_split_stride) {
+    __shared__ double red[kRedT];
     const long long i = blockIdx.x;
     const int split = blockIdx.y;
+    const int rpad = min(kRedT, ((R + 31) / 32) * 32);
+    const int qlanes = kRedT / rpad;
+    const int ql = threadIdx.x / rpad;
+    const int rr = threadIdx.x % rpad;
     const long long total = outer * inner;
     const long long per = (total + splits - 1) / splits;
     const long long lo = split * per, hi = min(total, lo + per);
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    // fast paths for two kept modes: the weight is one factor row
+    const bool two = kd.nmodes == 2;
+    const double* wfac = two ? kd.fac[keep == 0 ? 1 : 0] : nullptr;
+    for (int r0 = 0; r0 < R; r0 += rpad) {
+        const int r = r0 + rr;
         double acc = 0.0;
-        for (long long q = lo; q < hi; ++q) {
-            const long long o = q / inner, in = q % inner;
-            const double* src = p + ((o * sk + i) * inner + in) * R;
-            // weight = prod over kept modes l != keep (decompose o and in)
-            double w = 1.0;
-            long long rem = in;
-            for (int l = kd.nmodes - 1; l > keep; --l) {
-                const long long e = kd.ext[l];
-                w *= kd.fac[l][(rem % e) * R + r];
-                rem /= e;
+        if (ql < qlanes && r < R) {
+            long long q = lo + ql;
+            long long o = q / inner, in = q % inner;
+            const long long step_o = qlanes / inner, step_in = qlanes % inner;
+            double a0 = 0.0, a1 = 0.0;
+            int par = 0;
+            for (; q < hi; q += qlanes) {
+                const double v = __ldcs(p + ((o * sk + i) * inner + in) * R + r);
+                const double w = two ? __ldg(wfac + (keep == 0 ? in : o) * R + r)
+                                     : kept_weight(kd, keep, o, in, r, R);
+                if (par) a1 += v * w; else a0 += v * w;
+                par ^= 1;
+                in += step_in;
+                o += step_o;
+                if (in >= inner) { in -= inner; ++o; }
             }
-            rem = o;
-            for (int l = keep - 1; l >= 0; --l) {
-                const long long e = kd.ext[l];
-                w *= kd.fac[l][(rem % e) * R + r];
-                rem /= e;
-            }
-            acc += src[r] * w;
+            acc = a0 + a1;
         }
-        out[split * out_split_stride + i * R + r] = acc;
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < rpad && r < R) {
+            double sum = 0.0;
+            for (int l = 0; l < qlanes; ++l) sum += red[l * rpad + threadIdx.x];
+            out[split * out_split_stride + i * R + r] = sum;
+        }
+        __syncthreads();
     }
 }
-}  // namespace
-
-namespace {
 int reduce_splits(const KrpDesc& kept, int keep) {
-    long long sk = kept.ext[keep];
+    const long long sk = kept.ext[keep];
     long long total = 1;
     for (int l = 0; l < kept.nmodes; ++l)
         if (l != keep) total *= kept.ext[l];
-    const long long target = 2LL * num_sms();
+    const long long target = 8LL * num_sms();
     long long s = std::max<long long>(1, (target + sk - 1) / sk);
-    s = std::min<long long>(s, std::max<long long>(1, total / 8));
+    s = std::min<long long>(s, std::max<long long>(1, total / 32));
     return static_cast<int>(s);
 }
 }  // namespace
@@ -557,28 +592,27 @@ std::size_t reduce_kept_workspace_elems(const KrpDesc& kept, int keep, int R) {
     return s > 1 ? static_cast<std::size_t>(s) * kept.ext[keep] * R : 0;
 }
 
-void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, double* out,
-                        double* ws, std::size_t ws_elems, cudaStream_t st) {
+void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, double* out, double* ws,
+                        std::size_t ws_elems, cudaStream_t st) {
     long long outer = 1, inner = 1;
     for (int l = 0; l < keep; ++l) outer *= kept.ext[l];
     for (int l = keep + 1; l < kept.nmodes; ++l) inner *= kept.ext[l];
     const long long sk = kept.ext[keep];
     const int splits = reduce_splits(kept, keep);
-    const int threads = R >= 128 ? 128 : ((R + 31) / 32) * 32;
     double* dst = out;
     if (splits > 1) {
-        if (ws_elems < static_cast<std::size_t>(splits) * sk * R)
-            throw DeviceError("reduce_kept: workspace too small");
+        if (ws_elems < static_cast<std::size_t>(splits) * sk * R) throw DeviceError("reduce_kept: workspace too small");
         dst = ws;
     }
     dim3 grid(static_cast<unsigned>(sk), splits);
-    reduce_kept_kernel<<<grid, threads, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits,
-                                                 dst, sk * R); ::cpkit::count_launch(1);
+    reduce_kept_kernel<<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
+    count_launch(1);
     CPK_CUDA(cudaGetLastError());
     if (splits > 1) {
         const long long n = sk * R;
-        splitk_reduce_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 1024)), 256, 0,
-                               st>>>(ws, splits, n, out); ::cpkit::count_launch(1);
+        splitk_reduce_kernel<<<static_cast<int>(std::min<long long>((n + 255) / 256, 1024)), 256, 0, st>>>(ws, splits,
+                                                                                                           n, out);
+        count_launch(1);
         CPK_CUDA(cudaGetLastError());
     }
 }

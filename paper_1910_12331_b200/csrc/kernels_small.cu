@@ -6,6 +6,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "tile_gemm.cuh"
 
 namespace cpkit {
 
@@ -62,27 +63,67 @@ __global__ void sum_partials_kernel(const double* __restrict__ partials, int n, 
 }
 
 // ---- Gram S = A^T A with exact symmetry (matrix_ops.cpp:30-34).
-// One thread per (r <= z) entry, sequential sum over rows; modes [lo, hi).
-__global__ void grams_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
-                             const long long* __restrict__ rows, int lo, int R,
-                             double* __restrict__ grams) {
-    const int n = lo + blockIdx.y;
-    const double* a = base + offs[n];
-    const long long s = rows[n];
-    double* out = grams + static_cast<long long>(n) * R * R;
-    const int tri = R * (R + 1) / 2;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tri; e += gridDim.x * blockDim.x) {
-        // map e -> (r, z) with r <= z, row-major over the upper triangle
-        int r = 0, rem = e;
-        while (rem >= R - r) {
-            rem -= R - r;
-            ++r;
-        }
-        const int z = r + rem;
+// DMMA 32x32 tiles of the upper triangle, split over row chunks; the
+// finalize pass sums the chunks in order and mirrors r <= z, so S is
+// bitwise symmetric and deterministic.
+constexpr int kGramChunk = 64;
+__global__ void __launch_bounds__(tile::kThreads)
+gram_tiles_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
+                  const long long* __restrict__ rows, int lo, int nmodes, int R, int nsplit,
+                  double* __restrict__ partial) {
+    __shared__ tile::Smem sm;
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const int tri = tr * (tr + 1) / 2;
+    const int tasks = nmodes * tri * nsplit;
+    for (int task = blockIdx.x; task < tasks; task += gridDim.x) {
+        int rem = task;
+        const int sp = rem % nsplit; rem /= nsplit;
+        int tt = rem % tri; rem /= tri;
+        const int n = lo + rem;
+        int rt = 0;
+        while (tt >= tr - rt) { tt -= tr - rt; ++rt; }
+        const int zt = rt + tt;
+        const double* a = base + offs[n];
+        const long long s = rows[n];
+        const long long per = (s + nsplit - 1) / nsplit;
+        const long long i0 = sp * per, i1 = min(s, i0 + per);
+        const int K = static_cast<int>(max(0LL, i1 - i0));
+        const int r0 = rt * tile::kT, z0 = zt * tile::kT;
+        auto la = [&](int row, int k) -> double {
+            const int r = r0 + row;
+            return r < R ? a[(i0 + k) * R + r] : 0.0;
+        };
+        auto lb = [&](int k, int col) -> double {
+            const int z = z0 + col;
+            return z < R ? a[(i0 + k) * R + z] : 0.0;
+        };
+        double acc[4];
+        tile::tile_gemm(sm, K, la, lb, acc);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int g = lane >> 2, t = lane & 3;
+        double* out = partial + (static_cast<long long>(n - lo) * nsplit + sp) * R * R;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int r = r0 + (warp >> 2) * 16 + g + 8 * h;
+                const int z = z0 + (warp & 3) * 8 + 2 * t + c;
+                if (r < R && z < R && r <= z) out[r * R + z] = acc[2 * h + c];
+            }
+    }
+}
+__global__ void gram_finalize_kernel(const double* __restrict__ partial, int lo, int nmodes, int R,
+                                     int nsplit, double* __restrict__ grams) {
+    const long long RR = static_cast<long long>(R) * R;
+    const long long total = nmodes * RR;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long n = e / RR, w = e % RR;
+        const int r = static_cast<int>(w / R), z = static_cast<int>(w % R);
+        const int a = min(r, z), b = max(r, z);
         double acc = 0.0;
-        for (long long i = 0; i < s; ++i) acc += a[i * R + r] * a[i * R + z];
-        out[r * R + z] = acc;
-        out[z * R + r] = acc;
+        for (int sp = 0; sp < nsplit; ++sp) acc += partial[(n * nsplit + sp) * RR + a * R + b];
+        grams[(lo + n) * RR + w] = acc;
     }
 }
 
@@ -158,18 +199,37 @@ __global__ void residual_final_kernel(const double* __restrict__ partials, int n
     }
 }
 
-// G = A * Gamma - M   (s x R) (R x R)
-__global__ void gradient_kernel(const double* __restrict__ a, const double* __restrict__ gnn,
-                                const double* __restrict__ m, long long rows, int R,
-                                double* __restrict__ g) {
-    const long long total = rows * R;
-    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long i = e / R;
-        const int r = static_cast<int>(e % R);
-        double acc = 0.0;
-        for (int z = 0; z < R; ++z) acc += a[i * R + z] * gnn[z * R + r];
-        g[e] = acc - m[e];
+// G = A * Gamma - M   (s x R) (R x R), DMMA tiles with the subtraction in the epilogue
+__global__ void __launch_bounds__(tile::kThreads)
+gradient_kernel(const double* __restrict__ a, const double* __restrict__ gnn,
+                const double* __restrict__ m, long long rows, int R, double* __restrict__ g) {
+    __shared__ tile::Smem sm;
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const long long rt_n = (rows + tile::kT - 1) / tile::kT;
+    const long long tasks = rt_n * tr;
+    for (long long task = blockIdx.x; task < tasks; task += gridDim.x) {
+        const long long i0 = (task / tr) * tile::kT;
+        const int c0 = static_cast<int>(task % tr) * tile::kT;
+        auto la = [&](int row, int k) -> double {
+            const long long i = i0 + row;
+            return i < rows ? a[i * R + k] : 0.0;
+        };
+        auto lb = [&](int k, int col) -> double {
+            const int c = c0 + col;
+            return c < R ? gnn[k * R + c] : 0.0;
+        };
+        double acc[4];
+        tile::tile_gemm(sm, R, la, lb, acc);
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const int gg = lane >> 2, t = lane & 3;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long i = i0 + (warp >> 2) * 16 + gg + 8 * h;
+                const int col = c0 + (warp & 3) * 8 + 2 * t + c;
+                if (i < rows && col < R) g[i * R + col] = acc[2 * h + c] - m[i * R + col];
+            }
     }
 }
 
@@ -321,12 +381,22 @@ void launch_norm2(const double* x, std::uint64_t n, double* partials, int nparts
     CPK_CUDA(cudaGetLastError());
 }
 
+int gram_splits(std::int64_t smax) {
+    return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(32, (smax + kGramChunk - 1) / kGramChunk)));
+}
+std::size_t gram_workspace_elems(int nmodes, int R, std::int64_t smax) {
+    return static_cast<std::size_t>(nmodes) * gram_splits(smax) * R * R;
+}
 void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
-                  int hi, int R, double* grams, cudaStream_t st) {
-    const int tri = R * (R + 1) / 2;
-    dim3 grid(std::max(1, std::min((tri + 127) / 128, 256)), hi - lo);
-    grams_kernel<<<grid, 128, 0, st>>>(base, reinterpret_cast<const long long*>(offs),
-                                       reinterpret_cast<const long long*>(rows), lo, R, grams); ::cpkit::count_launch(1);
+                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st) {
+    const int nsplit = gram_splits(smax);
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const int tasks = (hi - lo) * tr * (tr + 1) / 2 * nsplit;
+    gram_tiles_kernel<<<std::min(tasks, 4 * 148), tile::kThreads, 0, st>>>(
+        base, reinterpret_cast<const long long*>(offs), reinterpret_cast<const long long*>(rows), lo, hi - lo, R,
+        nsplit, ws); ::cpkit::count_launch(1);
+    const long long total = static_cast<long long>(hi - lo) * R * R;
+    gram_finalize_kernel<<<grid_for(total, 256, 592), 256, 0, st>>>(ws, lo, hi - lo, R, nsplit, grams); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
 
@@ -357,8 +427,9 @@ void launch_residual(const double* m_last, const double* a_last, std::int64_t ro
 
 void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
                      double* g, cudaStream_t st) {
-    const long long n = rows * static_cast<long long>(R);
-    gradient_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(a, gnn, m, rows, R, g); ::cpkit::count_launch(1);
+    const long long tasks = ((rows + tile::kT - 1) / tile::kT) * ((R + tile::kT - 1) / tile::kT);
+    gradient_kernel<<<static_cast<int>(std::min<long long>(tasks, 4 * 148)), tile::kThreads, 0, st>>>(
+        a, gnn, m, rows, R, g); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
 

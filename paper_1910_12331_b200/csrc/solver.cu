@@ -368,6 +368,8 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     std::int64_t smax = 1;
     for (auto d : dims_) smax = std::max<std::int64_t>(smax, static_cast<std::int64_t>(d));
     anew_.resize(static_cast<std::size_t>(smax) * R_);
+    smax_ = smax;
+    gram_ws_.resize(gram_workspace_elems(N, R_, smax));
     scal_.resize(kNScal);
     partials_.resize(std::max(4096, 2 * norm2_parts(static_cast<std::uint64_t>(F_) * Bs_) + 8));
     status_.resize(std::max(N, 1));
@@ -631,7 +633,8 @@ void DeviceProblem::compute_all_mttkrp() {
 
 // ---- Gamma set / residual / gradient --------------------------------------
 void DeviceProblem::grams_all() {
-    launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), 0, order(), R_, grams_.get(), ctx_.stream);
+    launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), 0, order(), R_, smax_, gram_ws_.get(), grams_.get(),
+                 ctx_.stream);
 }
 void DeviceProblem::build_gamma_set() {
     grams_all();
@@ -804,7 +807,8 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
         CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], anew_.get(), rows * R_ * sizeof(double),
                                  cudaMemcpyDeviceToDevice, ctx_.stream));
         note_factor_update(n);
-        launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), n, n + 1, R_, grams_.get(), ctx_.stream);
+        launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), n, n + 1, R_, smax_, gram_ws_.get(), grams_.get(),
+                     ctx_.stream);
     }
     (void)RR;
     AlsSweepDiag diag;

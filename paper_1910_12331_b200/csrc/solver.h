@@ -259,7 +259,8 @@ private:
     DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
     int contractions_ = 0;
-    DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_;
+    DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_, gram_ws_;
+    std::int64_t smax_ = 1;
     DevBuf<double> scal_, partials_, slots_;
     DevBuf<int> status_, cgres_, flag_;
     DevBuf<unsigned int> barrier_;
