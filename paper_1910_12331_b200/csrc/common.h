@@ -152,8 +152,10 @@ void launch_scaled_add(double* y, const double* x, const double* scale_num, cons
                        double factor, std::uint64_t n, cudaStream_t st);
 
 // Cholesky-based SPD kernels (kernels_chol.cu); status: 0 ok, 1 ok after jitter, 2 singular
+// chol_factor_elems(count, R) doubles hold the factors (row stride R + 1).
+std::size_t chol_factor_elems(int count, int R);
 // factor count matrices (contiguous R x R); lambda is a host value; mode 0:
-// S + lambda I, mode 1: diag(S) *= (1 + lambda). Packed lower L per matrix.
+// S + lambda I, mode 1: diag(S) *= (1 + lambda). Lower L per matrix.
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode,
                        double* l_out, int* status, cudaStream_t st);
 void launch_chol_solve_rows(const double* l, int R, const double* b, std::int64_t rows, double* y,

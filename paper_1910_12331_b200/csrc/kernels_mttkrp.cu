@@ -422,7 +422,7 @@ FrontPlan plan_front(long long F, long long B, int R) {
     p.BM = pick_bm(B);
     p.mtiles = static_cast<int>((B + p.BM - 1) / p.BM);
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
-    const long long target = num_sms();
+    const long long target = static_cast<long long>(num_sms()) * (p.BM / 16 <= 5 ? 2 : 1);  // resident CTAs
     const long long kchunks = (F + kBK - 1) / kBK;
     long long splits = std::max<long long>(1, (target + base - 1) / base);
     splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));

@@ -363,7 +363,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     pair_.resize(static_cast<std::size_t>(N) * N * RR);
     gam_.resize(N * RR);
     pinv_.resize(N * RR);
-    chol_.resize(static_cast<std::size_t>(N) * R_ * (R_ + 1) / 2);
+    chol_.resize(chol_factor_elems(N, R_));
     chol_tmp_.resize(N * RR);
     std::int64_t smax = 1;
     for (auto d : dims_) smax = std::max<std::int64_t>(smax, static_cast<std::int64_t>(d));
