@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
     const double* s = s_all + static_cast<long long>(mat) * R * R;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     double* w = use_smem ? sh : out;
-    __shared__ double trace_sh, piv_sh;
+    __shared__ double trace_sh;
     __shared__ int fail_sh;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
 
@@ -68,24 +68,40 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
             }
         if (threadIdx.x == 0) fail_sh = 0;
         __syncthreads();
-        for (int j = 0; j < R; ++j) {
-            if (threadIdx.x == 0) {
-                const double x = w[j * LD + j];
-                if (!(x > 0.0) && !isnan(x)) fail_sh = 1;  // Eigen LLT: fail iff pivot <= 0
-                const double l = sqrt(x);
-                piv_sh = l;
-                w[j * LD + j] = l;
+        // blocked right-looking: warp 0 factors a kNb-column panel with warp-level
+        // syncs only, then all warps apply the rank-kNb trailing update.
+        constexpr int kNb = 16;
+        for (int j0 = 0; j0 < R && !fail_sh; j0 += kNb) {
+            const int j1 = min(R, j0 + kNb);
+            if (ty == 0) {
+                for (int j = j0; j < j1; ++j) {
+                    const double x = w[j * LD + j];
+                    if (!(x > 0.0) && !isnan(x)) {  // Eigen LLT: fail iff pivot <= 0
+                        if (tx == 0) fail_sh = 1;
+                        break;
+                    }
+                    const double l = sqrt(x);
+                    __syncwarp();
+                    for (int i = j + 1 + tx; i < R; i += 32) w[i * LD + j] /= l;
+                    if (tx == 0) w[j * LD + j] = l;
+                    __syncwarp();
+                    for (int i = j + 1 + tx; i < R; i += 32) {
+                        const double lij = w[i * LD + j];
+                        const int kend = min(j1, i + 1);
+                        for (int k = j + 1; k < kend; ++k) w[i * LD + k] -= lij * w[k * LD + j];
+                    }
+                    __syncwarp();
+                }
             }
             __syncthreads();
             if (fail_sh) break;
-            const double l = piv_sh;
-            for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) w[i * LD + j] /= l;
-            __syncthreads();
-            // trailing update a_ik -= l_ij l_kj, j < k <= i (rows over warps, cols over lanes)
-            for (int i = j + 1 + ty; i < R; i += ny) {
-                const double lij = w[i * LD + j];
-                for (int k = j + 1 + tx; k <= i; k += 32) w[i * LD + k] -= lij * w[k * LD + j];
-            }
+            // trailing update a_ik -= sum_{j in panel} l_ij l_kj, j1 <= k <= i
+            for (int i = j1 + ty; i < R; i += ny)
+                for (int k = j1 + tx; k <= i; k += 32) {
+                    double acc = w[i * LD + k];
+                    for (int j = j0; j < j1; ++j) acc -= w[i * LD + j] * w[k * LD + j];
+                    w[i * LD + k] = acc;
+                }
             __syncthreads();
         }
         if (!fail_sh) {

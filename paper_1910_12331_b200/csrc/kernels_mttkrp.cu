@@ -527,50 +527,81 @@ __device__ __forceinline__ double kept_weight(const KrpDev& kd, int keep, long l
     }
     return w;
 }
+// Each thread owns VW consecutive rank columns (16-byte loads when R is even)
+// and walks its q-lane with 4 independent loads in flight.
+template <int VW>
 __global__ void __launch_bounds__(kRedT) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
                                                              int R, long long outer, long long sk, long long inner,
                                                              int splits, double* __restrict__ out,
                                                              long long out_split_stride) {
-    __shared__ double red[kRedT];
+    __shared__ double red[kRedT * VW];
     const long long i = blockIdx.x;
     const int split = blockIdx.y;
-    const int rpad = min(kRedT, ((R + 31) / 32) * 32);
-    const int qlanes = kRedT / rpad;
-    const int ql = threadIdx.x / rpad;
-    const int rr = threadIdx.x % rpad;
+    const int cols = (R + VW - 1) / VW;  // threads needed per q-lane
+    const int cpad = min(kRedT, ((cols + 31) / 32) * 32);
+    const int qlanes = kRedT / cpad;
+    const int ql = threadIdx.x / cpad;
+    const int cc = threadIdx.x % cpad;
     const long long total = outer * inner;
     const long long per = (total + splits - 1) / splits;
     const long long lo = split * per, hi = min(total, lo + per);
-    // fast paths for two kept modes: the weight is one factor row
     const bool two = kd.nmodes == 2;
     const double* wfac = two ? kd.fac[keep == 0 ? 1 : 0] : nullptr;
-    for (int r0 = 0; r0 < R; r0 += rpad) {
-        const int r = r0 + rr;
-        double acc = 0.0;
-        if (ql < qlanes && r < R) {
+    for (int c0 = 0; c0 < cols; c0 += cpad) {
+        const int r = (c0 + cc) * VW;
+        double acc[VW];
+#pragma unroll
+        for (int v = 0; v < VW; ++v) acc[v] = 0.0;
+        if (r < R) {
+            const long long step_o = qlanes / inner, step_in = qlanes % inner;
             long long q = lo + ql;
             long long o = q / inner, in = q % inner;
-            const long long step_o = qlanes / inner, step_in = qlanes % inner;
-            double a0 = 0.0, a1 = 0.0;
-            int par = 0;
-            for (; q < hi; q += qlanes) {
-                const double v = __ldcs(p + ((o * sk + i) * inner + in) * R + r);
-                const double w = two ? __ldg(wfac + (keep == 0 ? in : o) * R + r)
-                                     : kept_weight(kd, keep, o, in, r, R);
-                if (par) a1 += v * w; else a0 += v * w;
-                par ^= 1;
-                in += step_in;
-                o += step_o;
-                if (in >= inner) { in -= inner; ++o; }
+            auto advance = [&](long long& oo, long long& ii) {
+                ii += step_in;
+                oo += step_o;
+                if (ii >= inner) { ii -= inner; ++oo; }
+            };
+            while (q < hi) {
+                constexpr int U = 4;
+                double pv[U][VW], wv[U][VW];
+                int cnt = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (q < hi) {
+                        const double* src = p + ((o * sk + i) * inner + in) * R + r;
+                        if (VW == 2) {
+                            const double2 t2 = __ldcs(reinterpret_cast<const double2*>(src));
+                            pv[u][0] = t2.x;
+                            pv[u][VW - 1] = t2.y;
+                        } else {
+                            pv[u][0] = __ldcs(src);
+                        }
+#pragma unroll
+                        for (int v = 0; v < VW; ++v)
+                            wv[u][v] = two ? __ldg(wfac + (keep == 0 ? in : o) * R + r + v)
+                                           : kept_weight(kd, keep, o, in, r + v, R);
+                        ++cnt;
+                        q += qlanes;
+                        advance(o, in);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (u < cnt)
+#pragma unroll
+                        for (int v = 0; v < VW; ++v) acc[v] += pv[u][v] * wv[u][v];
             }
-            acc = a0 + a1;
         }
-        red[threadIdx.x] = acc;
+#pragma unroll
+        for (int v = 0; v < VW; ++v) red[v * kRedT + threadIdx.x] = acc[v];
         __syncthreads();
-        if (threadIdx.x < rpad && r < R) {
-            double sum = 0.0;
-            for (int l = 0; l < qlanes; ++l) sum += red[l * rpad + threadIdx.x];
-            out[split * out_split_stride + i * R + r] = sum;
+        if (threadIdx.x < cpad && r < R) {
+#pragma unroll
+            for (int v = 0; v < VW; ++v) {
+                double sum = 0.0;
+                for (int l = 0; l < qlanes; ++l) sum += red[v * kRedT + l * cpad + threadIdx.x];
+                out[split * out_split_stride + i * R + r + v] = sum;
+            }
         }
         __syncthreads();
     }
@@ -605,7 +636,10 @@ void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, d
         dst = ws;
     }
     dim3 grid(static_cast<unsigned>(sk), splits);
-    reduce_kept_kernel<<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
+    if (R % 2 == 0)
+        reduce_kept_kernel<2><<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
+    else
+        reduce_kept_kernel<1><<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
     if (splits > 1) {
