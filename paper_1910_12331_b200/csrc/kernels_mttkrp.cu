@@ -530,7 +530,7 @@ __device__ __forceinline__ double kept_weight(const KrpDev& kd, int keep, long l
 // Each thread owns VW consecutive rank columns (16-byte loads when R is even)
 // and walks its q-lane with 4 independent loads in flight.
 template <int VW>
-__global__ void __launch_bounds__(kRedT) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
+__global__ void __launch_bounds__(kRedT, 1) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
                                                              int R, long long outer, long long sk, long long inner,
                                                              int splits, double* __restrict__ out,
                                                              long long out_split_stride) {
@@ -556,40 +556,43 @@ __global__ void __launch_bounds__(kRedT) reduce_kept_kernel(const double* __rest
             const long long step_o = qlanes / inner, step_in = qlanes % inner;
             long long q = lo + ql;
             long long o = q / inner, in = q % inner;
-            auto advance = [&](long long& oo, long long& ii) {
-                ii += step_in;
-                oo += step_o;
-                if (ii >= inner) { ii -= inner; ++oo; }
-            };
-            while (q < hi) {
-                constexpr int U = 4;
-                double pv[U][VW], wv[U][VW];
-                int cnt = 0;
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (q < hi) {
-                        const double* src = p + ((o * sk + i) * inner + in) * R + r;
-                        if (VW == 2) {
-                            const double2 t2 = __ldcs(reinterpret_cast<const double2*>(src));
-                            pv[u][0] = t2.x;
-                            pv[u][VW - 1] = t2.y;
-                        } else {
-                            pv[u][0] = __ldcs(src);
-                        }
-#pragma unroll
-                        for (int v = 0; v < VW; ++v)
-                            wv[u][v] = two ? __ldg(wfac + (keep == 0 ? in : o) * R + r + v)
-                                           : kept_weight(kd, keep, o, in, r + v, R);
-                        ++cnt;
-                        q += qlanes;
-                        advance(o, in);
-                    }
+            auto load = [&](long long oo, long long ii, double* pv, double* wv) {
+                const double* src = p + ((oo * sk + i) * inner + ii) * R + r;
+                if (VW == 2) {
+                    const double2 t2 = __ldcs(reinterpret_cast<const double2*>(src));
+                    pv[0] = t2.x;
+                    pv[VW - 1] = t2.y;
+                } else {
+                    pv[0] = __ldcs(src);
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    if (u < cnt)
+                for (int v = 0; v < VW; ++v)
+                    wv[v] = two ? __ldg(wfac + (keep == 0 ? ii : oo) * R + r + v) : kept_weight(kd, keep, oo, ii, r + v, R);
+            };
+            // four independent loads in flight per thread
+            for (; q + 3 * qlanes < hi; q += 4 * qlanes) {
+                long long o1 = o, i1 = in;
+                i1 += step_in; o1 += step_o; if (i1 >= inner) { i1 -= inner; ++o1; }
+                long long o2 = o1, i2 = i1;
+                i2 += step_in; o2 += step_o; if (i2 >= inner) { i2 -= inner; ++o2; }
+                long long o3 = o2, i3 = i2;
+                i3 += step_in; o3 += step_o; if (i3 >= inner) { i3 -= inner; ++o3; }
+                double p0[VW], p1[VW], p2[VW], p3[VW], w0[VW], w1[VW], w2[VW], w3[VW];
+                load(o, in, p0, w0);
+                load(o1, i1, p1, w1);
+                load(o2, i2, p2, w2);
+                load(o3, i3, p3, w3);
 #pragma unroll
-                        for (int v = 0; v < VW; ++v) acc[v] += pv[u][v] * wv[u][v];
+                for (int v = 0; v < VW; ++v) acc[v] += p0[v] * w0[v] + p1[v] * w1[v] + p2[v] * w2[v] + p3[v] * w3[v];
+                o = o3; in = i3;
+                in += step_in; o += step_o; if (in >= inner) { in -= inner; ++o; }
+            }
+            for (; q < hi; q += qlanes) {
+                double p0[VW], w0[VW];
+                load(o, in, p0, w0);
+#pragma unroll
+                for (int v = 0; v < VW; ++v) acc[v] += p0[v] * w0[v];
+                in += step_in; o += step_o; if (in >= inner) { in -= inner; ++o; }
             }
         }
 #pragma unroll
