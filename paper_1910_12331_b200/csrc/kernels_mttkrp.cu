@@ -185,24 +185,24 @@ __device__ __forceinline__ double lds64(std::uint32_t addr) {
 // tile; warp W is the TMA producer (one elected lane) feeding a `stages`-deep
 // ring of (X tile, KRP tile) buffers guarded by full/empty mbarriers.
 // grid: (n_tiles, m_tiles, splits); block: 32 * (W + 1).
-template <int NT, bool TRANS>
-__global__ void __launch_bounds__(288, 1)
+template <int NTW, bool TRANS>
+__global__ void __launch_bounds__(32 * 11, 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                 long long M, long long K, int R, int BM, int stages, long long k_per_split,
+                 long long M, long long K, int R, int BM, int WN, int BNS, int stages, long long k_per_split,
                  double* __restrict__ out, long long out_split_stride) {
-    constexpr int BN = 8 * NT;
-    constexpr int BNS = krp_stride<TRANS>(BN);
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
     char* const smem = smem_raw + (base - raw);
+    const int BN = 8 * NTW * WN;
     const int x_bytes = BM * kBK * 8;
     const int b_bytes = kBK * BNS * 8;
     const int stage_bytes = x_bytes + b_bytes;
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + stages * stage_bytes);
     std::uint64_t* empty = full + stages;
 
-    const int W = BM / 16;
+    const int WM = BM / 16;
+    const int W = WM * WN;  // DMMA warps; warp W is the producer
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n0 = blockIdx.x * BN;
     const long long m0 = static_cast<long long>(blockIdx.y) * BM;
@@ -244,12 +244,14 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         return;
     }
 
-    // ---------------- DMMA consumers
+    // ---------------- DMMA consumers: warp (wm, wn) owns rows [16 wm, +16) and
+    // n8-tiles [NTW wn, NTW (wn + 1)) of the CTA tile
     const int g = lane >> 2, t = lane & 3;
-    const int wm = warp * 16;
-    double acc[NT][4];
+    const int wm = (warp % WM) * 16;
+    const int wn = warp / WM;
+    double acc[NTW][4];
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
     // per-lane constant parts of the fragment addresses
     std::uint32_t aoff[8];
@@ -267,7 +269,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int krow = TRANS ? kperm(t + 4 * i) : t + 4 * i;
-        boff[i] = static_cast<std::uint32_t>((krow * BNS + g) * 8);
+        boff[i] = static_cast<std::uint32_t>((krow * BNS + g + 8 * NTW * wn) * 8);
     }
 
     for (int kt = 0; kt < nk; ++kt) {
@@ -284,7 +286,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
             for (int i = 0; i < 8; ++i) a[i] = lds64(abase + aoff[i]);
             const std::uint32_t bb = bs + ks * 16 * BNS * 8;
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
+            for (int j = 0; j < NTW; ++j) {
                 double b[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) b[i] = lds64(bb + boff[i] + j * 64);
@@ -299,8 +301,8 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     double* o = out + blockIdx.z * out_split_stride;
     const bool vec = (R % 2) == 0;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) {
-        const int col = n0 + 8 * j + 2 * t;
+    for (int j = 0; j < NTW; ++j) {
+        const int col = n0 + 8 * (NTW * wn + j) + 2 * t;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const long long row = m0 + wm + g + 8 * h;
@@ -347,47 +349,91 @@ int num_sms() {
     return sms;
 }
 
-// Rank tiling: n8 tiles per CTA (instantiated set) and number of column tiles.
-constexpr int kNtChoices[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16};
-void pick_nt(int R, int& nt, int& ntiles) {
-    ntiles = (R + 127) / 128;
-    const int need = (R + 8 * ntiles - 1) / (8 * ntiles);
-    nt = 16;
-    for (int c : kNtChoices)
-        if (c >= need) {
-            nt = c;
-            break;
-        }
+// ---- tile planning --------------------------------------------------------
+// CTA tile = (16 WM rows) x (8 NTW WN rank columns); WM x WN DMMA warps + 1
+// TMA producer warp. NTW comes from the instantiated set.
+constexpr int kNtwChoices[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16};
+int round_ntw(int need) {
+    for (int c : kNtwChoices)
+        if (c >= need) return c;
+    return 16;
 }
-
-// Rows per CTA: 16 x warps, warps in [4,8], minimising padded rows.
-int pick_bm(long long M) {
-    int best_w = 8;
+struct GemmPlan {
+    int ntw, wn, wm, ntiles, bns, stages, mtiles, splits;
+    long long kps;
+    int BM() const { return 16 * wm; }
+    int BN() const { return 8 * ntw * wn; }
+};
+int bns_for(int bn, bool trans) { return trans ? krp_stride<true>(bn) : krp_stride<false>(bn); }
+std::size_t stage_bytes_of(int BM, int bns) { return static_cast<std::size_t>(BM) * kBK * 8 + kBK * bns * 8; }
+std::size_t smem_bytes(const GemmPlan& p) {
+    return static_cast<std::size_t>(p.stages) * stage_bytes_of(p.BM(), p.bns) + p.stages * 16 + 1024;
+}
+// Rows per CTA: 16 x wm with wm in [lo, hi], minimising padded rows.
+int pick_wm(long long M, int lo, int hi) {
+    int best = hi;
     long long best_waste = -1;
-    for (int w = 8; w >= 4; --w) {
+    for (int w = hi; w >= lo; --w) {
         const long long bm = 16LL * w;
         const long long waste = ((M + bm - 1) / bm) * bm - M;
         if (best_waste < 0 || waste < best_waste) {
             best_waste = waste;
-            best_w = w;
+            best = w;
         }
     }
-    return 16 * best_w;
+    return best;
+}
+GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
+    GemmPlan p{};
+    // rank split: one CTA column covers up to 208 ranks (2 warp columns of 13 n8-tiles)
+    p.ntiles = (R + 207) / 208;
+    const int per = (R + p.ntiles - 1) / p.ntiles;  // ranks per CTA column
+    const int n8 = (per + 7) / 8;
+    if (trans) {
+        // split-K GEMM with a short M: choose rows to fit M, then add a
+        // second warp column when that leaves fewer than 8 DMMA warps.
+        p.wm = pick_wm(M, 4, 8);
+        p.wn = (p.wm <= 5 && n8 >= 8) ? 2 : 1;
+    } else {
+        p.wn = n8 > 16 ? 2 : 1;
+        p.wm = p.wn == 2 ? 4 : pick_wm(M, 6, 8);
+    }
+    p.ntw = round_ntw((n8 + p.wn - 1) / p.wn);
+    p.bns = bns_for(p.BN(), trans);
+    p.stages = 2;
+    for (int s = 6; s >= 2; --s) {
+        p.stages = s;
+        if (smem_bytes(p) <= 225 * 1024) break;
+    }
+    p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
+    p.splits = 1;
+    p.kps = K;
+    if (trans) {
+        const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
+        const long long kchunks = (K + kBK - 1) / kBK;
+        long long splits = std::max<long long>(1, (num_sms() + base - 1) / base);
+        splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
+        p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
+        p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
+    }
+    return p;
 }
 
 template <bool TRANS>
-void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, const CUtensorMap& xmap,
-              const CUtensorMap& kmap, long long M, long long K, int R, int BM, int stages, long long kps,
-              double* out, long long oss) {
+void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, long long M,
+              long long K, int R, double* out, long long oss) {
+    const std::size_t smem = smem_bytes(p);
+    const dim3 grid(p.ntiles, p.mtiles, p.splits);
+    const dim3 block(32 * (p.wm * p.wn + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
         auto fn = root_gemm_kernel<NTV, TRANS>;                                                    \
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
-        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, BM, stages, kps, out, oss);             \
+        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, out, oss); \
         break;                                                                                     \
     }
-    switch (nt) {
+    switch (p.ntw) {
         CPK_CASE(1) CPK_CASE(2) CPK_CASE(3) CPK_CASE(4) CPK_CASE(5) CPK_CASE(6) CPK_CASE(7)
         CPK_CASE(8) CPK_CASE(10) CPK_CASE(12) CPK_CASE(13) CPK_CASE(16)
         default: throw DeviceError("unsupported rank tile");
@@ -395,40 +441,6 @@ void dispatch(int nt, dim3 grid, dim3 block, std::size_t smem, cudaStream_t st, 
 #undef CPK_CASE
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
-}
-
-int bns_of(int nt, bool trans) { return trans ? krp_stride<true>(8 * nt) : krp_stride<false>(8 * nt); }
-
-std::size_t smem_bytes(int BM, int nt, bool trans, int stages) {
-    return static_cast<std::size_t>(stages) * (BM * kBK * 8 + kBK * bns_of(nt, trans) * 8) + stages * 16 + 1024;
-}
-
-// Pipeline depth: as deep as shared memory allows; small CTAs (<= 5 DMMA
-// warps) keep two CTAs resident per SM so >= 10 warps feed the DMMA pipe.
-int pick_stages(int BM, int nt, bool trans) {
-    const std::size_t budget = (BM / 16 <= 5 ? 112 : 225) * 1024;
-    for (int s = 6; s >= 2; --s)
-        if (smem_bytes(BM, nt, trans, s) <= budget) return s;
-    return 2;
-}
-
-struct FrontPlan {
-    int nt, ntiles, BM, mtiles, splits;
-    long long kps;
-};
-FrontPlan plan_front(long long F, long long B, int R) {
-    FrontPlan p{};
-    pick_nt(R, p.nt, p.ntiles);
-    p.BM = pick_bm(B);
-    p.mtiles = static_cast<int>((B + p.BM - 1) / p.BM);
-    const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
-    const long long target = static_cast<long long>(num_sms()) * (p.BM / 16 <= 5 ? 2 : 1);  // resident CTAs
-    const long long kchunks = (F + kBK - 1) / kBK;
-    long long splits = std::max<long long>(1, (target + base - 1) / base);
-    splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
-    p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
-    p.splits = static_cast<int>((F + p.kps - 1) / p.kps);
-    return p;
 }
 
 // Fill the KRP operand (K x Rs, Rs = R rounded to even) for a contraction.
@@ -450,39 +462,32 @@ std::size_t krp_workspace_elems(std::int64_t rows, int R) {
 // X is F x Bs row-major (Bs >= B, Bs even: the padded row stride).
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                       const KrpDesc& kb, double* krp, double* pf, cudaStream_t st) {
-    int nt, ntiles;
-    pick_nt(R, nt, ntiles);
-    const int BM = pick_bm(F);
-    const int stages = pick_stages(BM, nt, false);
+    const GemmPlan p = plan_gemm(F, B, R, false);
+    if (p.mtiles > 65535) throw LimitExceeded("root_back: too many row tiles");
     const int Rs = (R + 1) & ~1;
     fill_krp(kb, B, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16,
-                                      static_cast<std::uint32_t>(BM), true);
+                                      static_cast<std::uint32_t>(p.BM()), true);
     const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(B),
-                                      static_cast<std::uint32_t>(bns_of(nt, false)), kBK, false);
-    dim3 grid(ntiles, static_cast<unsigned>((F + BM - 1) / BM), 1);
-    if (grid.y > 65535) throw LimitExceeded("root_back: too many row tiles");
-    dispatch<false>(nt, grid, dim3(32 * (BM / 16 + 1)), smem_bytes(BM, nt, false, stages), st, xmap, kmap, F, B,
-                    R, BM, stages, B, pf, 0);
+                                      static_cast<std::uint32_t>(p.bns), kBK, false);
+    dispatch<false>(p, st, xmap, kmap, F, B, R, pf, 0);
 }
 
 std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R) {
-    const FrontPlan p = plan_front(F, B, R);
+    const GemmPlan p = plan_gemm(B, F, R, true);
     return p.splits > 1 ? static_cast<std::size_t>(p.splits) * B * R : 0;
 }
 
 void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                        const KrpDesc& kf, double* krp, double* pb, double* ws, std::size_t ws_elems,
                        cudaStream_t st) {
-    const FrontPlan p = plan_front(F, B, R);
-    const int stages = pick_stages(p.BM, p.nt, true);
+    const GemmPlan p = plan_gemm(B, F, R, true);
     const int Rs = (R + 1) & ~1;
     fill_krp(kf, F, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16, kBK,
                                       true);
     const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
-                                      static_cast<std::uint32_t>(bns_of(p.nt, true)), kBK, false);
-    dim3 grid(p.ntiles, p.mtiles, p.splits);
+                                      static_cast<std::uint32_t>(p.bns), kBK, false);
     double* out = pb;
     long long oss = 0;
     if (p.splits > 1) {
@@ -491,8 +496,7 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
         out = ws;
         oss = B * R;
     }
-    dispatch<true>(p.nt, grid, dim3(32 * (p.BM / 16 + 1)), smem_bytes(p.BM, p.nt, true, stages), st, xmap, kmap,
-                   B, F, R, p.BM, stages, p.kps, out, oss);
+    dispatch<true>(p, st, xmap, kmap, B, F, R, out, oss);
     if (p.splits > 1) {
         const long long n = B * static_cast<long long>(R);
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
@@ -530,7 +534,7 @@ __device__ __forceinline__ double kept_weight(const KrpDev& kd, int keep, long l
 // Each thread owns VW consecutive rank columns (16-byte loads when R is even)
 // and walks its q-lane with 4 independent loads in flight.
 template <int VW>
-__global__ void __launch_bounds__(kRedT, 1) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
+__global__ void __launch_bounds__(kRedT, 3) reduce_kept_kernel(const double* __restrict__ p, KrpDev kd, int keep,
                                                              int R, long long outer, long long sk, long long inner,
                                                              int splits, double* __restrict__ out,
                                                              long long out_split_stride) {
