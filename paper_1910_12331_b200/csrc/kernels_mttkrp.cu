@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.h"
@@ -394,6 +395,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
         // second warp column when that leaves fewer than 8 DMMA warps.
         p.wm = pick_wm(M, 4, 8);
         p.wn = (p.wm <= 5 && n8 >= 8) ? 2 : 1;
+        if (const char* e = std::getenv("CPKIT_TN_WN")) p.wn = std::atoi(e);
     } else {
         p.wn = n8 > 16 ? 2 : 1;
         p.wm = p.wn == 2 ? 4 : pick_wm(M, 6, 8);
@@ -411,7 +413,10 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     if (trans) {
         const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
         const long long kchunks = (K + kBK - 1) / kBK;
-        long long splits = std::max<long long>(1, (num_sms() + base - 1) / base);
+        // resident CTA slots per SM (smem and register limited); never exceed one wave
+        const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
+        const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
+        long long splits = std::max<long long>(1, (static_cast<long long>(num_sms()) * per_sm) / base);
         splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
         p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
         p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
