@@ -95,7 +95,9 @@ struct KrpDesc {
 //   back root:  P_F[F x R] = X[F x B] * KRP_B        (NN)
 //   front root: P_B[B x R] = X[F x B]^T * KRP_F      (TN, split-K)
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
-                      const KrpDesc& kb, double* krp, double* pf, cudaStream_t st);
+                      const KrpDesc& kb, double* krp, double* pf, double* splitk_ws, std::size_t splitk_ws_elems,
+                      cudaStream_t st);
+std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R);
 void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                        const KrpDesc& kf, double* krp, double* pb, double* splitk_ws,
                        std::size_t splitk_ws_elems, cudaStream_t st);

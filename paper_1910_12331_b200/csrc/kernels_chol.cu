@@ -29,26 +29,29 @@ inline bool chol_in_smem(int R) { return static_cast<std::size_t>(R) * lda_of(R)
 
 // mode 0: A = S + lambda I; mode 1: A = S with diag *= (1 + lambda), lambda'=0.
 // Jitter trace uses the matrix handed to factor_shifted (gauss_newton.cpp:190-207).
+// kSmem selects the working copy's address space at compile time (LDS/STS).
+template <bool kSmem>
 __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_all, int R, double lambda, int mode,
-                                                   double* __restrict__ l_all, int* __restrict__ status,
-                                                   int use_smem) {
+                                                   double* __restrict__ l_all, int* __restrict__ status) {
     extern __shared__ double sh[];
     const int LD = R + 1;
     const int mat = blockIdx.x;
     const double* s = s_all + static_cast<long long>(mat) * R * R;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
-    double* w = use_smem ? sh : out;
+    double* w = kSmem ? sh : out;
     __shared__ double trace_sh;
     __shared__ int fail_sh;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
 
-    if (threadIdx.x == 0) {
+    if (ty == 0) {  // trace, warp-parallel (fixed shuffle order)
         double tr = 0.0;
-        for (int i = 0; i < R; ++i) {
+        for (int i = tx; i < R; i += 32) {
             const double d = s[static_cast<long long>(i) * R + i];
             tr += (mode == 1) ? d * (1.0 + lambda) : d;
         }
-        trace_sh = tr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
+        if (tx == 0) trace_sh = tr;
     }
     __syncthreads();
     const double jitter = 1e-12 * trace_sh / static_cast<double>(R);
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
         st = 2;
         __syncthreads();
     }
-    if (use_smem)
+    if (kSmem)
         for (int i = ty; i < R; i += ny)
             for (int k = tx; k <= i; k += 32) out[i * LD + k] = w[i * LD + k];
     if (threadIdx.x == 0) status[mat] = st;
@@ -236,9 +239,13 @@ void launch_chol_batch(const double* s, int count, int R, const double* lambda, 
     if (R > 32 * kMaxBlk) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
     const bool use_smem = chol_in_smem(R);
     const std::size_t smem = use_smem ? static_cast<std::size_t>(R) * lda_of(R) * 8 : 0;
-    if (use_smem)
-        CPK_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    chol_kernel<<<count, 512, smem, st>>>(s, R, *lambda, mode, l_out, status, use_smem ? 1 : 0);
+    if (use_smem) {
+        CPK_CUDA(cudaFuncSetAttribute(chol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        chol_kernel<true><<<count, 512, smem, st>>>(s, R, *lambda, mode, l_out, status);
+    } else {
+        chol_kernel<false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status);
+    }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }

@@ -410,13 +410,14 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
     p.splits = 1;
     p.kps = K;
-    if (trans) {
-        const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
+    // split K when the output tiles alone cannot fill one resident wave
+    const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
+    const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
+    const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
+    const long long slots = static_cast<long long>(num_sms()) * per_sm;
+    if (base < slots) {
         const long long kchunks = (K + kBK - 1) / kBK;
-        // resident CTA slots per SM (smem and register limited); never exceed one wave
-        const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
-        const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
-        long long splits = std::max<long long>(1, (static_cast<long long>(num_sms()) * per_sm) / base);
+        long long splits = std::max<long long>(1, slots / base);  // never exceed one wave
         splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
         p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
         p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
@@ -466,7 +467,8 @@ std::size_t krp_workspace_elems(std::int64_t rows, int R) {
 
 // X is F x Bs row-major (Bs >= B, Bs even: the padded row stride).
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
-                      const KrpDesc& kb, double* krp, double* pf, cudaStream_t st) {
+                      const KrpDesc& kb, double* krp, double* pf, double* ws, std::size_t ws_elems,
+                      cudaStream_t st) {
     const GemmPlan p = plan_gemm(F, B, R, false);
     if (p.mtiles > 65535) throw LimitExceeded("root_back: too many row tiles");
     const int Rs = (R + 1) & ~1;
@@ -475,7 +477,27 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
                                       static_cast<std::uint32_t>(p.BM()), true);
     const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(B),
                                       static_cast<std::uint32_t>(p.bns), kBK, false);
-    dispatch<false>(p, st, xmap, kmap, F, B, R, pf, 0);
+    double* out = pf;
+    long long oss = 0;
+    if (p.splits > 1) {
+        if (ws_elems < static_cast<std::size_t>(p.splits) * F * R)
+            throw DeviceError("root_back: split-K workspace too small");
+        out = ws;
+        oss = F * R;
+    }
+    dispatch<false>(p, st, xmap, kmap, F, B, R, out, oss);
+    if (p.splits > 1) {
+        const long long n = F * static_cast<long long>(R);
+        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, pf);
+        count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+    }
+}
+
+std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R) {
+    const GemmPlan p = plan_gemm(F, B, R, false);
+    return p.splits > 1 ? static_cast<std::size_t>(p.splits) * F * R : 0;
 }
 
 std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R) {

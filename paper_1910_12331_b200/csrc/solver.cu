@@ -298,12 +298,20 @@ KruskalModel random_model_gaussian(const std::vector<std::uint64_t>& dims, std::
 Context::Context(int dev) : device(dev) {
     CPK_CUDA(cudaSetDevice(dev));
     CPK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CPK_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    for (auto& e : ev) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 Context::~Context() {
     comm.reset();
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (aux) cudaStreamDestroy(aux);
     if (stream) cudaStreamDestroy(stream);
 }
-void Context::sync() const { CPK_CUDA(cudaStreamSynchronize(stream)); }
+void Context::sync() const {
+    CPK_CUDA(cudaStreamSynchronize(aux));
+    CPK_CUDA(cudaStreamSynchronize(stream));
+}
 
 void shard_range(std::uint64_t extent, int rank, int world, std::uint64_t* lo, std::uint64_t* hi) {
     const std::uint64_t base = extent / static_cast<std::uint64_t>(world);
@@ -352,7 +360,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     PF_.resize(static_cast<std::size_t>(F_) * R_);
     PB_.resize(static_cast<std::size_t>(Bl_) * R_);
     // split-K and second-level workspaces
-    std::size_t ws = root_front_workspace_elems(F_, Bl_, R_);
+    std::size_t ws = std::max(root_front_workspace_elems(F_, Bl_, R_), root_back_workspace_elems(F_, Bl_, R_));
     {
         KrpDesc kf = krp(0, h_, A_.get(), false), kb = krp(h_, N, A_.get(), true);
         for (int n = 0; n < h_; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kf, n, R_));
@@ -542,7 +550,8 @@ void DeviceProblem::profile_read(double* ms, int* count) {
 void DeviceProblem::root_back() {
     const int N = order();
     prof_begin(kProfBack);
-    launch_root_back(x_.get(), F_, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get(), ctx_.stream);
+    launch_root_back(x_.get(), F_, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get(), ws_.get(),
+                     ws_.size(), ctx_.stream);
     prof_end();
     ++contractions_;
     pf_valid_ = true;
@@ -697,18 +706,33 @@ void DeviceProblem::spd_inverse(const double* dev_s, double lambda, double* dev_
     check_status(1, "spd_solve");
     launch_chol_inverse_batch(chol_.get(), 1, R_, dev_inv, chol_tmp_.get(), ctx_.stream);
 }
-// gauss_newton.cpp:190-207: per mode (Gamma(n,n) + lambda Reg)^-1
-void DeviceProblem::build_preconditioner(double lambda, RegShape shape) {
+// gauss_newton.cpp:190-207: per mode (Gamma(n,n) + lambda Reg)^-1. The N
+// Cholesky factorisations run on the side stream as soon as the Gamma set
+// exists, overlapping the residual / gradient work of gn_step.
+void DeviceProblem::launch_preconditioner_factor(double lambda, RegShape shape) {
     if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
     const int N = order();
     const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    CPK_CUDA(cudaEventRecord(ctx_.ev[0], ctx_.stream));  // Gamma set ready
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.aux, ctx_.ev[0], 0));
     for (int n = 0; n < N; ++n)
         CPK_CUDA(cudaMemcpyAsync(gam_.get() + n * RR, pair_.get() + (n * N + n) * RR, RR * 8,
-                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+                                 cudaMemcpyDeviceToDevice, ctx_.aux));
     launch_chol_batch(gam_.get(), N, R_, &lambda, shape == RegShape::identity ? 0 : 1, chol_.get(),
-                      status_.get(), ctx_.stream);
-    check_status(N, "spd_solve");
-    launch_chol_inverse_batch(chol_.get(), N, R_, pinv_.get(), chol_tmp_.get(), ctx_.stream);
+                      status_.get(), ctx_.aux);
+    CPK_CUDA(cudaEventRecord(ctx_.ev[1], ctx_.aux));
+    precond_pending_ = true;
+    precond_lambda_ = lambda;
+    precond_shape_ = shape;
+}
+void DeviceProblem::build_preconditioner(double lambda, RegShape shape) {
+    if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
+    if (!precond_pending_ || precond_lambda_ != lambda || precond_shape_ != shape)
+        launch_preconditioner_factor(lambda, shape);
+    precond_pending_ = false;
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
+    check_status(order(), "spd_solve");
+    launch_chol_inverse_batch(chol_.get(), order(), R_, pinv_.get(), chol_tmp_.get(), ctx_.stream);
 }
 
 // ---- J^T J v and CG ------------------------------------------------------------
@@ -748,6 +772,8 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
     CgResultInfo out;
     const double gnorm = norm_sum(G_.get());
     if (gnorm == 0.0) {
+        ctx_.sync();  // drop any speculative preconditioner factorisation
+        precond_pending_ = false;
         CPK_CUDA(cudaMemsetAsync(V_.get(), 0, off_[N] * sizeof(double), ctx_.stream));
         return out;
     }
@@ -796,12 +822,19 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
     double zero = 0.0;
     CPK_CUDA(cudaMemcpyAsync(scal_.get() + kStep, &zero, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
     grams_all();
+    const std::size_t LDR = chol_factor_elems(1, R_);
     for (int n = 0; n < N; ++n) {
-        launch_gamma_excl(grams_.get(), N, R_, n, gam_.get(), ctx_.stream);
+        // side stream: Gamma^(n) from the current grams, then its Cholesky factor,
+        // overlapping the MTTKRP of mode n on the main stream
+        CPK_CUDA(cudaEventRecord(ctx_.ev[2 + 2 * n], ctx_.stream));
+        CPK_CUDA(cudaStreamWaitEvent(ctx_.aux, ctx_.ev[2 + 2 * n], 0));
+        launch_gamma_excl(grams_.get(), N, R_, n, gam_.get() + n * RR, ctx_.aux);
+        launch_chol_batch(gam_.get() + n * RR, 1, R_, &lambda, 0, chol_.get() + n * LDR, status_.get() + n, ctx_.aux);
+        CPK_CUDA(cudaEventRecord(ctx_.ev[3 + 2 * n], ctx_.aux));
         mttkrp(n);
+        CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[3 + 2 * n], 0));
         const std::int64_t rows = static_cast<std::int64_t>(dims_[n]);
-        launch_chol_batch(gam_.get(), 1, R_, &lambda, 0, chol_.get(), status_.get() + n, ctx_.stream);
-        launch_chol_solve_rows(chol_.get(), R_, M_.get() + off_[n], rows, anew_.get(), ctx_.stream);
+        launch_chol_solve_rows(chol_.get() + n * LDR, R_, M_.get() + off_[n], rows, anew_.get(), ctx_.stream);
         launch_diff_norm_add(anew_.get(), A_.get() + off_[n], static_cast<std::uint64_t>(rows) * R_,
                              partials_.get(), scal_.get() + kStep, ctx_.stream);
         CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], anew_.get(), rows * R_ * sizeof(double),
@@ -837,18 +870,23 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     GnStepDiag diag;
     if (!m_all_valid_) compute_all_mttkrp();
     build_gamma_set();
+    launch_preconditioner_factor(schedule.lambda, cfg.schedule.shape);  // overlaps residual/gradient
     auto [res, fit] = residual_fitness(xnorm2, N - 1);
     (void)fit;
     diag.residual_before = res;
     diag.residual_after = res;
     if (res < cfg.residual_tol) {
         diag.halt = GnStepDiag::Halt::residual;
+        ctx_.sync();
+        precond_pending_ = false;
         return diag;
     }
     gradient();
     diag.grad_norm = norm_sum(G_.get());
     if (diag.grad_norm <= cfg.grad_tol) {
         diag.halt = GnStepDiag::Halt::gradient;
+        ctx_.sync();
+        precond_pending_ = false;
         return diag;
     }
     diag.lambda = schedule.lambda;

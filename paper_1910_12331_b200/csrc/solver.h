@@ -156,6 +156,9 @@ void nccl_unique_id(void* out128);
 struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;  // side stream: SPD factorisations overlap the MTTKRP
+    static constexpr int kEvents = 2 * kMaxOrder + 2;
+    cudaEvent_t ev[kEvents] = {};
     std::unique_ptr<Comm> comm;  // null: single GPU
     explicit Context(int dev);
     ~Context();
@@ -214,6 +217,8 @@ public:
     void jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape);
     CgResultInfo cp_cg(double lambda, const GnConfig& cfg);  // V from G (gauss_newton.cpp:279-349)
     void build_preconditioner(double lambda, RegShape shape);
+    // factor the preconditioner blocks on the side stream (joined by cp_cg)
+    void launch_preconditioner_factor(double lambda, RegShape shape);
     void spd_solve(const double* dev_s, const double* dev_b, std::int64_t rows, double lambda,
                    double* dev_y);
     void spd_inverse(const double* dev_s, double lambda, double* dev_inv);
@@ -267,6 +272,9 @@ private:
     DevBuf<std::int64_t> offs_dev_, rows_dev_;
     DevBuf<const double*> facptr_dev_;
     double* Mall_gather_ = nullptr;
+    bool precond_pending_ = false;
+    double precond_lambda_ = 0.0;
+    RegShape precond_shape_ = RegShape::identity;
     std::vector<std::int64_t> local_rows_;           // rows of each mode in the LOCAL tensor
     bool m_all_valid_ = false;                       // all M computed for current factors (GN reuse)
 
