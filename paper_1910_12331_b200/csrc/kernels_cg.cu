@@ -75,6 +75,7 @@ struct Dev {
     Layout L;
     int mode;  // 0 = full CG, 1 = single matvec (W given in W[0], result in Q)
 };
+extern __shared__ double cg_panel_smem[];  // tile_gemm_panel operand panels
 
 // slot regions (doubles): [0, tasksB) wq partials; then rz, nrm, fin per task C
 __device__ __forceinline__ double* slot_wq(const Dev& d) { return d.p.slots; }
@@ -84,7 +85,7 @@ __device__ __forceinline__ double* slot_fin(const Dev& d) { return d.p.slots + 3
 __device__ __forceinline__ double* bpart(const Dev& d) { return d.p.slots + 4 * d.L.tasksBC; }
 
 // ---- phase A: W' = Z + beta W_old (first: W' = Z; matvec: W' = W_in), B_p partials
-__device__ void phase_a(const Dev& d, Smem& sm, const double* Wold, double* Wnew, double beta,
+__device__ void phase_a(const Dev& d, RedSmem& sm, const double* Wold, double* Wnew, double beta,
                         bool first) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
@@ -119,7 +120,7 @@ __device__ void phase_a(const Dev& d, Smem& sm, const double* Wold, double* Wnew
             return v;
         };
         double acc[4];
-        tile_gemm(sm, K, la, lb, acc);
+        tile_gemm_panel(cg_panel_smem, K, la, lb, acc);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
         double* out = bpart(d) + (static_cast<long long>(ks) * L.order + pm) * R * R;
@@ -135,7 +136,7 @@ __device__ void phase_a(const Dev& d, Smem& sm, const double* Wold, double* Wnew
 }
 
 // ---- phase B: Q_n = [W'|A_n][Gnn; D^T] + lambda Reg(W'); wq partials
-__device__ void phase_b(const Dev& d, Smem& sm, const double* Wn_all, double* Qout) {
+__device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double* Qout) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
     const int R = L.R;
@@ -170,7 +171,7 @@ __device__ void phase_b(const Dev& d, Smem& sm, const double* Wn_all, double* Qo
             return dsum;
         };
         double acc[4];
-        tile_gemm(sm, 2 * R, la, lb, acc);
+        tile_gemm_panel(cg_panel_smem, 2 * R, la, lb, acc);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
         double part = 0.0;
@@ -194,7 +195,7 @@ __device__ void phase_b(const Dev& d, Smem& sm, const double* Wn_all, double* Qo
 }
 
 // ---- phase C: V += alpha W'; R' = R - alpha Q (init: R' = -G); Z = R' Pinv
-__device__ void phase_c(const Dev& d, Smem& sm, const double* Wn_all, const double* Rold_all,
+__device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const double* Rold_all,
                         double* Rnew_all, double alpha, bool init) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
@@ -220,7 +221,7 @@ __device__ void phase_c(const Dev& d, Smem& sm, const double* Wn_all, const doub
             return r < R ? Pinv[z * R + r] : 0.0;
         };
         double acc[4];
-        tile_gemm(sm, R, la, lb, acc);
+        tile_gemm_panel(cg_panel_smem, R, la, lb, acc);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
         double rz = 0.0, nrm = 0.0, bad = 0.0;
@@ -260,7 +261,7 @@ __device__ void phase_c(const Dev& d, Smem& sm, const double* Wn_all, const doub
 }
 
 // Broadcast helpers: thread 0 sums slots in task order.
-__device__ double sum_slots(Smem& sm, const double* slots, int n) {
+__device__ double sum_slots(RedSmem& sm, const double* slots, int n) {
     __syncthreads();
     if (threadIdx.x == 0) {
         double s = 0.0;
@@ -272,7 +273,7 @@ __device__ double sum_slots(Smem& sm, const double* slots, int n) {
     __syncthreads();
     return v;
 }
-__device__ double norm_sum_slots(const Dev& d, Smem& sm) {
+__device__ double norm_sum_slots(const Dev& d, RedSmem& sm) {
     __syncthreads();
     if (threadIdx.x == 0) {
         const volatile double* nr = slot_nrm(d);
@@ -290,8 +291,8 @@ __device__ double norm_sum_slots(const Dev& d, Smem& sm) {
     return v;
 }
 
-__global__ void __launch_bounds__(kThreads) cg_kernel(Dev d) {
-    __shared__ Smem sm;
+__global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__ Dev d) {
+    __shared__ RedSmem sm;
     const CgParams& p = d.p;
     const unsigned nb = gridDim.x;
     if (d.mode == 1) {
@@ -382,7 +383,9 @@ Layout make_layout(const CgParams& p, int grid) {
 int occupancy_grid(int device) {
     int sms = 0, per = 0;
     CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, 0));
+    CPK_CUDA(cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kPanelSmemBytes)));
+    CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, kPanelSmemBytes));
     return sms * std::max(1, per);
 }
 
@@ -390,17 +393,13 @@ void launch_coop(const Dev& d, int grid, cudaStream_t st) {
     Dev dd = d;
     void* args[] = {&dd};
     CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_kernel), dim3(grid),
-                                         dim3(kThreads), args, 0, st));
+                                         dim3(kThreads), args, kPanelSmemBytes, st));
     count_launch(1);
 }
 
 }  // namespace
 
-int cg_max_grid(int device) {
-    int sms = 0;
-    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    return std::min(occupancy_grid(device), sms);
-}
+int cg_max_grid(int device) { return occupancy_grid(device); }
 
 std::size_t cg_slots_needed(const CgParams& p) {
     const Layout L = make_layout(p, 148);

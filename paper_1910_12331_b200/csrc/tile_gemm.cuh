@@ -4,6 +4,8 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 namespace cpkit {
 namespace tile {
 
@@ -22,6 +24,10 @@ __device__ __forceinline__ void dmma16816(double* d, const double* a, const doub
           "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
+struct RedSmem {
+    double red[kThreads / 32 * 4];
+    double bcast[8];
+};
 struct Smem {
     double As[2][kT * kAS];
     double Bs[2][kKC * kBS];
@@ -78,8 +84,54 @@ __device__ __forceinline__ void tile_gemm(Smem& sm, int K, LA la, LB lb, double 
     }
 }
 
+// Panel variant: the whole A panel [32 x kp] and B panel [kp x 32] are loaded
+// into shared memory with every load of the panel in flight at once (deep
+// memory-level parallelism for L2-resident operands), then multiplied with no
+// further barriers. kp <= kPanel; longer K loops over panels.
+constexpr int kPanel = 192;
+constexpr int kPAS = kPanel + 4;   // A panel row stride: conflict-free a-fragments
+constexpr int kPBS = kT + 8;       // B panel row stride
+constexpr std::size_t kPanelSmemBytes = (kT * kPAS + kPanel * kPBS) * sizeof(double);
+
+template <typename LA, typename LB>
+__device__ __forceinline__ void tile_gemm_panel(double* psm, int K, LA la, LB lb, double acc[4]) {
+    double* As = psm;
+    double* Bs = psm + kT * kPAS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 2) * 16, wn = (warp & 3) * 8;
+    acc[0] = acc[1] = acc[2] = acc[3] = 0.0;
+    for (int k0 = 0; k0 < K; k0 += kPanel) {
+        const int kp = min(kPanel, K - k0);
+        const int kpad = (kp + 15) & ~15;
+        // A panel: element e -> (row = e / kpad, k = e % kpad)
+#pragma unroll 4
+        for (int e = tid; e < kT * kpad; e += kThreads) {
+            const int row = e / kpad, k = e - row * kpad;
+            As[row * kPAS + k] = (k < kp) ? la(row, k0 + k) : 0.0;
+        }
+        // B panel: element e -> (k = e / 32, col = e % 32)
+#pragma unroll 4
+        for (int e = tid; e < kpad * kT; e += kThreads) {
+            const int k = e >> 5, col = e & 31;
+            Bs[k * kPBS + col] = (k < kp) ? lb(k0 + k, col) : 0.0;
+        }
+        __syncthreads();
+        for (int c = 0; c < kpad; c += kKC) {
+            double a[8], b[4];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = As[(wm + g + 8 * (i & 1)) * kPAS + c + t + 4 * (i >> 1)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) b[i] = Bs[(c + t + 4 * i) * kPBS + wn + g];
+            dmma16816(acc, a, b);
+        }
+        __syncthreads();
+    }
+}
+
 // Fixed-order CTA reduction of one value per thread; returns to all threads.
-__device__ __forceinline__ double cta_sum(Smem& sm, double v) {
+template <class S>
+__device__ __forceinline__ double cta_sum(S& sm, double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
