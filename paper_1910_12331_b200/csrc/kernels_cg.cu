@@ -32,24 +32,21 @@ namespace {
 
 using namespace tile;
 
-__device__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+// Grid barrier on a monotonically increasing arrival counter: one
+// release-add per CTA, then acquire-polls until every CTA of this round has
+// arrived (no reset, no generation word, no full fences).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& round) {
     __syncthreads();
+    ++round;
     if (threadIdx.x == 0) {
-        volatile unsigned int* vb = bar;
-        const unsigned int gen = vb[1];
-        __threadfence();
-        const unsigned int arrived = atomicAdd(&bar[0], 1u);
-        if (arrived == nblocks - 1) {
-            atomicExch(&bar[0], 0u);
-            __threadfence();
-            atomicAdd(&bar[1], 1u);
-        } else {
-            for (unsigned long long spin = 0; vb[1] == gen; ++spin) {
-                __nanosleep(20);
-                if (spin > (1ull << 28)) __trap();  // never hang the GPU on a lost arrival
-            }
+        const unsigned int target = round * nblocks;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned int seen;
+        for (unsigned long long spin = 0;; ++spin) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+            if (static_cast<int>(seen - target) >= 0) break;
+            if (spin > (1ull << 30)) __trap();  // never hang the GPU on a lost arrival
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -114,8 +111,8 @@ __device__ void phase_a(const Dev& d, RedSmem& sm, const double* Wold, double* W
             const int z = z0 + col;
             if (z >= R) return 0.0;
             const long long e = (k0 + k) * R + z;
-            if (d.mode == 1) return Wo[e];
-            const double v = first ? Z[e] : Z[e] + beta * Wo[e];
+            if (d.mode == 1) return __ldcg(Wo + e);
+            const double v = first ? __ldcg(Z + e) : __ldcg(Z + e) + beta * __ldcg(Wo + e);
             if (writer) Wn[e] = v;
             return v;
         };
@@ -153,7 +150,7 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
         auto la = [&](int row, int kk) -> double {
             const long long i = row0 + row;
             if (i >= s) return 0.0;
-            return kk < R ? W[i * R + kk] : A[i * R + (kk - R)];
+            return kk < R ? __ldcg(W + i * R + kk) : A[i * R + (kk - R)];
         };
         auto lb = [&](int kk, int col) -> double {
             const int r = c0 + col;
@@ -165,7 +162,7 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
                 if (q == n) continue;
                 double b = 0.0;
                 for (int ks = 0; ks < L.ksplit; ++ks)
-                    b += bpart(d)[(static_cast<long long>(ks) * L.order + q) * RR + r * R + z];
+                    b += __ldcg(bpart(d) + (static_cast<long long>(ks) * L.order + q) * RR + r * R + z);
                 dsum += p.pair[(n * L.order + q) * RR + r * R + z] * b;
             }
             return dsum;
@@ -182,7 +179,7 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
                 const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
                 const int r = c0 + (warp & 3) * 8 + 2 * t + c;
                 if (i < s && r < R) {
-                    const double w = W[i * R + r];
+                    const double w = __ldcg(W + i * R + r);
                     const double reg = (p.shape == 0) ? p.lambda * w : w * (p.lambda * Gnn[r * R + r]);
                     const double q = acc[2 * h + c] + reg;
                     Qout[p.off[n] + i * R + r] = q;
@@ -210,7 +207,7 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
         const long long off = p.off[n];
         const double* Pinv = p.pinv + n * RR;
         auto rnew = [&](long long e) -> double {
-            return init ? -p.G[e] : Rold_all[e] - alpha * p.Q[e];
+            return init ? -p.G[e] : __ldcg(Rold_all + e) - alpha * __ldcg(p.Q + e);
         };
         auto la = [&](int row, int z) -> double {
             const long long i = row0 + row;
@@ -239,7 +236,7 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
                     if (init) {
                         v = 0.0;
                     } else {
-                        v = p.V[e] + alpha * Wn_all[e];
+                        v = __ldcg(p.V + e) + alpha * __ldcg(Wn_all + e);
                     }
                     p.V[e] = v;
                     Rnew_all[e] = rv;
@@ -260,51 +257,40 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
     }
 }
 
-// Broadcast helpers: thread 0 sums slots in task order.
+// Slot reductions: thread i reads slots i, i + 256, ... (L2 loads, all in
+// flight), then a fixed-shape CTA tree; every CTA gets the same bits.
 __device__ double sum_slots(RedSmem& sm, const double* slots, int n) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int i = 0; i < n; ++i) s += reinterpret_cast<const volatile double*>(slots)[i];
-        sm.bcast[0] = s;
-    }
-    __syncthreads();
-    const double v = sm.bcast[0];
-    __syncthreads();
-    return v;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += __ldcg(slots + i);
+    return cta_sum(sm, v);
 }
+// sum_n sqrt(sum of the mode-n slots) (norm_sum, gauss_newton.cpp:246-250)
 __device__ double norm_sum_slots(const Dev& d, RedSmem& sm) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const volatile double* nr = slot_nrm(d);
-        double total = 0.0;
-        for (int n = 0; n < d.L.order; ++n) {
-            double sq = 0.0;
-            for (int i = d.L.taskoff[n]; i < d.L.taskoff[n + 1]; ++i) sq += nr[i];
-            total += sqrt(sq);
-        }
-        sm.bcast[1] = total;
+    const double* nr = slot_nrm(d);
+    double total = 0.0;
+    for (int n = 0; n < d.L.order; ++n) {
+        double v = 0.0;
+        for (int i = d.L.taskoff[n] + threadIdx.x; i < d.L.taskoff[n + 1]; i += blockDim.x) v += __ldcg(nr + i);
+        total += sqrt(cta_sum(sm, v));
     }
-    __syncthreads();
-    const double v = sm.bcast[1];
-    __syncthreads();
-    return v;
+    return total;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__ Dev d) {
     __shared__ RedSmem sm;
     const CgParams& p = d.p;
     const unsigned nb = gridDim.x;
+    unsigned int round = 0;
     if (d.mode == 1) {
         // U = H W: W in W[0]; B_p from W then Q
         phase_a(d, sm, p.W[0], p.W[1], 0.0, false);
-        grid_barrier(p.barrier, nb);
+        grid_barrier(p.barrier, nb, round);
         phase_b(d, sm, p.W[0], p.Q);
         return;
     }
     // init: R = -G, Z = R Pinv, V = 0
     phase_c(d, sm, p.W[0], p.Rr[0], p.Rr[1], 0.0, true);
-    grid_barrier(p.barrier, nb);
+    grid_barrier(p.barrier, nb, round);
     int rc = 1;  // current residual buffer
     int wc = 0;  // current direction buffer (W_old)
     int it = 0;
@@ -333,9 +319,9 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
         }
         phase_a(d, sm, p.W[wc], p.W[wc ^ 1], beta, first);
         wc ^= 1;
-        grid_barrier(p.barrier, nb);
+        grid_barrier(p.barrier, nb, round);
         phase_b(d, sm, p.W[wc], p.Q);
-        grid_barrier(p.barrier, nb);
+        grid_barrier(p.barrier, nb, round);
         wq = sum_slots(sm, slot_wq(d), d.L.tasksBC);
         if (!(wq > 0.0)) {
             breakdown = 1;
@@ -344,7 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
         const double alpha = rz / wq;
         phase_c(d, sm, p.W[wc], p.Rr[rc], p.Rr[rc ^ 1], alpha, false);
         rc ^= 1;
-        grid_barrier(p.barrier, nb);
+        grid_barrier(p.barrier, nb, round);
         ++it;
         first = false;
     }
