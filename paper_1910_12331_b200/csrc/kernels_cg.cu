@@ -80,6 +80,39 @@ __device__ __forceinline__ double* slot_rz(const Dev& d) { return d.p.slots + d.
 __device__ __forceinline__ double* slot_nrm(const Dev& d) { return d.p.slots + 2 * d.L.tasksBC; }
 __device__ __forceinline__ double* slot_fin(const Dev& d) { return d.p.slots + 3 * d.L.tasksBC; }
 __device__ __forceinline__ double* bpart(const Dev& d) { return d.p.slots + 4 * d.L.tasksBC; }
+// D_n^T blocks (order x R x R) after the ksplit partial slabs of B_p
+__device__ __forceinline__ double* dt_buf(const Dev& d) {
+    return bpart(d) + static_cast<long long>(d.L.ksplit) * d.L.order * d.L.R * d.L.R;
+}
+
+// ---- phase A2: Bsum_p = sum_ks Bpart; D_n^T[z][r] = sum_{p != n} Gamma(n,p)[r][z] Bsum_p[r][z]
+// (gauss_newton.cpp:114-121 d = gamma(n,p) o (A_p^T W_p), folded over p once)
+__device__ void phase_a2(const Dev& d) {
+    const CgParams& p = d.p;
+    const Layout& L = d.L;
+    const int R = L.R, N = L.order;
+    const long long RR = static_cast<long long>(R) * R;
+    const double* bp = bpart(d);
+    double* dt = dt_buf(d);
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < RR;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(e / R), z = static_cast<int>(e % R);
+        double bs[kMaxOrder];
+        for (int q = 0; q < N; ++q) {
+            double b = 0.0;
+            for (int ks = 0; ks < L.ksplit; ++ks) b += __ldcg(bp + (static_cast<long long>(ks) * N + q) * RR + e);
+            bs[q] = b;
+        }
+        for (int n = 0; n < N; ++n) {
+            double dsum = 0.0;
+            for (int q = 0; q < N; ++q) {
+                if (q == n) continue;
+                dsum += p.pair[(n * N + q) * RR + e] * bs[q];
+            }
+            dt[n * RR + static_cast<long long>(z) * R + r] = dsum;
+        }
+    }
+}
 
 // ---- phase A: W' = Z + beta W_old (first: W' = Z; matvec: W' = W_in), B_p partials
 __device__ void phase_a(const Dev& d, RedSmem& sm, const double* Wold, double* Wnew, double beta,
@@ -156,16 +189,7 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
             const int r = c0 + col;
             if (r >= R) return 0.0;
             if (kk < R) return Gnn[kk * R + r];
-            const int z = kk - R;
-            double dsum = 0.0;
-            for (int q = 0; q < L.order; ++q) {
-                if (q == n) continue;
-                double b = 0.0;
-                for (int ks = 0; ks < L.ksplit; ++ks)
-                    b += __ldcg(bpart(d) + (static_cast<long long>(ks) * L.order + q) * RR + r * R + z);
-                dsum += p.pair[(n * L.order + q) * RR + r * R + z] * b;
-            }
-            return dsum;
+            return __ldcg(dt_buf(d) + n * RR + static_cast<long long>(kk - R) * R + r);
         };
         double acc[4];
         tile_gemm_panel(cg_panel_smem, 2 * R, la, lb, acc);
@@ -285,6 +309,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
         // U = H W: W in W[0]; B_p from W then Q
         phase_a(d, sm, p.W[0], p.W[1], 0.0, false);
         grid_barrier(p.barrier, nb, round);
+        phase_a2(d);
+        grid_barrier(p.barrier, nb, round);
         phase_b(d, sm, p.W[0], p.Q);
         return;
     }
@@ -319,6 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
         }
         phase_a(d, sm, p.W[wc], p.W[wc ^ 1], beta, first);
         wc ^= 1;
+        grid_barrier(p.barrier, nb, round);
+        phase_a2(d);
         grid_barrier(p.barrier, nb, round);
         phase_b(d, sm, p.W[wc], p.Q);
         grid_barrier(p.barrier, nb, round);
@@ -359,7 +387,7 @@ Layout make_layout(const CgParams& p, int grid) {
     L.taskoff[p.order] = off;
     L.tasksBC = off;
     const int base = p.order * L.tr * L.tr;
-    int ks = std::max(1, (grid + base - 1) / base);
+    int ks = std::max(1, grid / base);  // one round of the grid
     ks = static_cast<int>(std::min<long long>(ks, std::max<long long>(1, smax / 32)));
     L.ksplit = ks;
     L.tasksA = base * ks;
@@ -394,7 +422,7 @@ std::size_t cg_slots_needed(const CgParams& p) {
     for (int n = 0; n < p.order; ++n) smax = std::max<long long>(smax, p.rows[n]);
     const long long ksmax = std::max<long long>(1, smax / 32);
     return static_cast<std::size_t>(4 * L.tasksBC) +
-           static_cast<std::size_t>(ksmax) * p.order * p.R * p.R;
+           static_cast<std::size_t>(ksmax + 1) * p.order * p.R * p.R;
 }
 
 void run_cg(const CgParams& p, int grid, cudaStream_t st) {
