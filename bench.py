@@ -62,7 +62,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -213,17 +213,18 @@ def run_b200(args, rank, world, local_rank):
 
     peak_dmma = cpkit.probe_dmma_peak(local_rank)
 
-    # ---- warm-up, then exactly K timed sweeps (CUDA events on the problem's stream)
-    p.time_als_sweeps(0.0, max(1, args.warmup))
-    p.set_factors(init)
-    barrier()
-    launches0 = cpkit.kernel_launches()
-    p.profile(True)
+    # ---- warm-up, then exactly K timed sweeps (CUDA events on the problem's stream);
+    # clocks are sampled from just before the warm-up through the timed region
     with ClockSampler(local_rank) as clk:
+        p.time_als_sweeps(0.0, max(1, args.warmup))
+        p.set_factors(init)
+        barrier()
+        launches0 = cpkit.kernel_launches()
+        p.profile(True)
         ms = p.time_als_sweeps(0.0, args.steps)
-    prof_ms, prof_cnt = p.profile_read()
-    p.profile(False)
-    launches = cpkit.kernel_launches() - launches0
+        prof_ms, prof_cnt = p.profile_read()
+        p.profile(False)
+        launches = cpkit.kernel_launches() - launches0
     barrier()
     ms = max_over_ranks(ms)
     value = args.steps / (ms / 1e3)
@@ -233,7 +234,7 @@ def run_b200(args, rank, world, local_rank):
     root_ms = (prof_ms[0] + prof_ms[1]) / max(1, prof_cnt[0] + prof_cnt[1])
     achieved_tf = flops_per_root / (root_ms * 1e-3) / 1e12
     share = (prof_ms[0] + prof_ms[1]) / ms if ms > 0 else None
-    traffic = ncu_traffic().get("root_gemm_dram_bytes_per_launch")
+    traffic = ncu_traffic().get("root_gemm_dram_bytes_per_launch")  # committed ncu --set full capture
 
     # ---- secondary kernels: J^T J v (GN inner loop) and ||X||^2 streaming
     peaks = measured_peaks()
@@ -317,7 +318,7 @@ def run_b200(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)

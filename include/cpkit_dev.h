@@ -131,6 +131,10 @@ CPKIT_API cpkit_status cpkit_dev_random_factors(const uint64_t* dims, uint64_t o
                                                 double* out);
 CPKIT_API uint64_t cpkit_dev_problem_seed(uint64_t master, int rank, int problem);
 CPKIT_API uint64_t cpkit_dev_init_seed(uint64_t master, int rank, int problem, int init);
+/* Rows [lo, hi) of a last-mode extent owned by `shard` of `world` (the
+ * balanced contiguous split used by cpkit_dev_problem_create_sharded). */
+CPKIT_API cpkit_status cpkit_dev_shard_range(uint64_t extent, int shard, int world, uint64_t* lo,
+                                             uint64_t* hi);
 /* Device tensor slab back to host. */
 CPKIT_API cpkit_status cpkit_dev_download_tensor(cpkit_dev_problem* p, double* host_local);
 /* Number of kernels this library launched since load (for the bench). */

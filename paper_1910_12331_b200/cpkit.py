@@ -47,7 +47,7 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_profile_read", "cpkit_dev_time_jtj",
     "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
     "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
-    "cpkit_dev_init_seed", "cpkit_dev_download_tensor",
+    "cpkit_dev_init_seed", "cpkit_dev_download_tensor", "cpkit_dev_shard_range",
 )
 
 
@@ -506,6 +506,13 @@ def random_factors(dims, rank, seed, kind="uniform", a=0.0, b=1.0):
                                          0 if kind == "uniform" else 1, C.c_double(a),
                                          C.c_double(b), _ptr(out)))
     return unstack(out, dims, rank)
+
+
+def shard_range(extent: int, shard: int, world: int):
+    """Rows [lo, hi) of the last mode owned by `shard` (no GPU needed)."""
+    lo, hi = C.c_uint64(), C.c_uint64()
+    _chk(load().cpkit_dev_shard_range(_u64(extent), shard, world, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def problem_seed(master: int, rank: int, problem: int) -> int:

@@ -1025,6 +1025,11 @@ cpkit_status cpkit_dev_random_factors(const uint64_t* dims, uint64_t order, uint
         model_to_stacked(m, out);
     });
 }
+cpkit_status cpkit_dev_shard_range(uint64_t extent, int shard, int world, uint64_t* lo, uint64_t* hi) {
+    DEV_REQ(lo && hi && world >= 1 && shard >= 0 && shard < world);
+    cpkit::shard_range(extent, shard, world, lo, hi);
+    return CPKIT_OK;
+}
 uint64_t cpkit_dev_problem_seed(uint64_t master, int rank, int problem) {
     return cpkit::problem_seed(master, rank, problem);
 }

@@ -1,0 +1,109 @@
+"""Golden fixtures (tests/golden/golden_r01.json, made by make_golden.py from the
+KAT-pinned oracle): the oracle must keep reproducing them (CPU), and the device
+path must match them (GPU) at the parity tolerances."""
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def gold():
+    with open(os.path.join(HERE, "golden", "golden_r01.json")) as fh:
+        return json.load(fh)
+
+
+def hexd(v):
+    return struct.pack(">d", float(v)).hex()
+
+
+def blocks(flat_list, dims, rank):
+    return [np.asarray(a).reshape(d, rank) for a, d in zip(flat_list, dims)]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=float).ravel(), np.asarray(b, dtype=float).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+# ------------------------------------------------------------------ oracle (CPU)
+def test_oracle_rng_and_seeds_bitwise(orc, gold):
+    for k, v in gold["rng"].items():
+        name, args = k.split("(")
+        args = [int(a) for a in args.rstrip(")").split(",")]
+        if name == "mix64":
+            assert orc.mix64(args[0]) == v
+        elif name == "keyed":
+            assert orc.keyed(*args) == v
+        elif name == "uniform":
+            assert hexd(orc.uniform(*args, 0.0, 1.0)) == v
+        elif name == "gaussian":
+            assert hexd(orc.gaussian(*args)) == v
+    for k, v in gold["seeds"].items():
+        name, args = k.split("(")
+        args = [int(a) for a in args.rstrip(")").split(",")]
+        assert (orc.problem_seed(*args) if name == "problem_seed" else orc.init_seed(*args)) == v
+
+
+def test_oracle_reproduces_small_problem(orc, gold):
+    s = gold["small"]
+    dims, R = s["dims"], s["rank"]
+    truth = blocks(s["truth"], dims, R)
+    x = orc.reconstruct(truth)
+    assert [hexd(v) for v in x.ravel()[:8]] == s["x_hex_first8"]
+    assert np.array_equal(x.ravel(), np.asarray(s["x"]))
+    init = blocks(s["init"], dims, R)
+    ms, cnt = orc.mttkrp_tree_all(x, init)
+    assert cnt == s["contractions"]
+    for a, b in zip(ms, s["mttkrp"]):
+        assert rel(a, b) < 1e-14
+    _, recs, st = orc.gn_optimize(x, init, orc.GnConfig(max_iters=30))
+    assert st == s["gn_trace"]["status"] and len(recs) == len(s["gn_trace"]["records"])
+    for a, b in zip(recs, s["gn_trace"]["records"]):
+        assert a["cg_iters"] == b["cg_iters"] and abs(a["residual"] - b["residual"]) < 1e-14
+
+
+# ------------------------------------------------------------------ device (GPU)
+@pytest.mark.gpu
+def test_device_matches_golden(gold):
+    from paper_1910_12331_b200 import cpkit
+    s = gold["small"]
+    dims, R = s["dims"], s["rank"]
+    x = np.asarray(s["x"]).reshape(dims)
+    init = blocks(s["init"], dims, R)
+    # generator parity: device reconstruct of the truth model is bitwise equal
+    p = cpkit.DeviceProblem(dims, R)
+    p.generate(blocks(s["truth"], dims, R))
+    assert np.array_equal(p.download().ravel(), x.ravel())
+    assert cpkit.random_factors(dims, R, gold["seeds"]["problem_seed(0,5,0)"] * 0 +
+                                cpkit.problem_seed(0, R, 0))[0].ravel().tolist() == s["truth"][0]
+    p.upload(x)
+    p.set_factors(init)
+    assert abs(p.norm2() - s["xnorm2"]) <= 1e-14 * s["xnorm2"]
+    for n in range(len(dims)):
+        assert rel(p.mttkrp(n), s["mttkrp"][n]) < 1e-11
+    assert p.full_contractions == s["contractions"]
+    g, pr = p.gamma_set()
+    assert rel(g, s["grams"]) < 1e-11 and rel(pr, s["pairwise"]) < 1e-11
+    r, f = p.residual(s["xnorm2"])
+    assert abs(r - s["residual"][0]) < 1e-12
+    grad = p.gradient()
+    assert rel(np.concatenate([a.ravel() for a in grad]), np.concatenate(s["gradient"])) < 1e-11
+    mv = p.jtj_matvec(blocks(s["w"], dims, R), s["matvec_lambda"])
+    assert rel(np.concatenate([a.ravel() for a in mv]), np.concatenate(s["matvec"])) < 1e-11
+    v, it, cap, bd = p.cp_cg(grad, s["cg"]["lambda"])
+    assert (it, cap, bd) == (s["cg"]["iterations"], s["cg"]["hit_cap"], s["cg"]["breakdown"])
+    assert rel(np.concatenate([a.ravel() for a in v]), np.concatenate(s["cg"]["v"])) < 1e-9
+    _, rep = p.optimize({"optimizer": "gn", "gn": {"max_iters": 30}}, init)
+    j = rep.to_json()
+    assert j["status"] == s["gn_trace"]["status"]
+    assert [rr["cg_iters"] for rr in j["records"]] == [rr["cg_iters"] for rr in s["gn_trace"]["records"]]
+    assert abs(j["records"][-1]["fitness"] - s["gn_trace"]["records"][-1]["fitness"]) < 1e-8
+    _, rep = p.optimize({"optimizer": "als", "als": {"max_sweeps": 30}}, init)
+    j = rep.to_json()
+    assert j["status"] == s["als_trace"]["status"] and len(j["records"]) == len(s["als_trace"]["records"])
+    assert abs(j["records"][-1]["fitness"] - s["als_trace"]["records"][-1]["fitness"]) < 1e-8
