@@ -50,3 +50,18 @@ def mttkrp_unfold(x, factors, mode):
         if m != mode:
             kr = khatri_rao(kr, f)
     return matricize(x, mode) @ kr
+
+
+def swamp_factors(orc, dims, rank, seed, c=0.9):
+    """BASELINE config 3 ("swamp"): column r of mode n is sqrt(c) u_n + sqrt(1-c) v_{n,r},
+    normalised; u, v ~ N(0,1) from the keyed RNG on streams 0x5701+n / 0x5801+n."""
+    out = []
+    for n, s in enumerate(dims):
+        u = np.array([orc.gaussian(seed, 0x5701 + n, i) for i in range(s)])
+        a = np.empty((s, rank))
+        for r in range(rank):
+            v = np.array([orc.gaussian(seed, 0x5801 + n, r * s + i) for i in range(s)])
+            col = np.sqrt(c) * u + np.sqrt(1 - c) * v
+            a[:, r] = col / np.linalg.norm(col)
+        out.append(a)
+    return out
