@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 
 #include "common.h"
 
@@ -395,18 +396,27 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
         // second warp column when that leaves fewer than 8 DMMA warps.
         p.wm = pick_wm(M, 4, 8);
         p.wn = (p.wm <= 5 && n8 >= 8) ? 2 : 1;
-        if (const char* e = std::getenv("CPKIT_TN_WN")) p.wn = std::atoi(e);
+
     } else {
         p.wn = n8 > 16 ? 2 : 1;
         p.wm = p.wn == 2 ? 4 : pick_wm(M, 6, 8);
     }
+    // tuning overrides (experiments only): CPKIT_{NN,TN}_{WM,WN,NTW,STAGES}
+    auto env = [&](const char* key, int& v) {
+        const std::string name = std::string(trans ? "CPKIT_TN_" : "CPKIT_NN_") + key;
+        if (const char* e = std::getenv(name.c_str())) v = std::atoi(e);
+    };
+    env("WM", p.wm);
+    env("WN", p.wn);
     p.ntw = round_ntw((n8 + p.wn - 1) / p.wn);
+    env("NTW", p.ntw);
     p.bns = bns_for(p.BN(), trans);
     p.stages = 2;
     for (int s = 6; s >= 2; --s) {
         p.stages = s;
         if (smem_bytes(p) <= 225 * 1024) break;
     }
+    env("STAGES", p.stages);
     p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
     p.splits = 1;
     p.kps = K;
