@@ -149,25 +149,36 @@ struct KrpDev {
 };
 
 // KRP[k][r] = prod_j fac_j[i_j(k), r] for k < K, r < R; zero for R <= r < Rs.
-// Streams K x Rs doubles once per contraction (HBM-bound, coalesced writes).
-__global__ void krp_fill_kernel(KrpDev kd, long long K, int R, int Rs, double* __restrict__ out) {
-    const long long total = K * Rs;
-    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
-         e += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long k = e / Rs;
-        const int r = static_cast<int>(e - k * Rs);
-        double v = 0.0;
-        if (r < R) {
-            long long rem = k;
-            v = 1.0;
-            for (int j = kd.nmodes - 1; j >= 0; --j) {
-                const long long ext = kd.ext[j];
-                const long long i = rem % ext;
-                rem /= ext;
-                v *= kd.fac[j][i * R + r];
-            }
+// One warp per output row (index decomposition once per row), lanes over r
+// with 16-byte stores; streams K x Rs doubles once per contraction.
+__global__ void __launch_bounds__(256) krp_fill_kernel(KrpDev kd, long long K, int R, int Rs,
+                                                       double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    const int pairs = Rs / 2;  // Rs is even
+    for (long long k = blockIdx.x * static_cast<long long>(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += warps) {
+        const double* rowp[kMaxOrder];
+        long long rem = k;
+        for (int j = kd.nmodes - 1; j >= 0; --j) {
+            const long long ext = kd.ext[j];
+            const long long i = rem % ext;
+            rem /= ext;
+            rowp[j] = kd.fac[j] + i * R;
         }
-        out[e] = v;
+        double2* dst = reinterpret_cast<double2*>(out + k * Rs);
+        for (int c = lane; c < pairs; c += 32) {
+            const int r = 2 * c;
+            double v0 = 0.0, v1 = 0.0;
+            if (r < R) {
+                v0 = __ldg(rowp[0] + r);
+                for (int j = 1; j < kd.nmodes; ++j) v0 *= __ldg(rowp[j] + r);
+            }
+            if (r + 1 < R) {
+                v1 = __ldg(rowp[0] + r + 1);
+                for (int j = 1; j < kd.nmodes; ++j) v1 *= __ldg(rowp[j] + r + 1);
+            }
+            dst[c] = make_double2(v0, v1);
+        }
     }
 }
 
@@ -425,11 +436,24 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
     const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
     const long long slots = static_cast<long long>(num_sms()) * per_sm;
-    if (base < slots) {
+    if (base < 4 * slots) {
+        // choose the split count with the best wave efficiency (<= 2 waves),
+        // keeping >= 8 k-stages per split; ties go to fewer splits
         const long long kchunks = (K + kBK - 1) / kBK;
-        long long splits = std::max<long long>(1, slots / base);  // never exceed one wave
-        splits = std::min<long long>(splits, std::max<long long>(1, kchunks / 4));
-        p.kps = ((kchunks + splits - 1) / splits) * kBK;  // multiple of kBK: splits never share a stage
+        long long best = 1;
+        double best_eff = -1.0;
+        for (long long sp = 1; sp <= 64; ++sp) {
+            if (sp > 1 && kchunks / sp < 8) break;
+            const long long ctas = base * sp;
+            const long long waves = (ctas + slots - 1) / slots;
+            if (waves > std::max<long long>(2, (base + slots - 1) / slots)) break;
+            const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
+            if (eff > best_eff + 1e-9) {
+                best_eff = eff;
+                best = sp;
+            }
+        }
+        p.kps = ((kchunks + best - 1) / best) * kBK;  // multiple of kBK: splits never share a stage
         p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
     }
     return p;
@@ -462,8 +486,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
 // Fill the KRP operand (K x Rs, Rs = R rounded to even) for a contraction.
 void fill_krp(const KrpDesc& kd, long long K, int R, double* krp, cudaStream_t st) {
     const int Rs = (R + 1) & ~1;
-    const long long total = K * Rs;
-    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 16LL * num_sms()));
+    const int blocks = static_cast<int>(std::min<long long>((K + 7) / 8, 16LL * num_sms()));
     krp_fill_kernel<<<blocks, 256, 0, st>>>(to_dev(kd), K, R, Rs, krp);
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
