@@ -84,9 +84,13 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
                         break;
                     }
                     const double l = sqrt(x);
+                    const double inv = 1.0 / l;
                     __syncwarp();
-                    for (int i = j + 1 + tx; i < R; i += 32) w[i * LD + j] /= l;
-                    if (tx == 0) w[j * LD + j] = l;
+                    for (int i = j + 1 + tx; i < R; i += 32) w[i * LD + j] *= inv;
+                    if (tx == 0) {
+                        w[j * LD + j] = l;
+                        w[j * LD + R] = inv;  // padding column keeps 1 / L_jj for the solves
+                    }
                     __syncwarp();
                     for (int i = j + 1 + tx; i < R; i += 32) {
                         const double lij = w[i * LD + j];
@@ -115,12 +119,15 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
         __syncthreads();
     }
     if (kSmem)
-        for (int i = ty; i < R; i += ny)
+        for (int i = ty; i < R; i += ny) {
             for (int k = tx; k <= i; k += 32) out[i * LD + k] = w[i * LD + k];
+            if (tx == 0) out[i * LD + R] = w[i * LD + R];
+        }
     if (threadIdx.x == 0) status[mat] = st;
 }
 
-// One warp per rhs row: solve (L L^T) y = b, L lower with row stride LD.
+// One warp per rhs row: solve (L L^T) y = b, L lower with row stride LD;
+// column R of each row holds 1 / L_ii (written by chol_kernel).
 constexpr int kMaxBlk = 16;  // R <= 512
 constexpr int kSolveWarps = 8;
 template <bool kSmem>
@@ -133,8 +140,10 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
     const long long mat = blockIdx.y;
     const double* Lg = l_all + mat * l_stride;
     if (kSmem) {
-        for (int i = warp; i < R; i += kSolveWarps)
+        for (int i = warp; i < R; i += kSolveWarps) {
             for (int k = lane; k <= i; k += 32) lsh[i * LD + k] = Lg[i * LD + k];
+            if (lane == 0) lsh[i * LD + R] = Lg[i * LD + R];
+        }
         __syncthreads();
     }
     const double* L = kSmem ? lsh : Lg;
@@ -156,7 +165,7 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
                 const int iend = min(32, R - 32 * cb);
                 for (int il = 0; il < iend; ++il) {
                     const int i = 32 * cb + il;
-                    const double zi = __shfl_sync(0xffffffffu, v[cb], il) / L[i * LD + i];
+                    const double zi = __shfl_sync(0xffffffffu, v[cb], il) * L[i * LD + R];
                     if (lane == il) v[cb] = zi;
                     if (lane > il && lane + 32 * cb < R) v[cb] -= L[(lane + 32 * cb) * LD + i] * zi;
 #pragma unroll
@@ -174,7 +183,7 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
                 const int iend = min(32, R - 32 * cb);
                 for (int il = iend - 1; il >= 0; --il) {
                     const int i = 32 * cb + il;
-                    const double yi = __shfl_sync(0xffffffffu, v[cb], il) / L[i * LD + i];
+                    const double yi = __shfl_sync(0xffffffffu, v[cb], il) * L[i * LD + R];
                     if (lane == il) v[cb] = yi;
                     if (lane < il) v[cb] -= L[i * LD + lane + 32 * cb] * yi;
 #pragma unroll
