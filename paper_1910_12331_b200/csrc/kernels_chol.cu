@@ -5,13 +5,16 @@
 // the diagonal, else SingularSystem. spd_solve returns Y with
 // Y (S + lambda I) = B, spd_inverse the symmetrised inverse.
 //
-// Device design: L is kept as a dense square with odd row stride LD = R + 1
-// (row and column walks both conflict-free in shared memory). One CTA per
-// matrix factorises right-looking (each of the R steps is a 2-D parallel
-// rank-1 trailing update) in shared memory when LD * R fits, else in the
-// L2-resident global output. Solves run one warp per right-hand-side row,
-// lanes owning rhs entries in registers, L staged once per CTA in shared
-// memory, the 32-step blocks unrolled so every register index is static.
+// Device design. The factor L lives in global memory as a dense square with
+// odd row stride LD = R + 1; column R of row i holds 1 / L_ii so the solves
+// multiply instead of divide. One CTA factorises one matrix in shared memory
+// (square layout up to R ~ 165, packed lower triangle up to R ~ 233, global
+// square beyond), right-looking with ONE barrier per column: every thread
+// recomputes the pivot from shared memory, the rank-1 trailing update uses the
+// unscaled column and 1 / pivot, and the column is scaled one step later (no
+// later step reads it). Solves run one warp per right-hand-side row with the
+// rhs in registers, L staged in shared memory, and the block count NB a
+// template parameter so no predicated-off work is issued.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -22,15 +25,34 @@ namespace cpkit {
 
 namespace {
 
-constexpr std::size_t kSmemBudget = 200 * 1024;
+constexpr std::size_t kSmemBudget = 220 * 1024;
 
 inline int lda_of(int R) { return R + 1; }
-inline bool chol_in_smem(int R) { return static_cast<std::size_t>(R) * lda_of(R) * 8 <= kSmemBudget; }
+
+// Index maps. Square: row stride LD, inverse pivots in column R.
+// Packed: lower triangle row-major, inverse pivots after it.
+struct SqIdx {
+    int LD, R;
+    __device__ __forceinline__ int at(int i, int k) const { return i * LD + k; }
+    __device__ __forceinline__ int inv(int i) const { return i * LD + R; }
+};
+struct PkIdx {
+    int LD, R;  // LD unused
+    __device__ __forceinline__ int at(int i, int k) const { return ((i * (i + 1)) >> 1) + k; }
+    __device__ __forceinline__ int inv(int i) const { return ((R * (R + 1)) >> 1) + i; }
+};
+inline std::size_t sq_bytes(int R) { return static_cast<std::size_t>(R) * lda_of(R) * 8; }
+inline std::size_t pk_bytes(int R) { return (static_cast<std::size_t>(R) * (R + 1) / 2 + R) * 8; }
+enum Layout { kSquareSmem = 0, kPackedSmem = 1, kGlobal = 2 };
+inline Layout layout_of(int R) {
+    if (sq_bytes(R) <= kSmemBudget) return kSquareSmem;
+    if (pk_bytes(R) <= kSmemBudget) return kPackedSmem;
+    return kGlobal;
+}
 
 // mode 0: A = S + lambda I; mode 1: A = S with diag *= (1 + lambda), lambda'=0.
 // Jitter trace uses the matrix handed to factor_shifted (gauss_newton.cpp:190-207).
-// kSmem selects the working copy's address space at compile time (LDS/STS).
-template <bool kSmem>
+template <class Idx, bool kSmem>
 __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_all, int R, double lambda, int mode,
                                                    double* __restrict__ l_all, int* __restrict__ status) {
     extern __shared__ double sh[];
@@ -39,8 +61,8 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
     const double* s = s_all + static_cast<long long>(mat) * R * R;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     double* w = kSmem ? sh : out;
+    const Idx ix{LD, R};
     __shared__ double trace_sh;
-    __shared__ int fail_sh;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
 
     if (ty == 0) {  // trace, warp-parallel (fixed shuffle order)
@@ -56,7 +78,7 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
     __syncthreads();
     const double jitter = 1e-12 * trace_sh / static_cast<double>(R);
 
-    int st = 0;
+    int st = 2;
     for (int attempt = 0; attempt < 2; ++attempt) {
         const double add = (mode == 0 ? lambda : 0.0);
         for (int i = ty; i < R; i += ny)
@@ -67,70 +89,55 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
                     v += add;
                     if (attempt == 1) v += jitter;
                 }
-                w[i * LD + k] = v;
+                w[ix.at(i, k)] = v;
             }
-        if (threadIdx.x == 0) fail_sh = 0;
         __syncthreads();
-        // blocked right-looking: warp 0 factors a kNb-column panel with warp-level
-        // syncs only, then all warps apply the rank-kNb trailing update.
-        constexpr int kNb = 16;
-        for (int j0 = 0; j0 < R && !fail_sh; j0 += kNb) {
-            const int j1 = min(R, j0 + kNb);
-            if (ty == 0) {
-                for (int j = j0; j < j1; ++j) {
-                    const double x = w[j * LD + j];
-                    if (!(x > 0.0) && !isnan(x)) {  // Eigen LLT: fail iff pivot <= 0
-                        if (tx == 0) fail_sh = 1;
-                        break;
-                    }
-                    const double l = sqrt(x);
-                    const double inv = 1.0 / l;
-                    __syncwarp();
-                    for (int i = j + 1 + tx; i < R; i += 32) w[i * LD + j] *= inv;
-                    if (tx == 0) {
-                        w[j * LD + j] = l;
-                        w[j * LD + R] = inv;  // padding column keeps 1 / L_jj for the solves
-                    }
-                    __syncwarp();
-                    for (int i = j + 1 + tx; i < R; i += 32) {
-                        const double lij = w[i * LD + j];
-                        const int kend = min(j1, i + 1);
-                        for (int k = j + 1; k < kend; ++k) w[i * LD + k] -= lij * w[k * LD + j];
-                    }
-                    __syncwarp();
-                }
+        bool failed = false;
+        double inv_prev = 0.0;
+        for (int j = 0; j < R; ++j) {
+            // every thread reads the pivot (no serial hand-off, uniform branch)
+            const double x = w[ix.at(j, j)];
+            if (!(x > 0.0) && !isnan(x)) {  // Eigen LLT: fail iff pivot <= 0
+                failed = true;
+                break;
+            }
+            const double l = sqrt(x);
+            const double inv = 1.0 / l;
+            const double inv2 = inv * inv;
+            // scale column j-1 (no later step reads it)
+            if (j > 0)
+                for (int i = j + threadIdx.x; i < R; i += blockDim.x) w[ix.at(i, j - 1)] *= inv_prev;
+            // trailing update with the unscaled column j: a_ik -= a_ij a_kj / pivot
+            for (int i = j + 1 + ty; i < R; i += ny) {
+                const double aij = w[ix.at(i, j)] * inv2;
+                for (int k = j + 1 + tx; k <= i; k += 32) w[ix.at(i, k)] -= aij * w[ix.at(k, j)];
             }
             __syncthreads();
-            if (fail_sh) break;
-            // trailing update a_ik -= sum_{j in panel} l_ij l_kj, j1 <= k <= i
-            for (int i = j1 + ty; i < R; i += ny)
-                for (int k = j1 + tx; k <= i; k += 32) {
-                    double acc = w[i * LD + k];
-                    for (int j = j0; j < j1; ++j) acc -= w[i * LD + j] * w[k * LD + j];
-                    w[i * LD + k] = acc;
-                }
-            __syncthreads();
+            if (threadIdx.x == 0) {
+                w[ix.at(j, j)] = l;
+                w[ix.inv(j)] = inv;
+            }
+            inv_prev = inv;
         }
-        if (!fail_sh) {
+        __syncthreads();
+        if (!failed) {
             st = attempt;  // 0 ok, 1 ok after jitter
             break;
         }
-        st = 2;
-        __syncthreads();
     }
     if (kSmem)
         for (int i = ty; i < R; i += ny) {
-            for (int k = tx; k <= i; k += 32) out[i * LD + k] = w[i * LD + k];
-            if (tx == 0) out[i * LD + R] = w[i * LD + R];
+            for (int k = tx; k <= i; k += 32) out[i * LD + k] = w[ix.at(i, k)];
+            if (tx == 0) out[i * LD + R] = w[ix.inv(i)];
         }
     if (threadIdx.x == 0) status[mat] = st;
 }
 
-// One warp per rhs row: solve (L L^T) y = b, L lower with row stride LD;
-// column R of each row holds 1 / L_ii (written by chol_kernel).
-constexpr int kMaxBlk = 16;  // R <= 512
+// One warp per rhs row: solve (L L^T) y = b. L lower, row stride LD (global),
+// staged into shared memory with layout Idx; 1 / L_ii at ix.inv(i). NB =
+// number of 32-entry blocks of the rhs (R <= 32 NB).
 constexpr int kSolveWarps = 8;
-template <bool kSmem>
+template <int NB, class Idx, bool kSmem>
 __global__ void __launch_bounds__(32 * kSolveWarps)
 chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __restrict__ b, long long rows,
                        double* __restrict__ y, long long l_stride, long long rows_per_mat) {
@@ -139,84 +146,116 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long mat = blockIdx.y;
     const double* Lg = l_all + mat * l_stride;
+    const Idx ix{LD, R};
     if (kSmem) {
-        for (int i = warp; i < R; i += kSolveWarps) {
-            for (int k = lane; k <= i; k += 32) lsh[i * LD + k] = Lg[i * LD + k];
-            if (lane == 0) lsh[i * LD + R] = Lg[i * LD + R];
+        // batch the global loads (8 in flight per thread) before the shared stores
+        const int total = R * LD;
+        for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * blockDim.x;
+                v[u] = (e < total) ? __ldg(Lg + e) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int e = e0 + u * blockDim.x;
+                if (e < total) {
+                    const int i = e / LD, k = e - i * LD;
+                    if (k <= i) lsh[ix.at(i, k)] = v[u];
+                    else if (k == R) lsh[ix.inv(i)] = v[u];
+                }
+            }
         }
         __syncthreads();
     }
-    const double* L = kSmem ? lsh : Lg;
-    const int nblk = (R + 31) / 32;
+    auto Lat = [&](int i, int k) -> double { return kSmem ? lsh[ix.at(i, k)] : Lg[i * LD + k]; };
+    auto Linv = [&](int i) -> double { return kSmem ? lsh[ix.inv(i)] : Lg[i * LD + R]; };
     for (long long local = blockIdx.x * kSolveWarps + warp; local < rows_per_mat;
          local += static_cast<long long>(gridDim.x) * kSolveWarps) {
         const long long row = mat * rows_per_mat + local;
         if (row >= rows) break;
-        double v[kMaxBlk];
+        double v[NB];
 #pragma unroll
-        for (int c = 0; c < kMaxBlk; ++c) {
+        for (int c = 0; c < NB; ++c) {
             const int k = lane + 32 * c;
-            v[c] = (c < nblk && k < R) ? b[row * R + k] : 0.0;
+            v[c] = (k < R) ? b[row * R + k] : 0.0;
         }
-        // forward: z_i = v_i / L_ii ; v_k -= L_ki z_i (k > i)   [column walk, stride LD]
+        // forward: z_i = v_i / L_ii ; v_k -= L_ki z_i (k > i)
 #pragma unroll
-        for (int cb = 0; cb < kMaxBlk; ++cb) {
-            if (cb < nblk) {
-                const int iend = min(32, R - 32 * cb);
-                for (int il = 0; il < iend; ++il) {
-                    const int i = 32 * cb + il;
-                    const double zi = __shfl_sync(0xffffffffu, v[cb], il) * L[i * LD + R];
-                    if (lane == il) v[cb] = zi;
-                    if (lane > il && lane + 32 * cb < R) v[cb] -= L[(lane + 32 * cb) * LD + i] * zi;
+        for (int cb = 0; cb < NB; ++cb) {
+            const int iend = min(32, R - 32 * cb);
+            for (int il = 0; il < iend; ++il) {
+                const int i = 32 * cb + il;
+                const double zi = __shfl_sync(0xffffffffu, v[cb], il) * Linv(i);
+                if (lane == il) v[cb] = zi;
+                if (lane > il && lane + 32 * cb < R) v[cb] -= Lat(lane + 32 * cb, i) * zi;
 #pragma unroll
-                    for (int c = cb + 1; c < kMaxBlk; ++c) {
-                        const int k = lane + 32 * c;
-                        if (c < nblk && k < R) v[c] -= L[k * LD + i] * zi;
-                    }
+                for (int c = cb + 1; c < NB; ++c) {
+                    const int k = lane + 32 * c;
+                    if (k < R) v[c] -= Lat(k, i) * zi;
                 }
             }
         }
-        // backward with L^T: y_i = v_i / L_ii ; v_k -= L_ik y_i (k < i)   [row walk]
+        // backward with L^T: y_i = v_i / L_ii ; v_k -= L_ik y_i (k < i)
 #pragma unroll
-        for (int cb = kMaxBlk - 1; cb >= 0; --cb) {
-            if (cb < nblk) {
-                const int iend = min(32, R - 32 * cb);
-                for (int il = iend - 1; il >= 0; --il) {
-                    const int i = 32 * cb + il;
-                    const double yi = __shfl_sync(0xffffffffu, v[cb], il) * L[i * LD + R];
-                    if (lane == il) v[cb] = yi;
-                    if (lane < il) v[cb] -= L[i * LD + lane + 32 * cb] * yi;
+        for (int cb = NB - 1; cb >= 0; --cb) {
+            const int iend = min(32, R - 32 * cb);
+            for (int il = iend - 1; il >= 0; --il) {
+                const int i = 32 * cb + il;
+                const double yi = __shfl_sync(0xffffffffu, v[cb], il) * Linv(i);
+                if (lane == il) v[cb] = yi;
+                if (lane < il) v[cb] -= Lat(i, lane + 32 * cb) * yi;
 #pragma unroll
-                    for (int c = 0; c < cb; ++c) v[c] -= L[i * LD + lane + 32 * c] * yi;
-                }
+                for (int c = 0; c < cb; ++c) v[c] -= Lat(i, lane + 32 * c) * yi;
             }
         }
 #pragma unroll
-        for (int c = 0; c < kMaxBlk; ++c) {
+        for (int c = 0; c < NB; ++c) {
             const int k = lane + 32 * c;
-            if (c < nblk && k < R) y[row * R + k] = v[c];
+            if (k < R) y[row * R + k] = v[c];
         }
     }
 }
 
-void solve_rows(const double* l, int R, const double* b, long long rows, double* y, long long l_stride,
-                int nmats, long long rows_per_mat, cudaStream_t st) {
-    const std::size_t bytes = static_cast<std::size_t>(R) * lda_of(R) * 8;
-    const bool smem = bytes <= kSmemBudget;
+template <int NB>
+void solve_rows_nb(const double* l, int R, const double* b, long long rows, double* y, long long l_stride, int nmats,
+                   long long rows_per_mat, cudaStream_t st) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const long long per_mat_ctas = std::max<long long>(
         1, std::min<long long>((rows_per_mat + kSolveWarps - 1) / kSolveWarps, std::max(1, 2 * sms / nmats)));
-    dim3 grid(static_cast<unsigned>(per_mat_ctas), nmats);
-    if (smem) {
-        CPK_CUDA(cudaFuncSetAttribute(chol_solve_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(bytes)));
-        chol_solve_rows_kernel<true><<<grid, 32 * kSolveWarps, bytes, st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+    const dim3 grid(static_cast<unsigned>(per_mat_ctas), nmats);
+    const Layout lay = layout_of(R);
+    if (lay == kSquareSmem) {
+        auto fn = chol_solve_rows_kernel<NB, SqIdx, true>;
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        fn<<<grid, 32 * kSolveWarps, sq_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+    } else if (lay == kPackedSmem) {
+        auto fn = chol_solve_rows_kernel<NB, PkIdx, true>;
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
+        fn<<<grid, 32 * kSolveWarps, pk_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
     } else {
-        chol_solve_rows_kernel<false><<<grid, 32 * kSolveWarps, 0, st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+        chol_solve_rows_kernel<NB, SqIdx, false><<<grid, 32 * kSolveWarps, 0, st>>>(l, R, b, rows, y, l_stride,
+                                                                                    rows_per_mat);
     }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
+}
+
+void solve_rows(const double* l, int R, const double* b, long long rows, double* y, long long l_stride, int nmats,
+                long long rows_per_mat, cudaStream_t st) {
+    switch ((R + 31) / 32) {
+        case 1: solve_rows_nb<1>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 2: solve_rows_nb<2>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 3: solve_rows_nb<3>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 4: solve_rows_nb<4>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 5: solve_rows_nb<5>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 6: solve_rows_nb<6>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 7: solve_rows_nb<7>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 8: solve_rows_nb<8>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        default: solve_rows_nb<16>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+    }
 }
 
 __global__ void identity_rows_kernel(double* __restrict__ out, int count, int R) {
@@ -245,15 +284,18 @@ std::size_t chol_factor_elems(int count, int R) { return static_cast<std::size_t
 
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode, double* l_out, int* status,
                        cudaStream_t st) {
-    if (R > 32 * kMaxBlk) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
-    const bool use_smem = chol_in_smem(R);
-    const std::size_t smem = use_smem ? static_cast<std::size_t>(R) * lda_of(R) * 8 : 0;
-    if (use_smem) {
-        CPK_CUDA(cudaFuncSetAttribute(chol_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        chol_kernel<true><<<count, 512, smem, st>>>(s, R, *lambda, mode, l_out, status);
+    if (R > 512) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
+    const Layout lay = layout_of(R);
+    if (lay == kSquareSmem) {
+        auto fn = chol_kernel<SqIdx, true>;
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        fn<<<count, 512, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
+    } else if (lay == kPackedSmem) {
+        auto fn = chol_kernel<PkIdx, true>;
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
+        fn<<<count, 512, pk_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
     } else {
-        chol_kernel<false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status);
+        chol_kernel<SqIdx, false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status);
     }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
