@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     double* w = kSmem ? sh : out;
     const Idx ix{LD, R};
-    __shared__ double trace_sh;
+    __shared__ double trace_sh, piv_sh[3];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
 
     if (ty == 0) {  // trace, warp-parallel (fixed shuffle order)
@@ -91,18 +91,23 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
                 }
                 w[ix.at(i, k)] = v;
             }
+        // pivot of column 0 (thread 0); later pivots are produced by thread 0,
+        // which owns element (j+1, j+1) of step j's trailing update
+        if (threadIdx.x == 0) {
+            const double x = w[ix.at(0, 0)];
+            piv_sh[0] = x;
+            piv_sh[1] = sqrt(x);
+            piv_sh[2] = 1.0 / piv_sh[1];
+        }
         __syncthreads();
         bool failed = false;
         double inv_prev = 0.0;
         for (int j = 0; j < R; ++j) {
-            // every thread reads the pivot (no serial hand-off, uniform branch)
-            const double x = w[ix.at(j, j)];
-            if (!(x > 0.0) && !isnan(x)) {  // Eigen LLT: fail iff pivot <= 0
+            const double x = piv_sh[0], l = piv_sh[1], inv = piv_sh[2];
+            if (!(x > 0.0) && !isnan(x)) {  // Eigen LLT: fail iff pivot <= 0 (uniform branch)
                 failed = true;
                 break;
             }
-            const double l = sqrt(x);
-            const double inv = 1.0 / l;
             const double inv2 = inv * inv;
             // scale column j-1 (no later step reads it)
             if (j > 0)
@@ -112,11 +117,18 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
                 const double aij = w[ix.at(i, j)] * inv2;
                 for (int k = j + 1 + tx; k <= i; k += 32) w[ix.at(i, k)] -= aij * w[ix.at(k, j)];
             }
-            __syncthreads();
+            __syncthreads();  // (j+1, j+1) is final; pivot slots are free to overwrite
             if (threadIdx.x == 0) {
                 w[ix.at(j, j)] = l;
                 w[ix.inv(j)] = inv;
+                if (j + 1 < R) {
+                    const double xn = w[ix.at(j + 1, j + 1)];
+                    piv_sh[0] = xn;
+                    piv_sh[1] = sqrt(xn);
+                    piv_sh[2] = 1.0 / piv_sh[1];
+                }
             }
+            __syncthreads();
             inv_prev = inv;
         }
         __syncthreads();
