@@ -202,7 +202,7 @@ template <int NTW, bool TRANS>
 __global__ void __launch_bounds__(32 * 11, 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  long long M, long long K, int R, int BM, int WN, int BNS, int stages, long long k_per_split,
-                 double* __restrict__ out, long long out_split_stride) {
+                 int splits, double* __restrict__ out, long long out_split_stride) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
@@ -217,13 +217,22 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     const int WM = BM / 16;
     const int W = WM * WN;  // DMMA warps; warp W is the producer
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN;
-    const long long m0 = static_cast<long long>(blockIdx.y) * BM;
-    const long long kbeg = static_cast<long long>(blockIdx.z) * k_per_split;
-    const long long kend = min(K, kbeg + k_per_split);
-    const int nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
     const int nboxes = TRANS ? BM / 16 : kBK / 16;
     const int box_rows = TRANS ? kBK : BM;
+    // persistent work loop: unit u -> (n-tile, m-tile, split), n fastest so the
+    // CTAs sharing an X row panel run together (L2 reuse)
+    const int ntiles = (R + BN - 1) / BN;
+    const long long mtiles = (M + BM - 1) / BM;
+    const long long units = static_cast<long long>(ntiles) * mtiles * splits;
+    auto unit_geom = [&](long long u, int& n0, long long& m0, long long& kbeg, int& nk, int& split) {
+        n0 = static_cast<int>(u % ntiles) * BN;
+        const long long rest = u / ntiles;
+        m0 = (rest % mtiles) * BM;
+        split = static_cast<int>(rest / mtiles);
+        kbeg = static_cast<long long>(split) * k_per_split;
+        const long long kend = min(K, kbeg + k_per_split);
+        nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -235,23 +244,29 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     __syncthreads();
 
     if (warp == W) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: one ring across all of this CTA's units
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&xmap)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
-            for (int kt = 0; kt < nk; ++kt) {
-                const int s = kt % stages;
-                if (kt >= stages) mbar_wait(&empty[s], ((kt / stages) - 1) & 1);
-                const int kk = static_cast<int>(kbeg + static_cast<long long>(kt) * kBK);
-                char* xs = smem + s * stage_bytes;
-                mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
-                for (int b = 0; b < nboxes; ++b) {
-                    if (TRANS)
-                        tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(m0 + 16 * b), kk);
-                    else
-                        tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, kk + 16 * b, static_cast<int>(m0));
+            long long it = 0;  // global stage counter
+            for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+                int n0, nk, split;
+                long long m0, kbeg;
+                unit_geom(u, n0, m0, kbeg, nk, split);
+                for (int kt = 0; kt < nk; ++kt, ++it) {
+                    const int s = static_cast<int>(it % stages);
+                    if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+                    const int kk = static_cast<int>(kbeg + static_cast<long long>(kt) * kBK);
+                    char* xs = smem + s * stage_bytes;
+                    mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
+                    for (int b = 0; b < nboxes; ++b) {
+                        if (TRANS)
+                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(m0 + 16 * b), kk);
+                        else
+                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, kk + 16 * b, static_cast<int>(m0));
+                    }
+                    tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, kk);
                 }
-                tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, kk);
             }
         }
         return;
@@ -262,9 +277,6 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp % WM) * 16;
     const int wn = warp / WM;
-    double acc[NTW][4];
-#pragma unroll
-    for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
     // per-lane constant parts of the fragment addresses
     std::uint32_t aoff[8];
@@ -284,48 +296,59 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         const int krow = TRANS ? kperm(t + 4 * i) : t + 4 * i;
         boff[i] = static_cast<std::uint32_t>((krow * BNS + g + 8 * NTW * wn) * 8);
     }
-
-    for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % stages;
-        mbar_wait(&full[s], (kt / stages) & 1);
-        const std::uint32_t xs = base + s * stage_bytes;
-        const std::uint32_t bs = xs + x_bytes;
-#pragma unroll
-        for (int ks = 0; ks < kBK / 16; ++ks) {
-            double a[8];
-            // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
-            const std::uint32_t abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = lds64(abase + aoff[i]);
-            const std::uint32_t bb = bs + ks * 16 * BNS * 8;
-#pragma unroll
-            for (int j = 0; j < NTW; ++j) {
-                double b[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) b[i] = lds64(bb + boff[i] + j * 64);
-                dmma16816(acc[j], a, b);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    }
-
-    // epilogue: rows m0+wm+g(+8), cols n0+8j+2t(+1); 16-byte stores when aligned
-    double* o = out + blockIdx.z * out_split_stride;
     const bool vec = (R % 2) == 0;
+
+    long long it = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        int n0, nk, split;
+        long long m0, kbeg;
+        unit_geom(u, n0, m0, kbeg, nk, split);
+        double acc[NTW][4];
 #pragma unroll
-    for (int j = 0; j < NTW; ++j) {
-        const int col = n0 + 8 * (NTW * wn + j) + 2 * t;
+        for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+            const int s = static_cast<int>(it % stages);
+            mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
+            const std::uint32_t xs = base + s * stage_bytes;
+            const std::uint32_t bs = xs + x_bytes;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const long long row = m0 + wm + g + 8 * h;
-            if (row < M && col < R) {
-                double* dst = o + row * R + col;
-                if (vec) {
-                    *reinterpret_cast<double2*>(dst) = make_double2(acc[j][2 * h], acc[j][2 * h + 1]);
-                } else {
-                    dst[0] = acc[j][2 * h];
-                    if (col + 1 < R) dst[1] = acc[j][2 * h + 1];
+            for (int ks = 0; ks < kBK / 16; ++ks) {
+                double a[8];
+                // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
+                const std::uint32_t abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a[i] = lds64(abase + aoff[i]);
+                const std::uint32_t bb = bs + ks * 16 * BNS * 8;
+#pragma unroll
+                for (int j = 0; j < NTW; ++j) {
+                    double b[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) b[i] = lds64(bb + boff[i] + j * 64);
+                    dmma16816(acc[j], a, b);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+
+        // epilogue (overlaps the producer's loads for the next unit):
+        // rows m0+wm+g(+8), cols n0+8(NTW wn + j)+2t(+1); 16-byte stores when aligned
+        double* o = out + split * out_split_stride;
+#pragma unroll
+        for (int j = 0; j < NTW; ++j) {
+            const int col = n0 + 8 * (NTW * wn + j) + 2 * t;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long row = m0 + wm + g + 8 * h;
+                if (row < M && col < R) {
+                    double* dst = o + row * R + col;
+                    if (vec) {
+                        *reinterpret_cast<double2*>(dst) = make_double2(acc[j][2 * h], acc[j][2 * h + 1]);
+                    } else {
+                        dst[0] = acc[j][2 * h];
+                        if (col + 1 < R) dst[1] = acc[j][2 * h + 1];
+                    }
                 }
             }
         }
@@ -372,7 +395,7 @@ int round_ntw(int need) {
     return 16;
 }
 struct GemmPlan {
-    int ntw, wn, wm, ntiles, bns, stages, mtiles, splits;
+    int ntw, wn, wm, ntiles, bns, stages, mtiles, splits, per_sm;
     long long kps;
     int BM() const { return 16 * wm; }
     int BN() const { return 8 * ntw * wn; }
@@ -435,6 +458,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
     const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
     const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
+    p.per_sm = per_sm;
     const long long slots = static_cast<long long>(num_sms()) * per_sm;
     if (base < 4 * slots) {
         // choose the split count with the best wave efficiency (<= 2 waves),
@@ -463,14 +487,15 @@ template <bool TRANS>
 void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, long long M,
               long long K, int R, double* out, long long oss) {
     const std::size_t smem = smem_bytes(p);
-    const dim3 grid(p.ntiles, p.mtiles, p.splits);
+    const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
+    const dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
     const dim3 block(32 * (p.wm * p.wn + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
         auto fn = root_gemm_kernel<NTV, TRANS>;                                                    \
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
-        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, out, oss); \
+        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, p.splits, out, oss); \
         break;                                                                                     \
     }
     switch (p.ntw) {
@@ -503,7 +528,7 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
                       const KrpDesc& kb, double* krp, double* pf, double* ws, std::size_t ws_elems,
                       cudaStream_t st) {
     const GemmPlan p = plan_gemm(F, B, R, false);
-    if (p.mtiles > 65535) throw LimitExceeded("root_back: too many row tiles");
+    
     const int Rs = (R + 1) & ~1;
     fill_krp(kb, B, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16,
