@@ -190,6 +190,7 @@ struct CgParams {
     double cg_tol = 1e-3;
     int cap = 0;
     int* result = nullptr;         // [iters, hit_cap, breakdown, nonfinite, final_buffer]
+    unsigned long long* trace = nullptr;  // optional: CTA 0 phase timestamps (ns), 8 per iteration
 };
 void run_cg(const CgParams& p, int grid, cudaStream_t st);
 int cg_max_grid(int device);

@@ -300,6 +300,14 @@ __device__ double norm_sum_slots(const Dev& d, RedSmem& sm) {
     return total;
 }
 
+__device__ __forceinline__ void stamp(const Dev& d, int it, int k) {
+    if (d.p.trace && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        d.p.trace[it * 8 + k] = t;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__ Dev d) {
     __shared__ RedSmem sm;
     const CgParams& p = d.p;
@@ -343,13 +351,19 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
             hit_cap = 1;
             break;
         }
+        stamp(d, it, 0);
         phase_a(d, sm, p.W[wc], p.W[wc ^ 1], beta, first);
         wc ^= 1;
+        stamp(d, it, 1);
         grid_barrier(p.barrier, nb, round);
+        stamp(d, it, 2);
         phase_a2(d);
         grid_barrier(p.barrier, nb, round);
+        stamp(d, it, 3);
         phase_b(d, sm, p.W[wc], p.Q);
+        stamp(d, it, 4);
         grid_barrier(p.barrier, nb, round);
+        stamp(d, it, 5);
         wq = sum_slots(sm, slot_wq(d), d.L.tasksBC);
         if (!(wq > 0.0)) {
             breakdown = 1;
@@ -358,7 +372,9 @@ __global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__
         const double alpha = rz / wq;
         phase_c(d, sm, p.W[wc], p.Rr[rc], p.Rr[rc ^ 1], alpha, false);
         rc ^= 1;
+        stamp(d, it, 6);
         grid_barrier(p.barrier, nb, round);
+        stamp(d, it, 7);
         ++it;
         first = false;
     }

@@ -162,34 +162,37 @@ __global__ void gamma_excl_kernel(const double* __restrict__ grams, int order, i
 __global__ void residual_partial_kernel(const double* __restrict__ m, const double* __restrict__ a,
                                         long long n, const double* __restrict__ grams, int order,
                                         int R, double* __restrict__ partials) {
-    // blocks [0, gridDim.x-1): cross term; last block: model norm
-    if (blockIdx.x + 1 < gridDim.x) {
-        double acc = 0.0;
-        const long long stride = static_cast<long long>(gridDim.x - 1) * blockDim.x;
-        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
-             i += stride)
-            acc += m[i] * a[i];
-        const double s = block_sum(acc);
-        if (threadIdx.x == 0) partials[blockIdx.x] = s;
-    } else {
-        const long long rr = static_cast<long long>(R) * R;
-        double acc = 0.0;
-        for (long long e = threadIdx.x; e < rr; e += blockDim.x) {
-            double g = 1.0;
-            for (int q = 0; q < order; ++q) g *= grams[q * rr + e];
-            acc += g;
-        }
-        const double s = block_sum(acc);
-        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    // every block sums a grid-stride slice of the cross term <M, A> AND of the
+    // model norm sum_rz prod_m S^(m)_rz; partials[2b] / [2b+1]
+    const long long rr = static_cast<long long>(R) * R;
+    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+    double cross = 0.0, model = 0.0;
+#pragma unroll 4
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n; i += stride)
+        cross += m[i] * a[i];
+#pragma unroll 4
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < rr; e += stride) {
+        double g = 1.0;
+        for (int q = 0; q < order; ++q) g *= grams[q * rr + e];
+        model += g;
+    }
+    const double c = block_sum(cross);
+    const double md = block_sum(model);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = c;
+        partials[2 * blockIdx.x + 1] = md;
     }
 }
-__global__ void residual_final_kernel(const double* __restrict__ partials, int nparts,
+__global__ void residual_final_kernel(const double* __restrict__ partials, int nblocks,
                                       const double* __restrict__ xnorm2, double* __restrict__ out) {
-    double acc = 0.0;
-    for (int i = threadIdx.x; i < nparts - 1; i += blockDim.x) acc += partials[i];
-    const double cross = block_sum(acc);
+    double c = 0.0, md = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+        c += partials[2 * i];
+        md += partials[2 * i + 1];
+    }
+    const double cross = block_sum(c);
+    const double model = block_sum(md);
     if (threadIdx.x == 0) {
-        const double model = partials[nparts - 1];
         const double x2 = *xnorm2;
         double res2 = x2 - 2.0 * cross + model;
         if (res2 < 0.0) res2 = 0.0;
@@ -419,7 +422,7 @@ void launch_residual(const double* m_last, const double* a_last, std::int64_t ro
                      int order, int R, const double* xnorm2, double* partials, double* out2,
                      cudaStream_t st) {
     const long long n = rows * static_cast<long long>(R);
-    const int nb = grid_for(n, kRedThreads, 64) + 1;
+    const int nb = grid_for(std::max<long long>(n, static_cast<long long>(R) * R), kRedThreads, 128);
     residual_partial_kernel<<<nb, kRedThreads, 0, st>>>(m_last, a_last, n, grams, order, R, partials); ::cpkit::count_launch(1);
     residual_final_kernel<<<1, kRedThreads, 0, st>>>(partials, nb, xnorm2, out2); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());

@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -798,9 +800,27 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
     p.cg_tol = cfg.cg_tol;
     p.cap = cap;
     p.result = cgres_.get();
+    DevBuf<unsigned long long> trace;
+    const bool want_trace = std::getenv("CPKIT_CG_TRACE") != nullptr;
+    if (want_trace) {
+        trace.resize(64 * 8);
+        CPK_CUDA(cudaMemsetAsync(trace.get(), 0, 64 * 8 * 8, ctx_.stream));
+        p.trace = trace.get();
+    }
     prof_begin(kProfCg);
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);
     prof_end();
+    if (want_trace) {
+        std::vector<unsigned long long> h(64 * 8);
+        CPK_CUDA(cudaMemcpyAsync(h.data(), trace.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+        ctx_.sync();
+        for (int it = 0; it < 64 && h[it * 8]; ++it) {
+            std::fprintf(stderr, "cg it %2d:", it);
+            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %6.2f", (h[it * 8 + k] - h[it * 8 + k - 1]) * 1e-3);
+            if (it + 1 < 64 && h[(it + 1) * 8]) std::fprintf(stderr, " | next %6.2f", (h[(it + 1) * 8] - h[it * 8 + 7]) * 1e-3);
+            std::fprintf(stderr, " us\n");
+        }
+    }
     int res[5];
     CPK_CUDA(cudaMemcpyAsync(res, cgres_.get(), sizeof res, cudaMemcpyDeviceToHost, ctx_.stream));
     ctx_.sync();
