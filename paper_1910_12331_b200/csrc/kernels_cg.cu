@@ -98,15 +98,29 @@ __device__ void phase_a2(const Dev& d) {
          e += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(e / R), z = static_cast<int>(e % R);
         double bs[kMaxOrder];
+#pragma unroll
+        for (int q = 0; q < kMaxOrder; ++q) bs[q] = 0.0;
+        // partial slabs in chunks of 8 independent loads, summed in fixed (ks) order
         for (int q = 0; q < N; ++q) {
             double b = 0.0;
-            for (int ks = 0; ks < L.ksplit; ++ks) b += __ldcg(bp + (static_cast<long long>(ks) * N + q) * RR + e);
-            bs[q] = b;
+            for (int k0 = 0; k0 < L.ksplit; k0 += 8) {
+                double part[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    part[u] = (k0 + u < L.ksplit) ? __ldcg(bp + (static_cast<long long>(k0 + u) * N + q) * RR + e) : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k0 + u < L.ksplit) b += part[u];
+            }
+#pragma unroll
+            for (int qq = 0; qq < kMaxOrder; ++qq)
+                if (qq == q) bs[qq] = b;
         }
         for (int n = 0; n < N; ++n) {
             double dsum = 0.0;
-            for (int q = 0; q < N; ++q) {
-                if (q == n) continue;
+#pragma unroll
+            for (int q = 0; q < kMaxOrder; ++q) {
+                if (q >= N || q == n) continue;
                 dsum += p.pair[(n * N + q) * RR + e] * bs[q];
             }
             dt[n * RR + static_cast<long long>(z) * R + r] = dsum;
@@ -191,10 +205,22 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
             if (kk < R) return Gnn[kk * R + r];
             return __ldcg(dt_buf(d) + n * RR + static_cast<long long>(kk - R) * R + r);
         };
-        double acc[4];
-        tile_gemm_panel(cg_panel_smem, 2 * R, la, lb, acc);
+        // prefetch this thread's epilogue operands before the panel loads (overlapped)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
+        double wpre[4], gdiag[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
+                const int r = c0 + (warp & 3) * 8 + 2 * t + c;
+                const bool ok = i < s && r < R;
+                wpre[2 * h + c] = ok ? __ldcg(W + i * R + r) : 0.0;
+                gdiag[2 * h + c] = ok ? Gnn[r * R + r] : 0.0;
+            }
+        double acc[4];
+        tile_gemm_panel(cg_panel_smem, 2 * R, la, lb, acc);
         double part = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -203,8 +229,8 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
                 const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
                 const int r = c0 + (warp & 3) * 8 + 2 * t + c;
                 if (i < s && r < R) {
-                    const double w = __ldcg(W + i * R + r);
-                    const double reg = (p.shape == 0) ? p.lambda * w : w * (p.lambda * Gnn[r * R + r]);
+                    const double w = wpre[2 * h + c];
+                    const double reg = (p.shape == 0) ? p.lambda * w : w * (p.lambda * gdiag[2 * h + c]);
                     const double q = acc[2 * h + c] + reg;
                     Qout[p.off[n] + i * R + r] = q;
                     part += w * q;
@@ -241,10 +267,24 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
             const int r = c0 + col;
             return r < R ? Pinv[z * R + r] : 0.0;
         };
-        double acc[4];
-        tile_gemm_panel(cg_panel_smem, R, la, lb, acc);
+        // prefetch this thread's epilogue operands (R, Q, V, W') before the panel loads
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
+        double rpre[4], vpre[4], wpre[4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long i = row0 + (warp >> 2) * 16 + g + 8 * h;
+                const int r = c0 + (warp & 3) * 8 + 2 * t + c;
+                const bool ok = i < s && r < R;
+                const long long e = off + i * R + r;
+                rpre[2 * h + c] = ok ? rnew(e) : 0.0;
+                vpre[2 * h + c] = (ok && !init) ? __ldcg(p.V + e) : 0.0;
+                wpre[2 * h + c] = (ok && !init) ? __ldcg(Wn_all + e) : 0.0;
+            }
+        double acc[4];
+        tile_gemm_panel(cg_panel_smem, R, la, lb, acc);
         double rz = 0.0, nrm = 0.0, bad = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -254,14 +294,9 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
                 const int r = c0 + (warp & 3) * 8 + 2 * t + c;
                 if (i < s && r < R) {
                     const long long e = off + i * R + r;
-                    const double rv = rnew(e);
+                    const double rv = rpre[2 * h + c];
                     const double zv = acc[2 * h + c];
-                    double v;
-                    if (init) {
-                        v = 0.0;
-                    } else {
-                        v = __ldcg(p.V + e) + alpha * __ldcg(Wn_all + e);
-                    }
+                    const double v = init ? 0.0 : vpre[2 * h + c] + alpha * wpre[2 * h + c];
                     p.V[e] = v;
                     Rnew_all[e] = rv;
                     p.Z[e] = zv;

@@ -104,17 +104,41 @@ __device__ __forceinline__ void tile_gemm_panel(double* psm, int K, LA la, LB lb
     for (int k0 = 0; k0 < K; k0 += kPanel) {
         const int kp = min(kPanel, K - k0);
         const int kpad = (kp + 15) & ~15;
-        // A panel: element e -> (row = e / kpad, k = e % kpad)
-#pragma unroll 4
-        for (int e = tid; e < kT * kpad; e += kThreads) {
-            const int row = e / kpad, k = e - row * kpad;
-            As[row * kPAS + k] = (k < kp) ? la(row, k0 + k) : 0.0;
+        // A panel: element e -> (row = e / kpad, k = e % kpad); B panel: (k = e / 32, col = e % 32).
+        // Loads are issued in batches of 8 before their shared stores so each
+        // thread keeps 8 L2 requests in flight.
+        constexpr int kBatch = 8;
+        const int na = kT * kpad, nb = kpad * kT;
+        for (int e0 = tid; e0 < na; e0 += kBatch * kThreads) {
+            double v[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * kThreads;
+                const int row = e / kpad, k = e - row * kpad;
+                v[u] = (e < na && k < kp) ? la(row, k0 + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * kThreads;
+                if (e < na) {
+                    const int row = e / kpad, k = e - row * kpad;
+                    As[row * kPAS + k] = v[u];
+                }
+            }
         }
-        // B panel: element e -> (k = e / 32, col = e % 32)
-#pragma unroll 4
-        for (int e = tid; e < kpad * kT; e += kThreads) {
-            const int k = e >> 5, col = e & 31;
-            Bs[k * kPBS + col] = (k < kp) ? lb(k0 + k, col) : 0.0;
+        for (int e0 = tid; e0 < nb; e0 += kBatch * kThreads) {
+            double v[kBatch];
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * kThreads;
+                const int k = e >> 5, col = e & 31;
+                v[u] = (e < nb && k < kp) ? lb(k0 + k, col) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kBatch; ++u) {
+                const int e = e0 + u * kThreads;
+                if (e < nb) Bs[(e >> 5) * kPBS + (e & 31)] = v[u];
+            }
         }
         __syncthreads();
         for (int c = 0; c < kpad; c += kKC) {
