@@ -343,7 +343,7 @@ __device__ __forceinline__ void stamp(const Dev& d, int it, int k) {
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) cg_kernel(const __grid_constant__ Dev d) {
+__global__ void __launch_bounds__(kThreads, 2) cg_kernel(const __grid_constant__ Dev d) {
     __shared__ RedSmem sm;
     const CgParams& p = d.p;
     const unsigned nb = gridDim.x;
