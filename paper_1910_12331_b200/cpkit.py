@@ -296,7 +296,7 @@ class DeviceProblem:
         self.rank = int(rank)
         h = _vp()
         L = load()
-        if world == 1:
+        if world == 1 and nccl_id is None:
             _chk(L.cpkit_dev_problem_create(device, _dims(self.dims), _u64(len(self.dims)),
                                             _u64(self.rank), C.byref(h)))
         else:

@@ -697,10 +697,10 @@ cpkit_status cpkit_dev_problem_create_sharded(int device, const uint64_t* dims, 
     return guarded([&] {
         auto h = std::make_unique<cpkit_dev_problem>();
         h->ctx = std::make_unique<cpkit::Context>(device);
-        if (world > 1) {
-            if (!nccl_id128) throw cpkit::InvalidArgument("sharded problem needs an NCCL unique id");
-            h->ctx->comm = cpkit::make_nccl_comm(nccl_id128, shard, world);
-        }
+        // world == 1 with an id still routes the collectives through NCCL (a
+        // one-rank communicator), which exercises the sharded path on one GPU
+        if (world > 1 && !nccl_id128) throw cpkit::InvalidArgument("sharded problem needs an NCCL unique id");
+        if (nccl_id128) h->ctx->comm = cpkit::make_nccl_comm(nccl_id128, shard, world);
         h->p = std::make_unique<cpkit::DeviceProblem>(*h->ctx, std::vector<std::uint64_t>(dims, dims + order),
                                                       static_cast<int>(rank));
         *out = h.release();
