@@ -193,6 +193,7 @@ struct CgParams {
     unsigned long long* trace = nullptr;  // optional: CTA 0 phase timestamps (ns), 8 per iteration
 };
 void run_cg(const CgParams& p, int grid, cudaStream_t st);
+constexpr int cg_barrier_words() { return 4 + 1024; }  // grid barrier, CTA-order counters, per-SM slots
 int cg_max_grid(int device);
 std::size_t cg_slots_needed(const CgParams& p);
 // U = J^T J W + lambda Reg(W) (same task code as the CG phases)

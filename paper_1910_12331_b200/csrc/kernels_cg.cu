@@ -49,6 +49,54 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
         }
     }
     __syncthreads();
+    fence_async_global();  // later bulk copies (async proxy) see the data released by other CTAs
+}
+
+// Panel staging: bulk copies (one thread per row, one mbarrier) when every row
+// run is 16-byte aligned (R even), cp.async otherwise.
+struct Stager {
+    unsigned long long* bar;
+    unsigned parity;
+    bool bulk;
+    int vb;  // task-order rank of this CTA (see cta_rank)
+    __device__ __forceinline__ void begin() const {
+        if (bulk) fence_async_shared();  // prior generic smem accesses before async-proxy writes
+    }
+    template <int kLanes, class P1, class P2>
+    __device__ __forceinline__ void rows(double* dst, int stride, int nrows, int width, int valid, int split, P1 p1,
+                                         P2 p2) {
+        if (bulk) stage_rows_bulk(dst, stride, nrows, width, valid, split, p1, p2, bar);
+        else stage_rows<kLanes>(dst, stride, nrows, width, valid, split, p1, p2);
+    }
+    template <int kLanes, class P1>
+    __device__ __forceinline__ void rows(double* dst, int stride, int nrows, int width, int valid, P1 p1) {
+        rows<kLanes>(dst, stride, nrows, width, valid, width, p1, p1);
+    }
+    __device__ __forceinline__ void wait() {
+        if (bulk) {
+            bulk_wait(bar, parity);
+        } else {
+            cp_async_wait_all();
+            __syncthreads();
+        }
+    }
+};
+
+// Task-order rank: the hardware packs consecutive block indices onto the same
+// SMs, so phases with fewer tasks than CTAs would double up on half the SMs.
+// Rank CTAs by their slot on their SM first (slot-0 CTAs get ranks 0.., the
+// others ranks grid-1 downwards), so tasks 0..#SMs-1 land on distinct SMs.
+__device__ int cta_rank(unsigned int* words) {
+    __shared__ int rank;
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        const unsigned slot = atomicAdd(words + 4 + (smid & 1023u), 1u);
+        rank = slot == 0 ? static_cast<int>(atomicAdd(words + 1, 1u))
+                         : static_cast<int>(gridDim.x) - 1 - static_cast<int>(atomicAdd(words + 2, 1u));
+    }
+    __syncthreads();
+    return rank;
 }
 
 struct Layout {
@@ -72,7 +120,7 @@ struct Dev {
     Layout L;
     int mode;  // 0 = full CG, 1 = single matvec (W given in W[0], result in Q)
 };
-extern __shared__ double cg_panel_smem[];  // tile_gemm_panel operand panels
+extern __shared__ __align__(16) double cg_panel_smem[];  // staged operand panels
 
 // slot regions (doubles): [0, tasksB) wq partials; then rz, nrm, fin per task C
 __device__ __forceinline__ double* slot_wq(const Dev& d) { return d.p.slots; }
@@ -83,6 +131,14 @@ __device__ __forceinline__ double* bpart(const Dev& d) { return d.p.slots + 4 * 
 // D_n^T blocks (order x R x R) after the ksplit partial slabs of B_p
 __device__ __forceinline__ double* dt_buf(const Dev& d) {
     return bpart(d) + static_cast<long long>(d.L.ksplit) * d.L.order * d.L.R * d.L.R;
+}
+
+__device__ __forceinline__ void stamp(const Dev& d, const Stager& st, int it, int k) {
+    if (d.p.trace && st.vb == 0 && threadIdx.x == 0 && it >= 0 && it < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        d.p.trace[it * 16 + k] = t;
+    }
 }
 
 // ---- phase A2: Bsum_p = sum_ks Bpart; D_n^T[z][r] = sum_{p != n} Gamma(n,p)[r][z] Bsum_p[r][z]
@@ -129,12 +185,12 @@ __device__ void phase_a2(const Dev& d) {
 }
 
 // ---- phase A: W' = Z + beta W_old (first: W' = Z; matvec: W' = W_in), B_p partials
-__device__ void phase_a(const Dev& d, RedSmem& sm, const double* Wold, double* Wnew, double beta,
+__device__ void phase_a(const Dev& d, RedSmem& sm, Stager& st, const double* Wold, double* Wnew, double beta,
                         bool first) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
     const int R = L.R;
-    for (int task = blockIdx.x; task < L.tasksA; task += gridDim.x) {
+    for (int task = st.vb; task < L.tasksA; task += gridDim.x) {
         int rem = task;
         const int ks = rem % L.ksplit; rem /= L.ksplit;
         const int zt = rem % L.tr; rem /= L.tr;
@@ -150,42 +206,53 @@ __device__ void phase_a(const Dev& d, RedSmem& sm, const double* Wold, double* W
         double* Wn = Wnew + p.off[pm];
         const int r0 = rt * kT, z0 = zt * kT;
         const bool writer = (rt == 0) && d.mode == 0;
-        auto la = [&](int row, int k) -> double {
-            const int r = r0 + row;
-            return r < R ? A[(k0 + k) * R + r] : 0.0;
-        };
-        auto lb = [&](int k, int col) -> double {
-            const int z = z0 + col;
-            if (z >= R) return 0.0;
-            const long long e = (k0 + k) * R + z;
-            if (d.mode == 1) return __ldcg(Wo + e);
-            const double v = first ? __ldcg(Z + e) : __ldcg(Z + e) + beta * __ldcg(Wo + e);
-            if (writer) Wn[e] = v;
-            return v;
-        };
-        double acc[4];
-        tile_gemm_panel(cg_panel_smem, K, la, lb, acc);
+        // A_p^T panel (k-major) and W' panel: W_in (matvec), Z (first) or fma(beta, W_old, Z)
+        double* As = cg_panel_smem;
+        double* Bs = As + kPA * kKS;
+        double* Aux = Bs + kPA * kKS;
+        const bool comb = d.mode == 0 && !first;
+        const double* bsrc = d.mode == 1 ? Wo : Z;
+        const int vr = min(kT, R - r0), vz = min(kT, R - z0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int kk0 = 0; kk0 < K; kk0 += kPA) {
+            const int kp = min(kPA, K - kk0), kpad = pad8(kp);
+            const long long rb = (k0 + kk0) * R;
+            st.begin();
+            st.rows<16>(As, kKS, kpad, kT, vr, [&](int k) { return k < kp ? A + rb + k * R + r0 : nullptr; });
+            st.rows<16>(Bs, kKS, kpad, kT, vz, [&](int k) { return k < kp ? bsrc + rb + k * R + z0 : nullptr; });
+            if (comb) st.rows<16>(Aux, kKS, kpad, kT, vz, [&](int k) { return k < kp ? Wo + rb + k * R + z0 : nullptr; });
+            st.wait();
+            if (comb) {
+                combine(Bs, Aux, kpad * kKS, beta);
+                __syncthreads();
+            }
+            if (writer)
+                for (int e = threadIdx.x; e < kp * kT; e += kThreads)
+                    if ((e & 31) < vz) Wn[rb + (e >> 5) * R + z0 + (e & 31)] = Bs[(e >> 5) * kKS + (e & 31)];
+            mma_panel<true>(As, kKS, Bs, kpad, acc);
+            __syncthreads();
+        }
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
-        double* out = bpart(d) + (static_cast<long long>(ks) * L.order + pm) * R * R;
+        double* bout = bpart(d) + (static_cast<long long>(ks) * L.order + pm) * R * R;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int r = r0 + (warp >> 2) * 16 + g + 8 * h;
                 const int z = z0 + (warp & 3) * 8 + 2 * t + c;
-                if (r < R && z < R) out[r * R + z] = acc[2 * h + c];
+                if (r < R && z < R) bout[r * R + z] = acc[2 * h + c];
             }
     }
 }
 
 // ---- phase B: Q_n = [W'|A_n][Gnn; D^T] + lambda Reg(W'); wq partials
-__device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double* Qout) {
+__device__ void phase_b(const Dev& d, RedSmem& sm, Stager& st, const double* Wn_all, double* Qout, int it = -1) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
     const int R = L.R;
     const long long RR = static_cast<long long>(R) * R;
-    for (int task = blockIdx.x; task < L.tasksBC; task += gridDim.x) {
+    for (int task = st.vb; task < L.tasksBC; task += gridDim.x) {
         int n, rt, ct;
         decode_bc(L, task, n, rt, ct);
         const long long s = p.rows[n];
@@ -194,17 +261,7 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
         const double* W = Wn_all + p.off[n];
         const double* A = p.A + p.off[n];
         const double* Gnn = p.pair + (n * L.order + n) * RR;
-        auto la = [&](int row, int kk) -> double {
-            const long long i = row0 + row;
-            if (i >= s) return 0.0;
-            return kk < R ? __ldcg(W + i * R + kk) : A[i * R + (kk - R)];
-        };
-        auto lb = [&](int kk, int col) -> double {
-            const int r = c0 + col;
-            if (r >= R) return 0.0;
-            if (kk < R) return Gnn[kk * R + r];
-            return __ldcg(dt_buf(d) + n * RR + static_cast<long long>(kk - R) * R + r);
-        };
+        const double* Dt = dt_buf(d) + n * RR;
         // prefetch this thread's epilogue operands before the panel loads (overlapped)
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
@@ -219,8 +276,33 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
                 wpre[2 * h + c] = ok ? __ldcg(W + i * R + r) : 0.0;
                 gdiag[2 * h + c] = ok ? Gnn[r * R + r] : 0.0;
             }
-        double acc[4];
-        tile_gemm_panel(cg_panel_smem, 2 * R, la, lb, acc);
+        // [W' | A_n] (row-major) x [Gamma_nn ; D_n^T] (k-major); K = 2R in panels of kPB
+        double* As = cg_panel_smem;
+        double* Bs = As + kT * (kPB + 4);
+        const int vc = min(kT, R - c0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int kk0 = 0; kk0 < 2 * R; kk0 += kPB) {
+            const int kp = min(kPB, 2 * R - kk0), kpad = pad8(kp);
+            const int split = max(0, R - kk0);  // panel columns [0, split) from W', the rest from A_n
+            st.begin();
+            st.rows<32>(
+                As, kPB + 4, kT, kpad, kp, split,
+                [&](int row) {
+                    const long long i = row0 + row;
+                    return i < s ? W + i * R + kk0 : nullptr;
+                },
+                [&](int row) { return A + (row0 + row) * R + max(0, kk0 - R); });
+            st.rows<16>(Bs, kKS, kpad, kT, vc, [&](int k) {
+                const int kk = kk0 + k;
+                if (k >= kp) return static_cast<const double*>(nullptr);
+                return kk < R ? Gnn + static_cast<long long>(kk) * R + c0 : Dt + static_cast<long long>(kk - R) * R + c0;
+            });
+            st.wait();
+            if (kk0 == 0) stamp(d, st, it, 9);
+            mma_panel<false>(As, kPB + 4, Bs, kpad, acc);
+            __syncthreads();
+        }
+        stamp(d, st, it, 10);
         double part = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -237,18 +319,19 @@ __device__ void phase_b(const Dev& d, RedSmem& sm, const double* Wn_all, double*
                 }
             }
         const double tot = cta_sum(sm, part);
+        stamp(d, st, it, 11);
         if (threadIdx.x == 0 && d.mode == 0) slot_wq(d)[task] = tot;
     }
 }
 
 // ---- phase C: V += alpha W'; R' = R - alpha Q (init: R' = -G); Z = R' Pinv
-__device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const double* Rold_all,
-                        double* Rnew_all, double alpha, bool init) {
+__device__ void phase_c(const Dev& d, RedSmem& sm, Stager& st, const double* Wn_all, const double* Rold_all,
+                        double* Rnew_all, double alpha, bool init, int it = -1) {
     const CgParams& p = d.p;
     const Layout& L = d.L;
     const int R = L.R;
     const long long RR = static_cast<long long>(R) * R;
-    for (int task = blockIdx.x; task < L.tasksBC; task += gridDim.x) {
+    for (int task = st.vb; task < L.tasksBC; task += gridDim.x) {
         int n, rt, ct;
         decode_bc(L, task, n, rt, ct);
         const long long s = p.rows[n];
@@ -256,16 +339,9 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
         const int c0 = ct * kT;
         const long long off = p.off[n];
         const double* Pinv = p.pinv + n * RR;
+        // R' = fma(-alpha, Q, R_old) (init: -G), formed identically in the operand and the epilogue
         auto rnew = [&](long long e) -> double {
-            return init ? -p.G[e] : __ldcg(Rold_all + e) - alpha * __ldcg(p.Q + e);
-        };
-        auto la = [&](int row, int z) -> double {
-            const long long i = row0 + row;
-            return i < s ? rnew(off + i * R + z) : 0.0;
-        };
-        auto lb = [&](int z, int col) -> double {
-            const int r = c0 + col;
-            return r < R ? Pinv[z * R + r] : 0.0;
+            return init ? -1.0 * p.G[e] : __fma_rn(-alpha, __ldcg(p.Q + e), __ldcg(Rold_all + e));
         };
         // prefetch this thread's epilogue operands (R, Q, V, W') before the panel loads
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -283,8 +359,35 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
                 vpre[2 * h + c] = (ok && !init) ? __ldcg(p.V + e) : 0.0;
                 wpre[2 * h + c] = (ok && !init) ? __ldcg(Wn_all + e) : 0.0;
             }
-        double acc[4];
-        tile_gemm_panel(cg_panel_smem, R, la, lb, acc);
+        stamp(d, st, it, 15);
+        // R' (row-major, formed in shared memory) x Pinv (k-major)
+        double* As = cg_panel_smem;
+        double* Aux = As + kT * (kPC + 4);
+        double* Bs = Aux + kT * (kPC + 4);
+        const double* Ab = (init ? p.G : Rold_all) + off;
+        const int vc = min(kT, R - c0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int kk0 = 0; kk0 < R; kk0 += kPC) {
+            const int kp = min(kPC, R - kk0), kpad = pad8(kp);
+            auto rowp = [&](const double* base) {
+                return [=](int row) {
+                    const long long i = row0 + row;
+                    return i < s ? base + i * R + kk0 : nullptr;
+                };
+            };
+            st.begin();
+            st.rows<32>(As, kPC + 4, kT, kpad, kp, rowp(Ab));
+            if (!init) st.rows<32>(Aux, kPC + 4, kT, kpad, kp, rowp(p.Q + off));
+            st.rows<16>(Bs, kKS, kpad, kT, vc,
+                        [&](int k) { return k < kp ? Pinv + static_cast<long long>(kk0 + k) * R + c0 : nullptr; });
+            st.wait();
+            stamp(d, st, it, 12);
+            combine(As, init ? nullptr : Aux, kT * (kPC + 4), init ? -1.0 : -alpha);
+            __syncthreads();
+            mma_panel<false>(As, kPC + 4, Bs, kpad, acc);
+            __syncthreads();
+        }
+        stamp(d, st, it, 13);
         double rz = 0.0, nrm = 0.0, bad = 0.0;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -308,6 +411,7 @@ __device__ void phase_c(const Dev& d, RedSmem& sm, const double* Wn_all, const d
         const double trz = cta_sum(sm, rz);
         const double tnrm = cta_sum(sm, nrm);
         const double tbad = cta_sum(sm, bad);
+        stamp(d, st, it, 14);
         if (threadIdx.x == 0) {
             slot_rz(d)[task] = trz;
             slot_nrm(d)[task] = tnrm;
@@ -335,30 +439,31 @@ __device__ double norm_sum_slots(const Dev& d, RedSmem& sm) {
     return total;
 }
 
-__device__ __forceinline__ void stamp(const Dev& d, int it, int k) {
-    if (d.p.trace && blockIdx.x == 0 && threadIdx.x == 0 && it < 64) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        d.p.trace[it * 8 + k] = t;
-    }
-}
 
 __global__ void __launch_bounds__(kThreads, 2) cg_kernel(const __grid_constant__ Dev d) {
     __shared__ RedSmem sm;
+    __shared__ unsigned long long stage_bar;
     const CgParams& p = d.p;
     const unsigned nb = gridDim.x;
     unsigned int round = 0;
+    if (threadIdx.x == 0) bar_init(&stage_bar);
+    Stager st{&stage_bar, 0u, (d.L.R & 1) == 0, cta_rank(p.barrier)};  // (cta_rank syncs the CTA)
+    if (p.trace && threadIdx.x == 0 && st.vb < 1024) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[64 * 16 + st.vb] = smid;
+    }
     if (d.mode == 1) {
         // U = H W: W in W[0]; B_p from W then Q
-        phase_a(d, sm, p.W[0], p.W[1], 0.0, false);
+        phase_a(d, sm, st, p.W[0], p.W[1], 0.0, false);
         grid_barrier(p.barrier, nb, round);
         phase_a2(d);
         grid_barrier(p.barrier, nb, round);
-        phase_b(d, sm, p.W[0], p.Q);
+        phase_b(d, sm, st, p.W[0], p.Q);
         return;
     }
     // init: R = -G, Z = R Pinv, V = 0
-    phase_c(d, sm, p.W[0], p.Rr[0], p.Rr[1], 0.0, true);
+    phase_c(d, sm, st, p.W[0], p.Rr[0], p.Rr[1], 0.0, true);
     grid_barrier(p.barrier, nb, round);
     int rc = 1;  // current residual buffer
     int wc = 0;  // current direction buffer (W_old)
@@ -386,30 +491,31 @@ __global__ void __launch_bounds__(kThreads, 2) cg_kernel(const __grid_constant__
             hit_cap = 1;
             break;
         }
-        stamp(d, it, 0);
-        phase_a(d, sm, p.W[wc], p.W[wc ^ 1], beta, first);
+        stamp(d, st, it, 0);
+        phase_a(d, sm, st, p.W[wc], p.W[wc ^ 1], beta, first);
         wc ^= 1;
-        stamp(d, it, 1);
+        stamp(d, st, it, 1);
         grid_barrier(p.barrier, nb, round);
-        stamp(d, it, 2);
+        stamp(d, st, it, 2);
         phase_a2(d);
         grid_barrier(p.barrier, nb, round);
-        stamp(d, it, 3);
-        phase_b(d, sm, p.W[wc], p.Q);
-        stamp(d, it, 4);
+        stamp(d, st, it, 3);
+        phase_b(d, sm, st, p.W[wc], p.Q, it);
+        stamp(d, st, it, 4);
         grid_barrier(p.barrier, nb, round);
-        stamp(d, it, 5);
+        stamp(d, st, it, 5);
         wq = sum_slots(sm, slot_wq(d), d.L.tasksBC);
         if (!(wq > 0.0)) {
             breakdown = 1;
             break;
         }
         const double alpha = rz / wq;
-        phase_c(d, sm, p.W[wc], p.Rr[rc], p.Rr[rc ^ 1], alpha, false);
+        stamp(d, st, it, 8);
+        phase_c(d, sm, st, p.W[wc], p.Rr[rc], p.Rr[rc ^ 1], alpha, false, it);
         rc ^= 1;
-        stamp(d, it, 6);
+        stamp(d, st, it, 6);
         grid_barrier(p.barrier, nb, round);
-        stamp(d, it, 7);
+        stamp(d, st, it, 7);
         ++it;
         first = false;
     }
@@ -449,8 +555,8 @@ int occupancy_grid(int device) {
     int sms = 0, per = 0;
     CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CPK_CUDA(cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kPanelSmemBytes)));
-    CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, kPanelSmemBytes));
+                                  static_cast<int>(kAsyncSmemBytes)));
+    CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, kAsyncSmemBytes));
     return sms * std::max(1, per);
 }
 
@@ -458,7 +564,7 @@ void launch_coop(const Dev& d, int grid, cudaStream_t st) {
     Dev dd = d;
     void* args[] = {&dd};
     CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_kernel), dim3(grid),
-                                         dim3(kThreads), args, kPanelSmemBytes, st));
+                                         dim3(kThreads), args, kAsyncSmemBytes, st));
     count_launch(1);
 }
 
@@ -484,7 +590,7 @@ void run_cg(const CgParams& p, int grid, cudaStream_t st) {
     const Layout L0 = make_layout(p, grid);
     grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
     d.L = make_layout(p, grid);
-    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, 2 * sizeof(unsigned int), st));
+    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
     launch_coop(d, grid, st);
 }
 
@@ -500,7 +606,7 @@ void launch_jtj_matvec(const CgParams& p, const double* w, double* u, cudaStream
     const Layout L0 = make_layout(p, grid);
     grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
     d.L = make_layout(p, grid);
-    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, 2 * sizeof(unsigned int), st));
+    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
     launch_coop(d, grid, st);
 }
 

@@ -385,7 +385,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     status_.resize(std::max(N, 1));
     cgres_.resize(8);
     flag_.resize(4);
-    barrier_.resize(4);
+    barrier_.resize(cg_barrier_words());
     offs_dev_.resize(N + 1);
     rows_dev_.resize(N);
     std::vector<std::int64_t> rows(dims_.begin(), dims_.end());
@@ -803,22 +803,28 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
     DevBuf<unsigned long long> trace;
     const bool want_trace = std::getenv("CPKIT_CG_TRACE") != nullptr;
     if (want_trace) {
-        trace.resize(64 * 8);
-        CPK_CUDA(cudaMemsetAsync(trace.get(), 0, 64 * 8 * 8, ctx_.stream));
+        trace.resize(64 * 16 + 1024);
+        CPK_CUDA(cudaMemsetAsync(trace.get(), 0, (64 * 16 + 1024) * 8, ctx_.stream));
         p.trace = trace.get();
     }
     prof_begin(kProfCg);
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);
     prof_end();
     if (want_trace) {
-        std::vector<unsigned long long> h(64 * 8);
+        std::vector<unsigned long long> h(64 * 16 + 1024);
         CPK_CUDA(cudaMemcpyAsync(h.data(), trace.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx_.stream));
         ctx_.sync();
-        for (int it = 0; it < 64 && h[it * 8]; ++it) {
+        std::fprintf(stderr, "cg block->sm:");
+        for (int b = 0; b < 16; ++b) std::fprintf(stderr, " %llu", h[64 * 16 + b]);
+        std::fprintf(stderr, "\n");
+        auto dt = [&](int it, int a, int b) { return (static_cast<double>(h[it * 16 + b]) - static_cast<double>(h[it * 16 + a])) * 1e-3; };
+        for (int it = 0; it < 64 && h[it * 16]; ++it) {
             std::fprintf(stderr, "cg it %2d:", it);
-            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %6.2f", (h[it * 8 + k] - h[it * 8 + k - 1]) * 1e-3);
-            if (it + 1 < 64 && h[(it + 1) * 8]) std::fprintf(stderr, " | next %6.2f", (h[(it + 1) * 8] - h[it * 8 + 7]) * 1e-3);
-            std::fprintf(stderr, " us\n");
+            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %6.2f", dt(it, k - 1, k));
+            if (it + 1 < 64 && h[(it + 1) * 16])
+                std::fprintf(stderr, " | next %6.2f", (static_cast<double>(h[(it + 1) * 16]) - static_cast<double>(h[it * 16 + 7])) * 1e-3);
+            std::fprintf(stderr, " | B stage %5.2f mma %5.2f epi %5.2f | wq %5.2f C pre %5.2f stage %5.2f mma %5.2f epi %5.2f us\n",
+                         dt(it, 3, 9), dt(it, 9, 10), dt(it, 10, 11), dt(it, 5, 8), dt(it, 8, 15), dt(it, 15, 12), dt(it, 12, 13), dt(it, 13, 14));
         }
     }
     int res[5];

@@ -1,6 +1,7 @@
 // DMMA 32x32 tile GEMM building block shared by the CG phases and the small
 // dense kernels (Gram, gradient). 256 threads = 8 warps (2 x m16, 4 x n8).
 #pragma once
+#include <cstdint>
 
 #include <cuda_runtime.h>
 
@@ -13,7 +14,7 @@ constexpr int kT = 32;        // task tile edge
 constexpr int kKC = 16;       // k chunk
 constexpr int kThreads = 256;  // 8 warps: 2 (m16) x 4 (n8)
 constexpr int kAS = kKC + 4;  // A smem row stride (doubles): conflict-free a-fragments
-constexpr int kBS = kT + 8;   // B smem row stride
+constexpr int kBS = kT + 4;   // B smem row stride: conflict-free b-fragments (t*4+g)
 
 __device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {
     asm volatile(
@@ -90,7 +91,7 @@ __device__ __forceinline__ void tile_gemm(Smem& sm, int K, LA la, LB lb, double 
 // further barriers. kp <= kPanel; longer K loops over panels.
 constexpr int kPanel = 192;
 constexpr int kPAS = kPanel + 4;   // A panel row stride: conflict-free a-fragments
-constexpr int kPBS = kT + 8;       // B panel row stride
+constexpr int kPBS = kT + 4;       // B panel row stride
 constexpr std::size_t kPanelSmemBytes = (kT * kPAS + kPanel * kPBS) * sizeof(double);
 
 template <typename LA, typename LB>
@@ -150,6 +151,177 @@ __device__ __forceinline__ void tile_gemm_panel(double* psm, int K, LA la, LB lb
             dmma16816(acc, a, b);
         }
         __syncthreads();
+    }
+}
+
+// Asynchronous row-staged panels (CG phases). Operand rows are contiguous
+// runs in global memory, moved to shared memory with cp.async (16-byte .cg
+// copies where aligned, 8-byte otherwise): no registers are tied up and every
+// copy of a panel is in flight at once, so a panel costs one L2 round trip.
+// Layouts: A row-major [32][kp + 4] or k-major [k][kKS]; B k-major [k][kKS].
+// Panel depths are per phase so each phase fits its operands in one panel at
+// R = 100 within a 2-CTA/SM shared-memory budget; k is padded to 8.
+constexpr int kKS = kT + 4;  // k-major stride: fragments conflict-free (4 mod 16)
+constexpr int kPA = 120;     // phase A (k-major A_p^T, W', aux)
+constexpr int kPB = 200;     // phase B ([W'|A_n] row-major, [Gnn; D^T])
+constexpr int kPC = 128;     // phase C (R' row-major + aux, Pinv)
+constexpr int kSmemA = 3 * kPA * kKS;
+constexpr int kSmemB = kT * (kPB + 4) + kPB * kKS;
+constexpr int kSmemC = 2 * kT * (kPC + 4) + kPC * kKS;
+constexpr int kSmemMax = kSmemA > kSmemB ? (kSmemA > kSmemC ? kSmemA : kSmemC) : (kSmemB > kSmemC ? kSmemB : kSmemC);
+constexpr std::size_t kAsyncSmemBytes = kSmemMax * sizeof(double);
+
+__device__ __forceinline__ int pad8(int k) { return (k + 7) & ~7; }
+
+__device__ __forceinline__ void dmma1688(double* d, const double* a, const double* b) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},{%4,%5,%6,%7},{%8,%9},{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Rows r < nrows, columns c < width (even): c < valid copied from
+// p1(r)[c] (c < split) or p2(r)[c - split] (c >= split); c >= valid zeroed.
+// A null p1(r) zeroes the whole row. kLanes threads cooperate on one row.
+template <int kLanes, class P1, class P2>
+__device__ __forceinline__ void stage_rows(double* dst, int stride, int nrows, int width, int valid, int split,
+                                           P1 p1, P2 p2) {
+    const int lane = threadIdx.x % kLanes;
+    for (int r = threadIdx.x / kLanes; r < nrows; r += kThreads / kLanes) {
+        const double* s1 = p1(r);
+        const double* s2 = split < valid ? p2(r) - split : s1;
+        double* d = dst + r * stride;
+        for (int c = 2 * lane; c < width; c += 2 * kLanes) {
+            const double* sc = (c < split ? s1 : s2) + c;
+            const bool one_src = (c + 1 < split) || (c >= split);
+            if (s1 && one_src && c + 1 < valid && (reinterpret_cast<uintptr_t>(sc) & 15) == 0) {
+                cp_async16(d + c, sc);
+            } else {
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if (s1 && c + u < valid) cp_async8(d + c + u, (c + u < split ? s1 : s2) + c + u);
+                    else d[c + u] = 0.0;
+                }
+            }
+        }
+    }
+}
+template <int kLanes, class P1>
+__device__ __forceinline__ void stage_rows(double* dst, int stride, int nrows, int width, int valid, P1 p1) {
+    stage_rows<kLanes>(dst, stride, nrows, width, valid, width, p1, p1);
+}
+
+// ---- bulk-copy staging (R even: every row run is 16-byte aligned) ----------
+// One thread per row issues cp.async.bulk copies of the row's contiguous
+// run(s) straight into shared memory, signalling one mbarrier with the byte
+// count; padding is zeroed with plain stores (disjoint from the copies).
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
+    for (unsigned long long spin = 0;; ++spin) {
+        unsigned ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (spin > (1ull << 26)) __trap();  // a lost transaction traps instead of hanging the GPU
+    }
+}
+__device__ __forceinline__ void bulk_copy(double* dst, const double* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Same contract as stage_rows; requires every run start 16-byte aligned and
+// split, valid even. Rows are owned by threads r, r + 256, ...
+template <class P1, class P2>
+__device__ __forceinline__ void stage_rows_bulk(double* dst, int stride, int nrows, int width, int valid, int split,
+                                                P1 p1, P2 p2, unsigned long long* bar) {
+    unsigned bytes = 0;
+    for (int r = threadIdx.x; r < nrows; r += kThreads) {
+        const double* s1 = p1(r);
+        double* d = dst + r * stride;
+        if (!s1) {
+            for (int c = 0; c < width; c += 2) *reinterpret_cast<double2*>(d + c) = make_double2(0.0, 0.0);
+            continue;
+        }
+        const int n1 = min(split, valid), n2 = valid - n1;
+        const unsigned b = static_cast<unsigned>(n1 + n2) * 8u;
+        if (b) bar_expect(bar, b);
+        bytes += b;
+        if (n1) bulk_copy(d, s1, n1 * 8u, bar);
+        if (n2) bulk_copy(d + n1, p2(r), n2 * 8u, bar);
+        for (int c = valid; c < width; ++c) d[c] = 0.0;
+    }
+    (void)bytes;
+}
+template <class P1>
+__device__ __forceinline__ void stage_rows_bulk(double* dst, int stride, int nrows, int width, int valid, P1 p1,
+                                                unsigned long long* bar) {
+    stage_rows_bulk(dst, stride, nrows, width, valid, width, p1, p1, bar);
+}
+// All threads: wait for every copy of this panel (call after the staging calls).
+__device__ __forceinline__ void bulk_wait(unsigned long long* bar, unsigned& parity) {
+    __syncthreads();  // every expect_tx registered
+    if (threadIdx.x == 0) bar_arrive(bar);
+    bar_wait(bar, parity);
+    parity ^= 1u;
+}
+
+// v[e] = fma(coef, aux[e], v[e]) (aux == nullptr: v[e] = coef * v[e]) over n entries.
+__device__ __forceinline__ void combine(double* v, const double* aux, int n, double coef) {
+    for (int e = threadIdx.x; e < n; e += kThreads) v[e] = aux ? __fma_rn(coef, aux[e], v[e]) : coef * v[e];
+}
+
+// acc += A[32 x kpad] * B[kpad x 32] for this thread's fragment (kpad % 8 == 0).
+// kAKMajor: A stored [k][kKS]; else [row][lda].
+template <bool kAKMajor>
+__device__ __forceinline__ void mma_panel(const double* As, int lda, const double* Bs, int kpad, double acc[4]) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 2) * 16, wn = (warp & 3) * 8;
+    auto aval = [&](int row, int k) { return kAKMajor ? As[k * kKS + row] : As[row * lda + k]; };
+    int c = 0;
+    for (; c + kKC <= kpad; c += kKC) {
+        double a[8], b[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = aval(wm + g + 8 * (i & 1), c + t + 4 * (i >> 1));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = Bs[(c + t + 4 * i) * kKS + wn + g];
+        dmma16816(acc, a, b);
+    }
+    if (c < kpad) {  // k8 tail
+        double a[4], b[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = aval(wm + g + 8 * (i & 1), c + t + 4 * (i >> 1));
+#pragma unroll
+        for (int i = 0; i < 2; ++i) b[i] = Bs[(c + t + 4 * i) * kKS + wn + g];
+        dmma1688(acc, a, b);
     }
 }
 
