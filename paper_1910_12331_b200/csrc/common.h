@@ -193,6 +193,9 @@ struct CgParams {
     unsigned long long* trace = nullptr;  // optional: CTA 0 phase timestamps (ns), 8 per iteration
 };
 void run_cg(const CgParams& p, int grid, cudaStream_t st);
+// tile-resident CG (kernels_cg_res.cu); false when the problem does not fit it
+bool run_cg_resident(const CgParams& p, cudaStream_t st);
+std::size_t cg_res_slots_needed(const CgParams& p);
 constexpr int cg_barrier_words() { return 4 + 1024; }  // grid barrier, CTA-order counters, per-SM slots
 int cg_max_grid(int device);
 std::size_t cg_slots_needed(const CgParams& p);

@@ -24,6 +24,7 @@
 #include <algorithm>
 
 #include "common.h"
+#include "grid_sync.cuh"
 #include "tile_gemm.cuh"
 
 namespace cpkit {
@@ -31,26 +32,8 @@ namespace cpkit {
 namespace {
 
 using namespace tile;
-
-// Grid barrier on a monotonically increasing arrival counter: one
-// release-add per CTA, then acquire-polls until every CTA of this round has
-// arrived (no reset, no generation word, no full fences).
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& round) {
-    __syncthreads();
-    ++round;
-    if (threadIdx.x == 0) {
-        const unsigned int target = round * nblocks;
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        unsigned int seen;
-        for (unsigned long long spin = 0;; ++spin) {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
-            if (static_cast<int>(seen - target) >= 0) break;
-            if (spin > (1ull << 30)) __trap();  // never hang the GPU on a lost arrival
-        }
-    }
-    __syncthreads();
-    fence_async_global();  // later bulk copies (async proxy) see the data released by other CTAs
-}
+using gsync::grid_barrier;
+using gsync::cta_rank;
 
 // Panel staging: bulk copies (one thread per row, one mbarrier) when every row
 // run is 16-byte aligned (R even), cp.async otherwise.
@@ -81,23 +64,6 @@ struct Stager {
         }
     }
 };
-
-// Task-order rank: the hardware packs consecutive block indices onto the same
-// SMs, so phases with fewer tasks than CTAs would double up on half the SMs.
-// Rank CTAs by their slot on their SM first (slot-0 CTAs get ranks 0.., the
-// others ranks grid-1 downwards), so tasks 0..#SMs-1 land on distinct SMs.
-__device__ int cta_rank(unsigned int* words) {
-    __shared__ int rank;
-    if (threadIdx.x == 0) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        const unsigned slot = atomicAdd(words + 4 + (smid & 1023u), 1u);
-        rank = slot == 0 ? static_cast<int>(atomicAdd(words + 1, 1u))
-                         : static_cast<int>(gridDim.x) - 1 - static_cast<int>(atomicAdd(words + 2, 1u));
-    }
-    __syncthreads();
-    return rank;
-}
 
 struct Layout {
     int order, R, tr;            // tr = tiles along R
@@ -578,11 +544,13 @@ std::size_t cg_slots_needed(const CgParams& p) {
     long long smax = 1;
     for (int n = 0; n < p.order; ++n) smax = std::max<long long>(smax, p.rows[n]);
     const long long ksmax = std::max<long long>(1, smax / 32);
-    return static_cast<std::size_t>(4 * L.tasksBC) +
-           static_cast<std::size_t>(ksmax + 1) * p.order * p.R * p.R;
+    return std::max(static_cast<std::size_t>(4 * L.tasksBC) +
+                        static_cast<std::size_t>(ksmax + 1) * p.order * p.R * p.R,
+                    cg_res_slots_needed(p));
 }
 
 void run_cg(const CgParams& p, int grid, cudaStream_t st) {
+    if (run_cg_resident(p, st)) return;  // tile-resident kernel when the tiles fit the machine
     Dev d{};
     d.p = p;
     d.mode = 0;
