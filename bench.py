@@ -247,8 +247,12 @@ def run_b200(args, rank, world, local_rank):
     nrm_gbs = 8.0 * local_elems / (nrm_ms * 1e-3) / 1e9
 
     # ---- GN outer iterations (default config: varying lambda, CG cap min(sum s R, 10 R)=1000)
-    p.set_factors(init)
-    gn_ms, gn_cg = p.time_gn_steps({}, 2)
+    gn_runs = []
+    for i in range(4):  # first call warms the CG kernel's launch path; median of the rest
+        p.set_factors(init)
+        gn_runs.append(p.time_gn_steps({}, 2))
+    gn_ms = statistics.median(r[0] for r in gn_runs[1:])
+    gn_cg = gn_runs[-1][1]
 
     # ---- end to end through the public C ABI (host tensor in, host factors out)
     import torch

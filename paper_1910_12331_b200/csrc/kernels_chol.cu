@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -26,6 +27,10 @@ namespace cpkit {
 namespace {
 
 constexpr std::size_t kSmemBudget = 220 * 1024;
+#ifndef CPKIT_CHOL_ABLATE
+#define CPKIT_CHOL_ABLATE 0  // timing experiments only: 1 skip diag, 2 skip panel, 4 skip update
+#endif
+constexpr int kCholAblate = CPKIT_CHOL_ABLATE;
 
 inline int lda_of(int R) { return R + 1; }
 
@@ -143,6 +148,201 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
             if (tx == 0) out[i * LD + R] = w[ix.inv(i)];
         }
     if (threadIdx.x == 0) status[mat] = st;
+}
+
+// Blocked right-looking Cholesky for the square shared-memory layout: per
+// block of kNB columns, warp 0 factors the diagonal block warp-synchronously
+// (lane = row, no CTA barrier per column), then the CTA solves the panel below
+// it (one thread per row) and applies the symmetric rank-kNB update to the
+// trailing matrix (3 CTA barriers per block instead of 2 per column). Pivot
+// test, jitter retry and output layout are those of chol_kernel.
+// Warp-synchronous factorisation of the kb x kb diagonal block at (k0, k0)
+// (kb <= kNB <= 32): lane i holds row i in registers. No early exit, so the
+// row stays in registers. Returns true (all lanes) on a non-positive pivot.
+template <int kNB>
+__device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int kb) {
+    const int i = threadIdx.x & 31;
+    double r[kNB];
+#pragma unroll
+    for (int m = 0; m < kNB; ++m) r[m] = (i < kb && m <= i) ? w[(k0 + i) * LD + k0 + m] : 0.0;
+    bool failed = false;
+#pragma unroll
+    for (int j = 0; j < kNB; ++j) {
+        const double x = __shfl_sync(0xffffffffu, r[j], j);
+        if (j < kb && !failed && !(x > 0.0) && !isnan(x)) failed = true;  // Eigen LLT: fail iff pivot <= 0
+        const bool go = j < kb && !failed;
+        // one reciprocal square root on the column-to-column critical path
+        // (L_jj = x / sqrt(x) from it; within an ulp of sqrt and 1/sqrt)
+        const double inv = rsqrt(x), l = x * inv;
+        if (go && i > j) r[j] *= inv;
+        if (go && i == j) {
+            r[j] = l;
+            w[(k0 + j) * LD + R] = inv;
+        }
+#pragma unroll
+        for (int m = j + 1; m < kNB; ++m) {
+            const double lmj = __shfl_sync(0xffffffffu, r[j], m);
+            if (go && i >= m) r[m] -= r[j] * lmj;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < kNB; ++m)
+        if (i < kb && m <= i) w[(k0 + i) * LD + k0 + m] = r[m];
+    return failed;
+}
+
+template <int kNB>
+__global__ void __launch_bounds__(256) chol_blocked_kernel(const double* __restrict__ s_all, int R, double lambda,
+                                                           int mode, double* __restrict__ l_all,
+                                                           int* __restrict__ status) {
+    extern __shared__ double w[];
+    const int LD = R + 1;
+    const int mat = blockIdx.x;
+    const double* s = s_all + static_cast<long long>(mat) * R * R;
+    double* out = l_all + static_cast<long long>(mat) * R * LD;
+    __shared__ double trace_sh;
+    __shared__ int fail_sh;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+
+    if (warp == 0) {  // trace, warp-parallel (fixed shuffle order)
+        double tr = 0.0;
+        for (int i = lane; i < R; i += 32) {
+            const double d = s[static_cast<long long>(i) * R + i];
+            tr += (mode == 1) ? d * (1.0 + lambda) : d;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
+        if (lane == 0) trace_sh = tr;
+    }
+    __syncthreads();
+    const double jitter = 1e-12 * trace_sh / static_cast<double>(R);
+
+    int st = 2;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        const double add = (mode == 0 ? lambda : 0.0);
+        {
+            const int total = R * R;  // 8 global loads in flight per thread, then shared stores
+            for (int e0 = tid; e0 < total; e0 += 8 * blockDim.x) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    v[u] = (e < total) ? __ldg(s + e) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = e0 + u * blockDim.x;
+                    if (e < total) {
+                        const int i = e / R, k = e - i * R;
+                        double x = v[u];
+                        if (i == k) {
+                            if (mode == 1) x *= (1.0 + lambda);
+                            x += add;
+                            if (attempt == 1) x += jitter;
+                        }
+                        if (k <= i) w[i * LD + k] = x;
+                    }
+                }
+            }
+        }
+        if (tid == 0) fail_sh = 0;
+        __syncthreads();
+        for (int k0 = 0; k0 < R; k0 += kNB) {
+            const int kb = min(kNB, R - k0);
+            // 1. diagonal block (warp 0): lane i holds row i in registers; per column
+            //    the pivot and every L_mj travel by shuffle (no shared-memory round trips)
+            if (!(kCholAblate & 1) && warp == 0 && diag_factor<kNB>(w, LD, R, k0, kb)) fail_sh = 1;
+            __syncthreads();
+            if (fail_sh) break;
+            // 2. panel: L[i][k0+j] = (A[i][k0+j] - sum_{m<j} L[i][k0+m] L[k0+j][k0+m]) / L_jj,
+            //    one thread per row, the row in registers, two partial sums per dot
+            for (int i = k0 + kb + tid; i < R && !(kCholAblate & 2); i += blockDim.x) {
+                double* row = w + i * LD + k0;
+                double x[kNB];
+#pragma unroll
+                for (int m = 0; m < kNB; ++m) x[m] = (m < kb) ? row[m] : 0.0;
+#pragma unroll
+                for (int j = 0; j < kNB; ++j) {
+                    if (j < kb) {
+                        const double* lj = w + (k0 + j) * LD + k0;
+                        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+                        for (int m = 0; m + 1 < j; m += 2) {
+                            s0 += x[m] * lj[m];
+                            s1 += x[m + 1] * lj[m + 1];
+                        }
+                        if (j & 1) s0 += x[j - 1] * lj[j - 1];
+                        x[j] = (x[j] - (s0 + s1)) * w[(k0 + j) * LD + R];
+                    }
+                }
+#pragma unroll
+                for (int m = 0; m < kNB; ++m)
+                    if (m < kb) row[m] = x[m];
+            }
+            __syncthreads();
+            // 3. trailing update: A[i][m] -= sum_j L[i][k0+j] L[m][k0+j], k0+kb <= m <= i.
+            //    Full 16-column blocks: one DMMA m16n8k16 per 16x8 tile on or below the
+            //    diagonal (rows and columns past R read zero-padded... masked); tail block scalar.
+            {
+                const int t0 = k0 + kb, n = R - t0;
+                if (kCholAblate & 4) {
+                } else if (kb == 16 && kNB == 16 && n > 0) {
+                    const int g = lane >> 2, t = lane & 3;
+                    const int mt = (n + 15) / 16, nt = (n + 7) / 8;
+                    for (int tile = warp; tile < mt * nt; tile += nw) {
+                        const int bi = tile / nt, bj = tile - bi * nt;
+                        const int r0 = t0 + 16 * bi, c0 = t0 + 8 * bj;
+                        if (c0 > r0 + 15) continue;  // strictly above the diagonal
+                        double a[8], b[4], acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const int row = r0 + g + 8 * (q & 1), col = t + 4 * (q >> 1);
+                            a[q] = row < R ? w[row * LD + k0 + col] : 0.0;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int nn = c0 + g, kk = t + 4 * q;
+                            b[q] = nn < R ? w[nn * LD + k0 + kk] : 0.0;
+                        }
+                        asm volatile(
+                            "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
+                            "{%4,%5,%6,%7,%8,%9,%10,%11},{%12,%13,%14,%15},{%0,%1,%2,%3};"
+                            : "+d"(acc[0]), "+d"(acc[1]), "+d"(acc[2]), "+d"(acc[3])
+                            : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]),
+                              "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                const int row = r0 + g + 8 * h, col = c0 + 2 * t + c;
+                                if (row < R && col <= row) w[row * LD + col] -= acc[2 * h + c];
+                            }
+                    }
+                } else {
+                    for (int i = t0 + warp; i < R; i += nw) {
+                        const double* li = w + i * LD + k0;
+                        for (int m = t0 + lane; m <= i; m += 32) {
+                            const double* lm = w + m * LD + k0;
+                            double acc = w[i * LD + m];
+                            for (int j = 0; j < kb; ++j) acc -= li[j] * lm[j];
+                            w[i * LD + m] = acc;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (!fail_sh) {
+            st = attempt;  // 0 ok, 1 ok after jitter
+            break;
+        }
+        __syncthreads();
+    }
+    for (int i = warp; i < R; i += nw) {
+        for (int k = lane; k <= i; k += 32) out[i * LD + k] = w[i * LD + k];
+        if (lane == 0) out[i * LD + R] = w[i * LD + R];
+    }
+    if (tid == 0) status[mat] = st;
 }
 
 // One warp per rhs row: solve (L L^T) y = b. L lower, row stride LD (global),
@@ -298,7 +498,11 @@ void launch_chol_batch(const double* s, int count, int R, const double* lambda, 
                        cudaStream_t st) {
     if (R > 512) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
     const Layout lay = layout_of(R);
-    if (lay == kSquareSmem) {
+    if (lay == kSquareSmem && !std::getenv("CPKIT_CHOL_UNBLOCKED")) {
+        auto fn = chol_blocked_kernel<16>;
+        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        fn<<<count, 256, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
+    } else if (lay == kSquareSmem) {
         auto fn = chol_kernel<SqIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
         fn<<<count, 512, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
