@@ -82,6 +82,10 @@ __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* bar, unsigned byte
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx_only(std::uint64_t* bar, unsigned bytes) {  // no arrival
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned phase) {
     // bounded spin: a lost TMA transaction traps instead of hanging the GPU
     for (unsigned long long spin = 0;; ++spin) {
@@ -198,11 +202,12 @@ __device__ __forceinline__ double lds64(std::uint32_t addr) {
 // tile; warp W is the TMA producer (one elected lane) feeding a `stages`-deep
 // ring of (X tile, KRP tile) buffers guarded by full/empty mbarriers.
 // grid: (n_tiles, m_tiles, splits); block: 32 * (W + 1).
-template <int NTW, bool TRANS>
+template <int NTW, bool TRANS, bool GEN>
 __global__ void __launch_bounds__(32 * 11, 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                 long long M, long long K, int R, int BM, int WN, int BNS, int stages, long long k_per_split,
-                 int splits, double* __restrict__ out, long long out_split_stride) {
+                 const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int WN, int BNS,
+                 int stages, long long k_per_split, int splits, double* __restrict__ out,
+                 long long out_split_stride) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
@@ -213,6 +218,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     const int stage_bytes = x_bytes + b_bytes;
     std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + stages * stage_bytes);
     std::uint64_t* empty = full + stages;
+    std::uint64_t* krp_bar = empty + stages;  // GEN: factor rows of the stage landed
 
     const int WM = BM / 16;
     const int W = WM * WN;  // DMMA warps; warp W is the producer
@@ -238,37 +244,110 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         for (int s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], W);
+            mbar_init(&krp_bar[s], 1);
         }
         fence_barrier_init();
     }
     __syncthreads();
 
     if (warp == W) {
-        // ---------------- TMA producer: one ring across all of this CTA's units
+        // ---------------- producer: one ring across all of this CTA's units.
+        // X tiles by TMA (one elected lane). The KRP tile either by TMA from the
+        // materialised workspace or (GEN) computed by the whole warp straight
+        // into the stage: row k of the stage is prod_j fac_j[i_j(k)], lanes over
+        // rank pairs, the mixed-radix index advanced row to row (no division).
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&xmap)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
-            long long it = 0;  // global stage counter
-            for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-                int n0, nk, split;
-                long long m0, kbeg;
-                unit_geom(u, n0, m0, kbeg, nk, split);
-                for (int kt = 0; kt < nk; ++kt, ++it) {
-                    const int s = static_cast<int>(it % stages);
-                    if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
-                    const int kk = static_cast<int>(kbeg + static_cast<long long>(kt) * kBK);
-                    char* xs = smem + s * stage_bytes;
-                    mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
+            if (!GEN) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
+        }
+        if (!GEN && lane != 0) return;
+        // GEN: KRP row k = A_0[k / s1] o A_1[k % s1]; scale the landed A_1 rows of
+        // stage `i` in place by the A_0 row, then release the stage to the consumers
+        int pend_n0 = 0;
+        long long pend_kk = 0;
+        auto gen_finish = [&](long long i, int n0, long long kk) {
+            const int s = static_cast<int>(i % stages);
+            double* bsm = reinterpret_cast<double*>(smem + s * stage_bytes + x_bytes);
+            const long long s1 = kd.ext[1];
+            double2 a0v[2][2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long k = kk + 16 * h;
+                const bool ok = k < K;
+                const double* a0 = kd.fac[0] + (k / s1) * R + n0;
+#pragma unroll
+                for (int pass = 0; pass < 2; ++pass) {
+                    const int c = 2 * lane + 64 * pass;
+                    const bool c0 = ok && n0 + c < R, c1 = ok && n0 + c + 1 < R;
+                    a0v[h][pass] = make_double2(c0 ? __ldg(a0 + c) : 0.0, c1 ? __ldg(a0 + c + 1) : 0.0);
+                }
+            }
+            mbar_wait(&krp_bar[s], static_cast<unsigned>((i / stages) & 1));
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll 4
+                for (int q = 16 * h; q < 16 * h + 16; ++q) {
+#pragma unroll
+                    for (int pass = 0; pass < 2; ++pass) {
+                        const int c = 2 * lane + 64 * pass;
+                        if (c < BN) {
+                            double2* dst = reinterpret_cast<double2*>(bsm + q * BNS + c);
+                            const double2 v = *dst;
+                            const double2 f = a0v[h][pass];
+                            *dst = make_double2(v.x * f.x, v.y * f.y);
+                        }
+                    }
+                }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);  // releases the warp's shared stores
+        };
+        long long it = 0;  // global stage counter
+        for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+            int n0, nk, split;
+            long long m0, kbeg;
+            unit_geom(u, n0, m0, kbeg, nk, split);
+            for (int kt = 0; kt < nk; ++kt, ++it) {
+                const int s = static_cast<int>(it % stages);
+                if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+                const long long kk = kbeg + static_cast<long long>(kt) * kBK;
+                char* xs = smem + s * stage_bytes;
+                if (lane == 0) {
+                    if (GEN) {
+                        fence_proxy_async();  // the warp's earlier generic stores to this stage
+                        mbar_expect_tx_only(&full[s], static_cast<unsigned>(x_bytes));
+                    } else {
+                        mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
+                    }
                     for (int b = 0; b < nboxes; ++b) {
                         if (TRANS)
-                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(m0 + 16 * b), kk);
+                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(m0 + 16 * b),
+                                        static_cast<int>(kk));
                         else
-                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, kk + 16 * b, static_cast<int>(m0));
+                            tma_load_2d(&xmap, &full[s], xs + b * box_rows * 128, static_cast<int>(kk + 16 * b),
+                                        static_cast<int>(m0));
                     }
-                    tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, kk);
+                    if (!GEN) {
+                        tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, static_cast<int>(kk));
+                    } else {
+                        // A_1 rows of the two 16-row halves (s1 % 16 == 0: a half never wraps)
+                        mbar_expect_tx(&krp_bar[s], static_cast<unsigned>(b_bytes));
+                        const long long s1 = kd.ext[1];
+                        for (int h = 0; h < 2; ++h) {
+                            const long long k = kk + 16 * h;
+                            tma_load_2d(&kmap, &krp_bar[s], xs + x_bytes + h * 16 * BNS * 8, n0,
+                                        static_cast<int>(k % s1));
+                        }
+                    }
+                }
+                if (GEN) {
+                    // finish the previous stage while this one's copies are in flight
+                    if (it > 0) gen_finish(it - 1, pend_n0, pend_kk);
+                    pend_n0 = n0;
+                    pend_kk = kk;
                 }
             }
         }
+        if (GEN && it > 0) gen_finish(it - 1, pend_n0, pend_kk);
         return;
     }
 
@@ -403,7 +482,7 @@ struct GemmPlan {
 int bns_for(int bn, bool trans) { return trans ? krp_stride<true>(bn) : krp_stride<false>(bn); }
 std::size_t stage_bytes_of(int BM, int bns) { return static_cast<std::size_t>(BM) * kBK * 8 + kBK * bns * 8; }
 std::size_t smem_bytes(const GemmPlan& p) {
-    return static_cast<std::size_t>(p.stages) * stage_bytes_of(p.BM(), p.bns) + p.stages * 16 + 1024;
+    return static_cast<std::size_t>(p.stages) * stage_bytes_of(p.BM(), p.bns) + p.stages * 24 + 1024;
 }
 // Rows per CTA: 16 x wm with wm in [lo, hi], minimising padded rows.
 int pick_wm(long long M, int lo, int hi) {
@@ -483,19 +562,20 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     return p;
 }
 
-template <bool TRANS>
-void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, long long M,
-              long long K, int R, double* out, long long oss) {
+template <bool TRANS, bool GEN>
+void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, const KrpDev& kd,
+              long long M, long long K, int R, double* out, long long oss) {
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
     const dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
     const dim3 block(32 * (p.wm * p.wn + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
-        auto fn = root_gemm_kernel<NTV, TRANS>;                                                    \
+        auto fn = root_gemm_kernel<NTV, TRANS, GEN>;                                               \
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
-        fn<<<grid, block, smem, st>>>(xmap, kmap, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, p.splits, out, oss); \
+        fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, p.splits, out, \
+                                      oss);                                                        \
         break;                                                                                     \
     }
     switch (p.ntw) {
@@ -543,7 +623,7 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
         out = ws;
         oss = F * R;
     }
-    dispatch<false>(p, st, xmap, kmap, F, B, R, out, oss);
+    dispatch<false, false>(p, st, xmap, kmap, to_dev(kb), F, B, R, out, oss);
     if (p.splits > 1) {
         const long long n = F * static_cast<long long>(R);
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
@@ -568,11 +648,23 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
                        cudaStream_t st) {
     const GemmPlan p = plan_gemm(B, F, R, true);
     const int Rs = (R + 1) & ~1;
-    fill_krp(kf, F, R, krp, st);
+    // the Khatri-Rao operand is generated inside the GEMM's producer warp
+    // (no K x R workspace round trip) unless the rank tile is too wide for it
+    // Optional (CPKIT_KRP_GENERATE=1): form the two-mode Khatri-Rao operand inside
+    // the GEMM (A_1 rows by TMA, scaled by the A_0 row in shared memory by the
+    // producer warp) instead of materialising it. Measured at C2: 580 us vs
+    // 554 us fill + GEMM (the single producer warp starves the DMMA warps, 69%
+    // vs 81% pipe activity), so the materialised operand stays the default.
+    const bool gen = kf.nmodes == 2 && R % 2 == 0 && kf.ext[1] % 16 == 0 && p.BN() <= 128 &&
+                     std::getenv("CPKIT_KRP_GENERATE");
+    if (!gen) fill_krp(kf, F, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16, kBK,
                                       true);
-    const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
-                                      static_cast<std::uint32_t>(p.bns), kBK, false);
+    const CUtensorMap kmap =
+        gen ? make_map(kf.fac[1], static_cast<std::uint64_t>(R), static_cast<std::uint64_t>(kf.ext[1]),
+                       static_cast<std::uint32_t>(p.bns), 16, false)
+            : make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
+                       static_cast<std::uint32_t>(p.bns), kBK, false);
     double* out = pb;
     long long oss = 0;
     if (p.splits > 1) {
@@ -581,7 +673,8 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
         out = ws;
         oss = B * R;
     }
-    dispatch<true>(p, st, xmap, kmap, B, F, R, out, oss);
+    if (gen) dispatch<true, true>(p, st, xmap, kmap, to_dev(kf), B, F, R, out, oss);
+    else dispatch<true, false>(p, st, xmap, kmap, to_dev(kf), B, F, R, out, oss);
     if (p.splits > 1) {
         const long long n = B * static_cast<long long>(R);
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));

@@ -4,6 +4,8 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
+kfilt = sys.argv[3] if len(sys.argv) > 3 else None
+active = kfilt is None
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
@@ -15,6 +17,9 @@ for r in rows:
     if r[0] == "File Path":
         fname = r[1].split("/")[-1]; continue
     if r[0] == "Function Name":
+        active = kfilt is None or kfilt in r[1]
+        continue
+    if not active:
         continue
     if r[0] == "Line No":
         hdr = r; continue
