@@ -247,10 +247,15 @@ def run_b200(args, rank, world, local_rank):
     nrm_gbs = 8.0 * local_elems / (nrm_ms * 1e-3) / 1e9
 
     # ---- GN outer iterations (default config: varying lambda, CG cap min(sum s R, 10 R)=1000)
+    # GN: steady-state iterations. Each timed call starts from the same init with
+    # the tree pass of the starting point already cached (gn_optimize computes it
+    # once before its first iteration), so the per-iteration figure is one tree
+    # pass (the post-step residual) + gradient + preconditioner + CG + update.
+    GN_STEPS = 4
     gn_runs = []
     for i in range(4):  # first call warms the CG kernel's launch path; median of the rest
-        p.set_factors(init)
-        gn_runs.append(p.time_gn_steps({}, 2))
+        p.set_factors(init)  # time_gn_steps caches the starting point's tree pass before timing
+        gn_runs.append(p.time_gn_steps({}, GN_STEPS))
     gn_ms = statistics.median(r[0] for r in gn_runs[1:])
     gn_cg = gn_runs[-1][1]
 
@@ -298,8 +303,10 @@ def run_b200(args, rank, world, local_rank):
                 "norm2": {"ms": nrm_ms, "gbs": nrm_gbs, "hbm_frac": nrm_gbs / hbm,
                           "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             },
-            "gn": {"iters_per_s": 2 / (gn_ms * 1e-3), "ms_per_iter": gn_ms / 2, "cg_iters": gn_cg,
-                   "config": "default GnConfig (varying lambda, cg cap 1000)"},
+            "gn": {"iters_per_s": GN_STEPS / (gn_ms * 1e-3), "ms_per_iter": gn_ms / GN_STEPS,
+                   "cg_iters_total": gn_cg, "iters": GN_STEPS,
+                   "config": "default GnConfig (varying lambda, cg cap 1000), steady state: "
+                             "the starting point's tree pass cached before timing"},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(8 * local_elems + 8 * S * RANK),
                     "d2h_bytes_per_step": int(8 * S * RANK),

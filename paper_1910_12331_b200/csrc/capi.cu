@@ -1050,6 +1050,7 @@ cpkit_status cpkit_dev_time_gn_steps(cpkit_dev_problem* p, const char* gn_json, 
         cfg.validate();
         cpkit::RegSchedule s = cfg.schedule;
         const double xn2 = p->p->norm2();
+        p->p->prepare_gn();  // the starting point's tree pass (gn_optimize's setup), untimed
         int cg = 0;
         EventPair ev;
         CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));

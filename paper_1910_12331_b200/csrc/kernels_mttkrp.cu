@@ -479,7 +479,14 @@ struct GemmPlan {
     int BM() const { return 16 * wm; }
     int BN() const { return 8 * ntw * wn; }
 };
-int bns_for(int bn, bool trans) { return trans ? krp_stride<true>(bn) : krp_stride<false>(bn); }
+int bns_for(int bn, bool trans) {
+    if (const char* e = std::getenv(trans ? "CPKIT_TN_BNS_MOD" : "CPKIT_NN_BNS_MOD")) {  // experiments only
+        int s = bn;
+        while (s % 16 != std::atoi(e)) ++s;
+        return s;
+    }
+    return trans ? krp_stride<true>(bn) : krp_stride<false>(bn);
+}
 std::size_t stage_bytes_of(int BM, int bns) { return static_cast<std::size_t>(BM) * kBK * 8 + kBK * bns * 8; }
 std::size_t smem_bytes(const GemmPlan& p) {
     return static_cast<std::size_t>(p.stages) * stage_bytes_of(p.BM(), p.bns) + p.stages * 24 + 1024;

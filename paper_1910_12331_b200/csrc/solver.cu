@@ -763,7 +763,7 @@ void DeviceProblem::jtj_matvec(const double* dev_w, double* dev_u, double lambda
 }
 
 // gauss_newton.cpp:279-349; G must hold the gradient. Result in V.
-CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
+CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gnorm_in) {
     const int N = order();
     const RegShape shape = cfg.schedule.shape;
     int cap = cfg.cg_max_iters;
@@ -773,7 +773,7 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg) {
         cap = static_cast<int>(std::min<std::uint64_t>(total, 10ull * static_cast<std::uint64_t>(R_)));
     }
     CgResultInfo out;
-    const double gnorm = norm_sum(G_.get());
+    const double gnorm = gnorm_in >= 0.0 ? gnorm_in : norm_sum(G_.get());
     if (gnorm == 0.0) {
         ctx_.sync();  // drop any speculative preconditioner factorisation
         precond_pending_ = false;
@@ -923,7 +923,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
         return diag;
     }
     diag.lambda = schedule.lambda;
-    const CgResultInfo cg = cp_cg(diag.lambda, cfg);
+    const CgResultInfo cg = cp_cg(diag.lambda, cfg, diag.grad_norm);
     diag.cg_iters = cg.iterations;
     diag.cg_hit_cap = cg.hit_cap;
     diag.cg_breakdown = cg.breakdown;

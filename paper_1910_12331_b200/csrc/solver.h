@@ -215,7 +215,8 @@ public:
     void gradient();                                  // G (gauss_newton.cpp:81-94)
     double norm_sum(const double* dev_stacked);       // sum_n ||block_n||_F
     void jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape);
-    CgResultInfo cp_cg(double lambda, const GnConfig& cfg);  // V from G (gauss_newton.cpp:279-349)
+    // V from G (gauss_newton.cpp:279-349); gnorm = sum_n ||G_n|| when the caller has it (< 0: computed)
+    CgResultInfo cp_cg(double lambda, const GnConfig& cfg, double gnorm = -1.0);
     void build_preconditioner(double lambda, RegShape shape);
     // factor the preconditioner blocks on the side stream (joined by cp_cg)
     void launch_preconditioner_factor(double lambda, RegShape shape);
@@ -285,6 +286,14 @@ private:
     void second_level_front(int mode);
     void finish_mode(int mode);  // collectives on M^(mode)
     void compute_all_mttkrp();
+
+public:
+    // every M^(n) for the current factors (one tree pass), as gn_step's first call does
+    void prepare_gn() {
+        if (!m_all_valid_) compute_all_mttkrp();
+    }
+
+private:
     void grams_all();
     void check_status(int count, const char* what);
     double read_scalar(int idx);
