@@ -286,6 +286,20 @@ def run_trace(config: dict) -> Report:
     return Report(r)
 
 
+def run_likelihood(config: dict) -> Report:
+    """harness.cpp:488-550 on the device: one CTA per (rank, problem, init) instance."""
+    r = _vp()
+    _chk(load().cpkit_run_likelihood(json.dumps(config).encode(), C.byref(r)))
+    return Report(r)
+
+
+def run_matmul(config: dict) -> Report:
+    """harness.cpp:552-653 on the device: three arms per init, one CTA per instance."""
+    r = _vp()
+    _chk(load().cpkit_run_matmul(json.dumps(config).encode(), C.byref(r)))
+    return Report(r)
+
+
 # ------------------------------------------------------------------ cpkit_dev.h
 class DeviceProblem:
     """cpkit_dev_problem: tensor slab + factors + workspace resident on one GPU."""

@@ -18,6 +18,7 @@
 #include "../../include/cpkit_dev.h"
 #include "json.h"
 #include "solver.h"
+#include "tiny.h"
 
 using cpkit::Json;
 
@@ -27,10 +28,31 @@ struct cpkit_tensor {
 struct cpkit_model {
     cpkit::KruskalModel m;
 };
+struct cpkit_instance {  // InstanceResult (report.hpp:43-48)
+    cpkit::TerminalStatus status = cpkit::TerminalStatus::cap_hit;
+    int iterations = 0;
+    double final_residual = 1.0, best_residual = 1.0;
+};
 struct cpkit_report {
     std::string kind = "trace";
     Json config = Json::object();
     cpkit::ConvergenceReport trace;
+    struct LikRank {  // LikelihoodRankResult (report.hpp:50-56)
+        int rank = 0;
+        std::vector<std::vector<cpkit_instance>> instances;
+        std::vector<int> converged_inits_per_problem;
+        double fraction = 0.0;
+    };
+    std::vector<LikRank> likelihood;
+    struct Arm {  // MatmulArmResult (report.hpp:62-67)
+        std::string name;
+        double success_tol = 0.0;
+        std::vector<cpkit_instance> inits;
+        int converged = 0;
+    };
+    std::uint64_t matmul_n = 0;
+    int matmul_rank = 0;
+    std::vector<Arm> arms;
 };
 struct cpkit_dev_problem {
     std::unique_ptr<cpkit::Context> ctx;
@@ -105,6 +127,7 @@ struct Spec {
     InitDist init;
     std::uint64_t seed = 0;
     int threads = 0;
+    std::uint64_t matmul_n = 2;
 };
 
 cpkit::AlsConfig als_from_json(const Json& j) {
@@ -202,6 +225,7 @@ Spec spec_from_json(const Json& j) {  // harness.cpp:242-276
     family_from_json(problem, s);
     if (s.family == "matmul") {
         const std::uint64_t n = problem.value("matmul_n", 2ull);
+        s.matmul_n = n;
         s.dims = {n * n, n * n, n * n};
     } else if (problem.contains("dims")) {
         s.dims.clear();
@@ -308,6 +332,7 @@ Json resolved_json(const Spec& s) {
         p["b"] = s.fb;
     } else {
         p["family"] = s.family;
+        if (s.family == "matmul") p["matmul_n"] = static_cast<unsigned long long>(s.matmul_n);
     }
     Json dims = Json::array();
     for (auto d : s.dims) dims.push_back(Json(static_cast<unsigned long long>(d)));
@@ -327,10 +352,57 @@ Json resolved_json(const Spec& s) {
     return j;
 }
 
-Json report_to_json(const cpkit_report& r) {  // report.cpp:95-111 (trace kind)
+Json instance_to_json(const cpkit_instance& r) {  // report.cpp:56-61
+    Json o = Json::object();
+    o["status"] = cpkit::to_string(r.status);
+    o["iterations"] = r.iterations;
+    o["final_residual"] = r.final_residual;
+    o["best_residual"] = r.best_residual;
+    return o;
+}
+Json report_to_json(const cpkit_report& r) {  // report.cpp:95-141
     Json j = Json::object();
     j["kind"] = r.kind;
     j["config"] = r.config;
+    if (r.kind == "likelihood") {
+        Json ranks = Json::array();
+        for (const auto& rr : r.likelihood) {
+            Json problems = Json::array();
+            for (std::size_t p = 0; p < rr.instances.size(); ++p) {
+                Json inits = Json::array();
+                for (const auto& inst : rr.instances[p]) inits.push_back(instance_to_json(inst));
+                Json pj = Json::object();
+                pj["problem"] = static_cast<unsigned long long>(p);
+                pj["converged_inits"] = rr.converged_inits_per_problem[p];
+                pj["inits"] = inits;
+                problems.push_back(pj);
+            }
+            Json rj = Json::object();
+            rj["rank"] = rr.rank;
+            rj["fraction"] = rr.fraction;
+            rj["problems"] = problems;
+            ranks.push_back(rj);
+        }
+        j["ranks"] = ranks;
+        return j;
+    }
+    if (r.kind == "matmul") {
+        j["n"] = static_cast<unsigned long long>(r.matmul_n);
+        j["rank"] = r.matmul_rank;
+        Json arms = Json::array();
+        for (const auto& arm : r.arms) {
+            Json inits = Json::array();
+            for (const auto& inst : arm.inits) inits.push_back(instance_to_json(inst));
+            Json aj = Json::object();
+            aj["name"] = arm.name;
+            aj["success_tol"] = arm.success_tol;
+            aj["converged"] = arm.converged;
+            aj["inits"] = inits;
+            arms.push_back(aj);
+        }
+        j["arms"] = arms;
+        return j;
+    }
     j["status"] = cpkit::to_string(r.trace.status);
     Json recs = Json::array();
     for (const auto& rec : r.trace.records) {
@@ -347,8 +419,30 @@ Json report_to_json(const cpkit_report& r) {  // report.cpp:95-111 (trace kind)
     return j;
 }
 std::string fmt_double(double v) { return Json(v).dump(); }
-std::string report_to_csv(const cpkit_report& r) {  // report.cpp:254-266
+std::string report_to_csv(const cpkit_report& r) {  // report.cpp:254-300
     std::ostringstream os;
+    if (r.kind == "likelihood") {
+        os << "rank,problem,init,status,iterations,final_residual,best_residual\n";
+        for (const auto& rr : r.likelihood)
+            for (std::size_t p = 0; p < rr.instances.size(); ++p)
+                for (std::size_t i = 0; i < rr.instances[p].size(); ++i) {
+                    const auto& inst = rr.instances[p][i];
+                    os << rr.rank << ',' << p << ',' << i << ',' << cpkit::to_string(inst.status) << ','
+                       << inst.iterations << ',' << fmt_double(inst.final_residual) << ','
+                       << fmt_double(inst.best_residual) << '\n';
+                }
+        return os.str();
+    }
+    if (r.kind == "matmul") {
+        os << "arm,init,status,iterations,final_residual,best_residual\n";
+        for (const auto& arm : r.arms)
+            for (std::size_t i = 0; i < arm.inits.size(); ++i) {
+                const auto& inst = arm.inits[i];
+                os << arm.name << ',' << i << ',' << cpkit::to_string(inst.status) << ',' << inst.iterations << ','
+                   << fmt_double(inst.final_residual) << ',' << fmt_double(inst.best_residual) << '\n';
+            }
+        return os.str();
+    }
     os << "iter,residual,fitness,lambda,cg_iters,seconds\n";
     for (const auto& rec : r.trace.records)
         os << rec.iteration << ',' << fmt_double(rec.residual) << ',' << fmt_double(rec.fitness) << ','
@@ -402,6 +496,241 @@ void model_to_stacked(const cpkit::KruskalModel& m, double* buf) {
         std::memcpy(buf + at, a.data.data(), a.data.size() * 8);
         at += a.data.size();
     }
+}
+
+// ---- batched independent instances (harness.cpp:433-459, :488-653) ----------------------
+// Tensor entries in the reference's per-entry order (kruskal.cpp:76-90).
+std::vector<double> reconstruct_host(const cpkit::KruskalModel& m) {
+    const int N = static_cast<int>(m.dims.size());
+    std::uint64_t total = 1;
+    for (auto d : m.dims) total *= d;
+    std::vector<double> out(total);
+    std::vector<std::uint64_t> idx(N);
+    for (std::uint64_t f = 0; f < total; ++f) {
+        std::uint64_t rem = f;
+        for (int n = N - 1; n >= 0; --n) {
+            idx[n] = rem % m.dims[n];
+            rem /= m.dims[n];
+        }
+        double acc = 0.0;
+        for (std::int64_t r = 0; r < m.rank; ++r) {
+            double prod = 1.0;
+            for (int n = 0; n < N; ++n) {
+                const double v = m.factors[n].data[idx[n] * m.rank + r];
+                prod = prod * v;
+            }
+            acc = acc + prod;
+        }
+        out[f] = acc;
+    }
+    return out;
+}
+// matmul_tensor (generators.cpp:96-117): T[i n + j, i n + l, l n + j] = 1
+std::vector<double> matmul_data(std::uint64_t n) {
+    const std::uint64_t sq = n * n;
+    std::vector<double> t(sq * sq * sq, 0.0);
+    for (std::uint64_t i = 0; i < n; ++i)
+        for (std::uint64_t l = 0; l < n; ++l)
+            for (std::uint64_t jj = 0; jj < n; ++jj) t[((i * n + jj) * sq + i * n + l) * sq + l * n + jj] = 1.0;
+    return t;
+}
+
+struct BatchJob {
+    std::vector<std::uint64_t> dims;
+    int rank = 1;
+    bool gn = false;
+    cpkit::AlsConfig als;
+    cpkit::GnConfig gncfg;
+    std::vector<std::vector<double>> tensors;  // distinct problem tensors
+    std::vector<int> x_index;                  // instance -> tensor
+    std::vector<cpkit::KruskalModel> inits;    // instance starts
+};
+cpkit::TerminalStatus status_of(int s) {
+    switch (s) {
+        case 0: return cpkit::TerminalStatus::converged_residual;
+        case 1: return cpkit::TerminalStatus::converged_step;
+        case 2: return cpkit::TerminalStatus::cap_hit;
+        default: return cpkit::TerminalStatus::numerical_failure;
+    }
+}
+cpkit_instance summarize(const cpkit::ConvergenceReport& rep) {  // harness.cpp:433-441
+    cpkit_instance r;
+    r.status = rep.status;
+    r.iterations = static_cast<int>(rep.records.size());
+    r.final_residual = rep.final_residual();
+    r.best_residual = rep.best_residual();
+    return r;
+}
+
+// One CTA per instance (kernels_tiny.cu): device buffers of a launched batch.
+struct TinyRun {
+    int count = 0, S = 0;
+    bool want_factors = false;
+    cpkit::DevBuf<double> dx, da, dl, dfac, dfin, dbest;
+    cpkit::DevBuf<int> dxi, dst, dit;
+};
+// Launches the job's batch on `st` (asynchronously); nullptr when the shape
+// does not fit one CTA (or CPKIT_NO_TINY is set).
+std::unique_ptr<TinyRun> tiny_launch(const BatchJob& job, bool want_factors, cudaStream_t st) {
+    const int count = static_cast<int>(job.inits.size());
+    cpkit::TinyLayout lay{};
+    int numel = 0, S = 0;
+    const int N = static_cast<int>(job.dims.size());
+    if (count == 0 || !cpkit::tiny_layout(N, job.dims.data(), job.rank, lay, numel, S) || std::getenv("CPKIT_NO_TINY"))
+        return nullptr;
+    auto run = std::make_unique<TinyRun>();
+    run->count = count;
+    run->S = S;
+    run->want_factors = want_factors;
+    cpkit::TinyParams tp{};
+    tp.order = N;
+    tp.rank = job.rank;
+    tp.off[0] = 0;
+    for (int n = 0; n < N; ++n) {
+        tp.dims[n] = static_cast<int>(job.dims[n]);
+        tp.off[n + 1] = tp.off[n] + tp.dims[n] * job.rank;
+    }
+    tp.S = S;
+    tp.numel = numel;
+    tp.count = count;
+    tp.optimizer = job.gn ? 1 : 0;
+    tp.threads = (S <= 256 && job.rank <= 16 && numel <= 1024) ? 32 : cpkit::kTinyThreads;
+    tp.layout = lay;
+    std::vector<double> lambdas;
+    {
+        const auto& a = job.als;
+        tp.als.max_sweeps = a.max_sweeps;
+        tp.als.residual_tol = a.residual_tol;
+        tp.als.step_tol = a.step_tol;
+        tp.als.lambda0 = a.lambda0;
+        tp.als.decay_every = a.decay_every ? *a.decay_every : 0;
+        if (tp.als.decay_every > 0) {  // lambda_k = lambda0 / decay^k (als.cpp:66-67, host std::pow)
+            const int nk = a.max_sweeps / tp.als.decay_every + 1;
+            for (int k = 0; k < nk; ++k) lambdas.push_back(a.lambda0 / std::pow(a.decay_factor, static_cast<double>(k)));
+        }
+    }
+    {
+        const auto& g = job.gncfg;
+        tp.gn.grad_tol = g.grad_tol;
+        tp.gn.residual_tol = g.residual_tol;
+        tp.gn.step_tol = g.step_tol;
+        tp.gn.cg_tol = g.cg_tol;
+        tp.gn.max_iters = g.max_iters;
+        std::uint64_t total = 0;
+        for (auto d : job.dims) total += d * static_cast<std::uint64_t>(job.rank);
+        tp.gn.cap = g.cg_max_iters > 0 ? g.cg_max_iters
+                                       : static_cast<int>(std::min<std::uint64_t>(total, 10ull * job.rank));
+        tp.gn.mode = g.schedule.mode == cpkit::RegMode::varying ? 1 : 0;
+        tp.gn.shape = g.schedule.shape == cpkit::RegShape::diagonal ? 1 : 0;
+        tp.gn.lambda = g.schedule.lambda;
+        tp.gn.mu = g.schedule.mu;
+        tp.gn.lower = g.schedule.lower;
+        tp.gn.upper = g.schedule.upper;
+        tp.gn.direction = g.schedule.direction == cpkit::RegSchedule::Direction::up ? 1 : 0;
+        tp.gn.armijo = g.armijo ? 1 : 0;
+        const cpkit::ArmijoParams ap = g.armijo ? *g.armijo : cpkit::ArmijoParams{};
+        tp.gn.c1 = ap.c1;
+        tp.gn.shrink = ap.shrink;
+        tp.gn.max_backtracks = ap.max_backtracks;
+        tp.gn.beta_variant = g.cg_beta == cpkit::CgBetaVariant::stale_denominator ? 1 : 0;
+    }
+    std::vector<double> xs;
+    for (const auto& t : job.tensors) xs.insert(xs.end(), t.begin(), t.end());
+    std::vector<double> a0(static_cast<std::size_t>(count) * S);
+    for (int i = 0; i < count; ++i) model_to_stacked(job.inits[i], a0.data() + static_cast<std::size_t>(i) * S);
+    run->dx.resize(xs.size());
+    run->da.resize(a0.size());
+    run->dl.resize(std::max<std::size_t>(1, lambdas.size()));
+    run->dfac.resize(want_factors ? a0.size() : 1);
+    run->dfin.resize(count);
+    run->dbest.resize(count);
+    run->dxi.resize(count);
+    run->dst.resize(count);
+    run->dit.resize(count);
+    CPK_CUDA(cudaMemcpy(run->dx.get(), xs.data(), xs.size() * 8, cudaMemcpyHostToDevice));
+    CPK_CUDA(cudaMemcpy(run->da.get(), a0.data(), a0.size() * 8, cudaMemcpyHostToDevice));
+    if (!lambdas.empty())
+        CPK_CUDA(cudaMemcpy(run->dl.get(), lambdas.data(), lambdas.size() * 8, cudaMemcpyHostToDevice));
+    CPK_CUDA(cudaMemcpy(run->dxi.get(), job.x_index.data(), count * sizeof(int), cudaMemcpyHostToDevice));
+    tp.als.lambdas = run->dl.get();
+    tp.x = run->dx.get();
+    tp.x_index = run->dxi.get();
+    tp.init = run->da.get();
+    tp.factors_out = want_factors ? run->dfac.get() : nullptr;
+    tp.status = run->dst.get();
+    tp.iterations = run->dit.get();
+    tp.final_residual = run->dfin.get();
+    tp.best_residual = run->dbest.get();
+    cpkit::launch_tiny(tp, st);
+    return run;
+}
+// After the launch stream has drained: per-instance results (and factors).
+std::vector<cpkit_instance> tiny_collect(TinyRun& run, std::vector<std::vector<double>>* factors) {
+    const int count = run.count;
+    std::vector<int> st(count), it(count);
+    std::vector<double> fin(count), best(count);
+    CPK_CUDA(cudaMemcpy(st.data(), run.dst.get(), count * sizeof(int), cudaMemcpyDeviceToHost));
+    CPK_CUDA(cudaMemcpy(it.data(), run.dit.get(), count * sizeof(int), cudaMemcpyDeviceToHost));
+    CPK_CUDA(cudaMemcpy(fin.data(), run.dfin.get(), count * 8, cudaMemcpyDeviceToHost));
+    CPK_CUDA(cudaMemcpy(best.data(), run.dbest.get(), count * 8, cudaMemcpyDeviceToHost));
+    std::vector<cpkit_instance> out(count);
+    for (int i = 0; i < count; ++i) out[i] = {status_of(st[i]), it[i], fin[i], best[i]};
+    if (factors && run.want_factors) {
+        std::vector<double> f(static_cast<std::size_t>(count) * run.S);
+        CPK_CUDA(cudaMemcpy(f.data(), run.dfac.get(), f.size() * 8, cudaMemcpyDeviceToHost));
+        factors->assign(count, {});
+        for (int i = 0; i < count; ++i)
+            (*factors)[i].assign(f.begin() + static_cast<std::ptrdiff_t>(i) * run.S,
+                                 f.begin() + static_cast<std::ptrdiff_t>(i + 1) * run.S);
+    }
+    return out;
+}
+
+// Runs every instance of the job: one CTA per instance (kernels_tiny.cu) when
+// the shape fits a CTA, else one device problem per instance. factors (when
+// non-null) receives each instance's final stacked factors.
+std::vector<cpkit_instance> run_batch(const BatchJob& job, std::vector<std::vector<double>>* factors) {
+    const int count = static_cast<int>(job.inits.size());
+    std::vector<cpkit_instance> out(count);
+    if (count == 0) return out;
+    if (job.gn) job.gncfg.validate();
+    else job.als.validate();
+    int S = 0;
+    for (auto d : job.dims) S += static_cast<int>(d) * job.rank;
+    if (auto run = tiny_launch(job, factors != nullptr, 0)) {
+        CPK_CUDA(cudaDeviceSynchronize());
+        return tiny_collect(*run, factors);
+    }
+    // larger instances: one device problem per tensor, instances in sequence
+    cpkit::Context ctx(current_device());
+    if (factors) factors->assign(count, {});
+    for (std::size_t t = 0; t < job.tensors.size(); ++t) {
+        cpkit::DeviceProblem p(ctx, job.dims, job.rank);
+        p.upload_tensor(job.tensors[t].data());
+        for (int i = 0; i < count; ++i) {
+            if (job.x_index[i] != static_cast<int>(t)) continue;
+            cpkit::KruskalModel result = job.inits[i];
+            try {  // run_instance (harness.cpp:443-459)
+                if (job.gn) {
+                    auto [m, rep] = cpkit::gn_optimize(p, job.inits[i], job.gncfg);
+                    out[i] = summarize(rep);
+                    result = std::move(m);
+                } else {
+                    auto [m, rep] = cpkit::als_optimize(p, job.inits[i], job.als);
+                    out[i] = summarize(rep);
+                    result = std::move(m);
+                }
+            } catch (const cpkit::Error&) {
+                out[i] = cpkit_instance{};
+                out[i].status = cpkit::TerminalStatus::numerical_failure;
+            }
+            if (factors) {
+                (*factors)[i].resize(static_cast<std::size_t>(S));
+                model_to_stacked(result, (*factors)[i].data());
+            }
+        }
+    }
+    return out;
 }
 
 struct EventPair {
@@ -628,11 +957,224 @@ cpkit_status cpkit_run_trace(const char* config_json, cpkit_report** out) {
         *out = report.release();
     });
 }
-cpkit_status cpkit_run_likelihood(const char*, cpkit_report**) {
-    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_likelihood: experiment runner not provided by the B200 build");
+// run_likelihood (harness.cpp:488-550): ranks x problems x inits, per-rank
+// fraction of problems with at least one converged init. Each rank's instances
+// run as one batch (one CTA per instance).
+cpkit_status cpkit_run_likelihood(const char* config_json, cpkit_report** out) {
+    if (auto st = require(config_json && out, "cpkit_run_likelihood: null argument")) return st;
+    return guarded([&] {
+        const Spec spec = spec_from_json(Json::parse(config_json));
+        auto report = std::make_unique<cpkit_report>();
+        report->kind = "likelihood";
+        Json cfg = resolved_json(spec);
+        cfg["kind"] = "likelihood";
+        report->config = cfg;
+        const InitDist dist = resolved_init(spec);
+        std::vector<BatchJob> jobs;
+        for (int rank : spec.ranks) {
+            BatchJob job;
+            job.dims = spec.dims;
+            job.rank = rank;
+            job.gn = spec.optimizer == "gn";
+            job.als = spec.als;
+            job.gncfg = spec.gn;
+            for (int p = 0; p < spec.problems; ++p) {  // build_problem_tensor (harness.cpp:422-431)
+                if (spec.family == "matmul") {
+                    job.tensors.push_back(matmul_data(spec.matmul_n));
+                } else {
+                    const std::uint64_t ps = cpkit::problem_seed(spec.seed, rank, p);
+                    job.tensors.push_back(reconstruct_host(
+                        spec.family == "uniform" ? cpkit::random_model_uniform(spec.dims, rank, ps, spec.fa, spec.fb)
+                                                 : cpkit::random_model_gaussian(spec.dims, rank, ps)));
+                }
+                for (int i = 0; i < spec.inits; ++i) {
+                    const std::uint64_t is = cpkit::init_seed(spec.seed, rank, p, i);
+                    job.x_index.push_back(p);
+                    job.inits.push_back(dist.kind == InitKind::uniform
+                                            ? cpkit::random_model_uniform(spec.dims, rank, is, dist.a, dist.b)
+                                            : cpkit::random_model_gaussian(spec.dims, rank, is));
+                }
+            }
+            jobs.push_back(std::move(job));
+        }
+        // every rank's batch in flight at once (one stream each), then collect
+        std::vector<cudaStream_t> streams(jobs.size());
+        std::vector<std::unique_ptr<TinyRun>> runs(jobs.size());
+        for (std::size_t k = 0; k < jobs.size(); ++k) {
+            CPK_CUDA(cudaStreamCreateWithFlags(&streams[k], cudaStreamNonBlocking));
+            jobs[k].gn ? jobs[k].gncfg.validate() : jobs[k].als.validate();
+            runs[k] = tiny_launch(jobs[k], false, streams[k]);
+        }
+        for (std::size_t k = 0; k < jobs.size(); ++k) {
+            std::vector<cpkit_instance> res;
+            if (runs[k]) {
+                CPK_CUDA(cudaStreamSynchronize(streams[k]));
+                res = tiny_collect(*runs[k], nullptr);
+            } else {
+                res = run_batch(jobs[k], nullptr);
+            }
+            CPK_CUDA(cudaStreamDestroy(streams[k]));
+            cpkit_report::LikRank rr;
+            rr.rank = jobs[k].rank;
+            int with_success = 0;
+            for (int p = 0; p < spec.problems; ++p) {
+                std::vector<cpkit_instance> inits(res.begin() + p * spec.inits, res.begin() + (p + 1) * spec.inits);
+                int converged = 0;
+                for (const auto& r : inits)
+                    if (r.status == cpkit::TerminalStatus::converged_residual) ++converged;
+                if (converged > 0) ++with_success;
+                rr.instances.push_back(std::move(inits));
+                rr.converged_inits_per_problem.push_back(converged);
+            }
+            rr.fraction = static_cast<double>(with_success) / static_cast<double>(spec.problems);
+            report->likelihood.push_back(std::move(rr));
+        }
+        *out = report.release();
+    });
 }
-cpkit_status cpkit_run_matmul(const char*, cpkit_report**) {
-    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_matmul: experiment runner not provided by the B200 build");
+
+// run_matmul_protocol (harness.cpp:552-653): three arms per init on the n x n
+// matrix-multiplication tensor: ALS with decaying lambda, and ALS warm start
+// followed by GN (plain / Armijo). Each arm runs as one batch.
+cpkit_status cpkit_run_matmul(const char* config_json, cpkit_report** out) {
+    if (auto st = require(config_json && out, "cpkit_run_matmul: null argument")) return st;
+    return guarded([&] {
+        const Json j = Json::parse(config_json);
+        // MatmulProtocolSpec (harness.hpp:53-83, harness.cpp:295-376)
+        std::uint64_t n = j.value("n", 2ull);
+        int rank = j.value("rank", 7), inits = j.value("inits", 100), threads = j.value("threads", 0);
+        const std::uint64_t seed = j.value("seed", 0ull);
+        InitDist dist = init_from_json(j);
+        if (dist.kind == InitKind::family_default) dist.kind = InitKind::gaussian;
+        double als_lambda0 = 0.01, als_decay_factor = 2.0, als_residual_tol = 1e-8;
+        int als_decay_every = 100, als_max_sweeps = 20000;
+        int warm_sweeps = 200;
+        double warm_lambda = 0.01;
+        double gn_lambda = 1e-3, gn_residual_tol = 1e-8, gn_cg_tol = 1e-3, success_tol = 1e-5;
+        int gn_max_iters = 500;
+        if (j.contains("als")) {
+            const Json& a = j.at("als");
+            als_lambda0 = a.value("lambda0", als_lambda0);
+            als_decay_factor = a.value("decay_factor", als_decay_factor);
+            als_decay_every = a.value("decay_every", als_decay_every);
+            als_max_sweeps = a.value("max_sweeps", als_max_sweeps);
+            als_residual_tol = a.value("residual_tol", als_residual_tol);
+        }
+        if (j.contains("warm")) {
+            const Json& w = j.at("warm");
+            warm_sweeps = w.value("sweeps", warm_sweeps);
+            warm_lambda = w.value("lambda", warm_lambda);
+        }
+        if (j.contains("gn")) {
+            const Json& g = j.at("gn");
+            gn_lambda = g.value("lambda", gn_lambda);
+            gn_max_iters = g.value("max_iters", gn_max_iters);
+            gn_residual_tol = g.value("residual_tol", gn_residual_tol);
+            gn_cg_tol = g.value("cg_tol", gn_cg_tol);
+        }
+        success_tol = j.value("success_tol", success_tol);
+        if (n < 1) throw cpkit::InvalidArgument("matmul protocol: n must be >= 1");
+        if (rank < 1) throw cpkit::InvalidArgument("matmul protocol: rank must be >= 1");
+        if (inits < 1) throw cpkit::InvalidArgument("matmul protocol: inits must be >= 1");
+        if (als_lambda0 < 0 || warm_lambda < 0 || gn_lambda < 0)
+            throw cpkit::InvalidArgument("matmul protocol: negative lambda");
+        if (als_decay_every < 1 || als_max_sweeps < 0 || warm_sweeps < 0 || gn_max_iters < 0)
+            throw cpkit::InvalidArgument("matmul protocol: bad iteration counts");
+
+        auto report = std::make_unique<cpkit_report>();
+        report->kind = "matmul";
+        Json cfg = Json::object();  // MatmulProtocolSpec::resolved_json (harness.cpp:349-376)
+        cfg["n"] = static_cast<unsigned long long>(n);
+        cfg["rank"] = rank;
+        cfg["inits"] = inits;
+        cfg["seed"] = static_cast<unsigned long long>(seed);
+        cfg["threads"] = resolved_threads(threads);
+        cfg["init"] = init_to_json(dist);
+        Json ja = Json::object();
+        ja["lambda0"] = als_lambda0;
+        ja["decay_factor"] = als_decay_factor;
+        ja["decay_every"] = als_decay_every;
+        ja["max_sweeps"] = als_max_sweeps;
+        ja["residual_tol"] = als_residual_tol;
+        cfg["als"] = ja;
+        Json jw = Json::object();
+        jw["sweeps"] = warm_sweeps;
+        jw["lambda"] = warm_lambda;
+        cfg["warm"] = jw;
+        Json jg = Json::object();
+        jg["lambda"] = gn_lambda;
+        jg["max_iters"] = gn_max_iters;
+        jg["residual_tol"] = gn_residual_tol;
+        jg["cg_tol"] = gn_cg_tol;
+        cfg["gn"] = jg;
+        cfg["success_tol"] = success_tol;
+        cfg["kind"] = "matmul";
+        report->config = cfg;
+        report->matmul_n = n;
+        report->matmul_rank = rank;
+
+        const std::uint64_t sq = n * n;
+        const std::vector<std::uint64_t> dims{sq, sq, sq};
+        BatchJob base;
+        base.dims = dims;
+        base.rank = rank;
+        base.tensors.push_back(matmul_data(n));
+        for (int i = 0; i < inits; ++i) {
+            const std::uint64_t is = cpkit::init_seed(seed, rank, 0, i);
+            base.x_index.push_back(0);
+            base.inits.push_back(dist.kind == InitKind::uniform ? cpkit::random_model_uniform(dims, rank, is, dist.a, dist.b)
+                                                                : cpkit::random_model_gaussian(dims, rank, is));
+        }
+        // arm 0: ALS with decaying lambda
+        BatchJob als_arm = base;
+        als_arm.als.max_sweeps = als_max_sweeps;
+        als_arm.als.residual_tol = als_residual_tol;
+        als_arm.als.step_tol = 0.0;
+        als_arm.als.lambda0 = als_lambda0;
+        als_arm.als.decay_factor = als_decay_factor;
+        als_arm.als.decay_every = als_decay_every;
+        const std::vector<cpkit_instance> r0 = run_batch(als_arm, nullptr);
+        // warm start, then the two GN arms from the warm factors
+        BatchJob warm = base;
+        warm.als.max_sweeps = warm_sweeps;
+        warm.als.residual_tol = 0.0;
+        warm.als.step_tol = 0.0;
+        warm.als.lambda0 = warm_lambda;
+        std::vector<std::vector<double>> warm_f;
+        const std::vector<cpkit_instance> rw = run_batch(warm, &warm_f);
+        BatchJob gn_plain = base;
+        gn_plain.gn = true;
+        gn_plain.gncfg.max_iters = gn_max_iters;
+        gn_plain.gncfg.residual_tol = gn_residual_tol;
+        gn_plain.gncfg.step_tol = 0.0;
+        gn_plain.gncfg.cg_tol = gn_cg_tol;
+        gn_plain.gncfg.schedule = cpkit::RegSchedule::constant(gn_lambda);
+        for (int i = 0; i < inits; ++i)
+            gn_plain.inits[i] = model_from_stacked(dims, rank, warm_f[i].data());
+        BatchJob gn_armijo = gn_plain;
+        gn_armijo.gncfg.armijo = cpkit::ArmijoParams{};
+        std::vector<cpkit_instance> r1 = run_batch(gn_plain, nullptr);
+        std::vector<cpkit_instance> r2 = run_batch(gn_armijo, nullptr);
+        for (int i = 0; i < inits; ++i)
+            if (rw[i].status == cpkit::TerminalStatus::numerical_failure) {  // warm start threw
+                r1[i] = cpkit_instance{};
+                r1[i].status = cpkit::TerminalStatus::numerical_failure;
+                r2[i] = r1[i];
+            }
+        const char* names[3] = {"als_decay", "hybrid_gn", "hybrid_gn_armijo"};
+        const std::vector<cpkit_instance>* rs[3] = {&r0, &r1, &r2};
+        for (int arm = 0; arm < 3; ++arm) {
+            cpkit_report::Arm a;
+            a.name = names[arm];
+            a.success_tol = arm == 0 ? als_residual_tol : success_tol;
+            for (int i = 0; i < inits; ++i) {
+                if ((*rs[arm])[i].best_residual < a.success_tol) ++a.converged;
+                a.inits.push_back((*rs[arm])[i]);
+            }
+            report->arms.push_back(std::move(a));
+        }
+        *out = report.release();
+    });
 }
 cpkit_status cpkit_run_bench_matvec(const char*, cpkit_report**) {
     return fail(CPKIT_ERR_INTERNAL, "cpkit_run_bench_matvec: use cpkit_dev_time_jtj in the B200 build");

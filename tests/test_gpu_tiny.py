@@ -1,0 +1,155 @@
+"""Batched tiny-instance solver (one CTA per instance) behind cpkit_run_likelihood /
+cpkit_run_matmul (harness.cpp:488-653).
+
+The device solver mirrors the reference's loop orders with explicitly rounded
+operations, so every instance must reproduce the oracle restatement BITWISE:
+same terminal status, same iteration count, identical final and best residual.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ck():
+    from paper_1910_12331_b200 import cpkit
+    cpkit.load()
+    return cpkit
+
+
+def oracle_instance(orc, x, init, cfg, gn):
+    """run_instance + summarize (harness.cpp:433-459) on the oracle."""
+    try:
+        _, recs, st = (orc.gn_optimize if gn else orc.als_optimize)(x, init, cfg)
+    except orc.OracleError:
+        return ("numerical_failure", 0, 1.0, 1.0)
+    res = [r["residual"] for r in recs]
+    return (st, len(recs), res[-1] if res else 1.0, min([1.0] + res))
+
+
+def check_likelihood(orc, rep, dims, family_kind, fa, fb, seed, cfg, gn):
+    n_inst = 0
+    for rr in rep["ranks"]:
+        R = rr["rank"]
+        with_success = 0
+        for p, prob in enumerate(rr["problems"]):
+            truth = orc.random_model(dims, R, orc.problem_seed(seed, R, p), kind=family_kind, a=fa, b=fb)
+            x = orc.reconstruct(truth)
+            conv = 0
+            for i, inst in enumerate(prob["inits"]):
+                init_kind = "uniform" if (family_kind == "uniform" and fa >= 0.0) else "gaussian"
+                init = orc.random_model(dims, R, orc.init_seed(seed, R, p, i), kind=init_kind)
+                want = oracle_instance(orc, x, init, cfg, gn)
+                got = (inst["status"], inst["iterations"], inst["final_residual"], inst["best_residual"])
+                assert got == want, (R, p, i, got, want)
+                conv += inst["status"] == "converged_residual"
+                n_inst += 1
+            assert prob["converged_inits"] == conv
+            with_success += conv > 0
+        assert rr["fraction"] == with_success / len(rr["problems"])
+    return n_inst
+
+
+def test_likelihood_als_bitwise(orc, ck):
+    dims, seed = [4, 4, 4], 42
+    cfg = {"problem": {"family": "uniform11", "dims": dims, "ranks": [2, 3, 5]}, "optimizer": "als",
+           "problems": 2, "inits": 3, "seed": seed, "als": {"max_sweeps": 400}}
+    rep = ck.run_likelihood(cfg).to_json()
+    assert rep["kind"] == "likelihood" and rep["config"]["kind"] == "likelihood"
+    n = check_likelihood(orc, rep, dims, "uniform", -1.0, 1.0, seed, orc.AlsConfig(max_sweeps=400), False)
+    assert n == 18
+
+
+def test_likelihood_gn_bitwise(orc, ck):
+    dims, seed = [4, 4, 4], 7
+    cfg = {"problem": {"family": "uniform01", "dims": dims, "ranks": [1, 3, 6]}, "optimizer": "gn",
+           "problems": 2, "inits": 2, "seed": seed, "gn": {"max_iters": 60}}
+    rep = ck.run_likelihood(cfg).to_json()
+    check_likelihood(orc, rep, dims, "uniform", 0.0, 1.0, seed, orc.GnConfig(max_iters=60), True)
+
+
+def test_likelihood_gn_variants_bitwise(orc, ck):
+    # diagonal regulariser, Armijo, stale-denominator beta, order 4 and odd extents
+    dims, seed = [3, 4, 2, 3], 5
+    gn = {"max_iters": 40, "reg": {"mode": "varying", "shape": "diagonal"}, "armijo": {"enabled": True},
+          "cg_beta": "stale_denominator"}
+    cfg = {"problem": {"family": "gaussian", "dims": dims, "ranks": [2, 4]}, "optimizer": "gn",
+           "problems": 2, "inits": 2, "seed": seed, "gn": gn}
+    rep = ck.run_likelihood(cfg).to_json()
+    ocfg = orc.GnConfig(max_iters=40, reg_shape=1, armijo=1, cg_beta=1)
+    check_likelihood(orc, rep, dims, "gaussian", 0.0, 1.0, seed, ocfg, True)
+
+
+def test_likelihood_als_decay_bitwise(orc, ck):
+    dims, seed = [5, 3, 4], 11
+    als = {"max_sweeps": 300, "lambda0": 0.05, "decay_factor": 3.0, "decay_every": 7, "step_tol": 0.0}
+    cfg = {"problem": {"family": "uniform01", "dims": dims, "ranks": [2, 4]}, "optimizer": "als",
+           "problems": 1, "inits": 3, "seed": seed, "als": als}
+    rep = ck.run_likelihood(cfg).to_json()
+    ocfg = orc.AlsConfig(max_sweeps=300, lambda0=0.05, decay_factor=3.0, decay_every=7, step_tol=0.0)
+    check_likelihood(orc, rep, dims, "uniform", 0.0, 1.0, seed, ocfg, False)
+
+
+def test_matmul_protocol_bitwise(orc, ck):
+    n, rank, inits, seed = 2, 7, 3, 1
+    cfg = {"n": n, "rank": rank, "inits": inits, "seed": seed,
+           "als": {"max_sweeps": 1500}, "warm": {"sweeps": 60}, "gn": {"max_iters": 40}}
+    rep = ck.run_matmul(cfg).to_json()
+    assert rep["kind"] == "matmul" and rep["n"] == n and rep["rank"] == rank
+    arms = {a["name"]: a for a in rep["arms"]}
+    assert list(arms) == ["als_decay", "hybrid_gn", "hybrid_gn_armijo"]
+    sq = n * n
+    x = np.zeros((sq, sq, sq))
+    for i in range(n):
+        for l in range(n):
+            for j in range(n):
+                x[i * n + j, i * n + l, l * n + j] = 1.0
+    dims = [sq, sq, sq]
+    als_arm = orc.AlsConfig(max_sweeps=1500, residual_tol=1e-8, step_tol=0.0, lambda0=0.01, decay_factor=2.0,
+                            decay_every=100)
+    warm = orc.AlsConfig(max_sweeps=60, residual_tol=0.0, step_tol=0.0, lambda0=0.01)
+    gplain = orc.GnConfig(max_iters=40, residual_tol=1e-8, step_tol=0.0, cg_tol=1e-3, reg_mode=0, lambda_=1e-3)
+    garm = orc.GnConfig(max_iters=40, residual_tol=1e-8, step_tol=0.0, cg_tol=1e-3, reg_mode=0, lambda_=1e-3,
+                        armijo=1)
+    for i in range(inits):
+        init = orc.random_model(dims, rank, orc.init_seed(seed, rank, 0, i), kind="gaussian")
+        want0 = oracle_instance(orc, x, init, als_arm, False)
+        got0 = arms["als_decay"]["inits"][i]
+        assert (got0["status"], got0["iterations"], got0["final_residual"], got0["best_residual"]) == want0
+        wf, _, _ = orc.als_optimize(x, init, warm)
+        for name, gcfg in (("hybrid_gn", gplain), ("hybrid_gn_armijo", garm)):
+            want = oracle_instance(orc, x, wf, gcfg, True)
+            got = arms[name]["inits"][i]
+            assert (got["status"], got["iterations"], got["final_residual"], got["best_residual"]) == want, name
+    for name, a in arms.items():
+        assert a["converged"] == sum(r["best_residual"] < a["success_tol"] for r in a["inits"])
+
+
+def test_report_csv_schema(ck, tmp_path):
+    rep = ck.run_likelihood({"problem": {"family": "uniform01", "dims": [3, 3, 3], "ranks": [1, 2]},
+                             "optimizer": "als", "problems": 2, "inits": 2, "seed": 3})
+    path = tmp_path / "lik.csv"
+    rep.emit("csv", str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == "rank,problem,init,status,iterations,final_residual,best_residual"
+    assert len(lines) == 1 + 2 * 2 * 2
+    mm = ck.run_matmul({"n": 1, "rank": 1, "inits": 2, "seed": 0})
+    path2 = tmp_path / "mm.csv"
+    mm.emit("csv", str(path2))
+    rows = path2.read_text().splitlines()
+    assert rows[0] == "arm,init,status,iterations,final_residual,best_residual" and len(rows) == 1 + 3 * 2
+    j = mm.to_json()
+    assert all(a["converged"] == 2 for a in j["arms"])  # trivial instance converges in every arm
+
+
+def test_tiny_matches_per_instance_device_path(ck, monkeypatch):
+    # the CTA-per-instance solver and the general device path agree on statuses
+    cfg = {"problem": {"family": "uniform01", "dims": [4, 4, 4], "ranks": [2]}, "optimizer": "als",
+           "problems": 1, "inits": 3, "seed": 9, "als": {"max_sweeps": 200}}
+    a = ck.run_likelihood(cfg).to_json()
+    monkeypatch.setenv("CPKIT_NO_TINY", "1")
+    b = ck.run_likelihood(cfg).to_json()
+    for ia, ib in zip(a["ranks"][0]["problems"][0]["inits"], b["ranks"][0]["problems"][0]["inits"]):
+        assert ia["status"] == ib["status"] and ia["iterations"] == ib["iterations"]
+        assert abs(ia["final_residual"] - ib["final_residual"]) < 1e-8
