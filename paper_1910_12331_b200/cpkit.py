@@ -293,6 +293,20 @@ def run_likelihood(config: dict) -> Report:
     return Report(r)
 
 
+def run_bench_matvec(config: dict) -> Report:
+    """selftest.cpp:275-318: the implicit J^T J matvec timed on the device over sizes."""
+    r = _vp()
+    _chk(load().cpkit_run_bench_matvec(json.dumps(config).encode(), C.byref(r)))
+    return Report(r)
+
+
+def run_selftest_oracle(config: dict) -> Report:
+    """selftest.cpp:198-271: device operators vs dense routes evaluated on the device."""
+    r = _vp()
+    _chk(load().cpkit_run_selftest_oracle(json.dumps(config).encode(), C.byref(r)))
+    return Report(r)
+
+
 def run_matmul(config: dict) -> Report:
     """harness.cpp:552-653 on the device: three arms per init, one CTA per instance."""
     r = _vp()

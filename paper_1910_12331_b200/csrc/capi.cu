@@ -19,6 +19,7 @@
 #include "json.h"
 #include "solver.h"
 #include "tiny.h"
+#include "selftest.h"
 
 using cpkit::Json;
 
@@ -53,6 +54,20 @@ struct cpkit_report {
     std::uint64_t matmul_n = 0;
     int matmul_rank = 0;
     std::vector<Arm> arms;
+    struct BenchRow {  // report.hpp:75-81
+        std::uint64_t order = 0, s = 0;
+        int rank = 0, reps = 0;
+        double seconds_per_matvec = 0.0;
+    };
+    std::vector<BenchRow> bench;
+    struct Check {  // SelftestRow
+        std::string name;
+        int instances = 0;
+        double max_rel_error = 0.0, tolerance = 0.0;
+        bool pass = false;
+    };
+    std::vector<Check> checks;
+    bool all_pass = false;
 };
 struct cpkit_dev_problem {
     std::unique_ptr<cpkit::Context> ctx;
@@ -403,6 +418,35 @@ Json report_to_json(const cpkit_report& r) {  // report.cpp:95-141
         j["arms"] = arms;
         return j;
     }
+    if (r.kind == "bench") {
+        Json rows = Json::array();
+        for (const auto& b : r.bench) {
+            Json o = Json::object();
+            o["order"] = static_cast<unsigned long long>(b.order);
+            o["s"] = static_cast<unsigned long long>(b.s);
+            o["rank"] = b.rank;
+            o["reps"] = b.reps;
+            o["seconds_per_matvec"] = b.seconds_per_matvec;
+            rows.push_back(o);
+        }
+        j["rows"] = rows;
+        return j;
+    }
+    if (r.kind == "selftest") {
+        Json checks = Json::array();
+        for (const auto& c : r.checks) {
+            Json o = Json::object();
+            o["name"] = c.name;
+            o["instances"] = c.instances;
+            o["max_rel_error"] = c.max_rel_error;
+            o["tolerance"] = c.tolerance;
+            o["pass"] = c.pass;
+            checks.push_back(o);
+        }
+        j["checks"] = checks;
+        j["all_pass"] = r.all_pass;
+        return j;
+    }
     j["status"] = cpkit::to_string(r.trace.status);
     Json recs = Json::array();
     for (const auto& rec : r.trace.records) {
@@ -441,6 +485,20 @@ std::string report_to_csv(const cpkit_report& r) {  // report.cpp:254-300
                 os << arm.name << ',' << i << ',' << cpkit::to_string(inst.status) << ',' << inst.iterations << ','
                    << fmt_double(inst.final_residual) << ',' << fmt_double(inst.best_residual) << '\n';
             }
+        return os.str();
+    }
+    if (r.kind == "bench") {
+        os << "order,s,rank,reps,seconds_per_matvec\n";
+        for (const auto& b : r.bench)
+            os << b.order << ',' << b.s << ',' << b.rank << ',' << b.reps << ',' << fmt_double(b.seconds_per_matvec)
+               << '\n';
+        return os.str();
+    }
+    if (r.kind == "selftest") {
+        os << "check,instances,max_rel_error,tolerance,pass\n";
+        for (const auto& c : r.checks)
+            os << c.name << ',' << c.instances << ',' << fmt_double(c.max_rel_error) << ','
+               << fmt_double(c.tolerance) << ',' << (c.pass ? 1 : 0) << '\n';
         return os.str();
     }
     os << "iter,residual,fitness,lambda,cg_iters,seconds\n";
@@ -1176,11 +1234,313 @@ cpkit_status cpkit_run_matmul(const char* config_json, cpkit_report** out) {
         *out = report.release();
     });
 }
-cpkit_status cpkit_run_bench_matvec(const char*, cpkit_report**) {
-    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_bench_matvec: use cpkit_dev_time_jtj in the B200 build");
+// run_bench_matvec (selftest.cpp:275-318): the implicit J^T J matvec timed on
+// the device over sizes (warm-up, then the fastest of `reps` single launches,
+// CUDA events on the solver stream).
+cpkit_status cpkit_run_bench_matvec(const char* config_json, cpkit_report** out) {
+    if (auto st = require(out != nullptr, "cpkit_run_bench_matvec: null output")) return st;
+    return guarded([&] {
+        const Json j = parse_config(config_json);
+        const std::uint64_t order = j.value("order", 3ull);
+        std::vector<std::uint64_t> sizes{200};
+        std::vector<int> ranks{100};
+        if (j.contains("s")) {
+            sizes.clear();
+            for (const auto& v : j.at("s").items()) sizes.push_back(v.as_uint());
+        }
+        if (j.contains("ranks")) {
+            ranks.clear();
+            for (const auto& v : j.at("ranks").items()) ranks.push_back(static_cast<int>(v.as_int()));
+        }
+        const int reps = j.value("reps", 5);
+        const std::uint64_t seed = j.value("seed", 0ull);
+        if (order < 2 || sizes.empty() || ranks.empty() || reps < 1)
+            throw cpkit::InvalidArgument("bench: bad configuration");
+        auto report = std::make_unique<cpkit_report>();
+        report->kind = "bench";
+        Json cfg = Json::object();
+        cfg["kind"] = "bench";
+        cfg["order"] = static_cast<unsigned long long>(order);
+        Json js = Json::array(), jr = Json::array();
+        for (auto v : sizes) js.push_back(Json(static_cast<unsigned long long>(v)));
+        for (int v : ranks) jr.push_back(Json(v));
+        cfg["s"] = js;
+        cfg["ranks"] = jr;
+        cfg["reps"] = reps;
+        cfg["seed"] = static_cast<unsigned long long>(seed);
+        report->config = cfg;
+        cpkit::Context ctx(current_device());
+        for (std::uint64_t s : sizes)
+            for (int rank : ranks) {
+                const std::vector<std::uint64_t> dims(order, s);
+                const cpkit::KruskalModel model = cpkit::random_model_gaussian(dims, rank, cpkit::rng_derive(seed, s));
+                const cpkit::KruskalModel w =
+                    cpkit::random_model_gaussian(dims, rank, cpkit::rng_derive(cpkit::rng_derive(seed, s), rank));
+                cpkit::DeviceProblem p(ctx, dims, rank);
+                p.set_factors(model);
+                p.build_gamma_set();
+                std::vector<double> wh(static_cast<std::size_t>(order * s * rank));
+                model_to_stacked(w, wh.data());
+                cpkit::DevBuf<double> dw(wh.size()), du(wh.size());
+                CPK_CUDA(cudaMemcpy(dw.get(), wh.data(), wh.size() * 8, cudaMemcpyHostToDevice));
+                p.jtj_matvec(dw.get(), du.get(), 1e-3, cpkit::RegShape::identity);  // warm-up
+                double best = 1e300;
+                for (int rep = 0; rep < reps; ++rep) {
+                    EventPair ev;
+                    CPK_CUDA(cudaEventRecord(ev.a, ctx.stream));
+                    p.jtj_matvec(dw.get(), du.get(), 1e-3, cpkit::RegShape::identity);
+                    CPK_CUDA(cudaEventRecord(ev.b, ctx.stream));
+                    best = std::min(best, ev.ms() * 1e-3);
+                }
+                cpkit_report::BenchRow row;
+                row.order = order;
+                row.s = s;
+                row.rank = rank;
+                row.reps = reps;
+                row.seconds_per_matvec = best;
+                report->bench.push_back(row);
+            }
+        *out = report.release();
+    });
 }
-cpkit_status cpkit_run_selftest_oracle(const char*, cpkit_report**) {
-    return fail(CPKIT_ERR_INTERNAL, "cpkit_run_selftest_oracle: oracle checks live in tests/ for the B200 build");
+// run_selftest_oracle (selftest.cpp:198-271): the implicit device operators
+// against dense routes evaluated on the device (kernels_selftest.cu) on small
+// seeded instances: matvec vs explicit J^T J, gradient vs central differences,
+// J^T J diagonal blocks vs Gamma(n,n) (x) I, CG vs a dense SPD solve, tree vs
+// naive MTTKRP with the contraction budget, fast vs dense residual.
+cpkit_status cpkit_run_selftest_oracle(const char* config_json, cpkit_report** out) {
+    if (auto st = require(out != nullptr, "cpkit_run_selftest_oracle: null output")) return st;
+    return guarded([&] {
+        const Json j = parse_config(config_json);
+        const std::uint64_t seed = j.value("seed", 0ull);
+        const int instances = j.value("instances", 20);
+        if (instances < 1) throw cpkit::InvalidArgument("selftest: instances must be >= 1");
+        auto report = std::make_unique<cpkit_report>();
+        report->kind = "selftest";
+        Json cfg = Json::object();
+        cfg["kind"] = "selftest";
+        cfg["seed"] = static_cast<unsigned long long>(seed);
+        cfg["instances"] = instances;
+        report->config = cfg;
+        using cpkit::rng_derive;
+        using cpkit::rng_keyed;
+        auto random_dims = [](std::uint64_t sd, std::uint64_t salt, std::size_t order, std::uint64_t lo,
+                              std::uint64_t hi) {
+            std::vector<std::uint64_t> d(order);
+            for (std::size_t m = 0; m < order; ++m) d[m] = lo + rng_keyed(sd, salt, m, 7) % (hi - lo + 1);
+            return d;
+        };
+        auto dense_tensor = [](const std::vector<std::uint64_t>& d, std::uint64_t sd) {
+            std::uint64_t total = 1;
+            for (auto v : d) total *= v;
+            std::vector<double> t(total);
+            for (std::uint64_t f = 0; f < total; ++f) t[f] = cpkit::rng_gaussian(sd, 0xDD, f);
+            return t;
+        };
+        auto nrm = [](const std::vector<double>& v) {
+            double s = 0.0;
+            for (double x : v) s += x * x;
+            return std::sqrt(s);
+        };
+        // stacked (row-major factor blocks) -> vec_stack (column-major per factor, modes in order)
+        auto vec_stack = [](const std::vector<double>& st, const std::vector<std::uint64_t>& d, int R) {
+            std::vector<double> v(st.size());
+            std::size_t off = 0;
+            for (auto sn : d) {
+                for (std::uint64_t i = 0; i < sn; ++i)
+                    for (int r = 0; r < R; ++r) v[off + r * sn + i] = st[off + i * R + r];
+                off += sn * R;
+            }
+            return v;
+        };
+        struct Acc {
+            double max_rel = 0.0;
+            int n = 0;
+            void add(double r) {
+                max_rel = std::max(max_rel, r);
+                ++n;
+            }
+        } matvec, grad, diag, cgc, tree, resid;
+        int worst_contractions = 0;
+        cpkit::Context ctx(current_device());
+        for (int k = 0; k < instances; ++k) {
+            const std::uint64_t inst = rng_derive(cpkit::rng_mix64(seed), static_cast<std::uint64_t>(k));
+            const std::size_t order = 2 + rng_keyed(inst, 1, 0, 0) % 3;
+            const auto dims = random_dims(inst, 2, order, 2, 4);
+            const int rank = 1 + static_cast<int>(rng_keyed(inst, 3, 0, 0) % 3);
+            const cpkit::KruskalModel model = cpkit::random_model_gaussian(dims, rank, rng_derive(inst, 10));
+            const std::vector<double> x = dense_tensor(dims, rng_derive(inst, 11));
+            cpkit::DeviceProblem p(ctx, dims, rank);
+            p.upload_tensor(x.data());
+            p.set_factors(model);
+            const std::size_t vars = static_cast<std::size_t>(p.stacked_elems());
+            cpkit::DevBuf<double> H(vars * vars), dw(vars), du(vars), dfd(vars), dres(1), db(vars), dy(vars);
+            // dense row-major copy for the dense routes (the solver's slab has padded rows)
+            cpkit::DevBuf<double> dxd(x.size());
+            CPK_CUDA(cudaMemcpyAsync(dxd.get(), x.data(), x.size() * 8, cudaMemcpyHostToDevice, ctx.stream));
+            cpkit::launch_explicit_jtj(dims, rank, p.factors_device(), H.get(), ctx.stream);
+            std::vector<double> h(vars * vars);
+            CPK_CUDA(cudaMemcpyAsync(h.data(), H.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            // (1) matvec vs explicit J^T J
+            const cpkit::KruskalModel w = cpkit::random_model_gaussian(dims, rank, rng_derive(inst, 12));
+            std::vector<double> ws(vars), us(vars);
+            model_to_stacked(w, ws.data());
+            CPK_CUDA(cudaMemcpyAsync(dw.get(), ws.data(), vars * 8, cudaMemcpyHostToDevice, ctx.stream));
+            p.build_gamma_set();
+            p.jtj_matvec(dw.get(), du.get(), 0.0, cpkit::RegShape::identity);
+            CPK_CUDA(cudaMemcpyAsync(us.data(), du.get(), vars * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            ctx.sync();
+            {
+                const std::vector<double> wv = vec_stack(ws, dims, rank), got = vec_stack(us, dims, rank);
+                std::vector<double> expd(vars, 0.0), diff(vars);
+                for (std::size_t a = 0; a < vars; ++a)
+                    for (std::size_t b = 0; b < vars; ++b) expd[a] += h[a * vars + b] * wv[b];
+                for (std::size_t a = 0; a < vars; ++a) diff[a] = got[a] - expd[a];
+                matvec.add(nrm(diff) / nrm(expd));
+            }
+            // (2) gradient vs central differences (h = 1e-5)
+            for (std::size_t n = 0; n < order; ++n) p.mttkrp_naive(static_cast<int>(n));
+            p.gradient();
+            cpkit::launch_fd_gradient(dims, rank, p.factors_device(), dxd.get(), 1e-5, dfd.get(), ctx.stream);
+            std::vector<double> g(vars), fd(vars);
+            CPK_CUDA(cudaMemcpyAsync(g.data(), p.G(), vars * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            CPK_CUDA(cudaMemcpyAsync(fd.data(), dfd.get(), vars * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            ctx.sync();
+            {
+                double num = 0.0, den = 0.0;
+                for (std::size_t a = 0; a < vars; ++a) {
+                    num += (g[a] - fd[a]) * (g[a] - fd[a]);
+                    den += g[a] * g[a];
+                }
+                grad.add(std::sqrt(num / den));
+            }
+            // (3) diagonal blocks of J^T J vs Gamma(n,n) (x) I
+            {
+                const std::size_t RR = static_cast<std::size_t>(rank) * rank;
+                std::vector<double> grams(order * RR), pairs(order * order * RR);
+                p.download_gammas(grams.data(), pairs.data());
+                double worst = 0.0;
+                std::size_t off = 0;
+                for (std::size_t n = 0; n < order; ++n) {
+                    const std::size_t sz = dims[n] * rank;
+                    double num = 0.0, den = 0.0;
+                    for (std::size_t a = 0; a < sz; ++a)
+                        for (std::size_t b = 0; b < sz; ++b) {
+                            const std::size_t ra = a / dims[n], ia = a % dims[n], rb = b / dims[n], ib = b % dims[n];
+                            const double e = ia == ib ? pairs[(n * order + n) * RR + ra * rank + rb] : 0.0;
+                            const double d = h[(off + a) * vars + off + b] - e;
+                            num += d * d;
+                            den += e * e;
+                        }
+                    worst = std::max(worst, std::sqrt(num) / std::sqrt(den));
+                    off += sz;
+                }
+                diag.add(worst);
+            }
+            // (4) CG vs dense SPD solve of (J^T J + lambda I) v = -vec(g)
+            {
+                const double lambda = 1e-3;
+                cpkit::GnConfig c;
+                c.cg_tol = 1e-10;
+                c.cg_max_iters = 100000;
+                c.schedule = cpkit::RegSchedule::constant(lambda);
+                p.cp_cg(lambda, c);
+                std::vector<double> v(vars);
+                CPK_CUDA(cudaMemcpyAsync(v.data(), p.V(), vars * 8, cudaMemcpyDeviceToHost, ctx.stream));
+                const std::vector<double> gv = vec_stack(g, dims, rank);
+                std::vector<double> rhs(vars);
+                for (std::size_t a = 0; a < vars; ++a) rhs[a] = -gv[a];
+                CPK_CUDA(cudaMemcpyAsync(db.get(), rhs.data(), vars * 8, cudaMemcpyHostToDevice, ctx.stream));
+                // Cholesky of the vars x vars system (same device LLT as the ALS solves)
+                cpkit::DevBuf<double> dl(cpkit::chol_factor_elems(1, static_cast<int>(vars)));
+                cpkit::DevBuf<int> dst(1);
+                cpkit::launch_chol_batch(H.get(), 1, static_cast<int>(vars), &lambda, 0, dl.get(), dst.get(),
+                                         ctx.stream);
+                cpkit::launch_chol_solve_rows(dl.get(), static_cast<int>(vars), db.get(), 1, dy.get(), ctx.stream);
+                int stat = 0;
+                CPK_CUDA(cudaMemcpyAsync(&stat, dst.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+                std::vector<double> dense(vars);
+                CPK_CUDA(cudaMemcpyAsync(dense.data(), dy.get(), vars * 8, cudaMemcpyDeviceToHost, ctx.stream));
+                ctx.sync();
+                if (stat == 2) throw cpkit::SingularSystem("selftest: dense J^T J + lambda I not positive definite");
+                const std::vector<double> vv = vec_stack(v, dims, rank);
+                std::vector<double> diff(vars);
+                for (std::size_t a = 0; a < vars; ++a) diff[a] = vv[a] - dense[a];
+                cgc.add(nrm(diff) / nrm(dense));
+            }
+            // (6) fast vs dense residual
+            {
+                const double xn2 = p.norm2();
+                p.mttkrp_naive(static_cast<int>(order) - 1);
+                p.build_gamma_set();
+                const double fast = p.residual_fitness(xn2, static_cast<int>(order) - 1).first;
+                cpkit::launch_dense_residual(dims, rank, p.factors_device(), dxd.get(), dres.get(), ctx.stream);
+                double dense = 0.0;
+                CPK_CUDA(cudaMemcpyAsync(&dense, dres.get(), 8, cudaMemcpyDeviceToHost, ctx.stream));
+                ctx.sync();
+                resid.add(std::abs(fast - dense));
+            }
+            // (5) tree vs naive MTTKRP on wider orders, contraction budget
+            {
+                const std::size_t torder = 3 + rng_keyed(inst, 4, 0, 0) % 3;
+                const auto tdims = random_dims(inst, 5, torder, 2, 4);
+                const int trank = 2 + static_cast<int>(rng_keyed(inst, 6, 0, 0) % 3);
+                const cpkit::KruskalModel tm = cpkit::random_model_gaussian(tdims, trank, rng_derive(inst, 13));
+                const std::vector<double> tx = dense_tensor(tdims, rng_derive(inst, 14));
+                cpkit::DeviceProblem q(ctx, tdims, trank);
+                q.upload_tensor(tx.data());
+                cpkit::DevBuf<double> dtx(tx.size());
+                CPK_CUDA(cudaMemcpyAsync(dtx.get(), tx.data(), tx.size() * 8, cudaMemcpyHostToDevice, ctx.stream));
+                q.set_factors(tm);
+                q.invalidate_all();
+                q.reset_contraction_counter();
+                double worst = 0.0;
+                for (std::size_t n = 0; n < torder; ++n) {
+                    std::vector<double> a(tdims[n] * trank), b(tdims[n] * trank), d(a.size());
+                    q.mttkrp(static_cast<int>(n));
+                    q.download_mttkrp(static_cast<int>(n), a.data());
+                    cpkit::DevBuf<double> dm(a.size());
+                    cpkit::launch_dense_mttkrp(tdims, trank, q.factors_device(), dtx.get(), static_cast<int>(n),
+                                               dm.get(), ctx.stream);
+                    CPK_CUDA(cudaMemcpyAsync(b.data(), dm.get(), b.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+                    ctx.sync();
+                    for (std::size_t e = 0; e < a.size(); ++e) d[e] = a[e] - b[e];
+                    worst = std::max(worst, nrm(d) / nrm(b));
+                }
+                // budget: a fresh workspace computing every mode
+                q.invalidate_all();
+                q.reset_contraction_counter();
+                for (std::size_t n = 0; n < torder; ++n) q.mttkrp(static_cast<int>(n));
+                worst_contractions = std::max(worst_contractions, q.full_contractions());
+                tree.add(worst);
+            }
+        }
+        auto push = [&](const char* name, const Acc& a, double tol) {
+            cpkit_report::Check c;
+            c.name = name;
+            c.instances = a.n;
+            c.max_rel_error = a.max_rel;
+            c.tolerance = tol;
+            c.pass = a.max_rel <= tol;
+            report->checks.push_back(c);
+        };
+        push("hessian_matvec_vs_explicit_jtj", matvec, 1e-12);
+        push("gradient_vs_finite_difference", grad, 1e-6);
+        push("jtj_diagonal_blocks_vs_kron", diag, 1e-12);
+        push("cg_vs_dense_solve", cgc, 1e-6);
+        push("tree_mttkrp_vs_naive", tree, 1e-12);
+        push("fast_vs_dense_residual", resid, 1e-10);
+        cpkit_report::Check budget;
+        budget.name = "tree_contraction_budget";
+        budget.instances = instances;
+        budget.max_rel_error = worst_contractions;
+        budget.tolerance = 2.0;
+        budget.pass = worst_contractions <= 2;
+        report->checks.push_back(budget);
+        report->all_pass = true;
+        for (const auto& c : report->checks) report->all_pass = report->all_pass && c.pass;
+        *out = report.release();
+    });
 }
 
 // ---- reports ------------------------------------------------------------------------------

@@ -286,6 +286,11 @@ KruskalModel fill_model(const std::vector<std::uint64_t>& dims, std::int64_t ran
     return m;
 }
 }  // namespace
+std::uint64_t rng_mix64(std::uint64_t x) { return mix64(x); }
+std::uint64_t rng_derive(std::uint64_t h, std::uint64_t v) { return derive(h, v); }
+std::uint64_t rng_keyed(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, std::uint64_t salt) {
+    return keyed(seed, stream, index, salt);
+}
 KruskalModel random_model_uniform(const std::vector<std::uint64_t>& dims, std::int64_t rank,
                                   std::uint64_t seed, double a, double b) {  // generators.cpp:59-68
     if (!(a < b)) throw InvalidArgument("random_model: uniform needs a < b");

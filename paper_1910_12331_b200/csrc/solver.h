@@ -312,6 +312,9 @@ KruskalModel random_model_gaussian(const std::vector<std::uint64_t>& dims, std::
 std::uint64_t problem_seed(std::uint64_t master, int rank, int problem);
 std::uint64_t init_seed(std::uint64_t master, int rank, int problem, int init);
 double rng_uniform(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, double a, double b);
+std::uint64_t rng_mix64(std::uint64_t x);                       // rng.hpp:11-18
+std::uint64_t rng_derive(std::uint64_t h, std::uint64_t v);      // rng.hpp:20-23
+std::uint64_t rng_keyed(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, std::uint64_t salt);
 double rng_gaussian(std::uint64_t seed, std::uint64_t stream, std::uint64_t index);
 
 }  // namespace cpkit

@@ -153,3 +153,23 @@ def test_tiny_matches_per_instance_device_path(ck, monkeypatch):
     for ia, ib in zip(a["ranks"][0]["problems"][0]["inits"], b["ranks"][0]["problems"][0]["inits"]):
         assert ia["status"] == ib["status"] and ia["iterations"] == ib["iterations"]
         assert abs(ia["final_residual"] - ib["final_residual"]) < 1e-8
+
+
+def test_selftest_runner_all_pass(ck):
+    rep = ck.run_selftest_oracle({"seed": 3, "instances": 12}).to_json()
+    assert rep["kind"] == "selftest"
+    names = [c["name"] for c in rep["checks"]]
+    assert names == ["hessian_matvec_vs_explicit_jtj", "gradient_vs_finite_difference",
+                     "jtj_diagonal_blocks_vs_kron", "cg_vs_dense_solve", "tree_mttkrp_vs_naive",
+                     "fast_vs_dense_residual", "tree_contraction_budget"]
+    for c in rep["checks"]:
+        assert c["pass"], c
+        assert c["instances"] == 12
+    assert rep["all_pass"] is True
+
+
+def test_bench_matvec_runner(ck):
+    rep = ck.run_bench_matvec({"order": 3, "s": [50, 100], "ranks": [10, 20], "reps": 3, "seed": 1}).to_json()
+    assert rep["kind"] == "bench" and len(rep["rows"]) == 4
+    for row in rep["rows"]:
+        assert row["order"] == 3 and row["reps"] == 3 and 0.0 < row["seconds_per_matvec"] < 0.1
