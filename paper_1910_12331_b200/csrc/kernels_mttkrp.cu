@@ -186,6 +186,36 @@ __global__ void __launch_bounds__(256) krp_fill_kernel(KrpDev kd, long long K, i
     }
 }
 
+// Two-mode Khatri-Rao rows (the front root of orders 3-4): KRP[k] = A_0[k / s1] o A_1[k % s1].
+// Flat over 16-byte output pairs (fully coalesced stores), 4 pairs in flight per thread.
+__global__ void __launch_bounds__(256) krp_fill2_kernel(const double* __restrict__ a0, const double* __restrict__ a1,
+                                                        unsigned s1, unsigned K, int R, unsigned P2,
+                                                        double2* __restrict__ out) {
+    const unsigned total = K * P2;
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned q0 = blockIdx.x * blockDim.x + threadIdx.x; q0 < total; q0 += 4 * stride) {
+        double2 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned q = q0 + u * stride;
+            v[u] = make_double2(0.0, 0.0);
+            if (q < total) {
+                const unsigned k = q / P2, c = q - k * P2;
+                const unsigned i0 = k / s1, i1 = k - i0 * s1;
+                const int r = 2 * static_cast<int>(c);
+                if (r < R) v[u].x = __ldg(a0 + static_cast<std::size_t>(i0) * R + r) * __ldg(a1 + static_cast<std::size_t>(i1) * R + r);
+                if (r + 1 < R)
+                    v[u].y = __ldg(a0 + static_cast<std::size_t>(i0) * R + r + 1) * __ldg(a1 + static_cast<std::size_t>(i1) * R + r + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned q = q0 + u * stride;
+            if (q < total) out[q] = v[u];
+        }
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -600,6 +630,16 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
 // Fill the KRP operand (K x Rs, Rs = R rounded to even) for a contraction.
 void fill_krp(const KrpDesc& kd, long long K, int R, double* krp, cudaStream_t st) {
     const int Rs = (R + 1) & ~1;
+    if (kd.nmodes == 2 && K * (Rs / 2) < (1LL << 31) && !std::getenv("CPKIT_KRP_FILL_GENERIC")) {
+        const unsigned P2 = static_cast<unsigned>(Rs / 2);
+        const unsigned long long total = static_cast<unsigned long long>(K) * P2;
+        const int blocks = static_cast<int>(std::min<unsigned long long>((total + 1023) / 1024, 8ULL * num_sms()));
+        krp_fill2_kernel<<<blocks, 256, 0, st>>>(kd.fac[0], kd.fac[1], static_cast<unsigned>(kd.ext[1]),
+                                                 static_cast<unsigned>(K), R, P2, reinterpret_cast<double2*>(krp));
+        count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+        return;
+    }
     const int blocks = static_cast<int>(std::min<long long>((K + 7) / 8, 16LL * num_sms()));
     krp_fill_kernel<<<blocks, 256, 0, st>>>(to_dev(kd), K, R, Rs, krp);
     count_launch(1);

@@ -472,6 +472,20 @@ void launch_axpby(double* out, const double* a, double alpha, const double* x, s
     CPK_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void set_flag_scalar_kernel(int* flag, int fv, double* d, double dv) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        *flag = fv;
+        *d = dv;
+    }
+}
+}  // namespace
+// *flag = fv, *d = dv as a device op (capturable in a CUDA graph, unlike a pageable H2D copy)
+void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_t st) {
+    set_flag_scalar_kernel<<<1, 32, 0, st>>>(flag, fv, d, dv);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
 void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st) {
     all_finite_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(x, n, flag); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());

@@ -405,7 +405,10 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     slots_.resize(cg_slots_needed(cp));
 }
 
-DeviceProblem::~DeviceProblem() { profile_enable(false); }
+DeviceProblem::~DeviceProblem() {
+    drop_als_graph();
+    profile_enable(false);
+}
 
 KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {
     KrpDesc d{};
@@ -520,24 +523,33 @@ double DeviceProblem::norm2() {
 // ---- launch profiling ----------------------------------------------------------
 void DeviceProblem::profile_enable(bool on) {
     for (auto& e : prof_) {
-        cudaEventDestroy(e.a);
-        cudaEventDestroy(e.b);
+        if (e.a) cudaEventDestroy(e.a);
+        if (e.b) cudaEventDestroy(e.b);
     }
     prof_.clear();
     profile_ = on;
 }
+namespace {
+// event record that becomes a graph node when the stream is being captured
+void record_event(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CPK_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CPK_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else CPK_CUDA(cudaEventRecord(e, st));
+}
+}  // namespace
 void DeviceProblem::prof_begin(int kind) {
     if (!profile_) return;
     ProfEvent e{};
     e.kind = kind;
     CPK_CUDA(cudaEventCreate(&e.a));
     CPK_CUDA(cudaEventCreate(&e.b));
-    CPK_CUDA(cudaEventRecord(e.a, ctx_.stream));
+    record_event(e.a, ctx_.stream);  // a graph node inside a captured ALS sweep
     prof_.push_back(e);
 }
 void DeviceProblem::prof_end() {
     if (!profile_) return;
-    CPK_CUDA(cudaEventRecord(prof_.back().b, ctx_.stream));
+    record_event(prof_.back().b, ctx_.stream);
 }
 void DeviceProblem::profile_read(double* ms, int* count) {
     ctx_.sync();
@@ -546,8 +558,8 @@ void DeviceProblem::profile_read(double* ms, int* count) {
         count[k] = 0;
     }
     for (auto& e : prof_) {
-        float v = 0.0f;
-        CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
+        float v = e.ms;
+        if (v < 0.0f) CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
         ms[e.kind] += v;
         count[e.kind] += 1;
     }
@@ -850,15 +862,23 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gno
 }
 
 // ---- ALS sweep (als.cpp:22-52) ----------------------------------------------------
-AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
+void DeviceProblem::drop_als_graph() {
+    if (als_exec_) cudaGraphExecDestroy(als_exec_);
+    als_exec_ = nullptr;
+    for (auto& e : als_prof_) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    als_prof_.clear();
+}
+
+// The device work of one sweep (no host synchronisation, capturable).
+void DeviceProblem::als_sweep_body(double lambda) {
     const int N = order();
     const std::size_t RR = static_cast<std::size_t>(R_) * R_;
     reset_contraction_counter();
-    int one = 1;
-    CPK_CUDA(cudaMemcpyAsync(flag_.get(), &one, sizeof(int), cudaMemcpyHostToDevice, ctx_.stream));
+    launch_set_flag_scalar(flag_.get(), 1, scal_.get() + kStep, 0.0, ctx_.stream);
     launch_all_finite(A_.get(), off_[N], flag_.get(), ctx_.stream);  // model.validate()
-    double zero = 0.0;
-    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kStep, &zero, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
     grams_all();
     const std::size_t LDR = chol_factor_elems(1, R_);
     for (int n = 0; n < N; ++n) {
@@ -882,6 +902,53 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
                      ctx_.stream);
     }
     (void)RR;
+}
+
+AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
+    const int N = order();
+    // CUDA graph: one capture per (lambda, cache state, profiling); replays skip
+    // ~30 launch latencies per sweep. Single GPU only (the sharded sweep has
+    // NCCL collectives between its kernels).
+    const bool graphs = !ctx_.comm && !std::getenv("CPKIT_NO_GRAPH");
+    const SweepSig pre = sweep_sig();
+    bool replayed = false;
+    if (graphs && als_exec_ && lambda == als_lambda_ && pre == als_pre_) {
+        CPK_CUDA(cudaGraphLaunch(als_exec_, ctx_.stream));
+        count_launch(static_cast<int>(als_kernels_));  // the replay launches the captured kernels again
+        pf_valid_ = als_post_.pf;
+        pb_valid_ = als_post_.pb;
+        m_all_valid_ = als_post_.mall;
+        contractions_ = als_contr_;
+        replayed = true;
+    } else if (graphs) {
+        drop_als_graph();
+        const std::size_t prof0 = prof_.size();
+        const long long k0 = static_cast<long long>(kernel_launches());
+        CPK_CUDA(cudaStreamBeginCapture(ctx_.stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            als_sweep_body(lambda);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(ctx_.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        CPK_CUDA(cudaStreamEndCapture(ctx_.stream, &g));
+        CPK_CUDA(cudaGraphInstantiate(&als_exec_, g, 0));
+        CPK_CUDA(cudaGraphDestroy(g));
+        als_lambda_ = lambda;
+        als_pre_ = pre;
+        als_post_ = sweep_sig();
+        als_contr_ = contractions_;
+        als_kernels_ = static_cast<long long>(kernel_launches()) - k0;  // counted as captured, i.e. as launched by the first replay below
+        als_prof_.assign(prof_.begin() + static_cast<std::ptrdiff_t>(prof0), prof_.end());  // owned by the graph now
+        prof_.resize(prof0);
+        CPK_CUDA(cudaGraphLaunch(als_exec_, ctx_.stream));
+        replayed = true;
+    } else {
+        als_sweep_body(lambda);
+    }
     AlsSweepDiag diag;
     std::vector<int> st(N);
     int fin = 1;
@@ -890,6 +957,12 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
     CPK_CUDA(cudaMemcpyAsync(&diag.step_norm, scal_.get() + kStep, sizeof(double), cudaMemcpyDeviceToHost,
                              ctx_.stream));
     ctx_.sync();
+    if (replayed && profile_)  // the graph's event pairs, measured for this replay
+        for (const auto& e : als_prof_) {
+            float v = 0.0f;
+            CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
+            prof_.push_back({nullptr, nullptr, e.kind, v});
+        }
     if (!fin) throw InvalidArgument("model factor contains non-finite entries");
     for (int s : st)
         if (s == 2) throw SingularSystem("spd_solve: factorization failed after jitter retry");

@@ -248,7 +248,25 @@ private:
     struct ProfEvent {
         cudaEvent_t a, b;
         int kind;
+        float ms = -1.0f;  // >= 0: already measured (graph replays)
     };
+    // ALS sweep as a CUDA graph: captured once per (lambda, cache state,
+    // profiling) and replayed; host bookkeeping restored from the capture.
+    struct SweepSig {
+        bool pf, pb, mall, prof;
+        bool operator==(const SweepSig& o) const {
+            return pf == o.pf && pb == o.pb && mall == o.mall && prof == o.prof;
+        }
+    };
+    cudaGraphExec_t als_exec_ = nullptr;
+    double als_lambda_ = 0.0;
+    SweepSig als_pre_{}, als_post_{};
+    int als_contr_ = 0;
+    long long als_kernels_ = 0;  // kernel launches per replay (counted during capture)
+    std::vector<ProfEvent> als_prof_;  // event pairs recorded by the graph
+    SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_}; }
+    void drop_als_graph();
+    void als_sweep_body(double lambda);
     bool profile_ = false;
     std::vector<ProfEvent> prof_;
     void prof_begin(int kind);
