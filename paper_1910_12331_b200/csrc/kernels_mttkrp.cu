@@ -796,9 +796,15 @@ __global__ void __launch_bounds__(kRedT, 3) reduce_kept_kernel(const double* __r
                 } else {
                     pv[0] = __ldcs(src);
                 }
+                if (two && VW == 2) {
+                    const double2 w2 = __ldg(reinterpret_cast<const double2*>(wfac + (keep == 0 ? ii : oo) * R + r));
+                    wv[0] = w2.x;
+                    wv[VW - 1] = w2.y;
+                } else {
 #pragma unroll
-                for (int v = 0; v < VW; ++v)
-                    wv[v] = two ? __ldg(wfac + (keep == 0 ? ii : oo) * R + r + v) : kept_weight(kd, keep, oo, ii, r + v, R);
+                    for (int v = 0; v < VW; ++v)
+                        wv[v] = two ? __ldg(wfac + (keep == 0 ? ii : oo) * R + r + v) : kept_weight(kd, keep, oo, ii, r + v, R);
+                }
             };
             // four independent loads in flight per thread
             for (; q + 3 * qlanes < hi; q += 4 * qlanes) {
@@ -840,15 +846,90 @@ __global__ void __launch_bounds__(kRedT, 3) reduce_kept_kernel(const double* __r
         __syncthreads();
     }
 }
+// Two kept modes (order 3 and 4 roots): out[i, r] = sum_q P[base_i + q * stride, r] * W[q, r]
+// (keep = 0: rows q of slab i are contiguous; keep = 1: rows are sk apart),
+// 16-byte loads, 8 rows in flight per thread, q-lanes combined in fixed order.
+__global__ void __launch_bounds__(kRedT, 3) reduce_two_kernel(const double* __restrict__ p,
+                                                            const double* __restrict__ w, int R, long long base_step,
+                                                            long long stride, long long rows, int splits,
+                                                            double* __restrict__ out, long long out_split_stride) {
+    __shared__ double2 red[kRedT];
+    const long long i = blockIdx.x;
+    const int split = blockIdx.y;
+    const int pairs = R / 2;
+    const int cpad = min(kRedT, ((pairs + 31) / 32) * 32);
+    const int qlanes = kRedT / cpad;
+    const int ql = threadIdx.x / cpad, cc = threadIdx.x % cpad;
+    const long long per = (rows + splits - 1) / splits;
+    const long long lo = split * per, hi = min(rows, lo + per);
+    const double* src0 = p + i * base_step;
+    for (int c0 = 0; c0 < pairs; c0 += cpad) {
+        const int c = c0 + cc;
+        double2 acc = make_double2(0.0, 0.0);
+        if (c < pairs) {
+            const double2* ps = reinterpret_cast<const double2*>(src0) + c;
+            const double2* ws = reinterpret_cast<const double2*>(w) + c;
+            const long long ps_step = stride / 2, ws_step = R / 2;
+            long long q = lo + ql;
+            for (; q + 7 * qlanes < hi; q += 8 * qlanes) {
+                double2 pv[8], wv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const long long qq = q + u * qlanes;
+                    pv[u] = __ldcs(ps + qq * ps_step);
+                    wv[u] = __ldg(ws + qq * ws_step);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc.x += pv[u].x * wv[u].x;
+                    acc.y += pv[u].y * wv[u].y;
+                }
+            }
+            for (; q < hi; q += qlanes) {
+                const double2 pv = __ldcs(ps + q * ps_step), wv = __ldg(ws + q * ws_step);
+                acc.x += pv.x * wv.x;
+                acc.y += pv.y * wv.y;
+            }
+        }
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < cpad && c < pairs) {
+            double2 sum = make_double2(0.0, 0.0);
+            for (int l = 0; l < qlanes; ++l) {
+                sum.x += red[l * cpad + threadIdx.x].x;
+                sum.y += red[l * cpad + threadIdx.x].y;
+            }
+            *reinterpret_cast<double2*>(out + split * out_split_stride + i * R + 2 * c) = sum;
+        }
+        __syncthreads();
+    }
+}
+
 int reduce_splits(const KrpDesc& kept, int keep) {
     const long long sk = kept.ext[keep];
     long long total = 1;
     for (int l = 0; l < kept.nmodes; ++l)
         if (l != keep) total *= kept.ext[l];
-    const long long target = 8LL * num_sms();
-    long long s = std::max<long long>(1, (target + sk - 1) / sk);
-    s = std::min<long long>(s, std::max<long long>(1, total / 32));
-    return static_cast<int>(s);
+    // CTAs = sk * s; prefer an s that fills whole waves of 3 resident CTAs per SM
+    const long long wave = 3LL * num_sms();
+    if (kept.nmodes == 2 && sk >= num_sms() && !std::getenv("CPKIT_REDUCE_SPLITS")) return 1;  // measured best (C2)
+    const long long smax = std::max<long long>(1, total / 32);
+    if (const char* e = std::getenv("CPKIT_REDUCE_SPLITS"))
+        if (std::atoll(e) > 0) return static_cast<int>(std::min<long long>(smax, std::atoll(e)));
+    long long best = 1;
+    double best_eff = -1.0;
+    for (long long s = 1; s <= std::min<long long>(smax, 64); ++s) {
+        const long long ctas = sk * s;
+        if (ctas < wave && s < smax && sk * (s + 1) <= 4 * wave) continue;  // at least one full wave when possible
+        const long long waves = (ctas + wave - 1) / wave;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * wave);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+        if (ctas >= 4 * wave) break;
+    }
+    return static_cast<int>(best);
 }
 }  // namespace
 
@@ -870,7 +951,14 @@ void launch_reduce_kept(const double* p, const KrpDesc& kept, int keep, int R, d
         dst = ws;
     }
     dim3 grid(static_cast<unsigned>(sk), splits);
-    if (R % 2 == 0)
+    if (kept.nmodes == 2 && R % 2 == 0 && !std::getenv("CPKIT_REDUCE_GENERIC")) {
+        // keep 0: row (i, j) at (i * inner + j) R, weight A_1[j]; keep 1: row (o, i) at (o * sk + i) R, weight A_0[o]
+        const long long base_step = keep == 0 ? inner * R : R;
+        const long long stride = keep == 0 ? R : sk * R;
+        const long long rows = keep == 0 ? inner : outer;
+        reduce_two_kernel<<<grid, kRedT, 0, st>>>(p, kept.fac[keep == 0 ? 1 : 0], R, base_step, stride, rows, splits,
+                                                  dst, sk * R);
+    } else if (R % 2 == 0)
         reduce_kept_kernel<2><<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
     else
         reduce_kept_kernel<1><<<grid, kRedT, 0, st>>>(p, to_dev(kept), keep, R, outer, sk, inner, splits, dst, sk * R);
