@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 
 #include "common.h"
@@ -353,13 +354,38 @@ template <int NB, class Idx, bool kSmem>
 __global__ void __launch_bounds__(32 * kSolveWarps)
 chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __restrict__ b, long long rows,
                        double* __restrict__ y, long long l_stride, long long rows_per_mat) {
-    extern __shared__ double lsh[];
+    extern __shared__ __align__(16) double lsh[];
     const int LD = R + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const long long mat = blockIdx.y;
     const double* Lg = l_all + mat * l_stride;
     const Idx ix{LD, R};
-    if (kSmem) {
+    if (kSmem && std::is_same<Idx, SqIdx>::value) {
+        // square layout = the global layout: one bulk (TMA) copy of the whole factor
+        __shared__ __align__(8) unsigned long long bar;
+        const unsigned bytes = static_cast<unsigned>(R * LD * sizeof(double));
+        const unsigned sbar = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sbar) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sbar), "r"(bytes) : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    static_cast<unsigned>(__cvta_generic_to_shared(lsh))),
+                "l"(Lg), "r"(bytes), "r"(sbar)
+                : "memory");
+        }
+        __syncthreads();
+        for (;;) {
+            unsigned ok;
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                : "=r"(ok)
+                : "r"(sbar)
+                : "memory");
+            if (ok) break;
+        }
+    } else if (kSmem) {
         // batch the global loads (8 in flight per thread) before the shared stores
         const int total = R * LD;
         for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
