@@ -645,9 +645,10 @@ void DeviceProblem::note_factor_update(int mode) {
     else pb_valid_ = false;             // front-root key holds modes < h
     m_all_valid_ = false;
 }
-void DeviceProblem::invalidate_all() {
+void DeviceProblem::invalidate_all() {  // factors changed wholesale
     pf_valid_ = pb_valid_ = false;
     m_all_valid_ = false;
+    grams_valid_ = false;
 }
 void DeviceProblem::download_mttkrp(int mode, double* host) {
     CPK_CUDA(cudaMemcpyAsync(host, M_.get() + off_[mode], (off_[mode + 1] - off_[mode]) * sizeof(double),
@@ -661,8 +662,10 @@ void DeviceProblem::compute_all_mttkrp() {
 
 // ---- Gamma set / residual / gradient --------------------------------------
 void DeviceProblem::grams_all() {
+    if (grams_valid_) return;  // already gram(A_n) for the current factors
     launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), 0, order(), R_, smax_, gram_ws_.get(), grams_.get(),
                  ctx_.stream);
+    grams_valid_ = true;
 }
 void DeviceProblem::build_gamma_set() {
     grams_all();
@@ -680,6 +683,7 @@ void DeviceProblem::upload_gammas(const double* grams, const double* pair) {
     const int N = order();
     CPK_CUDA(cudaMemcpyAsync(grams_.get(), grams, N * RR * 8, cudaMemcpyHostToDevice, ctx_.stream));
     CPK_CUDA(cudaMemcpyAsync(pair_.get(), pair, N * N * RR * 8, cudaMemcpyHostToDevice, ctx_.stream));
+    grams_valid_ = false;  // caller-provided, not necessarily gram(A)
 }
 std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*last_src*/) {
     if (!(xnorm2 > 0.0)) throw InvalidArgument("residual_fitness: tensor norm must be positive");
@@ -918,6 +922,7 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
         pf_valid_ = als_post_.pf;
         pb_valid_ = als_post_.pb;
         m_all_valid_ = als_post_.mall;
+        grams_valid_ = als_post_.grams;
         contractions_ = als_contr_;
         replayed = true;
     } else if (graphs) {

@@ -253,9 +253,9 @@ private:
     // ALS sweep as a CUDA graph: captured once per (lambda, cache state,
     // profiling) and replayed; host bookkeeping restored from the capture.
     struct SweepSig {
-        bool pf, pb, mall, prof;
+        bool pf, pb, mall, prof, grams;
         bool operator==(const SweepSig& o) const {
-            return pf == o.pf && pb == o.pb && mall == o.mall && prof == o.prof;
+            return pf == o.pf && pb == o.pb && mall == o.mall && prof == o.prof && grams == o.grams;
         }
     };
     cudaGraphExec_t als_exec_ = nullptr;
@@ -264,7 +264,7 @@ private:
     int als_contr_ = 0;
     long long als_kernels_ = 0;  // kernel launches per replay (counted during capture)
     std::vector<ProfEvent> als_prof_;  // event pairs recorded by the graph
-    SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_}; }
+    SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_}; }
     void drop_als_graph();
     void als_sweep_body(double lambda);
     bool profile_ = false;
@@ -282,6 +282,7 @@ private:
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
     DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
+    bool grams_valid_ = false;  // grams_ == gram(A_n) for every n (skips recomputation; same values)
     int contractions_ = 0;
     DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_, gram_ws_;
     std::int64_t smax_ = 1;
