@@ -163,16 +163,25 @@ def run_reference(args, rank, world):
 
 # ------------------------------------------------------------------------ B200 arm
 def cpu_baseline_sample(x_host, init):
-    """Oracle ALS sweep on the host cores over the same tensor (reported only)."""
+    """Oracle ALS sweep on the host cores over the same tensor (reported only).
+    Two settings: all host cores (the reported value), and one
+    thread, the reference's own setting (Eigen without OpenMP)."""
     from oracle import oracle as orc
     cores = os.cpu_count() or 1
     orc.set_threads(cores)
     t = time.perf_counter()
     orc.als_sweep(x_host, init, 0.0)
     dt = time.perf_counter() - t
+    orc.set_threads(1)
+    t = time.perf_counter()
+    orc.als_sweep(x_host, init, 0.0)
+    dt1 = time.perf_counter() - t
+    orc.set_threads(cores)
     return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"1 ALS sweep of the full C2 tensor (oracle restatement of als.cpp:22-52, "
-                      f"{cores} threads, {dt:.2f}s)"}
+                      f"{cores} threads, {dt:.2f}s)",
+            "single_thread": {"value": 1.0 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"the same sweep on 1 thread, the reference's setting ({dt1:.2f}s)"}}
 
 
 def run_b200(args, rank, world, local_rank):
