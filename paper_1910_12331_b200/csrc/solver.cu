@@ -319,6 +319,7 @@ void Context::sync() const {
     CPK_CUDA(cudaStreamSynchronize(aux));
     CPK_CUDA(cudaStreamSynchronize(stream));
 }
+void Context::sync_main() const { CPK_CUDA(cudaStreamSynchronize(stream)); }
 
 void shard_range(std::uint64_t extent, int rank, int world, std::uint64_t* lo, std::uint64_t* hi) {
     const std::uint64_t base = extent / static_cast<std::uint64_t>(world);
@@ -339,6 +340,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N < 2) throw InvalidArgument("mttkrp: tensor order must be at least 2");
     if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
     if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
+    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hpin_), 16 * sizeof(double), cudaHostAllocDefault));
     CPK_CUDA(cudaSetDevice(ctx_.device));
     h_ = (N + 1) / 2;
     shard_range(dims_[N - 1], ctx_.rank(), ctx_.world(), &slab_lo_, &slab_hi_);
@@ -408,6 +410,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
 DeviceProblem::~DeviceProblem() {
     drop_als_graph();
     profile_enable(false);
+    if (hpin_) cudaFreeHost(hpin_);
 }
 
 KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {
@@ -506,11 +509,12 @@ void DeviceProblem::get_factors(KruskalModel& m) {
     get_factors(p);
 }
 
+// Scalar readback through pinned memory, waiting on the solver stream only, so
+// side-stream work (the speculative preconditioner factorisation) keeps running.
 double DeviceProblem::read_scalar(int idx) {
-    double v = 0.0;
-    CPK_CUDA(cudaMemcpyAsync(&v, scal_.get() + idx, sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
-    ctx_.sync();
-    return v;
+    CPK_CUDA(cudaMemcpyAsync(hpin_, scal_.get() + idx, sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync_main();
+    return hpin_[0];
 }
 
 double DeviceProblem::norm2() {
@@ -692,10 +696,9 @@ std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*l
     launch_residual(M_.get() + off_[N - 1], A_.get() + off_[N - 1], static_cast<std::int64_t>(dims_[N - 1]),
                     grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
                     ctx_.stream);
-    double rf[2];
-    CPK_CUDA(cudaMemcpyAsync(rf, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
-    ctx_.sync();
-    return {rf[0], rf[1]};
+    CPK_CUDA(cudaMemcpyAsync(hpin_, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync_main();
+    return {hpin_[0], hpin_[1]};
 }
 void DeviceProblem::gradient() {
     const int N = order();

@@ -165,6 +165,7 @@ struct Context {
     int rank() const { return comm ? comm->rank() : 0; }
     int world() const { return comm ? comm->world() : 1; }
     void sync() const;
+    void sync_main() const;  // the solver stream only (side-stream work keeps running)
 };
 
 // Slab of the last mode owned by a rank (balanced contiguous split).
@@ -282,7 +283,8 @@ private:
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
     DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
-    bool grams_valid_ = false;  // grams_ == gram(A_n) for every n (skips recomputation; same values)
+    bool grams_valid_ = false;
+    double* hpin_ = nullptr;  // pinned host slots for scalar readbacks  // grams_ == gram(A_n) for every n (skips recomputation; same values)
     int contractions_ = 0;
     DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_, gram_ws_;
     std::int64_t smax_ = 1;
