@@ -689,13 +689,17 @@ void DeviceProblem::upload_gammas(const double* grams, const double* pair) {
     CPK_CUDA(cudaMemcpyAsync(pair_.get(), pair, N * N * RR * 8, cudaMemcpyHostToDevice, ctx_.stream));
     grams_valid_ = false;  // caller-provided, not necessarily gram(A)
 }
-std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*last_src*/) {
+void DeviceProblem::residual_launch(double xnorm2) {
     if (!(xnorm2 > 0.0)) throw InvalidArgument("residual_fitness: tensor norm must be positive");
     const int N = order();
-    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kXnorm, &xnorm2, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
+    hpin_[8] = xnorm2;  // pinned upload slot (reused only after a later synchronisation)
+    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kXnorm, hpin_ + 8, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
     launch_residual(M_.get() + off_[N - 1], A_.get() + off_[N - 1], static_cast<std::int64_t>(dims_[N - 1]),
                     grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
                     ctx_.stream);
+}
+std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*last_src*/) {
+    residual_launch(xnorm2);
     CPK_CUDA(cudaMemcpyAsync(hpin_, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
     ctx_.sync_main();
     return {hpin_[0], hpin_[1]};
@@ -990,8 +994,15 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     if (!m_all_valid_) compute_all_mttkrp();
     build_gamma_set();
     launch_preconditioner_factor(schedule.lambda, cfg.schedule.shape);  // overlaps residual/gradient
-    auto [res, fit] = residual_fitness(xnorm2, N - 1);
-    (void)fit;
+    // residual and gradient norm in one readback (the gradient is computed even
+    // when the residual test halts: an unused buffer, no observable difference)
+    residual_launch(xnorm2);
+    gradient();
+    launch_block_norm_sum(G_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
+    CPK_CUDA(cudaMemcpyAsync(hpin_, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(hpin_ + 2, scal_.get() + kNormSum, sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync_main();
+    const double res = hpin_[0];
     diag.residual_before = res;
     diag.residual_after = res;
     if (res < cfg.residual_tol) {
@@ -1000,8 +1011,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
         precond_pending_ = false;
         return diag;
     }
-    gradient();
-    diag.grad_norm = norm_sum(G_.get());
+    diag.grad_norm = hpin_[2];
     if (diag.grad_norm <= cfg.grad_tol) {
         diag.halt = GnStepDiag::Halt::gradient;
         ctx_.sync();
@@ -1049,16 +1059,18 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
         launch_axpy(A_.get(), V_.get(), 1.0, S, ctx_.stream);
     }
     diag.alpha = alpha;
+    // step norm and the finiteness flag in one readback
     launch_block_norm_sum(V_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, alpha,
                           ctx_.stream);
-    diag.step_norm = read_scalar(kNormSum);
     invalidate_all();
-    int one = 1, fin = 1;
-    CPK_CUDA(cudaMemcpyAsync(flag_.get(), &one, sizeof(int), cudaMemcpyHostToDevice, ctx_.stream));
+    launch_set_flag_scalar(flag_.get(), 1, scal_.get() + kStep, 0.0, ctx_.stream);
     launch_all_finite(A_.get(), S, flag_.get(), ctx_.stream);
-    CPK_CUDA(cudaMemcpyAsync(&fin, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    int* fin_pin = reinterpret_cast<int*>(hpin_ + 4);
+    CPK_CUDA(cudaMemcpyAsync(hpin_ + 3, scal_.get() + kNormSum, sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
+    CPK_CUDA(cudaMemcpyAsync(fin_pin, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
     ctx_.sync();
-    if (!fin) throw NumericalFailure("gn_step: non-finite factors after update");
+    diag.step_norm = hpin_[3];
+    if (!*fin_pin) throw NumericalFailure("gn_step: non-finite factors after update");
     if (residual_after < 0.0) {
         compute_all_mttkrp();
         grams_all();

@@ -213,6 +213,7 @@ public:
     void download_gammas(double* grams, double* pair);
     void upload_gammas(const double* grams, const double* pair);
     std::pair<double, double> residual_fitness(double xnorm2, int last_src);  // kruskal.cpp:94-118
+    void residual_launch(double xnorm2);  // the same, result left in the scalar slots (no readback)
     void gradient();                                  // G (gauss_newton.cpp:81-94)
     double norm_sum(const double* dev_stacked);       // sum_n ||block_n||_F
     void jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape);
