@@ -391,3 +391,33 @@ def test_c_abi_errors(ck):
     with pytest.raises(ck.CpkitError) as e:
         ck.decompose(t, {"optimizer": "gn"})
     assert e.value.status == "invalid_argument"  # rank required
+
+
+def test_als_graph_replay_bitwise_and_lambda_decay(orc, monkeypatch):
+    """The ALS sweep runs as a CUDA graph replay (captured per lambda and cache state):
+    bitwise equal to the eager launch sequence, re-captured when the decay schedule
+    changes lambda, and the trace matches the oracle."""
+    from paper_1910_12331_b200 import cpkit
+    dims, R = [30, 26, 22], 6
+    truth = orc.random_model(dims, R, orc.problem_seed(0, R, 0))
+    x = orc.reconstruct(truth)
+    init = orc.random_model(dims, R, orc.init_seed(0, R, 0, 0))
+    cfg = {"optimizer": "als", "als": {"max_sweeps": 12, "residual_tol": 0.0, "step_tol": 0.0,
+                                       "lambda0": 1e-2, "decay_factor": 2.0, "decay_every": 3}}
+    p = cpkit.DeviceProblem(dims, R)
+    p.upload(x)
+    fa, ra = p.optimize(cfg, init)
+    monkeypatch.setenv("CPKIT_NO_GRAPH", "1")
+    q = cpkit.DeviceProblem(dims, R)
+    q.upload(x)
+    fb, rb = q.optimize(cfg, init)
+    for a, b in zip(fa, fb):
+        assert np.array_equal(a, b)
+    ja, jb = ra.to_json(), rb.to_json()
+    assert [r["residual"] for r in ja["records"]] == [r["residual"] for r in jb["records"]]
+    _, recs, st = orc.als_optimize(x, init, orc.AlsConfig(max_sweeps=12, residual_tol=0.0, step_tol=0.0,
+                                                          lambda0=1e-2, decay_factor=2.0, decay_every=3))
+    assert ja["status"] == st and len(ja["records"]) == len(recs)
+    for a, b in zip(ja["records"], recs):
+        assert a["lambda"] == b["lambda"]
+        assert abs(a["residual"] - b["residual"]) < 1e-10
