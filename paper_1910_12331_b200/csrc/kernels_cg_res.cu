@@ -438,6 +438,14 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         r_stamp(d, vb, it, 1);
         grid_barrier(p.barrier, nb, round);
         r_stamp(d, vb, it, 2);
+        // phase B's row panel [W' rows]: the sibling columns are final now, so
+        // their copies fly while A2 runs (own columns from registers)
+        if (has) {
+            copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (fv[k]) Rb[fi[k] * ld + c0 + fc[k]] = Wg[k];
+        }
         // ---- A2: B_p = sum of partial slabs; D_n^T[z][r] = sum_{p!=n} Gamma(n,p)[r][z] B_p[r][z].
         // A group of G (pow2 >= N) adjacent lanes per element e: lane q sums mode q's
         // slabs (all loads in flight), the group exchanges the B_p by shuffles and
@@ -488,7 +496,9 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         r_stamp(d, vb, it, 3);
         // ---- B: Q = [W' | A_n] [Gamma_nn ; D_n^T] + lambda Reg(W'); <W', Q> partial
         if (has) {
-            form_rows(p.W[0], nullptr, 1.0, Wg, Ds, r_dt(d) + n * RR + c0);
+            copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
+            cp_async_wait_all();  // the W' rows issued before A2 and the D slice
+            __syncthreads();
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
             warp_mma<false>(An, ld, wm, Ds, ks, wn, L.rk, acc);

@@ -596,7 +596,7 @@ void DeviceProblem::second_level_back(int mode) {
         launch_reduce_kept(PF_.get(), krp(0, h_, A_.get(), false), mode, R_, out, ws_.get(), ws_.size(),
                            ctx_.stream);
     }
-    if (ctx_.comm) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
+    if (ctx_.comm && !defer_coll_) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
 }
 void DeviceProblem::second_level_front(int mode) {
     const int N = order();
@@ -610,7 +610,7 @@ void DeviceProblem::second_level_front(int mode) {
         launch_reduce_kept(PB_.get(), krp(h_, N, A_.get(), true), mode - h_, R_, out, ws_.get(), ws_.size(),
                            ctx_.stream);
     }
-    if (ctx_.comm) {
+    if (ctx_.comm && !defer_coll_) {
         if (last) {
             const std::size_t per = static_cast<std::size_t>(slab_hi_ - slab_lo_) * R_;
             ctx_.comm->allgather(out, M_.get() + off_[mode], per, ctx_.stream);
@@ -659,8 +659,25 @@ void DeviceProblem::download_mttkrp(int mode, double* host) {
                              cudaMemcpyDeviceToHost, ctx_.stream));
     ctx_.sync();
 }
+// Every M^(n) of one factor set. Sharded: the N-1 partial s_n x R blocks
+// (contiguous in M) are all-reduced in ONE collective and the last mode's
+// slab rows all-gathered once (GN).
 void DeviceProblem::compute_all_mttkrp() {
-    for (int n = 0; n < order(); ++n) mttkrp(n);
+    const int N = order();
+    defer_coll_ = ctx_.comm != nullptr;
+    try {
+        for (int n = 0; n < N; ++n) mttkrp(n);
+    } catch (...) {
+        defer_coll_ = false;
+        throw;
+    }
+    defer_coll_ = false;
+    if (ctx_.comm) {
+        ctx_.comm->allreduce_sum(M_.get(), static_cast<std::size_t>(off_[N - 1]), ctx_.stream);
+        const std::size_t per = static_cast<std::size_t>(slab_hi_ - slab_lo_) * R_;
+        ctx_.comm->allgather(M_.get() + off_[N - 1] + static_cast<std::int64_t>(slab_lo_) * R_,
+                             M_.get() + off_[N - 1], per, ctx_.stream);
+    }
     m_all_valid_ = true;
 }
 

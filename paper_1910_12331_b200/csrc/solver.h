@@ -285,6 +285,7 @@ private:
     DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
     bool grams_valid_ = false;
+    bool defer_coll_ = false;  // compute_all_mttkrp batches the collectives
     double* hpin_ = nullptr;  // pinned host slots for scalar readbacks  // grams_ == gram(A_n) for every n (skips recomputation; same values)
     int contractions_ = 0;
     DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_, gram_ws_;
