@@ -254,6 +254,17 @@ def run_b200(args, rank, world, local_rank):
     jtj_flops = 6.0 * RANK * RANK * S
     nrm_ms = p.time_norm2(5)
     nrm_gbs = 8.0 * local_elems / (nrm_ms * 1e-3) / 1e9
+    # the same streaming kernel on a >= 1 GB tensor (bandwidth-bound
+    # kernels shown at a size where HBM, not launch latency, is the bound)
+    big = None
+    if world == 1:
+        bdims = [512, 512, 512]  # 1.07 GB
+        pb = cpkit.DeviceProblem(bdims, 1)
+        pb.generate(cpkit.random_factors(bdims, 1, 7))
+        big_ms = pb.time_norm2(10)
+        big_bytes = 8.0 * 512 ** 3
+        big = {"ms": big_ms, "gbs": big_bytes / (big_ms * 1e-3) / 1e9, "bytes": big_bytes}
+        pb.close()
 
     # ---- GN outer iterations (default config: varying lambda, CG cap min(sum s R, 10 R)=1000)
     # GN: steady-state iterations. Each timed call starts from the same init with
@@ -309,6 +320,7 @@ def run_b200(args, rank, world, local_rank):
                                "hbm_frac": jtj_bytes / (jtj_ms * 1e-3) / 1e9 / hbm,
                                "tflops": jtj_flops / (jtj_ms * 1e-3) / 1e12,
                                "bytes": jtj_bytes, "note": "3.4 MB working set, L2-resident, launch-bound"},
+                "norm2_1GB": None if big is None else {**big, "hbm_frac": big["gbs"] / hbm},
                 "norm2": {"ms": nrm_ms, "gbs": nrm_gbs, "hbm_frac": nrm_gbs / hbm,
                           "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             },
