@@ -659,11 +659,14 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
     const GemmPlan p = plan_gemm(F, B, R, false);
     
     const int Rs = (R + 1) & ~1;
-    fill_krp(kb, B, R, krp, st);
+    // a one-mode Khatri-Rao operand is the factor itself: map it directly (R even:
+    // 16-byte row stride), no workspace fill
+    const bool direct = kb.nmodes == 1 && R % 2 == 0;
+    if (!direct) fill_krp(kb, B, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16,
                                       static_cast<std::uint32_t>(p.BM()), true);
-    const CUtensorMap kmap = make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(B),
-                                      static_cast<std::uint32_t>(p.bns), kBK, false);
+    const CUtensorMap kmap = make_map(direct ? kb.fac[0] : krp, static_cast<std::uint64_t>(Rs),
+                                      static_cast<std::uint64_t>(B), static_cast<std::uint32_t>(p.bns), kBK, false);
     double* out = pf;
     long long oss = 0;
     if (p.splits > 1) {
@@ -706,13 +709,14 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
     // vs 81% pipe activity), so the materialised operand stays the default.
     const bool gen = kf.nmodes == 2 && R % 2 == 0 && kf.ext[1] % 16 == 0 && p.BN() <= 128 &&
                      std::getenv("CPKIT_KRP_GENERATE");
-    if (!gen) fill_krp(kf, F, R, krp, st);
+    const bool direct = kf.nmodes == 1 && R % 2 == 0;  // the factor itself (order-2 tensors)
+    if (!gen && !direct) fill_krp(kf, F, R, krp, st);
     const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16, kBK,
                                       true);
     const CUtensorMap kmap =
         gen ? make_map(kf.fac[1], static_cast<std::uint64_t>(R), static_cast<std::uint64_t>(kf.ext[1]),
                        static_cast<std::uint32_t>(p.bns), 16, false)
-            : make_map(krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
+            : make_map(direct ? kf.fac[0] : krp, static_cast<std::uint64_t>(Rs), static_cast<std::uint64_t>(F),
                        static_cast<std::uint32_t>(p.bns), kBK, false);
     double* out = pb;
     long long oss = 0;
