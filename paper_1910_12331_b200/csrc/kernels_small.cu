@@ -206,23 +206,32 @@ __global__ void residual_final_kernel(const double* __restrict__ partials, int n
 __global__ void __launch_bounds__(tile::kThreads)
 gradient_kernel(const double* __restrict__ a, const double* __restrict__ gnn,
                 const double* __restrict__ m, long long rows, int R, double* __restrict__ g) {
-    __shared__ tile::Smem sm;
-    const int tr = (R + tile::kT - 1) / tile::kT;
-    const long long rt_n = (rows + tile::kT - 1) / tile::kT;
+    // G = A Gamma(n,n) - M (gauss_newton.cpp:81-94): 32x32 output tiles, the A row
+    // panel and the Gamma column slice staged with cp.async (one round trip per
+    // panel of kPB columns), DMMA tiles
+    extern __shared__ __align__(16) double gsm[];
+    using namespace tile;
+    const int tr = (R + kT - 1) / kT;
+    const long long rt_n = (rows + kT - 1) / kT;
     const long long tasks = rt_n * tr;
+    double* As = gsm;
+    double* Bs = gsm + kT * (kPB + 4);
     for (long long task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const long long i0 = (task / tr) * tile::kT;
-        const int c0 = static_cast<int>(task % tr) * tile::kT;
-        auto la = [&](int row, int k) -> double {
-            const long long i = i0 + row;
-            return i < rows ? a[i * R + k] : 0.0;
-        };
-        auto lb = [&](int k, int col) -> double {
-            const int c = c0 + col;
-            return c < R ? gnn[k * R + c] : 0.0;
-        };
-        double acc[4];
-        tile::tile_gemm(sm, R, la, lb, acc);
+        const long long i0 = (task / tr) * kT;
+        const int c0 = static_cast<int>(task % tr) * kT;
+        const int vr = static_cast<int>(min(static_cast<long long>(kT), rows - i0)), vc = min(kT, R - c0);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int k0 = 0; k0 < R; k0 += kPB) {
+            const int kp = min(kPB, R - k0), kpad = pad8(kp);
+            stage_rows<32>(As, kPB + 4, kT, kpad, kp,
+                           [&](int row) { return row < vr ? a + (i0 + row) * R + k0 : nullptr; });
+            stage_rows<16>(Bs, kKS, kpad, kT, vc,
+                           [&](int k) { return k < kp ? gnn + static_cast<long long>(k0 + k) * R + c0 : nullptr; });
+            cp_async_wait_all();
+            __syncthreads();
+            mma_panel<false>(As, kPB + 4, Bs, kpad, acc);
+            __syncthreads();
+        }
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int gg = lane >> 2, t = lane & 3;
 #pragma unroll
@@ -431,7 +440,9 @@ void launch_residual(const double* m_last, const double* a_last, std::int64_t ro
 void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
                      double* g, cudaStream_t st) {
     const long long tasks = ((rows + tile::kT - 1) / tile::kT) * ((R + tile::kT - 1) / tile::kT);
-    gradient_kernel<<<static_cast<int>(std::min<long long>(tasks, 4 * 148)), tile::kThreads, 0, st>>>(
+    const std::size_t smem = (tile::kT * (tile::kPB + 4) + tile::kPB * tile::kKS) * sizeof(double);
+    CPK_CUDA(cudaFuncSetAttribute(gradient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    gradient_kernel<<<static_cast<int>(std::min<long long>(tasks, 2 * 148)), tile::kThreads, smem, st>>>(
         a, gnn, m, rows, R, g); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
