@@ -60,7 +60,7 @@ struct Ctx {
     double* inv;
     double* misc;  // scalar broadcast slots
     // GN
-    double *M, *G, *V, *Rr, *Z, *W, *Q, *At, *pairs, *pinv, *tb, *td, *add;
+    double *M, *G, *V, *Rr, *Z, *W, *Q, *At, *pairs, *pinv, *tb, *td, *add, *bp;
 };
 
 __device__ __forceinline__ int nthr() { return blockDim.x; }
@@ -430,36 +430,68 @@ __device__ int als_run(Ctx& c, const TinyAls& cfg, double xnorm2, int& iters, do
 }
 
 // ---- GN (gauss_newton.cpp:81-494) -------------------------------------------------------
+// stacked element e -> (mode n, row i, column r)
+__device__ __forceinline__ void stacked_index(const Ctx& c, int e, int& n, int& i, int& r) {
+    n = 0;
+    while (e >= c.P->off[n + 1]) ++n;
+    const int local = e - c.P->off[n];
+    i = local / c.R;
+    r = local - i * c.R;
+}
+
+// hessian_matvec (gauss_newton.cpp:96-136) in two parallel passes: every
+// B_p = A_p^T W_p, then every output element accumulates reg + sum_p add_p in
+// ascending p, each add_p with the reference's own k order (same operations
+// as the per-(n,p) GEMM sequence, two barriers instead of ~2 N^2).
 __device__ void matvec(Ctx& c, const double* w, double lambda, int shape, double* u) {
-    const int N = c.N, R = c.R;
-    for (int n = 0; n < N; ++n) {
-        const int rows = c.P->dims[n];
-        const double* gnn = c.pairs + (n * N + n) * R * R;
-        double* un = u + c.P->off[n];
-        const double* wn = w + c.P->off[n];
-        for (int e = threadIdx.x; e < rows * R; e += nthr()) {
-            const int r = e % R;
-            un[e] = shape == 0 ? fmul(lambda, wn[e]) : fmul(wn[e], fmul(lambda, gnn[r * R + r]));
-        }
-        __syncthreads();
-        for (int p = 0; p < N; ++p) {
-            if (p == n) {
-                gemm(wn, R, 1, gnn, R, 1, c.tb + 0, rows, R, R);  // add = W_n Gamma(n,n)
-                for (int e = threadIdx.x; e < rows * R; e += nthr()) un[e] = fadd(un[e], c.tb[e]);
-            } else {
-                const double* ap = c.A + c.P->off[p];
-                // b = A_p^T W_p (R x R)
-                gemm(ap, 1, R, w + c.P->off[p], R, 1, c.td, R, R, c.P->dims[p]);
-                const double* gnp = c.pairs + (n * N + p) * R * R;
-                for (int e = threadIdx.x; e < R * R; e += nthr()) c.td[e] = fmul(gnp[e], c.td[e]);
-                __syncthreads();
-                // add = A_n d^T
-                gemm(c.A + c.P->off[n], R, 1, c.td, 1, R, c.tb, rows, R, R);
-                for (int e = threadIdx.x; e < rows * R; e += nthr()) un[e] = fadd(un[e], c.tb[e]);
-            }
-            __syncthreads();
-        }
+    const int N = c.N, R = c.R, RR = R * R;
+    for (int e = threadIdx.x; e < N * RR; e += nthr()) {
+        const int p = e / RR, q = e - p * RR, i = q / R, j = q - i * R;
+        const double* ap = c.A + c.P->off[p];
+        const double* wp = w + c.P->off[p];
+        double acc = 0.0;
+        for (int kk = 0; kk < c.P->dims[p]; ++kk) acc = fadd(acc, fmul(ap[kk * R + i], wp[kk * R + j]));
+        c.bp[e] = acc;
     }
+    __syncthreads();
+    for (int e = threadIdx.x; e < c.S; e += nthr()) {
+        int n, i, r;
+        stacked_index(c, e, n, i, r);
+        const double* gnn = c.pairs + (n * N + n) * RR;
+        const double* wn = w + c.P->off[n];
+        const double* an = c.A + c.P->off[n];
+        double un = shape == 0 ? fmul(lambda, wn[i * R + r]) : fmul(wn[i * R + r], fmul(lambda, gnn[r * R + r]));
+        for (int p = 0; p < N; ++p) {
+            double add = 0.0;
+            if (p == n) {
+                for (int kk = 0; kk < R; ++kk) add = fadd(add, fmul(wn[i * R + kk], gnn[kk * R + r]));
+            } else {
+                const double* gnp = c.pairs + (n * N + p) * RR;
+                const double* b = c.bp + p * RR;
+                for (int kk = 0; kk < R; ++kk)
+                    add = fadd(add, fmul(an[i * R + kk], fmul(gnp[r * R + kk], b[r * R + kk])));
+            }
+            un = fadd(un, add);
+        }
+        u[e] = un;
+    }
+    __syncthreads();
+}
+
+// Z_n = R_n Pinv_n for every mode in one pass
+__device__ void apply_pinv(Ctx& c) {
+    const int N = c.N, R = c.R, RR = R * R;
+    (void)N;
+    for (int e = threadIdx.x; e < c.S; e += nthr()) {
+        int n, i, r;
+        stacked_index(c, e, n, i, r);
+        const double* rn = c.Rr + c.P->off[n];
+        const double* pn = c.pinv + n * RR;
+        double acc = 0.0;
+        for (int kk = 0; kk < R; ++kk) acc = fadd(acc, fmul(rn[i * R + kk], pn[kk * R + r]));
+        c.Z[e] = acc;
+    }
+    __syncthreads();
 }
 
 // returns iterations; flags: 1 hit cap, 2 breakdown; -1 non-finite (throws)
@@ -485,8 +517,7 @@ __device__ int cp_cg(Ctx& c, const TinyGn& cfg, double lambda, double gnorm, int
     }
     for (int e = threadIdx.x; e < S; e += nthr()) c.Rr[e] = -c.G[e];
     __syncthreads();
-    for (int n = 0; n < N; ++n)
-        gemm(c.Rr + c.P->off[n], R, 1, c.pinv + n * R * R, R, 1, c.Z + c.P->off[n], c.P->dims[n], R, R);
+    apply_pinv(c);
     for (int e = threadIdx.x; e < S; e += nthr()) c.W[e] = c.Z[e];
     __syncthreads();
     double rz = dot_sum(c, c.Rr, c.Z);
@@ -509,8 +540,7 @@ __device__ int cp_cg(Ctx& c, const TinyGn& cfg, double lambda, double gnorm, int
             c.Rr[e] = fsub(c.Rr[e], fmul(alpha, c.Q[e]));
         }
         __syncthreads();
-        for (int n = 0; n < N; ++n)
-            gemm(c.Rr + c.P->off[n], R, 1, c.pinv + n * R * R, R, 1, c.Z + c.P->off[n], c.P->dims[n], R, R);
+        apply_pinv(c);
         const double rz_new = dot_sum(c, c.Rr, c.Z);
         const double beta = cfg.beta_variant == 0 ? fdiv(rz_new, rz) : fdiv(rz_new, wq);
         for (int e = threadIdx.x; e < S; e += nthr()) c.W[e] = fadd(c.Z[e], fmul(beta, c.W[e]));
@@ -546,13 +576,16 @@ __device__ int gn_run(Ctx& c, const TinyGn& cfg, double xnorm2, int& iters, doub
         __syncthreads();
         const double res = residual(c, xnorm2, c.M + c.P->off[N - 1]);
         if (res < cfg.residual_tol) return 0;  // halt: converged_residual
-        for (int n = 0; n < N; ++n) {             // gradient (:81-94)
-            const int rows = c.P->dims[n];
-            gemm(c.A + c.P->off[n], R, 1, c.pairs + (n * N + n) * R * R, R, 1, c.G + c.P->off[n], rows, R, R);
-            for (int e = threadIdx.x; e < rows * R; e += nthr())
-                c.G[c.P->off[n] + e] = fsub(c.G[c.P->off[n] + e], c.M[c.P->off[n] + e]);
-            __syncthreads();
+        for (int e = threadIdx.x; e < S; e += nthr()) {  // gradient (:81-94): A_n Gamma(n,n) - M_n
+            int n, i, r;
+            stacked_index(c, e, n, i, r);
+            const double* an = c.A + c.P->off[n];
+            const double* gnn = c.pairs + (n * N + n) * R * R;
+            double acc = 0.0;
+            for (int kk = 0; kk < R; ++kk) acc = fadd(acc, fmul(an[i * R + kk], gnn[kk * R + r]));
+            c.G[e] = fsub(acc, c.M[e]);
         }
+        __syncthreads();
         double gnorm = 0.0;
         if (threadIdx.x == 0)
             for (int n = 0; n < N; ++n) {
@@ -660,6 +693,7 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_kernel(const __grid_constan
     c.pinv = sm + L.pinv;
     c.tb = sm + L.tb;
     c.td = sm + L.td;
+    c.bp = sm + L.bp;
 
     const double* xsrc = P.x + static_cast<long long>(P.x_index[inst]) * P.numel;
     for (int e = threadIdx.x; e < P.numel; e += blockDim.x) c.X[e] = xsrc[e];
@@ -747,6 +781,7 @@ bool tiny_layout(int order, const std::uint64_t* dims, int rank, TinyLayout& L, 
     L.pinv = take(order * RR);
     L.tb = take(std::max<long long>(smax * R, RR));
     L.td = take(RR);
+    L.bp = take(order * RR);
     L.total = static_cast<int>(at);
     return static_cast<std::size_t>(L.total) * sizeof(double) <= kTinySmemMax;
 }

@@ -15,7 +15,7 @@ constexpr int kTinyThreads = 128;
 constexpr std::size_t kTinySmemMax = 200 * 1024;
 
 struct TinyLayout {  // shared-memory offsets (doubles)
-    int x, a, root0, root1, t0, t1, grams, gam, l, inv, misc, m, add, g, v, r, z, w, q, at, pairs, pinv, tb, td;
+    int x, a, root0, root1, t0, t1, grams, gam, l, inv, misc, m, add, g, v, r, z, w, q, at, pairs, pinv, tb, td, bp;
     int total;
 };
 struct TinyAls {  // AlsConfig (als.hpp:11-22); lambdas[k] = lambda0 / decay^k (host std::pow)
