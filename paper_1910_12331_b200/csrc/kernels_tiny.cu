@@ -353,25 +353,31 @@ __device__ bool spd_inverse(const Ctx& c, const double* s, double lambda, double
 }
 
 // residual_fitness (kruskal.cpp:94-118); last = M^(N-1) or nullptr (naive MTTKRP)
-__device__ double residual(Ctx& c, double xnorm2, const double* last) {
+// grams_current: c.grams already holds gram(A_n) of the current factors (same
+// values the reference recomputes here)
+__device__ double residual(Ctx& c, double xnorm2, const double* last, bool grams_current = false) {
     const int N = c.N, R = c.R;
     if (last == nullptr) {
         mttkrp_naive(c, N - 1, c.add);
         last = c.add;
     }
     const int l = N - 1;
-    for (int n = 0; n < N; ++n) gram(c, c.A + c.P->off[n], c.P->dims[n], c.grams + n * R * R);
+    if (!grams_current)
+        for (int n = 0; n < N; ++n) gram(c, c.A + c.P->off[n], c.P->dims[n], c.grams + n * R * R);
+    // all = ones o S^(0) o ... elementwise in parallel, then the row-major sum on one thread
+    for (int e = threadIdx.x; e < R * R; e += nthr()) {
+        double v = 1.0;
+        for (int n = 0; n < N; ++n) v = fmul(v, c.grams[n * R * R + e]);
+        c.tb[e] = v;
+    }
+    __syncthreads();
     double res = 0.0;
     if (threadIdx.x == 0) {
         double cross = 0.0;
         const double* al = c.A + c.P->off[l];
         for (int i = 0; i < c.P->dims[l] * R; ++i) cross = fadd(cross, fmul(last[i], al[i]));
-        double mn = 0.0;  // all = ones o S^(0) o ... ; sum row-major
-        for (int e = 0; e < R * R; ++e) {
-            double v = 1.0;
-            for (int n = 0; n < N; ++n) v = fmul(v, c.grams[n * R * R + e]);
-            mn = fadd(mn, v);
-        }
+        double mn = 0.0;
+        for (int e = 0; e < R * R; ++e) mn = fadd(mn, c.tb[e]);
         double res2 = fadd(fsub(xnorm2, fmul(2.0, cross)), mn);
         if (res2 < 0.0) res2 = 0.0;
         res = __dsqrt_rn(fdiv(res2, xnorm2));
@@ -419,7 +425,7 @@ __device__ int als_run(Ctx& c, const TinyAls& cfg, double xnorm2, int& iters, do
             note_update(c, n);
             gram(c, an, rows, c.grams + n * R * R);
         }
-        const double res = residual(c, xnorm2, c.M + c.P->off[N - 1]);
+        const double res = residual(c, xnorm2, c.M + c.P->off[N - 1], true);
         iters = sweep;
         final_r = res;
         best_r = fmin(best_r, res);
@@ -574,7 +580,7 @@ __device__ int gn_run(Ctx& c, const TinyGn& cfg, double xnorm2, int& iters, doub
             c.pairs[e] = g;
         }
         __syncthreads();
-        const double res = residual(c, xnorm2, c.M + c.P->off[N - 1]);
+        const double res = residual(c, xnorm2, c.M + c.P->off[N - 1], true);
         if (res < cfg.residual_tol) return 0;  // halt: converged_residual
         for (int e = threadIdx.x; e < S; e += nthr()) {  // gradient (:81-94): A_n Gamma(n,n) - M_n
             int n, i, r;

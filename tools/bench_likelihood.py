@@ -11,9 +11,11 @@ ranks, problems, inits, seed, dims = [3, 5, 6, 7, 9], 30, 5, 42, [4, 4, 4]
 cfg = {"problem": {"family": "uniform11", "dims": dims, "ranks": ranks}, "optimizer": opt,
        "problems": problems, "inits": inits, "seed": seed}
 cpkit.run_likelihood({**cfg, "problems": 1, "inits": 1})  # warm
-t = time.perf_counter()
-rep = cpkit.run_likelihood(cfg).to_json()
-dev = time.perf_counter() - t
+dev = 1e9
+for _ in range(3):  # best of 3 (clock ramp after idle)
+    t = time.perf_counter()
+    rep = cpkit.run_likelihood(cfg).to_json()
+    dev = min(dev, time.perf_counter() - t)
 fr = {r["rank"]: r["fraction"] for r in rep["ranks"]}
 
 jobs = []
