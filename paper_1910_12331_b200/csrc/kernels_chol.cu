@@ -353,7 +353,8 @@ constexpr int kSolveWarps = 8;
 template <int NB, class Idx, bool kSmem>
 __global__ void __launch_bounds__(32 * kSolveWarps)
 chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __restrict__ b, long long rows,
-                       double* __restrict__ y, long long l_stride, long long rows_per_mat) {
+                       double* y, long long l_stride, long long rows_per_mat, const double* old,
+                       double* __restrict__ row_sq) {
     extern __shared__ __align__(16) double lsh[];
     const int LD = R + 1;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -448,6 +449,21 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
                 for (int c = 0; c < cb; ++c) v[c] -= Lat(i, lane + 32 * c) * yi;
             }
         }
+        if (old) {  // ALS step norm: this row's ||y - old||^2 (old may alias y: read first)
+            double sq = 0.0;
+#pragma unroll
+            for (int c = 0; c < NB; ++c) {
+                const int k = lane + 32 * c;
+                if (k < R) {
+                    const double d = v[c] - old[row * R + k];
+                    sq += d * d;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, o);
+            if (lane == 0) row_sq[row] = sq;
+            __syncwarp();
+        }
 #pragma unroll
         for (int c = 0; c < NB; ++c) {
             const int k = lane + 32 * c;
@@ -458,7 +474,7 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
 
 template <int NB>
 void solve_rows_nb(const double* l, int R, const double* b, long long rows, double* y, long long l_stride, int nmats,
-                   long long rows_per_mat, cudaStream_t st) {
+                   long long rows_per_mat, cudaStream_t st, const double* old = nullptr, double* row_sq = nullptr) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const long long per_mat_ctas = std::max<long long>(
@@ -468,31 +484,31 @@ void solve_rows_nb(const double* l, int R, const double* b, long long rows, doub
     if (lay == kSquareSmem) {
         auto fn = chol_solve_rows_kernel<NB, SqIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
-        fn<<<grid, 32 * kSolveWarps, sq_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+        fn<<<grid, 32 * kSolveWarps, sq_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat, old, row_sq);
     } else if (lay == kPackedSmem) {
         auto fn = chol_solve_rows_kernel<NB, PkIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
-        fn<<<grid, 32 * kSolveWarps, pk_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat);
+        fn<<<grid, 32 * kSolveWarps, pk_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat, old, row_sq);
     } else {
         chol_solve_rows_kernel<NB, SqIdx, false><<<grid, 32 * kSolveWarps, 0, st>>>(l, R, b, rows, y, l_stride,
-                                                                                    rows_per_mat);
+                                                                                    rows_per_mat, old, row_sq);
     }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
 
 void solve_rows(const double* l, int R, const double* b, long long rows, double* y, long long l_stride, int nmats,
-                long long rows_per_mat, cudaStream_t st) {
+                long long rows_per_mat, cudaStream_t st, const double* old = nullptr, double* row_sq = nullptr) {
     switch ((R + 31) / 32) {
-        case 1: solve_rows_nb<1>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 2: solve_rows_nb<2>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 3: solve_rows_nb<3>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 4: solve_rows_nb<4>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 5: solve_rows_nb<5>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 6: solve_rows_nb<6>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 7: solve_rows_nb<7>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        case 8: solve_rows_nb<8>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
-        default: solve_rows_nb<16>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st); break;
+        case 1: solve_rows_nb<1>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 2: solve_rows_nb<2>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 3: solve_rows_nb<3>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 4: solve_rows_nb<4>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 5: solve_rows_nb<5>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 6: solve_rows_nb<6>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 7: solve_rows_nb<7>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        case 8: solve_rows_nb<8>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
+        default: solve_rows_nb<16>(l, R, b, rows, y, l_stride, nmats, rows_per_mat, st, old, row_sq); break;
     }
 }
 
@@ -545,6 +561,10 @@ void launch_chol_batch(const double* s, int count, int R, const double* lambda, 
 
 void launch_chol_solve_rows(const double* l, int R, const double* b, std::int64_t rows, double* y, cudaStream_t st) {
     solve_rows(l, R, b, rows, y, 0, 1, rows, st);
+}
+void launch_chol_solve_rows_update(const double* l, int R, const double* b, std::int64_t rows, double* a,
+                                   double* row_sq, cudaStream_t st) {
+    solve_rows(l, R, b, rows, a, 0, 1, rows, st, a, row_sq);
 }
 
 void launch_chol_inverse_batch(const double* l, int count, int R, double* inv, double* tmp, cudaStream_t st) {

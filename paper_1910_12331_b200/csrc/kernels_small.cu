@@ -469,6 +469,11 @@ void launch_diff_norm_add(const double* a, const double* b, std::uint64_t n, dou
     CPK_CUDA(cudaGetLastError());
 }
 
+void launch_sqrt_add(const double* partials, int n, double* acc, cudaStream_t st) {
+    sqrt_add_kernel<<<1, kRedThreads, 0, st>>>(partials, n, acc); ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
 void launch_dot(const double* a, const double* b, std::uint64_t n, double* partials, double* out,
                 cudaStream_t st) {
     const int nb = grid_for(n, kRedThreads, 128);

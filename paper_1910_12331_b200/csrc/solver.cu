@@ -388,7 +388,8 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     smax_ = smax;
     gram_ws_.resize(gram_workspace_elems(N, R_, smax));
     scal_.resize(kNScal);
-    partials_.resize(std::max(4096, 2 * norm2_parts(static_cast<std::uint64_t>(F_) * Bs_) + 8));
+    partials_.resize(std::max<std::size_t>(std::max(4096, 2 * norm2_parts(static_cast<std::uint64_t>(F_) * Bs_) + 8),
+                                           static_cast<std::size_t>(smax)));  // >= one slot per factor row
     status_.resize(std::max(N, 1));
     cgres_.resize(8);
     flag_.resize(4);
@@ -920,11 +921,10 @@ void DeviceProblem::als_sweep_body(double lambda) {
         mttkrp(n);
         CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[3 + 2 * n], 0));
         const std::int64_t rows = static_cast<std::int64_t>(dims_[n]);
-        launch_chol_solve_rows(chol_.get() + n * LDR, R_, M_.get() + off_[n], rows, anew_.get(), ctx_.stream);
-        launch_diff_norm_add(anew_.get(), A_.get() + off_[n], static_cast<std::uint64_t>(rows) * R_,
-                             partials_.get(), scal_.get() + kStep, ctx_.stream);
-        CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], anew_.get(), rows * R_ * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+        // A_n <- M_n (Gamma + lambda I)^-1 in place; the step norm from per-row partials
+        launch_chol_solve_rows_update(chol_.get() + n * LDR, R_, M_.get() + off_[n], rows, A_.get() + off_[n],
+                                      partials_.get(), ctx_.stream);
+        launch_sqrt_add(partials_.get(), static_cast<int>(rows), scal_.get() + kStep, ctx_.stream);
         note_factor_update(n);
         launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), n, n + 1, R_, smax_, gram_ws_.get(), grams_.get(),
                      ctx_.stream);
