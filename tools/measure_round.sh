@@ -12,3 +12,8 @@ python tools/profile_cg.py > /dev/null && \
 ncu --set full --import-source on --clock-control none -k regex:cg_res_kernel -c 1 \
     -o gpurun_out/cg_full python tools/profile_cg.py > gpurun_out/ncu_cg.log 2>&1
 tail -c 600 gpurun_out/bench.json
+python tools/profile_tiny.py gn > /dev/null && \
+ncu --set full --import-source on --clock-control none -k regex:tiny_kernel -c 1 \
+    -o gpurun_out/tiny_full python tools/profile_tiny.py gn > gpurun_out/ncu_tiny.log 2>&1
+python tools/bench_likelihood.py gn > gpurun_out/likelihood.txt 2>&1
+python tools/bench_likelihood.py als >> gpurun_out/likelihood.txt 2>&1
