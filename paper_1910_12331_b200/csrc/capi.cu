@@ -652,7 +652,10 @@ std::unique_ptr<TinyRun> tiny_launch(const BatchJob& job, bool want_factors, cud
     tp.numel = numel;
     tp.count = count;
     tp.optimizer = job.gn ? 1 : 0;
-    tp.threads = (S <= 256 && job.rank <= 16 && numel <= 1024) ? 32 : cpkit::kTinyThreads;
+    // ALS is a chain of small serial solves (one warp: cheapest barriers); GN's
+    // matvec passes parallelise over the stacked entries (measured: ALS 32, GN 128)
+    tp.threads = (!job.gn && S <= 256 && job.rank <= 16 && numel <= 1024) ? 32 : cpkit::kTinyThreads;
+    if (const char* e = std::getenv("CPKIT_TINY_THREADS")) tp.threads = std::max(32, std::min(cpkit::kTinyThreads, std::atoi(e)));
     tp.layout = lay;
     std::vector<double> lambdas;
     {
