@@ -81,3 +81,25 @@ def test_cpkt1_format_matches_oracle_layout(ck, tmp_path):
     assert raw[:5] == b"CPKT1"
     assert np.frombuffer(raw[5:29], dtype="<u8").tolist() == [2, 2, 3]
     assert np.array_equal(np.frombuffer(raw[29:], dtype="<f8"), x.ravel())
+
+
+def test_runner_config_errors_before_any_device_work(ck):
+    """Runner configs are validated on the host (harness.cpp:203-220, :295-308,
+    selftest.cpp:201-203, :281-283) with the reference's status codes; no GPU needed."""
+    cases = [
+        (ck.run_likelihood, {"problem": {"family": "bogus", "dims": [2, 2]}}, 2),          # parse
+        (ck.run_likelihood, {"problem": {"family": "uniform01", "dims": [2, 2], "ranks": [0]}}, 1),
+        (ck.run_likelihood, {"problem": {"family": "uniform01", "dims": [2, 2]}, "optimizer": "nope"}, 2),
+        (ck.run_likelihood, {"problem": {"family": "uniform01"}}, 2),                      # dims required
+        (ck.run_matmul, {"n": 0}, 1),
+        (ck.run_matmul, {"rank": 0}, 1),
+        (ck.run_matmul, {"als": {"decay_every": 0}}, 1),
+        (ck.run_matmul, {"gn": {"lambda": -1.0}}, 1),
+        (ck.run_bench_matvec, {"order": 1}, 1),
+        (ck.run_bench_matvec, {"reps": 0}, 1),
+        (ck.run_selftest_oracle, {"instances": 0}, 1),
+    ]
+    for fn, cfg, code in cases:
+        with pytest.raises(ck.CpkitError) as e:
+            fn(cfg)
+        assert e.value.code == code, (fn.__name__, cfg, e.value)
