@@ -76,6 +76,10 @@ __device__ __forceinline__ double* r_slot_nrm(const RDev& d) { return d.p.slots 
 __device__ __forceinline__ double* r_slot_fin(const RDev& d) { return d.p.slots + 3 * d.L.tasks; }
 __device__ __forceinline__ double* r_bpart(const RDev& d, int p) { return d.p.slots + 4 * d.L.tasks + d.L.bp_off[p]; }
 __device__ __forceinline__ double* r_dt(const RDev& d) { return d.p.slots + 4 * d.L.tasks + d.L.dt_off; }
+// B_p = A_p^T W_p of the current direction, carried across iterations (order x R x R)
+__device__ __forceinline__ double* r_bsum(const RDev& d) {
+    return r_dt(d) + static_cast<long long>(d.L.order) * d.L.R * d.L.R;
+}
 
 // Fixed-order block sum (WARPS warps), result broadcast to every thread.
 template <int WARPS>
@@ -367,12 +371,36 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             r_slot_fin(d)[vb] = bad;
         }
     };
+    // This tile's share A_n[rows,:]^T Z[rows, cols] of A_n^T Z_n (R x tn slab).
+    // B_p(W') = A_p^T Z_p + beta B_p(W) then needs no pass of its own: one grid
+    // barrier per iteration fewer than forming A_p^T W' after W' exists.
+    auto z_partial = [&]() {
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) Ax[fi[k] * ks + fc[k]] = Zg[k];  // k-major operand [i][z]
+        __syncthreads();
+        double* bp = r_bpart(d, n) + static_cast<long long>(rt) * RR;
+        const int mtiles = L.rm / 16;
+        for (int j = warp; j < mtiles * NT; j += WARPS) {
+            const int mt = j / NT, nt = j % NT;
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            warp_mma<true>(An, ld, mt * 16, Ax, ks, nt * 8, L.tm, acc);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int r = mt * 16 + g + 8 * h, z = nt * 8 + 2 * t + c;
+                    if (r < R && z < vc) bp[static_cast<long long>(r) * R + c0 + z] = acc[2 * h + c];
+                }
+        }
+    };
     if (has) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (fv[k]) p.Rr[rc][fe[k]] = Rg[k];
         form_rows(p.G, nullptr, -1.0, Rg, nullptr, nullptr);
         phase_c_tail();
+        z_partial();
     }
     grid_barrier(p.barrier, nb, round);
 
@@ -411,42 +439,18 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             break;
         }
         r_stamp(d, vb, it, 0);
-        // ---- A: W' = Z + beta W; publish; partial A_n^T W' (R x tn)
+        // ---- A: W' = Z + beta W in registers (first: W' = Z), published for phase B
         if (has) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 Wg[k] = first ? Zg[k] : __fma_rn(beta, Wg[k], Zg[k]);
                 if (fv[k]) p.W[0][fe[k]] = Wg[k];
-                Ax[fi[k] * ks + fc[k]] = Wg[k];  // k-major operand [i][z]
-            }
-            __syncthreads();
-            double* bp = r_bpart(d, n) + static_cast<long long>(rt) * RR;
-            const int mtiles = L.rm / 16;
-            for (int j = warp; j < mtiles * NT; j += WARPS) {
-                const int mt = j / NT, nt = j % NT;
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                warp_mma<true>(An, ld, mt * 16, Ax, ks, nt * 8, L.tm, acc);
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int r = mt * 16 + g + 8 * h, z = nt * 8 + 2 * t + c;
-                        if (r < R && z < vc) bp[static_cast<long long>(r) * R + c0 + z] = acc[2 * h + c];
-                    }
             }
         }
         r_stamp(d, vb, it, 1);
-        grid_barrier(p.barrier, nb, round);
         r_stamp(d, vb, it, 2);
-        // phase B's row panel [W' rows]: the sibling columns are final now, so
-        // their copies fly while A2 runs (own columns from registers)
-        if (has) {
-            copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (fv[k]) Rb[fi[k] * ld + c0 + fc[k]] = Wg[k];
-        }
-        // ---- A2: B_p = sum of partial slabs; D_n^T[z][r] = sum_{p!=n} Gamma(n,p)[r][z] B_p[r][z].
+        // ---- A2: B_p(W') = sum of the A_p^T Z slabs + beta B_p(W);
+        // D_n^T[z][r] = sum_{p!=n} Gamma(n,p)[r][z] B_p[r][z].
         // A group of G (pow2 >= N) adjacent lanes per element e: lane q sums mode q's
         // slabs (all loads in flight), the group exchanges the B_p by shuffles and
         // lane q forms D_q.
@@ -477,6 +481,11 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                             if (k0 + u < nt) b += part[u];
                     }
                 }
+                if (act) {
+                    double* bs = r_bsum(d) + q * RR + e;
+                    if (!first) b = __fma_rn(beta, *bs, b);
+                    *bs = b;
+                }
                 const int gl = lane & ~(G - 1);
                 double dsum = 0.0;
 #pragma unroll
@@ -496,8 +505,12 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         r_stamp(d, vb, it, 3);
         // ---- B: Q = [W' | A_n] [Gamma_nn ; D_n^T] + lambda Reg(W'); <W', Q> partial
         if (has) {
+            copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (fv[k]) Rb[fi[k] * ld + c0 + fc[k]] = Wg[k];
             copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
-            cp_async_wait_all();  // the W' rows issued before A2 and the D slice
+            cp_async_wait_all();  // sibling W' columns and the D slice
             __syncthreads();
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
             warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
@@ -541,6 +554,7 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             }
             form_rows(p.Rr[rc], p.Q, -alpha, Rg, nullptr, nullptr);
             phase_c_tail();
+            z_partial();
         }
         rc ^= 1;
         r_stamp(d, vb, it, 6);
@@ -628,7 +642,7 @@ std::size_t cg_res_slots_needed(const CgParams& p) {
         RLayout L;
         make_rlayout(p, c.mt, c.nt, L);
         need = std::max(need, static_cast<std::size_t>(4 * L.tasks + L.dt_off) +
-                                  static_cast<std::size_t>(p.order) * p.R * p.R);
+                                  2 * static_cast<std::size_t>(p.order) * p.R * p.R);
     }
     return need;
 }
@@ -661,7 +675,7 @@ bool run_cg_resident(const CgParams& p, cudaStream_t st) {
         }
     }
     if (best < 0) return false;
-    if (static_cast<std::size_t>(4 * bestL.tasks + bestL.dt_off) + static_cast<std::size_t>(p.order) * p.R * p.R >
+    if (static_cast<std::size_t>(4 * bestL.tasks + bestL.dt_off) + 2 * static_cast<std::size_t>(p.order) * p.R * p.R >
         static_cast<std::size_t>(p.nslots))
         return false;
     RDev d{};
