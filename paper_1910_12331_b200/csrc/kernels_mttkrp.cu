@@ -117,7 +117,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 __device__ __forceinline__ void dmma16816(double* d, const double* a, const double* b) {
-    asm volatile(
+    asm(
         "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
         "{%4,%5,%6,%7,%8,%9,%10,%11},{%12,%13,%14,%15},{%0,%1,%2,%3};"
         : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
@@ -228,21 +228,30 @@ __device__ __forceinline__ double lds64(std::uint32_t addr) {
 // ---------------------------------------------------------------- root GEMM
 // TRANS=false: C[m][n] = sum_k X[m][k] KRP[k][n]   (X is M x K, row stride = xmap)
 // TRANS=true:  C[m][n] = sum_k X[k][m] KRP[k][n]   (X is K x M)
-// Warp-specialised: warps 0..W-1 issue DMMA on 16-row strips of the BM = 16W
-// tile; warp W is the TMA producer (one elected lane) feeding a `stages`-deep
-// ring of (X tile, KRP tile) buffers guarded by full/empty mbarriers.
-// grid: (n_tiles, m_tiles, splits); block: 32 * (W + 1).
-template <int NTW, bool TRANS, bool GEN>
-__global__ void __launch_bounds__(32 * 11, 1)
+// Warp-specialised: warps 0..W-1 issue DMMA, warp W is the TMA producer (one
+// elected lane) feeding a `stages`-deep ring of (X tile, KRP tile) buffers
+// guarded by full/empty mbarriers. The BM x BN CTA tile is a grid of
+// (BM/16) x (BN/8) m16n8 cells, dealt to the W DMMA warps as balanced
+// contiguous row-major runs of at most MAXC cells (a run spans at most two m16
+// rows): the tile need not be a multiple of the warp count, so BM can fit M and
+// BN the rank without padding while every SM sub-partition gets equal work.
+// Persistent grid over units (n-tile, m-tile, split); block: 32 * (W + 1).
+// Block-size bound per run length: long runs (many accumulators) get fewer
+// warps and more registers each.
+__host__ __device__ constexpr int root_max_threads(int maxc) { return maxc >= 9 ? 32 * 9 : maxc >= 6 ? 32 * 11 : 32 * 13; }
+
+// FULL: every warp's run is exactly MAXC cells inside one m16 row (no per-cell
+// predicates; the common case of a rank tile that the warps split evenly).
+template <int MAXC, bool TRANS, bool GEN, bool FULL>
+__global__ void __launch_bounds__(root_max_threads(MAXC), 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
-                 const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int WN, int BNS,
-                 int stages, long long k_per_split, int splits, double* __restrict__ out,
+                 const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int BN, int W,
+                 int BNS, int stages, long long k_per_split, int splits, double* __restrict__ out,
                  long long out_split_stride) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
     char* const smem = smem_raw + (base - raw);
-    const int BN = 8 * NTW * WN;
     const int x_bytes = BM * kBK * 8;
     const int b_bytes = kBK * BNS * 8;
     const int stage_bytes = x_bytes + b_bytes;
@@ -250,8 +259,6 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     std::uint64_t* empty = full + stages;
     std::uint64_t* krp_bar = empty + stages;  // GEN: factor rows of the stage landed
 
-    const int WM = BM / 16;
-    const int W = WM * WN;  // DMMA warps; warp W is the producer
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nboxes = TRANS ? BM / 16 : kBK / 16;
     const int box_rows = TRANS ? kBK : BM;
@@ -381,17 +388,26 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         return;
     }
 
-    // ---------------- DMMA consumers: warp (wm, wn) owns rows [16 wm, +16) and
-    // n8-tiles [NTW wn, NTW (wn + 1)) of the CTA tile
+    // ---------------- DMMA consumers: this warp's run of cells [cs, cs + cnt)
+    // of the (BM/16) x NT8 cell grid; the first n1 cells lie in m16 row r0,
+    // the rest in row r0 + 1
     const int g = lane >> 2, t = lane & 3;
-    const int wm = (warp % WM) * 16;
-    const int wn = warp / WM;
+    const int NT8 = BN / 8;
+    const int cells = (BM / 16) * NT8;
+    const int cbase = cells / W, cextra = cells % W;
+    const int cnt = FULL ? MAXC : cbase + (warp < cextra ? 1 : 0);
+    const int cs = warp * cbase + min(warp, cextra);
+    const int r0 = cs / NT8, c0 = cs - r0 * NT8;
+    const int n1 = FULL ? MAXC : min(cnt, NT8 - c0);
+    // byte offset of cell j's n8 column in a KRP k-row: 64 j + (j < n1 ? ofs_a : ofs_b)
+    const std::uint32_t ofs_a = static_cast<std::uint32_t>(c0 * 64), ofs_b = static_cast<std::uint32_t>(-n1 * 64);
+    const std::uint32_t rowstep = TRANS ? kBK * 128 : 16 * 128;  // next m16 row of the X tile
 
     // per-lane constant parts of the fragment addresses
     std::uint32_t aoff[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int mrow = wm + g + 8 * (i & 1);
+        const int mrow = 16 * r0 + g + 8 * (i & 1);
         if (!TRANS) {
             aoff[i] = static_cast<std::uint32_t>(swz(mrow, t + 4 * (i >> 1)));
         } else {
@@ -403,63 +419,106 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int krow = TRANS ? kperm(t + 4 * i) : t + 4 * i;
-        boff[i] = static_cast<std::uint32_t>((krow * BNS + g + 8 * NTW * wn) * 8);
+        boff[i] = static_cast<std::uint32_t>((krow * BNS + g) * 8);
     }
     const bool vec = (R % 2) == 0;
 
-    long long it = 0;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        int n0, nk, split;
-        long long m0, kbeg;
-        unit_geom(u, n0, m0, kbeg, nk, split);
-        double acc[NTW][4];
+    // The mainloop for a compile-time run length C (warps' counts differ by at
+    // most one: C is MAXC or MAXC - 1) and SPAN (the run crosses into row
+    // r0 + 1: both rows' A fragments are loaded and selected per cell), so no
+    // cell carries a runtime predicate and all loads can be hoisted.
+    auto mainloop = [&](auto c_tag, auto span_tag) {
+        constexpr int C = decltype(c_tag)::value;
+        constexpr bool SPAN = decltype(span_tag)::value;
+        long long it = 0;
+        for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+            int n0, nk, split;
+            long long m0, kbeg;
+            unit_geom(u, n0, m0, kbeg, nk, split);
+            double acc[C][4];
 #pragma unroll
-        for (int j = 0; j < NTW; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+            for (int j = 0; j < C; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
 
-        for (int kt = 0; kt < nk; ++kt, ++it) {
-            const int s = static_cast<int>(it % stages);
-            mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
-            const std::uint32_t xs = base + s * stage_bytes;
-            const std::uint32_t bs = xs + x_bytes;
+            for (int kt = 0; kt < nk; ++kt, ++it) {
+                const int s = static_cast<int>(it % stages);
+                mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
+                // plain shared loads (ordered after the full-barrier wait by its
+                // memory clobber, otherwise free for the scheduler to hoist)
+                const char* xs = smem + s * stage_bytes;
+                const char* bs = xs + x_bytes;
+                auto ld = [](const char* p, std::uint32_t off) { return *reinterpret_cast<const double*>(p + off); };
+                static_assert(kBK == 32, "two k16 steps per stage");
+                // NN: a unit's last stage may hold only 16 valid k (zero-filled
+                // beyond K): skip the empty half instead of multiplying zeros
+                // (TN: K per split is a multiple of kBK)
+                const bool half_stage =
+                    !TRANS && kt == nk - 1 &&
+                    min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
 #pragma unroll
-            for (int ks = 0; ks < kBK / 16; ++ks) {
-                double a[8];
-                // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
-                const std::uint32_t abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
+                for (int ks = 0; ks < kBK / 16; ++ks) {
+                    if (!TRANS && ks == 1 && half_stage) break;
+                    double a[8];
+                    // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
+                    const char* abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
 #pragma unroll
-                for (int i = 0; i < 8; ++i) a[i] = lds64(abase + aoff[i]);
-                const std::uint32_t bb = bs + ks * 16 * BNS * 8;
+                    for (int i = 0; i < 8; ++i) a[i] = ld(abase, aoff[i]);
+                    const char* bb = bs + ks * 16 * BNS * 8;
 #pragma unroll
-                for (int j = 0; j < NTW; ++j) {
-                    double b[4];
+                    for (int j = 0; j < C; ++j) {
+                        const bool first_row = !SPAN || j < n1;
+                        const std::uint32_t co = j * 64 + (first_row ? ofs_a : ofs_b);
+                        double b[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) b[i] = lds64(bb + boff[i] + j * 64);
-                    dmma16816(acc[j], a, b);
+                        for (int i = 0; i < 4; ++i) b[i] = ld(bb, boff[i] + co);
+                        if (SPAN && j == n1) {  // the run continues in row r0 + 1
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) a[i] = ld(abase + rowstep, aoff[i]);
+                        }
+                        dmma16816(acc[j], a, b);
+                    }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
 
-        // epilogue (overlaps the producer's loads for the next unit):
-        // rows m0+wm+g(+8), cols n0+8(NTW wn + j)+2t(+1); 16-byte stores when aligned
-        double* o = out + split * out_split_stride;
+            // epilogue (overlaps the producer's loads for the next unit):
+            // rows m0+16(r0 | r0+1)+g(+8), cols n0+8(cell column)+2t(+1); 16-byte stores when aligned
+            double* o = out + split * out_split_stride;
 #pragma unroll
-        for (int j = 0; j < NTW; ++j) {
-            const int col = n0 + 8 * (NTW * wn + j) + 2 * t;
+            for (int j = 0; j < C; ++j) {
+                const bool first_row = !SPAN || j < n1;
+                const int col = n0 + 8 * (first_row ? c0 + j : j - n1) + 2 * t;
+                const int rr = 16 * (r0 + (first_row ? 0 : 1));
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const long long row = m0 + wm + g + 8 * h;
-                if (row < M && col < R) {
-                    double* dst = o + row * R + col;
-                    if (vec) {
-                        *reinterpret_cast<double2*>(dst) = make_double2(acc[j][2 * h], acc[j][2 * h + 1]);
-                    } else {
-                        dst[0] = acc[j][2 * h];
-                        if (col + 1 < R) dst[1] = acc[j][2 * h + 1];
+                for (int h = 0; h < 2; ++h) {
+                    const long long row = m0 + rr + g + 8 * h;
+                    if (row < M && col < R) {
+                        double* dst = o + row * R + col;
+                        if (vec) {
+                            *reinterpret_cast<double2*>(dst) = make_double2(acc[j][2 * h], acc[j][2 * h + 1]);
+                        } else {
+                            dst[0] = acc[j][2 * h];
+                            if (col + 1 < R) dst[1] = acc[j][2 * h + 1];
+                        }
                     }
                 }
             }
+        }
+    };
+    using CFull = std::integral_constant<int, MAXC>;
+    using CLess = std::integral_constant<int, (MAXC > 1 ? MAXC - 1 : 1)>;
+    using Yes = std::integral_constant<bool, true>;
+    using No = std::integral_constant<bool, false>;
+    if (FULL) {
+        mainloop(CFull{}, No{});
+    } else {
+        const bool span = n1 < cnt;
+        if (cnt == MAXC) {
+            if (span) mainloop(CFull{}, Yes{});
+            else mainloop(CFull{}, No{});
+        } else {
+            if (span) mainloop(CLess{}, Yes{});
+            else mainloop(CLess{}, No{});
         }
     }
 }
@@ -497,17 +556,17 @@ int num_sms() {
 // ---- tile planning --------------------------------------------------------
 // CTA tile = (16 WM rows) x (8 NTW WN rank columns); WM x WN DMMA warps + 1
 // TMA producer warp. NTW comes from the instantiated set.
-constexpr int kNtwChoices[] = {1, 2, 3, 4, 5, 6, 7, 8, 10, 12, 13, 16};
-int round_ntw(int need) {
-    for (int c : kNtwChoices)
+constexpr int kMaxcChoices[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 13, 16};
+int round_maxc(int need) {
+    for (int c : kMaxcChoices)
         if (c >= need) return c;
-    return 16;
+    return -1;
 }
 struct GemmPlan {
-    int ntw, wn, wm, ntiles, bns, stages, mtiles, splits, per_sm;
+    int maxc, nw, wm, nt8, ntiles, bns, stages, mtiles, splits, per_sm;
     long long kps;
     int BM() const { return 16 * wm; }
-    int BN() const { return 8 * ntw * wn; }
+    int BN() const { return 8 * nt8; }
 };
 int bns_for(int bn, bool trans) {
     if (const char* e = std::getenv(trans ? "CPKIT_TN_BNS_MOD" : "CPKIT_NN_BNS_MOD")) {  // experiments only
@@ -521,83 +580,157 @@ std::size_t stage_bytes_of(int BM, int bns) { return static_cast<std::size_t>(BM
 std::size_t smem_bytes(const GemmPlan& p) {
     return static_cast<std::size_t>(p.stages) * stage_bytes_of(p.BM(), p.bns) + p.stages * 24 + 1024;
 }
-// Rows per CTA: 16 x wm with wm in [lo, hi], minimising padded rows.
-int pick_wm(long long M, int lo, int hi) {
-    int best = hi;
-    long long best_waste = -1;
-    for (int w = hi; w >= lo; --w) {
-        const long long bm = 16LL * w;
-        const long long waste = ((M + bm - 1) / bm) * bm - M;
-        if (best_waste < 0 || waste < best_waste) {
-            best_waste = waste;
-            best = w;
+// Fraction of the DMMA issue slots doing useful cells when wm x nt8 cells are
+// dealt to nw warps as balanced runs (the kernel's rule) and warp w issues on
+// SM sub-partition w % 4.
+double cell_efficiency(int wm, int nt8, int nw) {
+    const int cells = wm * nt8, base = cells / nw, extra = cells % nw;
+    int load[4] = {0, 0, 0, 0};
+    for (int w = 0; w < nw; ++w) load[w % 4] += base + (w < extra ? 1 : 0);
+    const int mx = std::max(std::max(load[0], load[1]), std::max(load[2], load[3]));
+    return static_cast<double>(cells) / (4.0 * mx);
+}
+// A run of maxc cells starting anywhere in a row of nt8 spans at most two rows.
+bool runs_fit(int wm, int nt8, int nw) {
+    const int cells = wm * nt8, base = cells / nw, extra = cells % nw;
+    for (int w = 0; w < nw; ++w) {
+        const int cs = w * base + std::min(w, extra), cnt = base + (w < extra ? 1 : 0);
+        if (cnt == 0) return false;
+        if ((cs % nt8) + cnt > 2 * nt8) return false;
+    }
+    return true;
+}
+// Split count with the best wave efficiency (<= 2 waves or the unsplit count),
+// keeping >= 8 k-stages per split; ties go to fewer splits.
+long long best_splits(long long base, long long slots, long long K, double* eff_out) {
+    const long long kchunks = (K + kBK - 1) / kBK;
+    long long best = 1;
+    double best_eff = -1.0;
+    for (long long sp = 1; sp <= 64; ++sp) {
+        if (sp > 1 && kchunks / sp < 8) break;
+        const long long ctas = base * sp;
+        const long long waves = (ctas + slots - 1) / slots;
+        if (sp > 1 && waves > std::max<long long>(2, (base + slots - 1) / slots)) break;
+        const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = sp;
         }
     }
+    if (eff_out) *eff_out = best_eff;
     return best;
 }
+int resident_per_sm(const GemmPlan& p) {
+    // ptxas may use up to the launch bound's share of the register file
+    const int per_thread = std::min(255, 65536 / root_max_threads(p.maxc)) & ~7;
+    const int regs = 32 * (p.nw + 1) * per_thread;
+    return std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
+}
+// Every warp's run is exactly maxc cells in one row (the kernel's FULL case).
+bool runs_full(const GemmPlan& p) {
+    const int cells = p.wm * p.nt8;
+    if (cells % p.nw != 0 || cells / p.nw != p.maxc) return false;
+    return p.nt8 % p.maxc == 0;
+}
+
 GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     GemmPlan p{};
-    // rank split: one CTA column covers up to 208 ranks (2 warp columns of 13 n8-tiles)
+    // rank split: one CTA column covers up to 208 ranks (26 n8 cells)
     p.ntiles = (R + 207) / 208;
     const int per = (R + p.ntiles - 1) / p.ntiles;  // ranks per CTA column
-    const int n8 = (per + 7) / 8;
-    if (trans) {
-        // split-K GEMM (the output is short; split-K fills the machine): eight
-        // DMMA warps per CTA, as two warp columns when the rank tile is wide.
-        // Measured (C2 TN 554 -> 536 us, C4 TN 616 -> 434 us) against fitting
-        // BM to M with fewer warps.
-        p.wn = n8 >= 8 ? 2 : 1;
-        p.wm = p.wn == 2 ? 4 : 8;
-
-    } else {
-        p.wn = n8 > 16 ? 2 : 1;
-        p.wm = p.wn == 2 ? 4 : pick_wm(M, 6, 8);
+    p.nt8 = (per + 7) / 8;
+    // Tile search: BM = 16 wm rows (wm in [4, 10]), nw in {8, 12} DMMA warps,
+    // rank tile nt8p >= nt8 n8 cells (padding lets every warp own a full run).
+    // Score = useful DMMA slots (cell dealing across sub-partitions, rank
+    // padding) x row padding x wave quantisation (split-K counted), with a
+    // preference for runs that stay in one row at full length (no second A
+    // fragment, no spills). Measured at C2: TN 80 x 104 tiles on 8 warps
+    // (two-row runs) 483 us vs 516 us for the former 64 x 112; NN 128 x 104
+    // (full runs) 436 us, 64 x 112 (full) 450 us, 64 x 104 (two-row runs) 512 us.
+    double best_score = -1.0;
+    GemmPlan best = p;
+    for (int wm = 4; wm <= 10; ++wm) {
+        for (int nw : {8, 12}) {
+            for (int nt8p = p.nt8; nt8p <= p.nt8 + 4 && nt8p <= 26; ++nt8p) {
+                GemmPlan c = p;
+                c.wm = wm;
+                c.nw = nw;
+                c.nt8 = nt8p;
+                c.maxc = round_maxc((wm * nt8p + nw - 1) / nw);
+                if (c.maxc < 0 || !runs_fit(wm, nt8p, nw)) continue;
+                if (32 * (nw + 1) > root_max_threads(c.maxc)) continue;  // register budget
+                const bool full = runs_full(c);
+                if (c.maxc >= 10 && !full) continue;  // the long two-row runs spill
+                c.bns = bns_for(c.BN(), trans);
+                c.stages = 2;
+                for (int s = 6; s >= 2; --s) {
+                    c.stages = s;
+                    if (smem_bytes(c) <= 225 * 1024) break;
+                }
+                if (smem_bytes(c) > 225 * 1024) continue;
+                c.per_sm = resident_per_sm(c);
+                const long long mt = (M + c.BM() - 1) / c.BM();
+                const double m_eff = static_cast<double>(M) / static_cast<double>(mt * c.BM());
+                double w_eff = 1.0;
+                best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
+                            K, &w_eff);
+                const double score = cell_efficiency(wm, nt8p, nw) * (static_cast<double>(p.nt8) / nt8p) * m_eff *
+                                     w_eff * (full ? 1.0 : trans ? 0.97 : 0.85) * (1.0 + 0.002 * wm) *
+                                     (c.stages >= 3 ? 1.0 : 0.97);
+                if (score > best_score + 1e-12) {
+                    best_score = score;
+                    best = c;
+                }
+            }
+        }
     }
-    // tuning overrides (experiments only): CPKIT_{NN,TN}_{WM,WN,NTW,STAGES}
+    if (best_score < 0.0) {
+        // no candidate (cannot happen for nt8 <= 26): eight warps, one full-length run each
+        best.wm = p.nt8 > 16 ? 4 : 8;
+        best.nw = 8;
+        best.maxc = round_maxc(p.nt8 > 16 ? (p.nt8 + 1) / 2 : p.nt8);
+        best.nt8 = p.nt8 > 16 ? 2 * best.maxc : best.maxc;
+        best.bns = bns_for(best.BN(), trans);
+        best.stages = 2;
+        for (int s = 6; s >= 2; --s) {
+            best.stages = s;
+            if (smem_bytes(best) <= 225 * 1024) break;
+        }
+    }
+    p = best;
+    // tuning overrides (experiments only): CPKIT_{NN,TN}_{WM,NW,STAGES}
     auto env = [&](const char* key, int& v) {
         const std::string name = std::string(trans ? "CPKIT_TN_" : "CPKIT_NN_") + key;
         if (const char* e = std::getenv(name.c_str())) v = std::atoi(e);
     };
+    const int wm0 = p.wm, nw0 = p.nw, nt0 = p.nt8;
     env("WM", p.wm);
-    env("WN", p.wn);
-    p.ntw = round_ntw((n8 + p.wn - 1) / p.wn);
-    env("NTW", p.ntw);
-    p.bns = bns_for(p.BN(), trans);
-    p.stages = 2;
-    for (int s = 6; s >= 2; --s) {
-        p.stages = s;
-        if (smem_bytes(p) <= 225 * 1024) break;
+    env("NW", p.nw);
+    env("NT8", p.nt8);
+    if (p.wm != wm0 || p.nw != nw0 || p.nt8 != nt0) {
+        p.maxc = round_maxc((p.wm * p.nt8 + p.nw - 1) / p.nw);
+        if (p.maxc < 0 || !runs_fit(p.wm, p.nt8, p.nw) || 32 * (p.nw + 1) > root_max_threads(p.maxc))
+            throw DeviceError("CPKIT tile override: bad warp count");
+        p.bns = bns_for(p.BN(), trans);
+        p.stages = 2;
+        for (int s = 6; s >= 2; --s) {
+            p.stages = s;
+            if (smem_bytes(p) <= 225 * 1024) break;
+        }
     }
     env("STAGES", p.stages);
+    p.per_sm = resident_per_sm(p);
     p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
-    p.splits = 1;
-    p.kps = K;
-    // split K when the output tiles alone cannot fill one resident wave
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
-    const int regs = 32 * (p.wm * p.wn + 1) * (p.ntw >= 10 ? 168 : 128);
-    const int per_sm = std::max(1, std::min<int>(static_cast<int>((228 * 1024) / smem_bytes(p)), 65536 / regs));
-    p.per_sm = per_sm;
-    const long long slots = static_cast<long long>(num_sms()) * per_sm;
-    if (base < 4 * slots) {
-        // choose the split count with the best wave efficiency (<= 2 waves),
-        // keeping >= 8 k-stages per split; ties go to fewer splits
-        const long long kchunks = (K + kBK - 1) / kBK;
-        long long best = 1;
-        double best_eff = -1.0;
-        for (long long sp = 1; sp <= 64; ++sp) {
-            if (sp > 1 && kchunks / sp < 8) break;
-            const long long ctas = base * sp;
-            const long long waves = (ctas + slots - 1) / slots;
-            if (waves > std::max<long long>(2, (base + slots - 1) / slots)) break;
-            const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
-            if (eff > best_eff + 1e-9) {
-                best_eff = eff;
-                best = sp;
-            }
-        }
-        p.kps = ((kchunks + best - 1) / best) * kBK;  // multiple of kBK: splits never share a stage
-        p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
-    }
+    const long long slots = static_cast<long long>(num_sms()) * p.per_sm;
+    const long long sp = best_splits(base, slots, K, nullptr);
+    const long long kchunks = (K + kBK - 1) / kBK;
+    p.kps = ((kchunks + sp - 1) / sp) * kBK;  // multiple of kBK: splits never share a stage
+    p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
+    if (std::getenv("CPKIT_PLAN_DEBUG"))
+        std::fprintf(stderr, "plan %s M=%lld K=%lld R=%d: wm=%d nw=%d nt8=%d maxc=%d full=%d stages=%d splits=%d\n",
+                     trans ? "TN" : "NN", M, K, R, p.wm, p.nw, p.nt8, p.maxc, runs_full(p) ? 1 : 0, p.stages,
+                     p.splits);
     return p;
 }
 
@@ -607,19 +740,21 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
     const dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
-    const dim3 block(32 * (p.wm * p.wn + 1));
+    const dim3 block(32 * (p.nw + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
-        auto fn = root_gemm_kernel<NTV, TRANS, GEN>;                                               \
+        auto fn = runs_full(p) ? root_gemm_kernel<NTV, TRANS, GEN, true>                          \
+                               : root_gemm_kernel<NTV, TRANS, GEN, false>;                         \
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
-        fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.wn, p.bns, p.stages, p.kps, p.splits, out, \
+        fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.BN(), p.nw, p.bns, p.stages, p.kps,  \
+                                      p.splits, out, \
                                       oss);                                                        \
         break;                                                                                     \
     }
-    switch (p.ntw) {
+    switch (p.maxc) {
         CPK_CASE(1) CPK_CASE(2) CPK_CASE(3) CPK_CASE(4) CPK_CASE(5) CPK_CASE(6) CPK_CASE(7)
-        CPK_CASE(8) CPK_CASE(10) CPK_CASE(12) CPK_CASE(13) CPK_CASE(16)
+        CPK_CASE(8) CPK_CASE(9) CPK_CASE(10) CPK_CASE(12) CPK_CASE(13) CPK_CASE(16)
         default: throw DeviceError("unsupported rank tile");
     }
 #undef CPK_CASE
