@@ -102,6 +102,14 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
                        const KrpDesc& kf, double* krp, double* pb, double* splitk_ws,
                        std::size_t splitk_ws_elems, cudaStream_t st);
 std::size_t root_front_workspace_elems(std::int64_t F, std::int64_t B, int R);
+// order-3 multi-sweep dimension tree: single-mode root contraction of mode c in {0, 1}
+void launch_root_single(const double* x, std::int64_t s0, std::int64_t s1, std::int64_t Bl, std::int64_t Bs, int c,
+                        const double* fac, int R, double* out, double* ws, std::size_t ws_elems, cudaStream_t st);
+std::size_t root_single_workspace_elems(std::int64_t s0, std::int64_t s1, std::int64_t Bs, int R);
+// out[b][c][r] = in[b][r][c] (the multi-sweep tree's mode-permuted tensor copies)
+void launch_transpose_batched(const double* in, std::int64_t batch, std::int64_t rows, std::int64_t cols,
+                              std::int64_t in_ld, std::int64_t in_bs, double* out, std::int64_t out_ld,
+                              std::int64_t out_bs, cudaStream_t st);
 std::size_t krp_workspace_elems(std::int64_t rows, int R);
 
 // Second dimension-tree level: P over kept modes (ext[0..k), R) reduced to the

@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(root_max_threads(MAXC), 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int BN, int W,
                  int BNS, int stages, long long k_per_split, int splits, double* __restrict__ out,
-                 long long out_split_stride) {
+                 long long out_split_stride, int brel) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
@@ -364,7 +364,9 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
                                         static_cast<int>(m0));
                     }
                     if (!GEN) {
-                        tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, static_cast<int>(kk));
+                        // brel: batched contraction, the B operand restarts at row 0 in
+                        // every split (rows past its extent are TMA zero fill)
+                        tma_load_2d(&kmap, &full[s], xs + x_bytes, n0, static_cast<int>(brel ? kk - kbeg : kk));
                     } else {
                         // A_1 rows of the two 16-row halves (s1 % 16 == 0: a half never wraps)
                         mbar_expect_tx(&krp_bar[s], static_cast<unsigned>(b_bytes));
@@ -448,15 +450,14 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
                 const char* bs = xs + x_bytes;
                 auto ld = [](const char* p, std::uint32_t off) { return *reinterpret_cast<const double*>(p + off); };
                 static_assert(kBK == 32, "two k16 steps per stage");
-                // NN: a unit's last stage may hold only 16 valid k (zero-filled
-                // beyond K): skip the empty half instead of multiplying zeros
-                // (TN: K per split is a multiple of kBK)
+                // a unit's last stage may hold only 16 valid k (its B rows beyond
+                // the unit's k range are zero): skip the empty half instead of
+                // multiplying zeros
                 const bool half_stage =
-                    !TRANS && kt == nk - 1 &&
-                    min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
+                    kt == nk - 1 && min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
 #pragma unroll
                 for (int ks = 0; ks < kBK / 16; ++ks) {
-                    if (!TRANS && ks == 1 && half_stage) break;
+                    if (ks == 1 && half_stage) break;
                     double a[8];
                     // NN: box ks holds k in [16ks, 16ks+16). TN: rows 16ks.. of every m-box.
                     const char* abase = TRANS ? xs + ks * 16 * 128 : xs + ks * BM * 128;
@@ -633,7 +634,9 @@ bool runs_full(const GemmPlan& p) {
     return p.nt8 % p.maxc == 0;
 }
 
-GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
+// fixed_kps > 0: batched contraction, split s covers k in [s kps, (s+1) kps)
+// and writes its own output slab (no split search, no reduction).
+GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0) {
     GemmPlan p{};
     // rank split: one CTA column covers up to 208 ranks (26 n8 cells)
     p.ntiles = (R + 207) / 208;
@@ -672,8 +675,14 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
                 const long long mt = (M + c.BM() - 1) / c.BM();
                 const double m_eff = static_cast<double>(M) / static_cast<double>(mt * c.BM());
                 double w_eff = 1.0;
-                best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
-                            K, &w_eff);
+                if (fixed_kps > 0) {
+                    const long long units = static_cast<long long>(c.ntiles) * mt * ((K + fixed_kps - 1) / fixed_kps);
+                    const long long slots = static_cast<long long>(num_sms()) * c.per_sm;
+                    w_eff = static_cast<double>(units) / static_cast<double>(((units + slots - 1) / slots) * slots);
+                } else {
+                    best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
+                                K, &w_eff);
+                }
                 const double score = cell_efficiency(wm, nt8p, nw) * (static_cast<double>(p.nt8) / nt8p) * m_eff *
                                      w_eff * (full ? 1.0 : trans ? 0.97 : 0.85) * (1.0 + 0.002 * wm) *
                                      (c.stages >= 3 ? 1.0 : 0.97);
@@ -723,9 +732,13 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
     p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
     const long long slots = static_cast<long long>(num_sms()) * p.per_sm;
-    const long long sp = best_splits(base, slots, K, nullptr);
-    const long long kchunks = (K + kBK - 1) / kBK;
-    p.kps = ((kchunks + sp - 1) / sp) * kBK;  // multiple of kBK: splits never share a stage
+    if (fixed_kps > 0) {
+        p.kps = fixed_kps;
+    } else {
+        const long long sp = best_splits(base, slots, K, nullptr);
+        const long long kchunks = (K + kBK - 1) / kBK;
+        p.kps = ((kchunks + sp - 1) / sp) * kBK;  // multiple of kBK: splits never share a stage
+    }
     p.splits = static_cast<int>((K + p.kps - 1) / p.kps);
     if (std::getenv("CPKIT_PLAN_DEBUG"))
         std::fprintf(stderr, "plan %s M=%lld K=%lld R=%d: wm=%d nw=%d nt8=%d maxc=%d full=%d stages=%d splits=%d\n",
@@ -736,7 +749,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans) {
 
 template <bool TRANS, bool GEN>
 void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, const KrpDev& kd,
-              long long M, long long K, int R, double* out, long long oss) {
+              long long M, long long K, int R, double* out, long long oss, int brel = 0) {
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
     const dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
@@ -748,8 +761,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
         fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.BN(), p.nw, p.bns, p.stages, p.kps,  \
-                                      p.splits, out, \
-                                      oss);                                                        \
+                                      p.splits, out, oss, brel);                                   \
         break;                                                                                     \
     }
     switch (p.maxc) {
@@ -869,6 +881,100 @@ void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int
         splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, pb);
         count_launch(1);
         CPK_CUDA(cudaGetLastError());
+    }
+}
+
+// ---------------------------------------------------------------- layout
+// Batched 2-D transpose: out[b][c][r] = in[b][r][c] for r < rows, c < cols.
+// Builds the mode-permuted tensor copies of the order-3 multi-sweep tree
+// (X^(0)[i1][i2][i0], X^(1)[i0][i2][i1]) once per tensor upload, so every
+// single-mode root is the same NN GEMM as the back root. 32 x 32 tiles staged
+// through shared memory: both the reads and the writes are row-coalesced.
+namespace {
+__global__ void __launch_bounds__(256) transpose_batched_kernel(const double* __restrict__ in, long long rows,
+                                                                long long cols, long long in_ld, long long in_bs,
+                                                                double* __restrict__ out, long long out_ld,
+                                                                long long out_bs, long long batch) {
+    __shared__ double tile[32][33];
+    const long long c0 = static_cast<long long>(blockIdx.x) * 32, r0 = static_cast<long long>(blockIdx.y) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (long long b = blockIdx.z; b < batch; b += gridDim.z) {
+        const double* src = in + b * in_bs;
+        double* dst = out + b * out_bs;
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const long long r = r0 + ty + j, c = c0 + tx;
+            tile[ty + j][tx] = (r < rows && c < cols) ? __ldcs(src + r * in_ld + c) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+            const long long c = c0 + ty + j, r = r0 + tx;
+            if (r < rows && c < cols) dst[c * out_ld + r] = tile[tx][ty + j];
+        }
+        __syncthreads();
+    }
+}
+}  // namespace
+
+void launch_transpose_batched(const double* in, std::int64_t batch, std::int64_t rows, std::int64_t cols,
+                              std::int64_t in_ld, std::int64_t in_bs, double* out, std::int64_t out_ld,
+                              std::int64_t out_bs, cudaStream_t st) {
+    if (batch <= 0 || rows <= 0 || cols <= 0) return;
+    const dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32),
+                    static_cast<unsigned>(std::min<long long>(batch, 65535)));
+    transpose_batched_kernel<<<grid, 256, 0, st>>>(in, rows, cols, in_ld, in_bs, out, out_ld, out_bs, batch);
+    count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+
+// Single-mode roots of the order-3 multi-sweep dimension tree: contract ONE
+// mode c < 2 of X [s0][s1][Bs] with its factor as a TN GEMM whose B operand
+// is the factor itself (no Khatri-Rao operand, nothing to fill):
+//   c = 0: P_0[(i1, i2)][r] = sum_i0 X[i0][(i1, i2)] A_0[i0][r]  (X viewed as s0 x s1 Bs)
+//   c = 1: P_1[i0][i2][r]   = sum_i1 X[(i0, i1)][i2] A_1[i1][r]  (s0 batches of s1 rows:
+//          split i0 is batch i0, its B rows restart at A_1 row 0 and its
+//          output is slab i0; a stage running past s1 meets TMA zero rows of A_1)
+// These are the reference's own first contraction steps (contract_mode,
+// mttkrp.cpp:46-62) for a mode other than the last.
+std::size_t root_single_workspace_elems(std::int64_t s0, std::int64_t s1, std::int64_t Bs, int R) {
+    const GemmPlan p = plan_gemm(s1 * Bs, s0, R, true);
+    return p.splits > 1 ? static_cast<std::size_t>(p.splits) * s1 * Bs * R : 0;
+}
+
+void launch_root_single(const double* x, std::int64_t s0, std::int64_t s1, std::int64_t Bl, std::int64_t Bs, int c,
+                        const double* fac, int R, double* out, double* ws, std::size_t ws_elems, cudaStream_t st) {
+    if (R % 2 != 0) throw DeviceError("root_single: the factor is the B operand and needs an even rank");
+    if (c == 0) {
+        const long long M = s1 * Bs, K = s0;
+        const GemmPlan p = plan_gemm(M, K, R, true);
+        const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(M), static_cast<std::uint64_t>(K), 16, kBK, true);
+        const CUtensorMap kmap = make_map(fac, static_cast<std::uint64_t>(R), static_cast<std::uint64_t>(s0),
+                                          static_cast<std::uint32_t>(p.bns), kBK, false);
+        double* o = out;
+        long long oss = 0;
+        if (p.splits > 1) {
+            if (ws_elems < static_cast<std::size_t>(p.splits) * M * R) throw DeviceError("root_single: workspace too small");
+            o = ws;
+            oss = M * R;
+        }
+        dispatch<true, false>(p, st, xmap, kmap, KrpDev{}, M, K, R, o, oss);
+        if (p.splits > 1) {
+            const long long n = M * static_cast<long long>(R);
+            const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
+            splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, p.splits, n, out);
+            count_launch(1);
+            CPK_CUDA(cudaGetLastError());
+        }
+    } else if (c == 1) {
+        const long long K = s0 * s1;
+        const GemmPlan p = plan_gemm(Bl, K, R, true, s1);
+        const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(K), 16, kBK, true);
+        const CUtensorMap kmap = make_map(fac, static_cast<std::uint64_t>(R), static_cast<std::uint64_t>(s1),
+                                          static_cast<std::uint32_t>(p.bns), kBK, false);
+        dispatch<true, false>(p, st, xmap, kmap, KrpDev{}, Bl, K, R, out, Bl * static_cast<long long>(R), 1);
+    } else {
+        throw DeviceError("root_single: mode must be 0 or 1");
     }
 }
 

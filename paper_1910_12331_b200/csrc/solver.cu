@@ -363,17 +363,53 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
 
     x_.resize(static_cast<std::size_t>(F_) * static_cast<std::size_t>(Bs_));
     if (Bs_ != Bl_) CPK_CUDA(cudaMemset(x_.get(), 0, x_.size() * sizeof(double)));
-    krp_.resize(krp_workspace_elems(std::max(F_, Bl_), R_));
+    krp_.resize(krp_workspace_elems(std::max<std::int64_t>(std::max(F_, Bl_), N == 3 ? std::max(local_rows_[0], local_rows_[1]) : 0), R_));
     A_.resize(S); Atrial_.resize(S); M_.resize(S); G_.resize(S); V_.resize(S); Z_.resize(S); Q_.resize(S);
     for (int i = 0; i < 2; ++i) { Rr_[i].resize(S); W_[i].resize(S); }
     PF_.resize(static_cast<std::size_t>(F_) * R_);
     PB_.resize(static_cast<std::size_t>(Bl_) * R_);
+    if (N == 3 && !std::getenv("CPKIT_ALS_TREE")) {
+        // the permuted copies need 2 more tensors; keep half of the free memory spare
+        std::size_t free_b = 0, total_b = 0;
+        CPK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        ld0_ = (local_rows_[0] + 1) & ~1LL;
+        ld1_ = (local_rows_[1] + 1) & ~1LL;
+        const double copy_b = 8.0 * static_cast<double>(Bl_) *
+                              static_cast<double>(local_rows_[1] * ld0_ + local_rows_[0] * ld1_);
+        const char* ce = std::getenv("CPKIT_MSDT_COPIES");
+        msdt_copies_ = ce ? std::atoi(ce) != 0 : copy_b + 8.0 * static_cast<double>(local_elems_) < 0.5 * free_b;
+        // without copies the single-mode roots are TN GEMMs with the factor as the B operand
+        msdt_ = msdt_copies_ || (R_ % 2 == 0 && Bs_ == Bl_);
+    }
+    if (msdt_)
+        PM_.resize(static_cast<std::size_t>(std::max(local_rows_[0], local_rows_[1])) * Bl_ * R_);
+    if (msdt_copies_) {
+        X0_.resize(static_cast<std::size_t>(local_rows_[1] * Bl_ * ld0_));
+        X1_.resize(static_cast<std::size_t>(local_rows_[0] * Bl_ * ld1_));
+        CPK_CUDA(cudaMemset(X0_.get(), 0, X0_.size() * sizeof(double)));  // stride padding stays zero
+        CPK_CUDA(cudaMemset(X1_.get(), 0, X1_.size() * sizeof(double)));
+    }
     // split-K and second-level workspaces
     std::size_t ws = std::max(root_front_workspace_elems(F_, Bl_, R_), root_back_workspace_elems(F_, Bl_, R_));
     {
         KrpDesc kf = krp(0, h_, A_.get(), false), kb = krp(h_, N, A_.get(), true);
         for (int n = 0; n < h_; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kf, n, R_));
         for (int n = h_; n < N; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kb, n - h_, R_));
+        if (msdt_copies_) {
+            ws = std::max(ws, root_back_workspace_elems(local_rows_[1] * Bl_, local_rows_[0], R_));
+            ws = std::max(ws, root_back_workspace_elems(local_rows_[0] * Bl_, local_rows_[1], R_));
+        }
+        if (msdt_) {
+            if (!msdt_copies_) ws = std::max(ws, root_single_workspace_elems(local_rows_[0], local_rows_[1], Bs_, R_));
+            for (int c = 0; c < 2; ++c) {
+                KrpDesc kd{};
+                kd.nmodes = 2;
+                int j = 0;
+                for (int m = 0; m < N; ++m)
+                    if (m != c) kd.ext[j++] = local_rows_[m];
+                for (int keep = 0; keep < 2; ++keep) ws = std::max(ws, reduce_kept_workspace_elems(kd, keep, R_));
+            }
+        }
     }
     ws_.resize(std::max<std::size_t>(ws, 1));
     grams_.resize(N * RR);
@@ -433,7 +469,16 @@ void DeviceProblem::upload_tensor(const double* host_local) {
     else
         CPK_CUDA(cudaMemcpy2DAsync(x_.get(), Bs_ * sizeof(double), host_local, Bl_ * sizeof(double),
                                    Bl_ * sizeof(double), F_, cudaMemcpyHostToDevice, ctx_.stream));
+    build_msdt_copies();
     invalidate_all();
+}
+void DeviceProblem::build_msdt_copies() {
+    if (!msdt_copies_) return;
+    const std::int64_t s0 = local_rows_[0], s1 = local_rows_[1];
+    // X^(0)[i1][i2][i0]: batch i1, rows i0 (stride s1 Bs), cols i2
+    launch_transpose_batched(x_.get(), s1, s0, Bl_, s1 * Bs_, Bs_, X0_.get(), ld0_, Bl_ * ld0_, ctx_.stream);
+    // X^(1)[i0][i2][i1]: batch i0, rows i1 (stride Bs), cols i2
+    launch_transpose_batched(x_.get(), s0, s1, Bl_, Bs_, s1 * Bs_, X1_.get(), ld1_, Bl_ * ld1_, ctx_.stream);
 }
 void DeviceProblem::download_tensor(double* host_local) {
     if (Bs_ == Bl_)
@@ -476,6 +521,7 @@ void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noi
     if (Bs_ != Bl_)
         CPK_CUDA(cudaMemcpy2DAsync(x_.get(), Bs_ * sizeof(double), xd, Bl_ * sizeof(double), Bl_ * sizeof(double),
                                    F_, cudaMemcpyDeviceToDevice, ctx_.stream));
+    build_msdt_copies();
     ctx_.sync();
     invalidate_all();
 }
@@ -621,6 +667,79 @@ void DeviceProblem::second_level_front(int mode) {
     }
 }
 
+// ---- order-3 ALS: multi-sweep dimension tree --------------------------------
+// The ALS update order 0, 1, 2, 0, 1, 2, ... lets one first-level contraction
+// serve two consecutive updates: P_c = X x_c A_c with c the mode updated
+// neither now nor next stays valid for both (A_c does not change in between),
+// and M^(n) is P_c contracted with the other kept factor, the one updated
+// just before (the same second-level step as mttkrp.cpp:63-75). The roots
+// rotate c = 2, 1, 0 (X A_2 is the tree's back root; X x_1 A_1 and X x_0 A_0
+// are single-mode TN contractions), 3 roots per 2 sweeps instead of 4, and no
+// Khatri-Rao operand. Each M^(n) is the same sum as the reference tree's, in
+// a different association order (roundoff-level differences).
+void DeviceProblem::root_single(int c) {
+    prof_begin(kProfFront);
+    if (msdt_copies_) {
+        // P_c = X^(c) A_c: rows (other kept index pairs), the back root's NN GEMM
+        KrpDesc kc{};
+        kc.nmodes = 1;
+        kc.ext[0] = local_rows_[c];
+        kc.fac[0] = A_.get() + off_[c];
+        const std::int64_t rows = local_rows_[1 - c] * Bl_;
+        launch_root_back(c == 0 ? X0_.get() : X1_.get(), rows, local_rows_[c], c == 0 ? ld0_ : ld1_, R_, kc,
+                         krp_.get(), PM_.get(), ws_.get(), ws_.size(), ctx_.stream);
+    } else {
+        launch_root_single(x_.get(), local_rows_[0], local_rows_[1], Bl_, Bs_, c, A_.get() + off_[c], R_, PM_.get(),
+                           ws_.get(), ws_.size(), ctx_.stream);
+    }
+    prof_end();
+    ++contractions_;
+    pm_mode_ = c;
+}
+void DeviceProblem::second_level_pm(int mode) {
+    const int N = order();
+    KrpDesc kd{};
+    kd.nmodes = 2;
+    int keep = -1;
+    for (int m = 0, j = 0; m < N; ++m) {
+        if (m == pm_mode_) continue;
+        if (m == mode) keep = j;
+        const bool last = m == N - 1;
+        kd.ext[j] = local_rows_[m];
+        kd.fac[j] = A_.get() + off_[m] + (last ? static_cast<std::int64_t>(slab_lo_) * R_ : 0);
+        ++j;
+    }
+    const bool last = mode == N - 1;
+    double* out = M_.get() + off_[mode] + (last ? static_cast<std::int64_t>(slab_lo_) * R_ : 0);
+    launch_reduce_kept(PM_.get(), kd, keep, R_, out, ws_.get(), ws_.size(), ctx_.stream);
+    if (ctx_.comm && !defer_coll_) {
+        if (last) {
+            const std::size_t per = static_cast<std::size_t>(slab_hi_ - slab_lo_) * R_;
+            ctx_.comm->allgather(out, M_.get() + off_[mode], per, ctx_.stream);
+        } else {
+            ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
+        }
+    }
+}
+void DeviceProblem::mttkrp_msdt(int mode) {
+    if (pf_valid_ && mode != 2) {  // P_2 = X A_2 serves modes 0 and 1
+        second_level_back(mode);
+        return;
+    }
+    if (pm_mode_ >= 0 && pm_mode_ != mode) {
+        second_level_pm(mode);
+        return;
+    }
+    const int c = (mode + 2) % 3;  // updated neither now nor next
+    if (c == 2) {
+        root_back();
+        second_level_back(mode);
+    } else {
+        root_single(c);
+        second_level_pm(mode);
+    }
+}
+
 void DeviceProblem::mttkrp(int mode) {
     if (mode < 0 || mode >= order()) throw InvalidArgument("mttkrp: mode out of range");
     if (mode < h_) {
@@ -648,10 +767,12 @@ void DeviceProblem::mttkrp_naive(int mode) {
 void DeviceProblem::note_factor_update(int mode) {
     if (mode >= h_) pf_valid_ = false;  // back-root key holds modes >= h
     else pb_valid_ = false;             // front-root key holds modes < h
+    if (mode == pm_mode_) pm_mode_ = -1;
     m_all_valid_ = false;
 }
 void DeviceProblem::invalidate_all() {  // factors changed wholesale
     pf_valid_ = pb_valid_ = false;
+    pm_mode_ = -1;
     m_all_valid_ = false;
     grams_valid_ = false;
 }
@@ -667,7 +788,17 @@ void DeviceProblem::compute_all_mttkrp() {
     const int N = order();
     defer_coll_ = ctx_.comm != nullptr;
     try {
-        for (int n = 0; n < N; ++n) mttkrp(n);
+        if (msdt_copies_) {
+            // order 3: M^(0), M^(1) from the back root X A_2; M^(2) from the
+            // single-mode root X x_1 A_1 (NN GEMM on the permuted copy, then the
+            // i0 contraction) instead of the Khatri-Rao front root
+            mttkrp(0);
+            mttkrp(1);
+            if (pm_mode_ != 1) root_single(1);
+            second_level_pm(2);
+        } else {
+            for (int n = 0; n < N; ++n) mttkrp(n);
+        }
     } catch (...) {
         defer_coll_ = false;
         throw;
@@ -892,13 +1023,14 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gno
 
 // ---- ALS sweep (als.cpp:22-52) ----------------------------------------------------
 void DeviceProblem::drop_als_graph() {
-    if (als_exec_) cudaGraphExecDestroy(als_exec_);
-    als_exec_ = nullptr;
-    for (auto& e : als_prof_) {
-        cudaEventDestroy(e.a);
-        cudaEventDestroy(e.b);
+    for (auto& g : als_graphs_) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        for (auto& e : g.prof) {
+            cudaEventDestroy(e.a);
+            cudaEventDestroy(e.b);
+        }
     }
-    als_prof_.clear();
+    als_graphs_.clear();
 }
 
 // The device work of one sweep (no host synchronisation, capturable).
@@ -918,7 +1050,8 @@ void DeviceProblem::als_sweep_body(double lambda) {
         launch_gamma_excl(grams_.get(), N, R_, n, gam_.get() + n * RR, ctx_.aux);
         launch_chol_batch(gam_.get() + n * RR, 1, R_, &lambda, 0, chol_.get() + n * LDR, status_.get() + n, ctx_.aux);
         CPK_CUDA(cudaEventRecord(ctx_.ev[3 + 2 * n], ctx_.aux));
-        mttkrp(n);
+        if (msdt_) mttkrp_msdt(n);
+        else mttkrp(n);
         CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[3 + 2 * n], 0));
         const std::int64_t rows = static_cast<std::int64_t>(dims_[n]);
         // A_n <- M_n (Gamma + lambda I)^-1 in place; the step norm from per-row partials
@@ -940,17 +1073,22 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
     const bool graphs = !ctx_.comm && !std::getenv("CPKIT_NO_GRAPH");
     const SweepSig pre = sweep_sig();
     bool replayed = false;
-    if (graphs && als_exec_ && lambda == als_lambda_ && pre == als_pre_) {
-        CPK_CUDA(cudaGraphLaunch(als_exec_, ctx_.stream));
-        count_launch(static_cast<int>(als_kernels_));  // the replay launches the captured kernels again
-        pf_valid_ = als_post_.pf;
-        pb_valid_ = als_post_.pb;
-        m_all_valid_ = als_post_.mall;
-        grams_valid_ = als_post_.grams;
-        contractions_ = als_contr_;
+    AlsGraph* hit = nullptr;
+    if (graphs)
+        for (auto& g : als_graphs_)
+            if (g.lambda == lambda && g.pre == pre) hit = &g;
+    if (hit) {
+        CPK_CUDA(cudaGraphLaunch(hit->exec, ctx_.stream));
+        count_launch(static_cast<int>(hit->kernels));  // the replay launches the captured kernels again
+        pf_valid_ = hit->post.pf;
+        pb_valid_ = hit->post.pb;
+        m_all_valid_ = hit->post.mall;
+        grams_valid_ = hit->post.grams;
+        pm_mode_ = hit->post.pm;
+        contractions_ = hit->contr;
         replayed = true;
     } else if (graphs) {
-        drop_als_graph();
+        if (als_graphs_.size() >= kAlsGraphs) drop_als_graph();
         const std::size_t prof0 = prof_.size();
         const long long k0 = static_cast<long long>(kernel_launches());
         CPK_CUDA(cudaStreamBeginCapture(ctx_.stream, cudaStreamCaptureModeThreadLocal));
@@ -964,16 +1102,19 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
         }
         cudaGraph_t g = nullptr;
         CPK_CUDA(cudaStreamEndCapture(ctx_.stream, &g));
-        CPK_CUDA(cudaGraphInstantiate(&als_exec_, g, 0));
+        AlsGraph ag;
+        CPK_CUDA(cudaGraphInstantiate(&ag.exec, g, 0));
         CPK_CUDA(cudaGraphDestroy(g));
-        als_lambda_ = lambda;
-        als_pre_ = pre;
-        als_post_ = sweep_sig();
-        als_contr_ = contractions_;
-        als_kernels_ = static_cast<long long>(kernel_launches()) - k0;  // counted as captured, i.e. as launched by the first replay below
-        als_prof_.assign(prof_.begin() + static_cast<std::ptrdiff_t>(prof0), prof_.end());  // owned by the graph now
+        ag.lambda = lambda;
+        ag.pre = pre;
+        ag.post = sweep_sig();
+        ag.contr = contractions_;
+        ag.kernels = static_cast<long long>(kernel_launches()) - k0;  // counted as captured, i.e. as launched by the first replay below
+        ag.prof.assign(prof_.begin() + static_cast<std::ptrdiff_t>(prof0), prof_.end());  // owned by the graph now
         prof_.resize(prof0);
-        CPK_CUDA(cudaGraphLaunch(als_exec_, ctx_.stream));
+        als_graphs_.push_back(std::move(ag));
+        hit = &als_graphs_.back();
+        CPK_CUDA(cudaGraphLaunch(hit->exec, ctx_.stream));
         replayed = true;
     } else {
         als_sweep_body(lambda);
@@ -987,7 +1128,7 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
                              ctx_.stream));
     ctx_.sync();
     if (replayed && profile_)  // the graph's event pairs, measured for this replay
-        for (const auto& e : als_prof_) {
+        for (const auto& e : hit->prof) {
             float v = 0.0f;
             CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
             prof_.push_back({nullptr, nullptr, e.kind, v});

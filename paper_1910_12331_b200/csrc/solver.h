@@ -256,17 +256,24 @@ private:
     // profiling) and replayed; host bookkeeping restored from the capture.
     struct SweepSig {
         bool pf, pb, mall, prof, grams;
+        int pm;
         bool operator==(const SweepSig& o) const {
-            return pf == o.pf && pb == o.pb && mall == o.mall && prof == o.prof && grams == o.grams;
+            return pf == o.pf && pb == o.pb && mall == o.mall && prof == o.prof && grams == o.grams && pm == o.pm;
         }
     };
-    cudaGraphExec_t als_exec_ = nullptr;
-    double als_lambda_ = 0.0;
-    SweepSig als_pre_{}, als_post_{};
-    int als_contr_ = 0;
-    long long als_kernels_ = 0;  // kernel launches per replay (counted during capture)
-    std::vector<ProfEvent> als_prof_;  // event pairs recorded by the graph
-    SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_}; }
+    // (the multi-sweep tree alternates two cache states, so up to kAlsGraphs
+    // captures are kept, keyed by lambda and the state at sweep start)
+    struct AlsGraph {
+        cudaGraphExec_t exec = nullptr;
+        double lambda = 0.0;
+        SweepSig pre{}, post{};
+        int contr = 0;
+        long long kernels = 0;  // kernel launches per replay (counted during capture)
+        std::vector<ProfEvent> prof;  // event pairs recorded by the graph
+    };
+    static constexpr std::size_t kAlsGraphs = 4;
+    std::vector<AlsGraph> als_graphs_;
+    SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_, pm_mode_}; }
     void drop_als_graph();
     void als_sweep_body(double lambda);
     bool profile_ = false;
@@ -284,6 +291,20 @@ private:
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
     DevBuf<double> PF_, PB_, ws_, krp_;
     bool pf_valid_ = false, pb_valid_ = false;
+    // Order-3 ALS multi-sweep dimension tree: PM_ caches the single-mode root
+    // P_c = X x_c A_c (c = pm_mode_ in {0, 1}; -1 = none). Every root serves
+    // the next two mode updates, so a sweep pair needs 3 roots instead of 4.
+    bool msdt_ = false;
+    int pm_mode_ = -1;
+    DevBuf<double> PM_;
+    // Mode-permuted copies of the local tensor, X^(0)[i1][i2][i0] and
+    // X^(1)[i0][i2][i1] (row strides ld0_/ld1_, even for TMA), made once per
+    // upload when memory allows: the single-mode roots then run as the same
+    // NN GEMM as the back root instead of a TN GEMM with transposed operands.
+    bool msdt_copies_ = false;
+    std::int64_t ld0_ = 0, ld1_ = 0;
+    DevBuf<double> X0_, X1_;
+    void build_msdt_copies();
     bool grams_valid_ = false;
     bool defer_coll_ = false;  // compute_all_mttkrp batches the collectives
     double* hpin_ = nullptr;  // pinned host slots for scalar readbacks  // grams_ == gram(A_n) for every n (skips recomputation; same values)
@@ -307,6 +328,9 @@ private:
     void root_front();
     void second_level_back(int mode);
     void second_level_front(int mode);
+    void root_single(int c);          // P_c into PM_ (c in {0, 1})
+    void second_level_pm(int mode);   // M^(mode) from PM_
+    void mttkrp_msdt(int mode);       // ALS: M^(mode) from whichever cached root serves it
     void finish_mode(int mode);  // collectives on M^(mode)
     void compute_all_mttkrp();
 

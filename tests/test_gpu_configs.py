@@ -135,10 +135,13 @@ def test_full_size_properties(ck, name, dims, R):
     # ALS sweeps decrease the fast residual (als.cpp monotonicity, lambda = 0)
     p.set_factors(init)
     prev = 1.0
+    counts = []
     for _ in range(3):
         step, cnt = p.als_sweep(0.0)
-        assert cnt == 2
+        counts.append(cnt)
         p.mttkrp(len(dims) - 1, download=False)
         r, _ = p.residual(xn2)
         assert r <= prev + 1e-12
         prev = r
+    # order 3: multi-sweep dimension tree (3 roots per 2 sweeps); else the reference tree (2 per sweep)
+    assert counts == ([2, 1, 2] if len(dims) == 3 else [2, 2, 2])

@@ -325,6 +325,54 @@ def test_als_sweep_matches_oracle(orc, ck, dims, rank):
     assert vec_rel_err(p.get_factors(), f_ref) < 1e-10
 
 
+# Order-3 ALS runs the multi-sweep dimension tree (each single-mode root serves
+# two consecutive updates; roots rotate c = 2, 1, 0). Sweep by sweep it must
+# track the oracle's reference tree at roundoff level, with 3 roots per 2 sweeps.
+# Extents cover batched-root stages that run past s1 (s1 % 32 != 0, s1 % 16 != 0).
+# copies=1: the single-mode roots run as NN GEMMs on mode-permuted tensor
+# copies; copies=0: TN GEMMs on X itself (needs an even rank and last extent).
+MSDT_CASES = [([24, 20, 18], 6), ([10, 37, 22], 8), ([33, 48, 16], 20), ([6, 5, 4], 2)]
+
+
+@pytest.mark.parametrize("copies", ["1", "0"])
+@pytest.mark.parametrize("dims,rank", MSDT_CASES + [([9, 11, 7], 5), ([13, 6, 3], 3)])
+def test_als_msdt_tracks_oracle(orc, ck, dims, rank, copies, monkeypatch):
+    if copies == "0" and (rank % 2 or dims[-1] % 2):
+        pytest.skip("TN single-mode roots need an even rank and last extent")
+    monkeypatch.setenv("CPKIT_MSDT_COPIES", copies)
+    t = orc.random_model(dims, rank, 3)
+    x = orc.reconstruct(t) + 1e-3 * np.random.default_rng(5).standard_normal(dims)
+    f = orc.random_model(dims, rank, 4)
+    p = make(ck, x, f)
+    counts = []
+    for sweep in range(6):
+        f, step_ref, _, _ = orc.als_sweep(x, f, 1e-4)
+        step, cnt = p.als_sweep(1e-4)
+        counts.append(cnt)
+        assert abs(step - step_ref) <= 1e-9 * step_ref, (sweep, step, step_ref)
+        assert vec_rel_err(p.get_factors(), f) < 1e-10, sweep
+    assert counts == [2, 1, 2, 1, 2, 1]
+    # every M^(n) of the final factors still matches the tree after the rotation
+    ref, _ = orc.mttkrp_tree_all(x, f)
+    for n in range(3):
+        assert rel_err(p.mttkrp(n), ref[n]) < KTOL
+
+
+def test_als_msdt_single_roots_match_oracle(orc, ck):
+    """The single-mode roots feed M^(n) exactly as the tree does: after a sweep
+    pair every mode's MTTKRP of the current factors from each route agrees."""
+    dims, rank = [40, 36, 30], 10
+    x = np.random.default_rng(9).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 12)
+    p = make(ck, x, f)
+    for _ in range(2):
+        p.als_sweep(0.0)
+    cur = p.get_factors()
+    ref, _ = orc.mttkrp_tree_all(x, cur)
+    for n in range(3):
+        assert rel_err(p.mttkrp(n), ref[n]) < KTOL
+
+
 def _c1(orc):
     """BASELINE config 1: order 3, s=50, R=5, uniform[0,1) truth, exact rank."""
     dims, rank = [50, 50, 50], 5
