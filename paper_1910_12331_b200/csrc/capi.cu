@@ -1860,8 +1860,14 @@ cpkit_status cpkit_dev_time_als_sweeps(cpkit_dev_problem* p, double lambda, int 
     DEV_REQ(p && ms && sweeps > 0);
     return guarded([&] {
         EventPair ev;
+        // each sweep's diagnostics are read back (as the driver does), with
+        // the next sweep already queued behind it
         CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
-        for (int i = 0; i < sweeps; ++i) p->p->als_sweep(lambda);
+        for (int i = 0; i < sweeps; ++i) {
+            p->p->als_sweep_launch(lambda, false);
+            if (p->p->als_sweeps_pending() > 1) p->p->als_sweep_finish();
+        }
+        while (p->p->als_sweeps_pending() > 0) p->p->als_sweep_finish();
         CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
         *ms = ev.ms();
     });

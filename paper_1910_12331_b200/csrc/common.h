@@ -153,6 +153,8 @@ void launch_axpby(double* out, const double* a, double alpha, const double* x, s
                   cudaStream_t st);
 void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st);
 void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_t st);
+void launch_pack_sweep(const double* scal, int kstep, int kres, const int* flag, const int* status, int n,
+                       double* out_mapped, cudaStream_t st);
 // Dense evaluation of a Kruskal model + keyed-RNG noise (generators / reconstruct)
 void launch_reconstruct(const KrpDesc& all, int R, double* out, std::uint64_t offset, std::uint64_t n,
                         cudaStream_t st);

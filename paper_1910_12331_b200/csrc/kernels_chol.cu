@@ -160,30 +160,53 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
 // Warp-synchronous factorisation of the kb x kb diagonal block at (k0, k0)
 // (kb <= kNB <= 32): lane i holds row i in registers. No early exit, so the
 // row stays in registers. Returns true (all lanes) on a non-positive pivot.
+// 1/sqrt(x) for a positive normal x without the libdevice special-case call
+// (whose divergent branch forces every later warp shuffle onto the slow
+// collective path): MUFU seed, then two cubic Newton steps (>= 60 bits).
+__device__ __forceinline__ double rsqrt_pos(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+        const double e = __fma_rn(-x * y, y, 1.0);
+        y = __fma_rn(y * e, __fma_rn(0.375, e, 0.5), y);
+    }
+    return y;
+}
+
 template <int kNB>
 __device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int kb) {
+    __syncwarp();
     const int i = threadIdx.x & 31;
     double r[kNB];
 #pragma unroll
     for (int m = 0; m < kNB; ++m) r[m] = (i < kb && m <= i) ? w[(k0 + i) * LD + k0 + m] : 0.0;
     bool failed = false;
+    // the pivot of the next column, computed by its own lane from its own row
+    // (the same fma the row update applies, so bitwise the same value): the
+    // column-to-column chain is shuffle -> rsqrt -> scale -> fma -> shuffle
+    double nextp = r[0];
 #pragma unroll
     for (int j = 0; j < kNB; ++j) {
-        const double x = __shfl_sync(0xffffffffu, r[j], j);
+        const double x = __shfl_sync(0xffffffffu, nextp, j);
         if (j < kb && !failed && !(x > 0.0) && !isnan(x)) failed = true;  // Eigen LLT: fail iff pivot <= 0
         const bool go = j < kb && !failed;
-        // one reciprocal square root on the column-to-column critical path
-        // (L_jj = x / sqrt(x) from it; within an ulp of sqrt and 1/sqrt)
-        const double inv = rsqrt(x), l = x * inv;
-        if (go && i > j) r[j] *= inv;
+        // one reciprocal square root on the critical path (L_jj = x / sqrt(x))
+        const double inv = rsqrt_pos(x > 0.0 ? x : 1.0), l = x * inv;
+        double lij = r[j];
+        if (go && i > j) lij = r[j] * inv;
         if (go && i == j) {
-            r[j] = l;
+            lij = l;
             w[(k0 + j) * LD + R] = inv;
         }
+        r[j] = lij;
+        if (j + 1 < kNB) nextp = (go && i >= j + 1) ? __fma_rn(-lij, lij, r[j + 1]) : r[j + 1];
 #pragma unroll
-        for (int m = j + 1; m < kNB; ++m) {
-            const double lmj = __shfl_sync(0xffffffffu, r[j], m);
-            if (go && i >= m) r[m] -= r[j] * lmj;
+        for (int m = 0; m < kNB; ++m) {
+            if (m > j) {
+                const double lmj = __shfl_sync(0xffffffffu, lij, m);
+                if (go && i >= m) r[m] = __fma_rn(-lij, lmj, r[m]);
+            }
         }
     }
 #pragma unroll

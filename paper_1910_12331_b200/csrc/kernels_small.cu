@@ -496,6 +496,27 @@ __global__ void set_flag_scalar_kernel(int* flag, int fv, double* d, double dv) 
     }
 }
 }  // namespace
+namespace {
+__global__ void pack_sweep_kernel(const double* __restrict__ scal, int kstep, int kres, const int* __restrict__ flag,
+                                  const int* __restrict__ status, int n, double* out) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        out[0] = scal[kstep];
+        out[1] = scal[kres];
+        out[2] = scal[kres + 1];
+        out[3] = static_cast<double>(*flag);
+        for (int i = 0; i < n; ++i) out[4 + i] = static_cast<double>(status[i]);
+    }
+}
+}  // namespace
+// One sweep's diagnostics (step norm, residual, fitness, finiteness flag,
+// per-mode SPD status) written straight into mapped pinned host memory:
+// no copy-engine operation and no synchronisation on the solver stream.
+void launch_pack_sweep(const double* scal, int kstep, int kres, const int* flag, const int* status, int n,
+                       double* out_mapped, cudaStream_t st) {
+    pack_sweep_kernel<<<1, 32, 0, st>>>(scal, kstep, kres, flag, status, n, out_mapped);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
 // *flag = fv, *d = dv as a device op (capturable in a CUDA graph, unlike a pageable H2D copy)
 void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_t st) {
     set_flag_scalar_kernel<<<1, 32, 0, st>>>(flag, fv, d, dv);

@@ -305,7 +305,12 @@ KruskalModel random_model_gaussian(const std::vector<std::uint64_t>& dims, std::
 Context::Context(int dev) : device(dev) {
     CPK_CUDA(cudaSetDevice(dev));
     CPK_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    CPK_CUDA(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    // the side stream carries the latency-bound SPD factorisations (one CTA
+    // each): top priority, so their CTA is placed before a concurrent
+    // bandwidth kernel fills every SM
+    int lo = 0, hi = 0;
+    CPK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CPK_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, hi));
     for (auto& e : ev) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 Context::~Context() {
@@ -341,6 +346,11 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
     if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
     CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hpin_), 16 * sizeof(double), cudaHostAllocDefault));
+    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), kSweepSlots * kSlotDoubles * sizeof(double),
+                           cudaHostAllocMapped));
+    CPK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dmap_), hmap_, 0));
+    als_graphs_.reserve(kAlsGraphs);  // in-flight sweeps hold pointers to their graphs
+    for (auto& e : slot_ev_) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CPK_CUDA(cudaSetDevice(ctx_.device));
     h_ = (N + 1) / 2;
     shard_range(dims_[N - 1], ctx_.rank(), ctx_.world(), &slab_lo_, &slab_hi_);
@@ -445,9 +455,15 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
 }
 
 DeviceProblem::~DeviceProblem() {
+    if (!pending_.empty()) cudaStreamSynchronize(ctx_.stream);
+    pending_.clear();
+    done_.clear();
     drop_als_graph();
     profile_enable(false);
     if (hpin_) cudaFreeHost(hpin_);
+    if (hmap_) cudaFreeHost(hmap_);
+    for (auto& e : slot_ev_)
+        if (e) cudaEventDestroy(e);
 }
 
 KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {
@@ -847,6 +863,13 @@ void DeviceProblem::residual_launch(double xnorm2) {
                     grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
                     ctx_.stream);
 }
+// The residual with ||X||^2 already in its device slot (norm2() leaves it there).
+void DeviceProblem::residual_launch_dev() {
+    const int N = order();
+    launch_residual(M_.get() + off_[N - 1], A_.get() + off_[N - 1], static_cast<std::int64_t>(dims_[N - 1]),
+                    grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
+                    ctx_.stream);
+}
 std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*last_src*/) {
     residual_launch(xnorm2);
     CPK_CUDA(cudaMemcpyAsync(hpin_, scal_.get() + kRes, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx_.stream));
@@ -1066,7 +1089,23 @@ void DeviceProblem::als_sweep_body(double lambda) {
 }
 
 AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
+    als_sweep_launch(lambda, false);
+    return als_sweep_finish();
+}
+
+void DeviceProblem::als_snapshot_factors() {
+    CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), off_[order()] * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx_.stream));
+}
+void DeviceProblem::als_restore_factors() {
+    CPK_CUDA(cudaMemcpyAsync(A_.get(), Atrial_.get(), off_[order()] * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx_.stream));
+    invalidate_all();
+}
+
+void DeviceProblem::als_sweep_launch(double lambda, bool with_residual) {
     const int N = order();
+    while (static_cast<int>(pending_.size()) >= kSweepSlots - 1) done_.push_back(complete_oldest());
     // CUDA graph: one capture per (lambda, cache state, profiling); replays skip
     // ~30 launch latencies per sweep. Single GPU only (the sharded sweep has
     // NCCL collectives between its kernels).
@@ -1077,6 +1116,12 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
     if (graphs)
         for (auto& g : als_graphs_)
             if (g.lambda == lambda && g.pre == pre) hit = &g;
+    if (hit && profile_)
+        for (const auto& q : pending_)
+            if (q.graph == hit) {
+                drain_pending();
+                break;
+            }
     if (hit) {
         CPK_CUDA(cudaGraphLaunch(hit->exec, ctx_.stream));
         count_launch(static_cast<int>(hit->kernels));  // the replay launches the captured kernels again
@@ -1088,7 +1133,10 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
         contractions_ = hit->contr;
         replayed = true;
     } else if (graphs) {
-        if (als_graphs_.size() >= kAlsGraphs) drop_als_graph();
+        if (als_graphs_.size() >= kAlsGraphs) {
+            drain_pending();  // in-flight replays still reference them
+            drop_als_graph();
+        }
         const std::size_t prof0 = prof_.size();
         const long long k0 = static_cast<long long>(kernel_launches());
         CPK_CUDA(cudaStreamBeginCapture(ctx_.stream, cudaStreamCaptureModeThreadLocal));
@@ -1103,7 +1151,7 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
         cudaGraph_t g = nullptr;
         CPK_CUDA(cudaStreamEndCapture(ctx_.stream, &g));
         AlsGraph ag;
-        CPK_CUDA(cudaGraphInstantiate(&ag.exec, g, 0));
+        CPK_CUDA(cudaGraphInstantiate(&ag.exec, g, cudaGraphInstantiateFlagUseNodePriority));
         CPK_CUDA(cudaGraphDestroy(g));
         ag.lambda = lambda;
         ag.pre = pre;
@@ -1119,25 +1167,51 @@ AlsSweepDiag DeviceProblem::als_sweep(double lambda) {
     } else {
         als_sweep_body(lambda);
     }
-    AlsSweepDiag diag;
-    std::vector<int> st(N);
-    int fin = 1;
-    CPK_CUDA(cudaMemcpyAsync(st.data(), status_.get(), N * sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
-    CPK_CUDA(cudaMemcpyAsync(&fin, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
-    CPK_CUDA(cudaMemcpyAsync(&diag.step_norm, scal_.get() + kStep, sizeof(double), cudaMemcpyDeviceToHost,
-                             ctx_.stream));
-    ctx_.sync();
-    if (replayed && profile_)  // the graph's event pairs, measured for this replay
-        for (const auto& e : hit->prof) {
+    if (with_residual) residual_launch_dev();
+    const int slot = next_slot_;
+    next_slot_ = (next_slot_ + 1) % kSweepSlots;
+    launch_pack_sweep(scal_.get(), kStep, kRes, flag_.get(), status_.get(), N, dmap_ + slot * kSlotDoubles,
+                      ctx_.stream);
+    CPK_CUDA(cudaEventRecord(slot_ev_[slot], ctx_.stream));
+    pending_.push_back({slot, contractions_, replayed && profile_ ? hit : nullptr});
+}
+
+DeviceProblem::SweepResult DeviceProblem::complete_oldest() {
+    const PendingSweep q = pending_.front();
+    pending_.erase(pending_.begin());
+    CPK_CUDA(cudaEventSynchronize(slot_ev_[q.slot]));
+    const double* h = hmap_ + q.slot * kSlotDoubles;
+    if (q.graph)  // the graph's event pairs, measured for this replay
+        for (const auto& e : q.graph->prof) {
             float v = 0.0f;
             CPK_CUDA(cudaEventElapsedTime(&v, e.a, e.b));
             prof_.push_back({nullptr, nullptr, e.kind, v});
         }
-    if (!fin) throw InvalidArgument("model factor contains non-finite entries");
-    for (int s : st)
-        if (s == 2) throw SingularSystem("spd_solve: factorization failed after jitter retry");
-    diag.full_contractions = contractions_;
-    return diag;
+    SweepResult r;
+    r.diag.step_norm = h[0];
+    r.diag.full_contractions = q.contr;
+    r.res = h[1];
+    r.fit = h[2];
+    if (h[3] == 0.0) r.err = 1;
+    for (int n = 0; n < order() && !r.err; ++n)
+        if (h[4 + n] == 2.0) r.err = 2;
+    return r;
+}
+
+AlsSweepDiag DeviceProblem::als_sweep_finish(double* res, double* fit) {
+    SweepResult r;
+    if (!done_.empty()) {
+        r = done_.front();
+        done_.erase(done_.begin());
+    } else {
+        if (pending_.empty()) throw InvalidArgument("als_sweep_finish: no sweep in flight");
+        r = complete_oldest();
+    }
+    if (res) *res = r.res;
+    if (fit) *fit = r.fit;
+    if (r.err == 1) throw InvalidArgument("model factor contains non-finite entries");
+    if (r.err == 2) throw SingularSystem("spd_solve: factorization failed after jitter retry");
+    return r.diag;
 }
 
 // ---- GN step (gauss_newton.cpp:360-449) -------------------------------------------
@@ -1246,27 +1320,65 @@ std::pair<KruskalModel, ConvergenceReport> als_optimize(DeviceProblem& p, Kruska
     cfg.validate();
     model.validate();
     p.set_factors(model);
-    const double xnorm2 = p.norm2();
+    const double xnorm2 = p.norm2();  // also leaves ||X||^2 in its device slot for the residuals
     if (!(xnorm2 > 0.0)) throw InvalidArgument("als_optimize: tensor norm must be positive");
     ConvergenceReport report;
     report.status = TerminalStatus::cap_hit;
-    const auto t0 = std::chrono::steady_clock::now();
-    for (int sweep = 1; sweep <= cfg.max_sweeps; ++sweep) {
+    auto lambda_of = [&](int sweep) {
         double lambda = cfg.lambda0;
         if (cfg.decay_every)
             lambda /= std::pow(cfg.decay_factor, static_cast<double>((sweep - 1) / *cfg.decay_every));
-        AlsSweepDiag diag = p.als_sweep(lambda);
-        auto [res, fit] = p.residual_fitness(xnorm2, p.order() - 1);
+        return lambda;
+    };
+    // B200 change: sweep k+1 is queued before the host reads sweep k's step
+    // norm and residual, so the per-sweep host round trip overlaps device
+    // work. When sweep k stops the run, the speculative sweep is drained and
+    // the factors restored from the copy taken before it (same result as the
+    // reference's sequential loop; the caches are rebuilt on demand).
+    const bool pipeline = !std::getenv("CPKIT_ALS_NO_PIPELINE");
+    auto drain = [&] {
+        while (p.als_sweeps_pending() > 0) {
+            try {
+                p.als_sweep_finish();
+            } catch (...) {  // a discarded speculative sweep's failure is not the run's
+            }
+        }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    if (cfg.max_sweeps >= 1) p.als_sweep_launch(lambda_of(1), true);
+    for (int sweep = 1; sweep <= cfg.max_sweeps; ++sweep) {
+        const double lambda = lambda_of(sweep);
+        const bool spec = pipeline && sweep < cfg.max_sweeps;
+        if (spec) {
+            p.als_snapshot_factors();
+            p.als_sweep_launch(lambda_of(sweep + 1), true);
+        }
+        double res = 1.0, fit = 0.0;
+        AlsSweepDiag diag;
+        try {
+            diag = p.als_sweep_finish(&res, &fit);
+        } catch (...) {
+            drain();
+            throw;
+        }
         const double seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         report.records.push_back({sweep, res, fit, lambda, 0, seconds});
+        bool stop = false;
         if (res < cfg.residual_tol) {
             report.status = TerminalStatus::converged_residual;
-            break;
-        }
-        if (diag.step_norm < cfg.step_tol) {
+            stop = true;
+        } else if (diag.step_norm < cfg.step_tol) {
             report.status = TerminalStatus::converged_step;
+            stop = true;
+        }
+        if (stop) {
+            if (spec) {
+                drain();
+                p.als_restore_factors();
+            }
             break;
         }
+        if (!spec && sweep < cfg.max_sweeps) p.als_sweep_launch(lambda_of(sweep + 1), true);
     }
     p.get_factors(model);
     return {std::move(model), std::move(report)};

@@ -214,6 +214,7 @@ public:
     void upload_gammas(const double* grams, const double* pair);
     std::pair<double, double> residual_fitness(double xnorm2, int last_src);  // kruskal.cpp:94-118
     void residual_launch(double xnorm2);  // the same, result left in the scalar slots (no readback)
+    void residual_launch_dev();           // the same with ||X||^2 already in its device slot
     void gradient();                                  // G (gauss_newton.cpp:81-94)
     double norm_sum(const double* dev_stacked);       // sum_n ||block_n||_F
     void jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape);
@@ -227,6 +228,16 @@ public:
     void spd_inverse(const double* dev_s, double lambda, double* dev_inv);
 
     AlsSweepDiag als_sweep(double lambda);            // als.cpp:22-52
+    // Pipelined sweeps: launch queues one sweep (optionally followed by the
+    // residual of its result, the driver's per-sweep check) and its packed
+    // diagnostics without synchronising; finish waits for the oldest queued
+    // sweep and decodes them (throws as als_sweep does). At most kSweepSlots
+    // sweeps are in flight.
+    void als_sweep_launch(double lambda, bool with_residual);
+    AlsSweepDiag als_sweep_finish(double* res = nullptr, double* fit = nullptr);
+    int als_sweeps_pending() const { return static_cast<int>(pending_.size() + done_.size()); }
+    void als_snapshot_factors();   // A -> Atrial (device copy, stream-ordered)
+    void als_restore_factors();    // Atrial -> A, caches dropped
     GnStepDiag gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);  // :360-449
 
     // stacked device buffers (N blocks of s_n x R)
@@ -273,6 +284,26 @@ private:
     };
     static constexpr std::size_t kAlsGraphs = 4;
     std::vector<AlsGraph> als_graphs_;
+    static constexpr int kSweepSlots = 4, kSlotDoubles = 4 + kMaxOrder;
+    struct PendingSweep {
+        int slot, contr;
+        AlsGraph* graph;  // profiled replay whose event pairs are read at finish (or null)
+    };
+    std::vector<PendingSweep> pending_;  // FIFO
+    struct SweepResult {
+        AlsSweepDiag diag;
+        double res = 1.0, fit = 0.0;
+        int err = 0;  // 1 non-finite factor, 2 singular SPD system
+    };
+    std::vector<SweepResult> done_;  // completed, not yet handed to the caller (FIFO)
+    SweepResult complete_oldest();   // waits for pending_.front() and decodes it
+    void drain_pending() {
+        while (!pending_.empty()) done_.push_back(complete_oldest());
+    }
+    int next_slot_ = 0;
+    double* hmap_ = nullptr;  // mapped pinned slots (kSweepSlots x kSlotDoubles)
+    double* dmap_ = nullptr;  // their device alias
+    cudaEvent_t slot_ev_[kSweepSlots] = {};
     SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_, pm_mode_}; }
     void drop_als_graph();
     void als_sweep_body(double lambda);

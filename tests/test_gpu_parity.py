@@ -408,6 +408,30 @@ def test_c1_als_trace_matches_oracle(orc, ck):
     assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
 
 
+@pytest.mark.parametrize("cfg", [{"max_sweeps": 300}, {"max_sweeps": 7}, {"max_sweeps": 300, "step_tol": 1e-3},
+                                 {"max_sweeps": 40, "lambda0": 1e-2, "decay_every": 5}])
+def test_als_pipelined_driver_equals_sequential(ck, orc, cfg, monkeypatch):
+    """als_optimize queues sweep k+1 before reading sweep k (restoring the
+    factors when k stops the run): records and factors are bitwise those of
+    the sequential loop, for every stop rule (residual, cap, step norm)."""
+    dims, rank, x, init = _c1(orc)
+    runs = []
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("CPKIT_ALS_NO_PIPELINE", flag)
+        else:
+            monkeypatch.delenv("CPKIT_ALS_NO_PIPELINE", raising=False)
+        p = ck.DeviceProblem(dims, rank)
+        p.upload(x)
+        got, rep = p.optimize({"optimizer": "als", "als": cfg}, init)
+        j = rep.to_json()
+        runs.append((got, j["status"], [(r["residual"], r["lambda"]) for r in j["records"]]))
+    (f1, s1, r1), (f2, s2, r2) = runs
+    assert s1 == s2 and r1 == r2
+    for a, b in zip(f1, f2):
+        assert np.array_equal(a, b)
+
+
 # ---------------------------------------------------------------- C ABI end to end
 def test_decompose_through_c_abi(orc, ck):
     # test_capi.cpp:96-126 shape: gaussian [4,4,4] rank 2, GN
