@@ -171,6 +171,8 @@ std::size_t chol_factor_elems(int count, int R);
 // S + lambda I, mode 1: diag(S) *= (1 + lambda). Lower L per matrix.
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode,
                        double* l_out, int* status, cudaStream_t st);
+void launch_chol_batch_src(double* s, const double* grams, int order, int excl, int count, int R,
+                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st);
 // ALS update: a <- rows solved in place, row_sq[i] = ||a_new_i - a_old_i||^2
 void launch_chol_solve_rows_update(const double* l, int R, const double* b, std::int64_t rows, double* a,
                                    double* row_sq, cudaStream_t st);

@@ -166,12 +166,10 @@ __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_
 __device__ __forceinline__ double rsqrt_pos(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-#pragma unroll
-    for (int it = 0; it < 2; ++it) {
-        const double e = __fma_rn(-x * y, y, 1.0);
-        y = __fma_rn(y * e, __fma_rn(0.375, e, 0.5), y);
-    }
-    return y;
+    // the seed is good to 20 bits on sm_100a (tools/probe/rsqrt_prec.cu): one
+    // cubic step lands within ~1.2 ulp, the same as two
+    const double e = __fma_rn(-x * y, y, 1.0);
+    return __fma_rn(y * e, __fma_rn(0.375, e, 0.5), y);
 }
 
 template <int kNB>
@@ -215,46 +213,82 @@ __device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int k
     return failed;
 }
 
+// Input of one factorisation: an explicit R x R matrix s, or (grams != null)
+// Gamma^(excl) = Ones o S^(m) for ascending m != excl formed on load from the
+// Gram matrices, the same products in the same order as gamma_excl_kernel
+// (als.cpp:34-37 / kruskal.cpp:42-65), so no separate Gamma pass.
+struct CholSrc {
+    const double* s;
+    const double* grams;
+    int order, excl;
+};
+__device__ __forceinline__ double chol_src_at(const CholSrc& src, const double* s, long long rr, int e) {
+    if (!src.grams) return __ldg(s + e);
+    double g = 1.0;
+    for (int m = 0; m < src.order; ++m)
+        if (m != src.excl) g *= __ldg(src.grams + m * rr + e);
+    return g;
+}
+
 template <int kNB>
-__global__ void __launch_bounds__(256) chol_blocked_kernel(const double* __restrict__ s_all, int R, double lambda,
+__global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, int R, double lambda,
                                                            int mode, double* __restrict__ l_all,
                                                            int* __restrict__ status) {
     extern __shared__ double w[];
     const int LD = R + 1;
     const int mat = blockIdx.x;
-    const double* s = s_all + static_cast<long long>(mat) * R * R;
+    const long long rr = static_cast<long long>(R) * R;
+    const double* s = src.s + static_cast<long long>(mat) * rr;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     __shared__ double trace_sh;
     __shared__ int fail_sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 
-    if (warp == 0) {  // trace, warp-parallel (fixed shuffle order)
-        double tr = 0.0;
-        for (int i = lane; i < R; i += 32) {
-            const double d = s[static_cast<long long>(i) * R + i];
-            tr += (mode == 1) ? d * (1.0 + lambda) : d;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
-        if (lane == 0) trace_sh = tr;
-    }
-    __syncthreads();
-    const double jitter = 1e-12 * trace_sh / static_cast<double>(R);
-
     int st = 2;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        const double add = (mode == 0 ? lambda : 0.0);
-        {
-            const int total = R * R;  // 8 global loads in flight per thread, then shared stores
-            for (int e0 = tid; e0 < total; e0 += 8 * blockDim.x) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int e = e0 + u * blockDim.x;
-                    v[u] = (e < total) ? __ldg(s + e) : 0.0;
+        double jitter = 0.0;
+        if (attempt == 1) {  // the trace only matters for the retry (warp-parallel, fixed shuffle order)
+            if (warp == 0) {
+                double tr = 0.0;
+                for (int i = lane; i < R; i += 32) {
+                    const double d = chol_src_at(src, s, rr, i * R + i);
+                    tr += (mode == 1) ? d * (1.0 + lambda) : d;
                 }
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
+                for (int o = 16; o > 0; o >>= 1) tr += __shfl_down_sync(0xffffffffu, tr, o);
+                if (lane == 0) trace_sh = tr;
+            }
+            __syncthreads();
+            jitter = 1e-12 * trace_sh / static_cast<double>(R);
+        }
+        const double add = (mode == 0 ? lambda : 0.0);
+        {
+            const int total = R * R;  // 16 elements (up to 32 loads) in flight per thread, then shared stores
+            for (int e0 = tid; e0 < total; e0 += 16 * blockDim.x) {
+                double v[16];
+                if (!src.grams) {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int e = e0 + u * blockDim.x;
+                        v[u] = (e < total) ? __ldg(s + e) : 0.0;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) v[u] = 1.0;
+                    for (int m = 0; m < src.order; ++m) {
+                        if (m == src.excl) continue;
+                        double f[16];
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) {
+                            const int e = e0 + u * blockDim.x;
+                            f[u] = (e < total) ? __ldg(src.grams + m * rr + e) : 1.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) v[u] *= f[u];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
                     const int e = e0 + u * blockDim.x;
                     if (e < total) {
                         const int i = e / R, k = e - i * R;
@@ -561,12 +595,24 @@ std::size_t chol_factor_elems(int count, int R) { return static_cast<std::size_t
 
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode, double* l_out, int* status,
                        cudaStream_t st) {
+    launch_chol_batch_src(const_cast<double*>(s), nullptr, 0, -1, count, R, lambda, mode, l_out, status, st);
+}
+// grams != null: factor Gamma^(excl) formed from the Gram matrices on load when
+// the blocked kernel serves R (count 1); otherwise Gamma is formed into `s`
+// first (s must then be an R x R workspace).
+void launch_chol_batch_src(double* s, const double* grams, int order, int excl, int count, int R,
+                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st) {
     if (R > 512) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
     const Layout lay = layout_of(R);
-    if (lay == kSquareSmem && !std::getenv("CPKIT_CHOL_UNBLOCKED")) {
+    const bool blocked = lay == kSquareSmem && !std::getenv("CPKIT_CHOL_UNBLOCKED");
+    if (grams && !blocked) {
+        launch_gamma_excl(grams, order, R, excl, s, st);
+        grams = nullptr;
+    }
+    if (blocked) {
         auto fn = chol_blocked_kernel<16>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
-        fn<<<count, 256, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
+        fn<<<count, 256, sq_bytes(R), st>>>(CholSrc{s, grams, order, excl}, R, *lambda, mode, l_out, status);
     } else if (lay == kSquareSmem) {
         auto fn = chol_kernel<SqIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));

@@ -1070,8 +1070,8 @@ void DeviceProblem::als_sweep_body(double lambda) {
         // overlapping the MTTKRP of mode n on the main stream
         CPK_CUDA(cudaEventRecord(ctx_.ev[2 + 2 * n], ctx_.stream));
         CPK_CUDA(cudaStreamWaitEvent(ctx_.aux, ctx_.ev[2 + 2 * n], 0));
-        launch_gamma_excl(grams_.get(), N, R_, n, gam_.get() + n * RR, ctx_.aux);
-        launch_chol_batch(gam_.get() + n * RR, 1, R_, &lambda, 0, chol_.get() + n * LDR, status_.get() + n, ctx_.aux);
+        launch_chol_batch_src(gam_.get() + n * RR, grams_.get(), N, n, 1, R_, &lambda, 0, chol_.get() + n * LDR,
+                              status_.get() + n, ctx_.aux);
         CPK_CUDA(cudaEventRecord(ctx_.ev[3 + 2 * n], ctx_.aux));
         if (msdt_) mttkrp_msdt(n);
         else mttkrp(n);
