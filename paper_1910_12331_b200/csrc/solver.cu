@@ -310,7 +310,8 @@ Context::Context(int dev) : device(dev) {
     // bandwidth kernel fills every SM
     int lo = 0, hi = 0;
     CPK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CPK_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, hi));
+    const char* pe = std::getenv("CPKIT_AUX_PRIORITY");
+    CPK_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, (pe && std::atoi(pe) == 0) ? lo : hi));
     for (auto& e : ev) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 Context::~Context() {
