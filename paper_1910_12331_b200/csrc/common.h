@@ -153,6 +153,7 @@ void launch_axpby(double* out, const double* a, double alpha, const double* x, s
                   cudaStream_t st);
 void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st);
 void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_t st);
+void launch_pack_values(const double* d, int nd, const int* iv, int ni, double* out_mapped, cudaStream_t st);
 void launch_pack_sweep(const double* scal, int kstep, int kres, const int* flag, const int* status, int n,
                        double* out_mapped, cudaStream_t st);
 // Dense evaluation of a Kruskal model + keyed-RNG noise (generators / reconstruct)
@@ -172,7 +173,10 @@ std::size_t chol_factor_elems(int count, int R);
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode,
                        double* l_out, int* status, cudaStream_t st);
 void launch_chol_batch_src(double* s, const double* grams, int order, int excl, int count, int R,
-                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st);
+                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st,
+                           long long s_stride = 0);
+void launch_chol_batch_strided(const double* s, long long s_stride, int count, int R, const double* lambda, int mode,
+                               double* l_out, int* status, cudaStream_t st);
 // ALS update: a <- rows solved in place, row_sq[i] = ||a_new_i - a_old_i||^2
 void launch_chol_solve_rows_update(const double* l, int R, const double* b, std::int64_t rows, double* a,
                                    double* row_sq, cudaStream_t st);

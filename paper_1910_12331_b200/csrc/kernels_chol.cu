@@ -60,11 +60,12 @@ inline Layout layout_of(int R) {
 // Jitter trace uses the matrix handed to factor_shifted (gauss_newton.cpp:190-207).
 template <class Idx, bool kSmem>
 __global__ void __launch_bounds__(512) chol_kernel(const double* __restrict__ s_all, int R, double lambda, int mode,
-                                                   double* __restrict__ l_all, int* __restrict__ status) {
+                                                   double* __restrict__ l_all, int* __restrict__ status,
+                                                   long long s_stride) {
     extern __shared__ double sh[];
     const int LD = R + 1;
     const int mat = blockIdx.x;
-    const double* s = s_all + static_cast<long long>(mat) * R * R;
+    const double* s = s_all + static_cast<long long>(mat) * s_stride;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     double* w = kSmem ? sh : out;
     const Idx ix{LD, R};
@@ -221,6 +222,7 @@ struct CholSrc {
     const double* s;
     const double* grams;
     int order, excl;
+    long long s_stride;  // elements between consecutive input matrices
 };
 __device__ __forceinline__ double chol_src_at(const CholSrc& src, const double* s, long long rr, int e) {
     if (!src.grams) return __ldg(s + e);
@@ -238,7 +240,7 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
     const int LD = R + 1;
     const int mat = blockIdx.x;
     const long long rr = static_cast<long long>(R) * R;
-    const double* s = src.s + static_cast<long long>(mat) * rr;
+    const double* s = src.s + static_cast<long long>(mat) * src.s_stride;
     double* out = l_all + static_cast<long long>(mat) * R * LD;
     __shared__ double trace_sh;
     __shared__ int fail_sh;
@@ -597,12 +599,21 @@ void launch_chol_batch(const double* s, int count, int R, const double* lambda, 
                        cudaStream_t st) {
     launch_chol_batch_src(const_cast<double*>(s), nullptr, 0, -1, count, R, lambda, mode, l_out, status, st);
 }
+// count matrices read in place s_stride elements apart (e.g. the diagonal
+// blocks Gamma(n,n) of the pair array)
+void launch_chol_batch_strided(const double* s, long long s_stride, int count, int R, const double* lambda, int mode,
+                               double* l_out, int* status, cudaStream_t st) {
+    launch_chol_batch_src(const_cast<double*>(s), nullptr, 0, -1, count, R, lambda, mode, l_out, status, st,
+                          s_stride);
+}
 // grams != null: factor Gamma^(excl) formed from the Gram matrices on load when
 // the blocked kernel serves R (count 1); otherwise Gamma is formed into `s`
 // first (s must then be an R x R workspace).
 void launch_chol_batch_src(double* s, const double* grams, int order, int excl, int count, int R,
-                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st) {
+                           const double* lambda, int mode, double* l_out, int* status, cudaStream_t st,
+                           long long s_stride) {
     if (R > 512) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
+    if (s_stride <= 0) s_stride = static_cast<long long>(R) * R;
     const Layout lay = layout_of(R);
     const bool blocked = lay == kSquareSmem && !std::getenv("CPKIT_CHOL_UNBLOCKED");
     if (grams && !blocked) {
@@ -612,17 +623,17 @@ void launch_chol_batch_src(double* s, const double* grams, int order, int excl, 
     if (blocked) {
         auto fn = chol_blocked_kernel<16>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
-        fn<<<count, 256, sq_bytes(R), st>>>(CholSrc{s, grams, order, excl}, R, *lambda, mode, l_out, status);
+        fn<<<count, 256, sq_bytes(R), st>>>(CholSrc{s, grams, order, excl, s_stride}, R, *lambda, mode, l_out, status);
     } else if (lay == kSquareSmem) {
         auto fn = chol_kernel<SqIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
-        fn<<<count, 512, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
+        fn<<<count, 512, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status, s_stride);
     } else if (lay == kPackedSmem) {
         auto fn = chol_kernel<PkIdx, true>;
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
-        fn<<<count, 512, pk_bytes(R), st>>>(s, R, *lambda, mode, l_out, status);
+        fn<<<count, 512, pk_bytes(R), st>>>(s, R, *lambda, mode, l_out, status, s_stride);
     } else {
-        chol_kernel<SqIdx, false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status);
+        chol_kernel<SqIdx, false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status, s_stride);
     }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());

@@ -508,6 +508,20 @@ __global__ void pack_sweep_kernel(const double* __restrict__ scal, int kstep, in
     }
 }
 }  // namespace
+namespace {
+__global__ void pack_values_kernel(const double* __restrict__ d, int nd, const int* __restrict__ iv, int ni,
+                                   double* out) {
+    for (int i = threadIdx.x; i < nd + ni; i += blockDim.x)
+        out[i] = i < nd ? d[i] : static_cast<double>(iv[i - nd]);
+}
+}  // namespace
+// out[0..nd) = d[0..nd), out[nd..nd+ni) = iv[0..ni) as doubles, into mapped
+// pinned host memory (stream-ordered, no copy engine, no synchronisation).
+void launch_pack_values(const double* d, int nd, const int* iv, int ni, double* out_mapped, cudaStream_t st) {
+    pack_values_kernel<<<1, 32, 0, st>>>(d, nd, iv, ni, out_mapped);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
 // One sweep's diagnostics (step norm, residual, fitness, finiteness flag,
 // per-mode SPD status) written straight into mapped pinned host memory:
 // no copy-engine operation and no synchronisation on the solver stream.

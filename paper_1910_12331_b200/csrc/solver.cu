@@ -347,7 +347,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
     if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
     CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hpin_), 16 * sizeof(double), cudaHostAllocDefault));
-    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), kSweepSlots * kSlotDoubles * sizeof(double),
+    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), (kGnMapOff + kGnMapDoubles) * sizeof(double),
                            cudaHostAllocMapped));
     CPK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dmap_), hmap_, 0));
     als_graphs_.reserve(kAlsGraphs);  // in-flight sweeps hold pointers to their graphs
@@ -918,11 +918,9 @@ void DeviceProblem::launch_preconditioner_factor(double lambda, RegShape shape) 
     const std::size_t RR = static_cast<std::size_t>(R_) * R_;
     CPK_CUDA(cudaEventRecord(ctx_.ev[0], ctx_.stream));  // Gamma set ready
     CPK_CUDA(cudaStreamWaitEvent(ctx_.aux, ctx_.ev[0], 0));
-    for (int n = 0; n < N; ++n)
-        CPK_CUDA(cudaMemcpyAsync(gam_.get() + n * RR, pair_.get() + (n * N + n) * RR, RR * 8,
-                                 cudaMemcpyDeviceToDevice, ctx_.aux));
-    launch_chol_batch(gam_.get(), N, R_, &lambda, shape == RegShape::identity ? 0 : 1, chol_.get(),
-                      status_.get(), ctx_.aux);
+    // Gamma(n,n) read in place from the pair array (diagonal blocks, (N+1) R^2 apart)
+    launch_chol_batch_strided(pair_.get(), static_cast<long long>(N + 1) * RR, N, R_, &lambda,
+                              shape == RegShape::identity ? 0 : 1, chol_.get(), status_.get(), ctx_.aux);
     CPK_CUDA(cudaEventRecord(ctx_.ev[1], ctx_.aux));
     precond_pending_ = true;
     precond_lambda_ = lambda;
@@ -1220,7 +1218,122 @@ AlsSweepDiag DeviceProblem::als_sweep_finish(double* res, double* fit) {
 // (one fused set of two root contractions computes every M^(n) of the new
 // factors; M^(N-1) gives residual_after and the rest is cached for the next
 // step), instead of a third, naive contraction (:442-444).
+// B200 change: the default step (no Armijo search) runs start to finish on
+// the device with ONE host synchronisation. The reference's early exits
+// (residual / gradient halt, gauss_newton.cpp:370-389), the preconditioner's
+// SingularSystem and cp_cg's non-finite check are decided afterwards from
+// values packed into mapped pinned memory; a step that must not have happened
+// is undone from the device copy of the pre-step factors. Same results as the
+// phase-by-phase version (`CPKIT_GN_SYNC=1`, used for Armijo).
 GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
+    if (cfg.armijo || std::getenv("CPKIT_GN_SYNC")) return gn_step_sync(cfg, schedule, xnorm2);
+    const int N = order();
+    const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
+    double* hm = hmap_ + kGnMapOff;   // [res, fit, gnorm | cg 5 | status N | step, fin | res_after, fit_after]
+    double* dm = dmap_ + kGnMapOff;
+    const int o_cg = 3, o_st = 8, o_step = 8 + N, o_after = 10 + N;
+    if (!m_all_valid_) compute_all_mttkrp();
+    build_gamma_set();
+    launch_preconditioner_factor(schedule.lambda, cfg.schedule.shape);  // side stream, overlaps residual/gradient
+    residual_launch(xnorm2);
+    gradient();
+    launch_block_norm_sum(G_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
+    launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm, ctx_.stream);
+    launch_pack_values(scal_.get() + kNormSum, 1, nullptr, 0, dm + 2, ctx_.stream);
+    als_snapshot_factors();  // pre-step factors (restored when the step must not happen)
+    // preconditioner inverse (its factorisation status is checked at the end)
+    precond_pending_ = false;
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
+    launch_chol_inverse_batch(chol_.get(), N, R_, pinv_.get(), chol_tmp_.get(), ctx_.stream);
+    launch_pack_values(nullptr, 0, status_.get(), N, dm + o_st, ctx_.stream);
+    CgParams p = base_params(N, R_, dims_, off_);
+    int cap = cfg.cg_max_iters;
+    if (cap <= 0) {  // default_cg_cap (gauss_newton.cpp:267-275)
+        std::uint64_t total = 0;
+        for (auto d : dims_) total += d * static_cast<std::uint64_t>(R_);
+        cap = static_cast<int>(std::min<std::uint64_t>(total, 10ull * static_cast<std::uint64_t>(R_)));
+    }
+    p.A = A_.get();
+    p.pair = pair_.get();
+    p.pinv = pinv_.get();
+    p.G = G_.get();
+    p.V = V_.get();
+    p.Rr[0] = Rr_[0].get();
+    p.Rr[1] = Rr_[1].get();
+    p.W[0] = W_[0].get();
+    p.W[1] = W_[1].get();
+    p.Z = Z_.get();
+    p.Q = Q_.get();
+    p.slots = slots_.get();
+    p.nslots = static_cast<int>(slots_.size());
+    p.barrier = barrier_.get();
+    p.lambda = schedule.lambda;
+    p.shape = cfg.schedule.shape == RegShape::identity ? 0 : 1;
+    p.beta_variant = cfg.cg_beta == CgBetaVariant::standard ? 0 : 1;
+    p.cg_tol = cfg.cg_tol;
+    p.cap = cap;
+    p.result = cgres_.get();
+    prof_begin(kProfCg);
+    run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);  // G = 0: 0 iterations, V = 0 (cp_cg's shortcut)
+    prof_end();
+    launch_pack_values(nullptr, 0, cgres_.get(), 5, dm + o_cg, ctx_.stream);
+    launch_axpy(A_.get(), V_.get(), 1.0, S, ctx_.stream);
+    launch_block_norm_sum(V_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
+    launch_set_flag_scalar(flag_.get(), 1, scal_.get() + kStep, 0.0, ctx_.stream);
+    launch_all_finite(A_.get(), S, flag_.get(), ctx_.stream);
+    launch_pack_values(scal_.get() + kNormSum, 1, flag_.get(), 1, dm + o_step, ctx_.stream);
+    invalidate_all();
+    // residual_after from the next iteration's tree pass (cached for the next step)
+    compute_all_mttkrp();
+    grams_all();
+    residual_launch(xnorm2);
+    launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);
+    ctx_.sync_main();
+
+    GnStepDiag diag;
+    const double res = hm[0];
+    diag.residual_before = res;
+    diag.residual_after = res;
+    auto undo = [&] {  // the step must not have happened: pre-step factors, caches rebuilt on demand
+        als_restore_factors();
+        ctx_.sync_main();
+    };
+    if (res < cfg.residual_tol) {
+        undo();
+        diag.halt = GnStepDiag::Halt::residual;
+        return diag;
+    }
+    diag.grad_norm = hm[2];
+    if (diag.grad_norm <= cfg.grad_tol) {
+        undo();
+        diag.halt = GnStepDiag::Halt::gradient;
+        return diag;
+    }
+    diag.lambda = schedule.lambda;
+    if (diag.grad_norm != 0.0) {
+        for (int n = 0; n < N; ++n)
+            if (hm[o_st + n] == 2.0) {
+                undo();
+                throw SingularSystem("spd_solve: factorization failed after jitter retry");
+            }
+        if (hm[o_cg + 3] != 0.0) {
+            undo();
+            throw NumericalFailure("cp_cg: non-finite iterate");
+        }
+        diag.cg_iters = static_cast<int>(hm[o_cg]);
+        diag.cg_hit_cap = hm[o_cg + 1] != 0.0;
+        diag.cg_breakdown = hm[o_cg + 2] != 0.0;
+    }
+    diag.alpha = 1.0;
+    diag.step_norm = hm[o_step];
+    if (hm[o_step + 1] == 0.0) throw NumericalFailure("gn_step: non-finite factors after update");
+    diag.residual_after = hm[o_after];
+    diag.stepped = true;
+    schedule = schedule_next(schedule);
+    return diag;
+}
+
+GnStepDiag DeviceProblem::gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
     const int N = order();
     const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
     GnStepDiag diag;

@@ -239,6 +239,8 @@ public:
     void als_snapshot_factors();   // A -> Atrial (device copy, stream-ordered)
     void als_restore_factors();    // Atrial -> A, caches dropped
     GnStepDiag gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);  // :360-449
+    // the same step with a host decision after every phase (Armijo needs it)
+    GnStepDiag gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);
 
     // stacked device buffers (N blocks of s_n x R)
     double* G() { return G_.get(); }
@@ -301,7 +303,8 @@ private:
         while (!pending_.empty()) done_.push_back(complete_oldest());
     }
     int next_slot_ = 0;
-    double* hmap_ = nullptr;  // mapped pinned slots (kSweepSlots x kSlotDoubles)
+    double* hmap_ = nullptr;  // mapped pinned slots (kSweepSlots x kSlotDoubles), then the GN step's area
+    static constexpr int kGnMapOff = kSweepSlots * kSlotDoubles, kGnMapDoubles = 16 + 2 * kMaxOrder;
     double* dmap_ = nullptr;  // their device alias
     cudaEvent_t slot_ev_[kSweepSlots] = {};
     SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_, pm_mode_}; }

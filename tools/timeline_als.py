@@ -17,10 +17,17 @@ torch.cuda.init()
 for _ in range(6):
     p.als_sweep(0.0)
 torch.cuda.synchronize()
+if mode == "gn":
+    p.time_gn_steps({}, 2)  # warm
+    p.set_factors(init)
+    p.time_gn_steps({}, 1)
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
-    p.time_als_sweeps(float(os.environ.get("LAM", "0")), 4)  # the bench's pipelined loop
+    if mode == "gn":
+        p.time_gn_steps({}, 2)
+    else:
+        p.time_als_sweeps(float(os.environ.get("LAM", "0")), 4)  # the bench's pipelined loop
     torch.cuda.synchronize()
-out = os.path.join(os.environ.get("OUT", "gpurun_out"), "timeline_als.json")
+out = os.path.join(os.environ.get("OUT", "gpurun_out"), f"timeline_{mode}.json")
 prof.export_chrome_trace(out)
 ev = [e for e in json.load(open(out))["traceEvents"] if e.get("cat") == "kernel"]
 ev.sort(key=lambda e: e["ts"])
@@ -32,6 +39,6 @@ for e in ev:
     name = name.split("(")[0][:60]
     print(f"{e['ts'] - t0:9.1f} {e['dur']:7.1f}  gap {gap:6.1f}  s{e['args'].get('stream')}  {name}")
     busy_end = max(busy_end, e["ts"] + e["dur"])
-print(f"total span {busy_end - t0:.1f} us for 4 sweeps")
+print(f"total span {busy_end - t0:.1f} us ({mode})")
 idle = sum(max(0.0, b["ts"] - max(e["ts"] + e["dur"] for e in ev[:i + 1])) for i, b in enumerate(ev[1:]))
 print(f"idle (no kernel running) {idle:.1f} us")
