@@ -785,9 +785,11 @@ void DeviceProblem::note_factor_update(int mode) {
     if (mode >= h_) pf_valid_ = false;  // back-root key holds modes >= h
     else pb_valid_ = false;             // front-root key holds modes < h
     if (mode == pm_mode_) pm_mode_ = -1;
+    pinv_ready_ = false;
     m_all_valid_ = false;
 }
 void DeviceProblem::invalidate_all() {  // factors changed wholesale
+    pinv_ready_ = false;
     pf_valid_ = pb_valid_ = false;
     pm_mode_ = -1;
     m_all_valid_ = false;
@@ -925,6 +927,23 @@ void DeviceProblem::launch_preconditioner_factor(double lambda, RegShape shape) 
     precond_pending_ = true;
     precond_lambda_ = lambda;
     precond_shape_ = shape;
+}
+void DeviceProblem::launch_precond_chain(double lambda, RegShape shape, bool grams_and_gamma) {
+    if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
+    const int N = order();
+    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
+    CPK_CUDA(cudaEventRecord(ctx_.ev[0], ctx_.stream));  // factors (and, if not recomputed, Gamma set) ready
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.aux, ctx_.ev[0], 0));
+    if (grams_and_gamma) {
+        launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), 0, N, R_, smax_, gram_ws_.get(), grams_.get(),
+                     ctx_.aux);
+        launch_gamma_pairs(grams_.get(), N, R_, pair_.get(), ctx_.aux);
+        grams_valid_ = true;
+    }
+    launch_chol_batch_strided(pair_.get(), static_cast<long long>(N + 1) * RR, N, R_, &lambda,
+                              shape == RegShape::identity ? 0 : 1, chol_.get(), status_.get(), ctx_.aux);
+    launch_chol_inverse_batch(chol_.get(), N, R_, pinv_.get(), chol_tmp_.get(), ctx_.aux);
+    CPK_CUDA(cudaEventRecord(ctx_.ev[1], ctx_.aux));
 }
 void DeviceProblem::build_preconditioner(double lambda, RegShape shape) {
     if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
@@ -1232,19 +1251,22 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     double* hm = hmap_ + kGnMapOff;   // [res, fit, gnorm | cg 5 | status N | step, fin | res_after, fit_after]
     double* dm = dmap_ + kGnMapOff;
     const int o_cg = 3, o_st = 8, o_step = 8 + N, o_after = 10 + N;
+    const RegShape shape = cfg.schedule.shape;
     if (!m_all_valid_) compute_all_mttkrp();
-    build_gamma_set();
-    launch_preconditioner_factor(schedule.lambda, cfg.schedule.shape);  // side stream, overlaps residual/gradient
+    if (!(pinv_ready_ && pinv_lambda_ == schedule.lambda && pinv_shape_ == shape)) {
+        build_gamma_set();
+        launch_precond_chain(schedule.lambda, shape, false);  // side stream, overlaps residual/gradient
+    }
+    pinv_ready_ = false;
+    precond_pending_ = false;
     residual_launch(xnorm2);
     gradient();
     launch_block_norm_sum(G_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm, ctx_.stream);
     launch_pack_values(scal_.get() + kNormSum, 1, nullptr, 0, dm + 2, ctx_.stream);
     als_snapshot_factors();  // pre-step factors (restored when the step must not happen)
-    // preconditioner inverse (its factorisation status is checked at the end)
-    precond_pending_ = false;
+    // preconditioner inverse ready (its factorisation status is checked at the end)
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
-    launch_chol_inverse_batch(chol_.get(), N, R_, pinv_.get(), chol_tmp_.get(), ctx_.stream);
     launch_pack_values(nullptr, 0, status_.get(), N, dm + o_st, ctx_.stream);
     CgParams p = base_params(N, R_, dims_, off_);
     int cap = cfg.cg_max_iters;
@@ -1283,9 +1305,16 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     launch_all_finite(A_.get(), S, flag_.get(), ctx_.stream);
     launch_pack_values(scal_.get() + kNormSum, 1, flag_.get(), 1, dm + o_step, ctx_.stream);
     invalidate_all();
+    // the next step's Grams, Gamma set and preconditioner (lambda of the next
+    // schedule state) on the side stream, hidden behind the tree pass
+    const RegSchedule next = schedule_next(schedule);
+    launch_precond_chain(next.lambda, shape, true);
+    pinv_ready_ = true;
+    pinv_lambda_ = next.lambda;
+    pinv_shape_ = shape;
     // residual_after from the next iteration's tree pass (cached for the next step)
     compute_all_mttkrp();
-    grams_all();
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));  // Grams
     residual_launch(xnorm2);
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);
     ctx_.sync_main();
@@ -1296,7 +1325,8 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     diag.residual_after = res;
     auto undo = [&] {  // the step must not have happened: pre-step factors, caches rebuilt on demand
         als_restore_factors();
-        ctx_.sync_main();
+        pinv_ready_ = false;
+        ctx_.sync();
     };
     if (res < cfg.residual_tol) {
         undo();

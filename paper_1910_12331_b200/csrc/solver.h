@@ -242,6 +242,17 @@ public:
     // the same step with a host decision after every phase (Armijo needs it)
     GnStepDiag gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);
 
+private:
+    // Side-stream chain for a GN step's preconditioner: [Grams + Gamma set,]
+    // Cholesky of Gamma(n,n) (+ lambda) and its inverse into pinv_; records
+    // ctx_.ev[1]. pinv_ready_ marks a chain launched ahead for (lambda, shape).
+    void launch_precond_chain(double lambda, RegShape shape, bool grams_and_gamma);
+    bool pinv_ready_ = false;
+    double pinv_lambda_ = 0.0;
+    RegShape pinv_shape_ = RegShape::identity;
+
+public:
+
     // stacked device buffers (N blocks of s_n x R)
     double* G() { return G_.get(); }
     double* V() { return V_.get(); }
