@@ -752,7 +752,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
               long long M, long long K, int R, double* out, long long oss, int brel = 0) {
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
-    const dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
+    dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
     const dim3 block(32 * (p.nw + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
@@ -760,6 +760,11 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
                                : root_gemm_kernel<NTV, TRANS, GEN, false>;                         \
         CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
                                       static_cast<int>(smem)));                                    \
+        if (std::getenv("CPKIT_GRID_OCC")) { /* experiments: grid from the real occupancy */        \
+            int occ = 1;                                                                           \
+            CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, static_cast<int>(block.x), smem)); \
+            grid.x = static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * std::max(occ, 1))); \
+        }                                                                                          \
         fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.BN(), p.nw, p.bns, p.stages, p.kps,  \
                                       p.splits, out, oss, brel);                                   \
         break;                                                                                     \
