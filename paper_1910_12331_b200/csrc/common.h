@@ -94,9 +94,10 @@ struct KrpDesc {
 // workspace (krp_workspace_elems) filled with the Khatri-Rao operand.
 //   back root:  P_F[F x R] = X[F x B] * KRP_B        (NN)
 //   front root: P_B[B x R] = X[F x B]^T * KRP_F      (TN, split-K)
+// reserve_sms: SMs to leave to a concurrent side-stream kernel during the full waves
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                       const KrpDesc& kb, double* krp, double* pf, double* splitk_ws, std::size_t splitk_ws_elems,
-                      cudaStream_t st);
+                      cudaStream_t st, int reserve_sms = 0);
 std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R);
 void launch_root_front(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                        const KrpDesc& kf, double* krp, double* pb, double* splitk_ws,

@@ -603,12 +603,12 @@ bool runs_fit(int wm, int nt8, int nw) {
 }
 // Split count with the best wave efficiency (<= 2 waves or the unsplit count),
 // keeping >= 8 k-stages per split; ties go to fewer splits.
-long long best_splits(long long base, long long slots, long long K, double* eff_out) {
+long long best_splits(long long base, long long slots, long long K, double* eff_out, int min_chunks = 8) {
     const long long kchunks = (K + kBK - 1) / kBK;
     long long best = 1;
     double best_eff = -1.0;
     for (long long sp = 1; sp <= 64; ++sp) {
-        if (sp > 1 && kchunks / sp < 8) break;
+        if (sp > 1 && kchunks / sp < min_chunks) break;
         const long long ctas = base * sp;
         const long long waves = (ctas + slots - 1) / slots;
         if (sp > 1 && waves > std::max<long long>(2, (base + slots - 1) / slots)) break;
@@ -636,7 +636,7 @@ bool runs_full(const GemmPlan& p) {
 
 // fixed_kps > 0: batched contraction, split s covers k in [s kps, (s+1) kps)
 // and writes its own output slab (no split search, no reduction).
-GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0) {
+GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0, int min_chunks = 8) {
     GemmPlan p{};
     // rank split: one CTA column covers up to 208 ranks (26 n8 cells)
     p.ntiles = (R + 207) / 208;
@@ -681,7 +681,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
                     w_eff = static_cast<double>(units) / static_cast<double>(((units + slots - 1) / slots) * slots);
                 } else {
                     best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
-                                K, &w_eff);
+                                K, &w_eff, min_chunks);
                 }
                 const double score = cell_efficiency(wm, nt8p, nw) * (static_cast<double>(p.nt8) / nt8p) * m_eff *
                                      w_eff * (full ? 1.0 : trans ? 0.97 : 0.85) * (1.0 + 0.002 * wm) *
@@ -735,7 +735,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
     if (fixed_kps > 0) {
         p.kps = fixed_kps;
     } else {
-        const long long sp = best_splits(base, slots, K, nullptr);
+        const long long sp = best_splits(base, slots, K, nullptr, min_chunks);
         const long long kchunks = (K + kBK - 1) / kBK;
         p.kps = ((kchunks + sp - 1) / sp) * kBK;  // multiple of kBK: splits never share a stage
     }
@@ -749,10 +749,12 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
 
 template <bool TRANS, bool GEN>
 void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, const KrpDev& kd,
-              long long M, long long K, int R, double* out, long long oss, int brel = 0) {
+              long long M, long long K, int R, double* out, long long oss, int brel = 0, long long max_ctas = 0) {
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
-    dim3 grid(static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * p.per_sm)));
+    long long cap = static_cast<long long>(num_sms()) * p.per_sm;
+    if (max_ctas > 0) cap = std::min(cap, max_ctas);
+    dim3 grid(static_cast<unsigned>(std::min<long long>(units, cap)));
     const dim3 block(32 * (p.nw + 1));
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
@@ -798,6 +800,37 @@ void fill_krp(const KrpDesc& kd, long long K, int R, double* krp, cudaStream_t s
     CPK_CUDA(cudaGetLastError());
 }
 
+// Wave-quantisation tail of an unsplit NN root: the rows of the full waves
+// run as one launch, the last partial wave's rows as a second launch split
+// over k (its own plan, >= 3 k-stages per split) and reduced in fixed order.
+// The kernel itself is unchanged. rows_main == M: no tail launch.
+// reserve_sms: SMs left to a concurrent side-stream kernel (the SPD
+// factorisation beside an ALS/GN root) while the full waves run.
+struct BackSplit {
+    GemmPlan main, tail;
+    long long rows_main, main_ctas;
+};
+BackSplit plan_back(long long M, long long K, int R, int reserve_sms) {
+    BackSplit b;
+    b.main = plan_gemm(M, K, R, false);
+    b.rows_main = M;
+    b.main_ctas = 0;
+    const GemmPlan& p = b.main;
+    if (p.splits != 1 || p.ntiles != 1 || std::getenv("CPKIT_NO_TAIL_LAUNCH")) return b;
+    const long long slots = static_cast<long long>(num_sms() - reserve_sms) * p.per_sm;
+    const long long units = p.mtiles;
+    const long long rem = units % slots;
+    if (units <= slots || rem == 0 || 2 * rem > slots) return b;
+    const long long rows_main = (units - rem) * p.BM();
+    GemmPlan tail = plan_gemm(M - rows_main, K, R, false, 0, 3);
+    if (tail.splits < 2) return b;
+    b.main = plan_gemm(rows_main, K, R, false);
+    b.tail = tail;
+    b.rows_main = rows_main;
+    b.main_ctas = slots;
+    return b;
+}
+
 }  // namespace
 
 std::size_t krp_workspace_elems(std::int64_t rows, int R) {
@@ -807,9 +840,38 @@ std::size_t krp_workspace_elems(std::int64_t rows, int R) {
 // X is F x Bs row-major (Bs >= B, Bs even: the padded row stride).
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                       const KrpDesc& kb, double* krp, double* pf, double* ws, std::size_t ws_elems,
-                      cudaStream_t st) {
-    const GemmPlan p = plan_gemm(F, B, R, false);
-    
+                      cudaStream_t st, int reserve_sms) {
+    const BackSplit bs = plan_back(F, B, R, reserve_sms);
+    if (bs.rows_main < F && ws_elems >= static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R) {
+        const int Rs2 = (R + 1) & ~1;
+        const bool direct2 = kb.nmodes == 1 && R % 2 == 0;
+        if (!direct2) fill_krp(kb, B, R, krp, st);
+        const CUtensorMap kmap = make_map(direct2 ? kb.fac[0] : krp, static_cast<std::uint64_t>(Rs2),
+                                          static_cast<std::uint64_t>(B), static_cast<std::uint32_t>(bs.main.bns), kBK,
+                                          false);
+        // full waves: rows [0, rows_main)
+        const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(bs.rows_main),
+                                          16, static_cast<std::uint32_t>(bs.main.BM()), true);
+        dispatch<false, false>(bs.main, st, xmap, kmap, to_dev(kb), bs.rows_main, B, R, pf, 0, 0, bs.main_ctas);
+        // tail rows, split over k into the workspace, then the fixed-order reduce
+        const long long mt = F - bs.rows_main;
+        const CUtensorMap xmap_t = make_map(x + bs.rows_main * Bs, static_cast<std::uint64_t>(Bs),
+                                            static_cast<std::uint64_t>(mt), 16,
+                                            static_cast<std::uint32_t>(bs.tail.BM()), true);
+        const CUtensorMap kmap_t = bs.tail.bns == bs.main.bns
+                                       ? kmap
+                                       : make_map(direct2 ? kb.fac[0] : krp, static_cast<std::uint64_t>(Rs2),
+                                                  static_cast<std::uint64_t>(B),
+                                                  static_cast<std::uint32_t>(bs.tail.bns), kBK, false);
+        dispatch<false, false>(bs.tail, st, xmap_t, kmap_t, to_dev(kb), mt, B, R, ws, mt * R);
+        const long long n = mt * static_cast<long long>(R);
+        const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
+        splitk_reduce_kernel<<<blocks, 256, 0, st>>>(ws, bs.tail.splits, n, pf + bs.rows_main * R);
+        count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+        return;
+    }
+    const GemmPlan& p = bs.main;
     const int Rs = (R + 1) & ~1;
     // a one-mode Khatri-Rao operand is the factor itself: map it directly (R even:
     // 16-byte row stride), no workspace fill
@@ -838,7 +900,15 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
 }
 
 std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R) {
-    const GemmPlan p = plan_gemm(F, B, R, false);
+    std::size_t w = 0;
+    for (int reserve = 0; reserve <= 1; ++reserve) {
+        const BackSplit bs = plan_back(F, B, R, reserve);
+        if (bs.rows_main < F) w = std::max<std::size_t>(w, static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R);
+    }
+    if (w) return w;
+    const BackSplit bs = plan_back(F, B, R, 0);
+    if (bs.rows_main < F) return static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R;
+    const GemmPlan& p = bs.main;
     return p.splits > 1 ? static_cast<std::size_t>(p.splits) * F * R : 0;
 }
 

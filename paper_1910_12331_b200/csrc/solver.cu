@@ -638,7 +638,7 @@ void DeviceProblem::root_back() {
     const int N = order();
     prof_begin(kProfBack);
     launch_root_back(x_.get(), F_, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get(), ws_.get(),
-                     ws_.size(), ctx_.stream);
+                     ws_.size(), ctx_.stream, side_busy_ ? 1 : 0);
     prof_end();
     ++contractions_;
     pf_valid_ = true;
@@ -704,7 +704,7 @@ void DeviceProblem::root_single(int c) {
         kc.fac[0] = A_.get() + off_[c];
         const std::int64_t rows = local_rows_[1 - c] * Bl_;
         launch_root_back(c == 0 ? X0_.get() : X1_.get(), rows, local_rows_[c], c == 0 ? ld0_ : ld1_, R_, kc,
-                         krp_.get(), PM_.get(), ws_.get(), ws_.size(), ctx_.stream);
+                         krp_.get(), PM_.get(), ws_.get(), ws_.size(), ctx_.stream, side_busy_ ? 1 : 0);
     } else {
         launch_root_single(x_.get(), local_rows_[0], local_rows_[1], Bl_, Bs_, c, A_.get() + off_[c], R_, PM_.get(),
                            ws_.get(), ws_.size(), ctx_.stream);
@@ -1091,8 +1091,10 @@ void DeviceProblem::als_sweep_body(double lambda) {
         launch_chol_batch_src(gam_.get() + n * RR, grams_.get(), N, n, 1, R_, &lambda, 0, chol_.get() + n * LDR,
                               status_.get() + n, ctx_.aux);
         CPK_CUDA(cudaEventRecord(ctx_.ev[3 + 2 * n], ctx_.aux));
+        side_busy_ = true;
         if (msdt_) mttkrp_msdt(n);
         else mttkrp(n);
+        side_busy_ = false;
         CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[3 + 2 * n], 0));
         const std::int64_t rows = static_cast<std::int64_t>(dims_[n]);
         // A_n <- M_n (Gamma + lambda I)^-1 in place; the step norm from per-row partials
@@ -1313,7 +1315,9 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     pinv_lambda_ = next.lambda;
     pinv_shape_ = shape;
     // residual_after from the next iteration's tree pass (cached for the next step)
+    side_busy_ = true;
     compute_all_mttkrp();
+    side_busy_ = false;
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));  // Grams
     residual_launch(xnorm2);
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);

@@ -341,6 +341,8 @@ private:
     // the next two mode updates, so a sweep pair needs 3 roots instead of 4.
     bool msdt_ = false;
     int pm_mode_ = -1;
+    // a side-stream SPD factorisation is in flight: roots leave it one SM
+    bool side_busy_ = false;
     DevBuf<double> PM_;
     // Mode-permuted copies of the local tensor, X^(0)[i1][i2][i0] and
     // X^(1)[i0][i2][i1] (row strides ld0_/ld1_, even for TMA), made once per

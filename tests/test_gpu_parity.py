@@ -53,6 +53,22 @@ def test_mttkrp_tree_matches_oracle(orc, ck, dims, rank):
     assert p.full_contractions == ref_cnt <= 2
 
 
+# Back roots with more tiles than one wave and a partial last wave: the last
+# wave's rows run as a separate split-K launch (fixed-order reduce). Results
+# match the oracle, repeat bitwise, and agree with the single launch.
+@pytest.mark.parametrize("dims,rank", [([160, 130, 30], 24), ([150, 200, 40], 100), ([40, 500, 36], 50)])
+def test_root_tail_launch(orc, ck, dims, rank, monkeypatch):
+    x = np.random.default_rng(rank).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 21)
+    ref, _ = orc.mttkrp_tree_all(x, f)
+    p = make(ck, x, f)
+    a = p.mttkrp_naive(0)
+    assert rel_err(a, ref[0]) < KTOL
+    assert np.array_equal(a, p.mttkrp_naive(0))
+    monkeypatch.setenv("CPKIT_NO_TAIL_LAUNCH", "1")
+    assert rel_err(p.mttkrp_naive(0), a) < 1e-13
+
+
 @pytest.mark.parametrize("dims,rank", [([3, 4, 2], 3), ([6, 5, 4, 3], 5), ([30, 20, 10], 9)])
 def test_mttkrp_naive_and_unfolding(orc, ck, dims, rank):
     x = gauss_tensor(orc, dims, 5) if np.prod(dims) < 5000 else \
