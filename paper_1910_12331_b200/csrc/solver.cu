@@ -392,6 +392,18 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
         // without copies the single-mode roots are TN GEMMs with the factor as the B operand
         msdt_ = msdt_copies_ || (R_ % 2 == 0 && Bs_ == Bl_);
     }
+    if (N >= 4) {
+        std::size_t free_b = 0, total_b = 0;
+        CPK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        ldT_ = (F_ + 1) & ~1LL;
+        const double copy_b = 8.0 * static_cast<double>(Bl_) * static_cast<double>(ldT_);
+        const char* ce = std::getenv("CPKIT_FRONT_COPY");
+        front_copy_ = ce ? std::atoi(ce) != 0 : copy_b + 8.0 * static_cast<double>(local_elems_) < 0.5 * free_b;
+        if (front_copy_) {
+            XT_.resize(static_cast<std::size_t>(Bl_ * ldT_));
+            CPK_CUDA(cudaMemset(XT_.get(), 0, XT_.size() * sizeof(double)));  // stride padding stays zero
+        }
+    }
     if (msdt_)
         PM_.resize(static_cast<std::size_t>(std::max(local_rows_[0], local_rows_[1])) * Bl_ * R_);
     if (msdt_copies_) {
@@ -406,6 +418,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
         KrpDesc kf = krp(0, h_, A_.get(), false), kb = krp(h_, N, A_.get(), true);
         for (int n = 0; n < h_; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kf, n, R_));
         for (int n = h_; n < N; ++n) ws = std::max(ws, reduce_kept_workspace_elems(kb, n - h_, R_));
+        if (front_copy_) ws = std::max(ws, root_back_workspace_elems(Bl_, F_, R_));
         if (msdt_copies_) {
             ws = std::max(ws, root_back_workspace_elems(local_rows_[1] * Bl_, local_rows_[0], R_));
             ws = std::max(ws, root_back_workspace_elems(local_rows_[0] * Bl_, local_rows_[1], R_));
@@ -490,6 +503,8 @@ void DeviceProblem::upload_tensor(const double* host_local) {
     invalidate_all();
 }
 void DeviceProblem::build_msdt_copies() {
+    if (front_copy_)  // X^T [B_local][F]
+        launch_transpose_batched(x_.get(), 1, F_, Bl_, Bs_, 0, XT_.get(), ldT_, 0, ctx_.stream);
     if (!msdt_copies_) return;
     const std::int64_t s0 = local_rows_[0], s1 = local_rows_[1];
     // X^(0)[i1][i2][i0]: batch i1, rows i0 (stride s1 Bs), cols i2
@@ -645,8 +660,12 @@ void DeviceProblem::root_back() {
 }
 void DeviceProblem::root_front() {
     prof_begin(kProfFront);
-    launch_root_front(x_.get(), F_, Bl_, Bs_, R_, krp(0, h_, A_.get(), false), krp_.get(), PB_.get(), ws_.get(),
-                      ws_.size(), ctx_.stream);
+    if (front_copy_)  // P_B = X^T KRP_F on the transposed copy: the back root's NN GEMM
+        launch_root_back(XT_.get(), Bl_, F_, ldT_, R_, krp(0, h_, A_.get(), false), krp_.get(), PB_.get(), ws_.get(),
+                         ws_.size(), ctx_.stream, side_busy_ ? 1 : 0);
+    else
+        launch_root_front(x_.get(), F_, Bl_, Bs_, R_, krp(0, h_, A_.get(), false), krp_.get(), PB_.get(), ws_.get(),
+                          ws_.size(), ctx_.stream);
     prof_end();
     ++contractions_;
     pb_valid_ = true;

@@ -351,7 +351,12 @@ private:
     bool msdt_copies_ = false;
     std::int64_t ld0_ = 0, ld1_ = 0;
     DevBuf<double> X0_, X1_;
-    void build_msdt_copies();
+    // Order >= 4: X^T [B_local][F] (row stride ldT_) when memory allows, so the
+    // front root P_B = X^T KRP_F runs as the NN GEMM instead of the TN one.
+    bool front_copy_ = false;
+    std::int64_t ldT_ = 0;
+    DevBuf<double> XT_;
+    void build_msdt_copies();  // every layout copy of the tensor (MSDT copies, X^T)
     bool grams_valid_ = false;
     bool defer_coll_ = false;  // compute_all_mttkrp batches the collectives
     double* hpin_ = nullptr;  // pinned host slots for scalar readbacks  // grams_ == gram(A_n) for every n (skips recomputation; same values)

@@ -69,6 +69,21 @@ def test_root_tail_launch(orc, ck, dims, rank, monkeypatch):
     assert rel_err(p.mttkrp_naive(0), a) < 1e-13
 
 
+# Orders >= 4 run the front root on a transposed tensor copy (NN GEMM) when
+# memory allows; the TN kernel on X itself stays covered with the copy off.
+@pytest.mark.parametrize("copy", ["0", "1"])
+@pytest.mark.parametrize("dims,rank", [([6, 5, 7, 9], 6), ([17, 19, 23, 11], 7), ([3, 2, 2, 3, 2], 2)])
+def test_front_root_copy_and_tn(orc, ck, dims, rank, copy, monkeypatch):
+    monkeypatch.setenv("CPKIT_FRONT_COPY", copy)
+    x = np.random.default_rng(sum(dims)).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 31)
+    ref, ref_cnt = orc.mttkrp_tree_all(x, f)
+    p = make(ck, x, f)
+    for n in range(len(dims)):
+        assert rel_err(p.mttkrp(n), ref[n]) < KTOL, n
+    assert p.full_contractions == ref_cnt
+
+
 @pytest.mark.parametrize("dims,rank", [([3, 4, 2], 3), ([6, 5, 4, 3], 5), ([30, 20, 10], 9)])
 def test_mttkrp_naive_and_unfolding(orc, ck, dims, rank):
     x = gauss_tensor(orc, dims, 5) if np.prod(dims) < 5000 else \
