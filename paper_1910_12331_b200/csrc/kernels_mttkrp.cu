@@ -607,13 +607,22 @@ long long best_splits(long long base, long long slots, long long K, double* eff_
     const long long kchunks = (K + kBK - 1) / kBK;
     long long best = 1;
     double best_eff = -1.0;
+    // Fewer tiles than one wave (e.g. C4's 79 row tiles): splits may go up to
+    // 8 waves, each split's extra output pass (read by the fixed-order reduce,
+    // ~24 sp / K of the GEMM's time) charged against its wave efficiency.
+    // Otherwise at most 2 waves (the NN root's partial last wave is handled by
+    // a separate tail launch, plan_back).
+    const long long max_waves = base < slots ? 8 : std::max<long long>(2, (base + slots - 1) / slots);
+    double best_score = -1.0;
     for (long long sp = 1; sp <= 64; ++sp) {
         if (sp > 1 && kchunks / sp < min_chunks) break;
         const long long ctas = base * sp;
         const long long waves = (ctas + slots - 1) / slots;
-        if (sp > 1 && waves > std::max<long long>(2, (base + slots - 1) / slots)) break;
+        if (sp > 1 && waves > max_waves) break;
         const double eff = static_cast<double>(ctas) / static_cast<double>(waves * slots);
-        if (eff > best_eff + 1e-9) {
+        const double score = base < slots && sp > 1 ? eff / (1.0 + 24.0 * static_cast<double>(sp) / K) : eff;
+        if (score > best_score + 1e-9) {
+            best_score = score;
             best_eff = eff;
             best = sp;
         }
