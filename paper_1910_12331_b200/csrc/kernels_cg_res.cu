@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             break;
         }
         const double alpha = rz / wq;
+        r_stamp(d, vb, it, 9);
         if (has) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -553,8 +554,11 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                 }
             }
             form_rows(p.Rr[rc], p.Q, -alpha, Rg, nullptr, nullptr);
+            r_stamp(d, vb, it, 10);
             phase_c_tail();
+            r_stamp(d, vb, it, 11);
             z_partial();
+            r_stamp(d, vb, it, 12);
         }
         rc ^= 1;
         r_stamp(d, vb, it, 6);

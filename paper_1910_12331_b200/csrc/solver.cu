@@ -1062,11 +1062,10 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gno
             for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %6.2f", dt(it, k - 1, k));
             if (it + 1 < 64 && h[(it + 1) * 16])
                 std::fprintf(stderr, " | next %6.2f", (static_cast<double>(h[(it + 1) * 16]) - static_cast<double>(h[it * 16 + 7])) * 1e-3);
-            if (h[it * 16 + 9])
-                std::fprintf(stderr, " | B stage %5.2f mma %5.2f epi %5.2f | wq %5.2f C pre %5.2f stage %5.2f mma %5.2f epi %5.2f",
-                             dt(it, 3, 9), dt(it, 9, 10), dt(it, 10, 11), dt(it, 5, 8), dt(it, 8, 15), dt(it, 15, 12),
-                             dt(it, 12, 13), dt(it, 13, 14));
-            else if (h[it * 16 + 8])
+            if (h[it * 16 + 12])
+                std::fprintf(stderr, " | C wq %5.2f rows %5.2f tail %5.2f zpart %5.2f", dt(it, 5, 9), dt(it, 9, 10),
+                             dt(it, 10, 11), dt(it, 11, 12));
+            if (h[it * 16 + 8])
                 std::fprintf(stderr, " | A2 work %5.2f", dt(it, 2, 8));
             std::fprintf(stderr, " us\n");
         }
