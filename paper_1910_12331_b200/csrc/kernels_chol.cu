@@ -22,6 +22,7 @@
 #include <cstdlib>
 
 #include "common.h"
+#include "tile_gemm.cuh"
 
 namespace cpkit {
 
@@ -32,6 +33,17 @@ constexpr std::size_t kSmemBudget = 220 * 1024;
 #define CPKIT_CHOL_ABLATE 0  // timing experiments only: 1 skip diag, 2 skip panel, 4 skip update
 #endif
 constexpr int kCholAblate = CPKIT_CHOL_ABLATE;
+#ifndef CPKIT_CHOL_TRACE
+#define CPKIT_CHOL_TRACE 0  // timing experiments only: per-phase globaltimer stamps of CTA 0
+#endif
+__device__ unsigned long long g_chol_trace[64];
+__device__ __forceinline__ void chol_stamp(int k) {
+    if (CPKIT_CHOL_TRACE && blockIdx.x == 0 && threadIdx.x == 0 && k < 64) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_chol_trace[k] = t;
+    }
+}
 
 inline int lda_of(int R) { return R + 1; }
 
@@ -175,39 +187,44 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
 
 template <int kNB>
 __device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int kb) {
+    static_assert(kNB % 2 == 0 && kNB <= 32, "diagonal block: even width, one warp");
+    __shared__ __align__(16) double colb[32];  // column j of L, broadcast to the warp
     __syncwarp();
     const int i = threadIdx.x & 31;
     double r[kNB];
 #pragma unroll
     for (int m = 0; m < kNB; ++m) r[m] = (i < kb && m <= i) ? w[(k0 + i) * LD + k0 + m] : 0.0;
     bool failed = false;
-    // the pivot of the next column, computed by its own lane from its own row
-    // (the same fma the row update applies, so bitwise the same value): the
-    // column-to-column chain is shuffle -> rsqrt -> scale -> fma -> shuffle
-    double nextp = r[0];
+    // The pivot of the next column is computed by its own lane from its own row
+    // (the same fma as the row update, so bitwise the same value) and shuffled
+    // right away, so the column-to-column chain is shuffle -> rsqrt -> scale ->
+    // fma -> shuffle with the rank-1 update off it. The update reads column j
+    // from shared memory (one warp-wide store, vector loads) and runs
+    // unpredicated: entries above the diagonal, rows >= kb and every update
+    // after a failed pivot are never stored or read as results.
+    double x = __shfl_sync(0xffffffffu, r[0], 0);
 #pragma unroll
     for (int j = 0; j < kNB; ++j) {
-        const double x = __shfl_sync(0xffffffffu, nextp, j);
+        if (CPKIT_CHOL_TRACE && k0 == 0 && blockIdx.x == 0 && i == 0) g_chol_trace[24 + j] = clock64();
         if (j < kb && !failed && !(x > 0.0) && !isnan(x)) failed = true;  // Eigen LLT: fail iff pivot <= 0
-        const bool go = j < kb && !failed;
-        // one reciprocal square root on the critical path (L_jj = x / sqrt(x))
-        const double inv = rsqrt_pos(x > 0.0 ? x : 1.0), l = x * inv;
-        double lij = r[j];
-        if (go && i > j) lij = r[j] * inv;
-        if (go && i == j) {
-            lij = l;
-            w[(k0 + j) * LD + R] = inv;
-        }
+        const double inv = rsqrt_pos(x > 0.0 ? x : 1.0), l = x * inv;  // L_jj = x / sqrt(x)
+        const double lij = i > j ? r[j] * inv : (i == j ? l : r[j]);
+        if (j + 1 < kNB) x = __shfl_sync(0xffffffffu, __fma_rn(-lij, lij, r[j + 1]), j + 1);
+        if (i == j && j < kb && !failed) w[(k0 + j) * LD + R] = inv;
         r[j] = lij;
-        if (j + 1 < kNB) nextp = (go && i >= j + 1) ? __fma_rn(-lij, lij, r[j + 1]) : r[j + 1];
+        if (j + 1 < kNB) {
+            colb[i] = lij;
+            __syncwarp();
 #pragma unroll
-        for (int m = 0; m < kNB; ++m) {
-            if (m > j) {
-                const double lmj = __shfl_sync(0xffffffffu, lij, m);
-                if (go && i >= m) r[m] = __fma_rn(-lij, lmj, r[m]);
+            for (int m = (j + 1) & ~1; m < kNB; m += 2) {
+                const double2 c = *reinterpret_cast<const double2*>(colb + m);
+                if (m > j) r[m] = __fma_rn(-lij, c.x, r[m]);
+                if (m + 1 > j) r[m + 1] = __fma_rn(-lij, c.y, r[m + 1]);
             }
+            __syncwarp();
         }
     }
+    if (CPKIT_CHOL_TRACE && k0 == 0 && blockIdx.x == 0 && i == 0) g_chol_trace[24 + kNB] = clock64();
 #pragma unroll
     for (int m = 0; m < kNB; ++m)
         if (i < kb && m <= i) w[(k0 + i) * LD + k0 + m] = r[m];
@@ -246,6 +263,7 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
     __shared__ int fail_sh;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
 
+    chol_stamp(0);
     int st = 2;
     for (int attempt = 0; attempt < 2; ++attempt) {
         double jitter = 0.0;
@@ -265,54 +283,60 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
         }
         const double add = (mode == 0 ? lambda : 0.0);
         {
-            const int total = R * R;  // 16 elements (up to 32 loads) in flight per thread, then shared stores
-            for (int e0 = tid; e0 < total; e0 += 16 * blockDim.x) {
-                double v[16];
-                if (!src.grams) {
+            // lower triangle straight into shared memory (async 8-byte copies, all
+            // in flight); for Gamma the first Gram factor, the others multiplied in
+            // after, in ascending mode order (bitwise gamma_excl's 1 * S_a * S_b ...)
+            int first = -1;
+            if (src.grams)
+                for (int m = 0; m < src.order && first < 0; ++m)
+                    if (m != src.excl) first = m;
+            const double* s0 = src.grams ? (first >= 0 ? src.grams + first * rr : nullptr) : s;
+            if (s0) {
+                for (int i = warp; i < R; i += nw)
+                    for (int k = lane; k <= i; k += 32) tile::cp_async8(w + i * LD + k, s0 + i * R + k);
+            } else {  // order 1 (no other mode): Gamma = Ones
+                for (int i = warp; i < R; i += nw)
+                    for (int k = lane; k <= i; k += 32) w[i * LD + k] = 1.0;
+            }
+            tile::cp_async_wait_all();
+            __syncthreads();
+            if (src.grams && first >= 0) {
+                for (int m = first + 1; m < src.order; ++m) {
+                    if (m == src.excl) continue;
+                    const double* sm = src.grams + m * rr;
+                    for (int i = warp; i < R; i += nw) {
+                        double f[4];
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const int e = e0 + u * blockDim.x;
-                        v[u] = (e < total) ? __ldg(s + e) : 0.0;
-                    }
-                } else {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) v[u] = 1.0;
-                    for (int m = 0; m < src.order; ++m) {
-                        if (m == src.excl) continue;
-                        double f[16];
-#pragma unroll
-                        for (int u = 0; u < 16; ++u) {
-                            const int e = e0 + u * blockDim.x;
-                            f[u] = (e < total) ? __ldg(src.grams + m * rr + e) : 1.0;
+                        for (int c = 0; c < 4; ++c) {
+                            const int k = lane + 32 * c;
+                            f[c] = k <= i ? __ldg(sm + i * R + k) : 1.0;
                         }
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) v[u] *= f[u];
+                        for (int c = 0; c < 4; ++c)
+                            if (lane + 32 * c <= i) w[i * LD + lane + 32 * c] *= f[c];
+                        for (int k = lane + 128; k <= i; k += 32) w[i * LD + k] *= __ldg(sm + i * R + k);
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int e = e0 + u * blockDim.x;
-                    if (e < total) {
-                        const int i = e / R, k = e - i * R;
-                        double x = v[u];
-                        if (i == k) {
-                            if (mode == 1) x *= (1.0 + lambda);
-                            x += add;
-                            if (attempt == 1) x += jitter;
-                        }
-                        if (k <= i) w[i * LD + k] = x;
-                    }
-                }
+                __syncthreads();
+            }
+            for (int i = tid; i < R; i += blockDim.x) {  // the diagonal: shape, lambda, jitter
+                double x = w[i * LD + i];
+                if (mode == 1) x *= (1.0 + lambda);
+                x += add;
+                if (attempt == 1) x += jitter;
+                w[i * LD + i] = x;
             }
         }
         if (tid == 0) fail_sh = 0;
         __syncthreads();
+        chol_stamp(1);
         for (int k0 = 0; k0 < R; k0 += kNB) {
             const int kb = min(kNB, R - k0);
             // 1. diagonal block (warp 0): lane i holds row i in registers; per column
             //    the pivot and every L_mj travel by shuffle (no shared-memory round trips)
             if (!(kCholAblate & 1) && warp == 0 && diag_factor<kNB>(w, LD, R, k0, kb)) fail_sh = 1;
             __syncthreads();
+            chol_stamp(2 + 3 * (k0 / kNB));
             if (fail_sh) break;
             // 2. panel: L[i][k0+j] = (A[i][k0+j] - sum_{m<j} L[i][k0+m] L[k0+j][k0+m]) / L_jj,
             //    one thread per row, the row in registers, two partial sums per dot
@@ -340,6 +364,7 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
                     if (m < kb) row[m] = x[m];
             }
             __syncthreads();
+            chol_stamp(3 + 3 * (k0 / kNB));
             // 3. trailing update: A[i][m] -= sum_j L[i][k0+j] L[m][k0+j], k0+kb <= m <= i.
             //    Full 16-column blocks: one DMMA m16n8k16 per 16x8 tile on or below the
             //    diagonal (rows and columns past R read zero-padded... masked); tail block scalar.
@@ -391,6 +416,7 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
                 }
             }
             __syncthreads();
+            chol_stamp(4 + 3 * (k0 / kNB));
         }
         if (!fail_sh) {
             st = attempt;  // 0 ok, 1 ok after jitter
@@ -398,11 +424,20 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
         }
         __syncthreads();
     }
-    for (int i = warp; i < R; i += nw) {
-        for (int k = lane; k <= i; k += 32) out[i * LD + k] = w[i * LD + k];
-        if (lane == 0) out[i * LD + R] = w[i * LD + R];
+    // the factor (same R x (R+1) layout as in shared memory) in one bulk copy
+    __syncthreads();
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out),
+                     "r"(static_cast<unsigned>(__cvta_generic_to_shared(w))),
+                     "r"(static_cast<unsigned>(R * LD * sizeof(double)))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        status[mat] = st;
     }
-    if (tid == 0) status[mat] = st;
+    __syncthreads();
+    chol_stamp(63);
 }
 
 // One warp per rhs row: solve (L L^T) y = b. L lower, row stride LD (global),
@@ -595,6 +630,22 @@ __global__ void symmetrize_kernel(const double* __restrict__ y, int count, int R
 
 std::size_t chol_factor_elems(int count, int R) { return static_cast<std::size_t>(count) * R * lda_of(R); }
 
+void print_chol_trace() {  // timing experiments only (CPKIT_CHOL_TRACE builds)
+    unsigned long long h[64];
+    CPK_CUDA(cudaDeviceSynchronize());
+    CPK_CUDA(cudaMemcpyFromSymbol(h, g_chol_trace, sizeof h));
+    std::fprintf(stderr, "chol: load %.2f us |", (h[1] - h[0]) * 1e-3);
+    unsigned long long prev = h[1];
+    for (int b = 0; b < 20 && h[4 + 3 * b]; ++b) {
+        std::fprintf(stderr, " [%d] diag %.2f panel %.2f trail %.2f", b, (h[2 + 3 * b] - prev) * 1e-3,
+                     (h[3 + 3 * b] - h[2 + 3 * b]) * 1e-3, (h[4 + 3 * b] - h[3 + 3 * b]) * 1e-3);
+        prev = h[4 + 3 * b];
+    }
+    std::fprintf(stderr, " | out %.2f | total %.2f us\n", (h[63] - prev) * 1e-3, (h[63] - h[0]) * 1e-3);
+    std::fprintf(stderr, "chol diag block 0 cycles per column:");
+    for (int j = 0; j < 16; ++j) std::fprintf(stderr, " %llu", h[25 + j] - h[24 + j]);
+    std::fprintf(stderr, "\n");
+}
 void launch_chol_batch(const double* s, int count, int R, const double* lambda, int mode, double* l_out, int* status,
                        cudaStream_t st) {
     launch_chol_batch_src(const_cast<double*>(s), nullptr, 0, -1, count, R, lambda, mode, l_out, status, st);
@@ -637,6 +688,7 @@ void launch_chol_batch_src(double* s, const double* grams, int order, int excl, 
     }
     count_launch(1);
     CPK_CUDA(cudaGetLastError());
+    if (CPKIT_CHOL_TRACE) print_chol_trace();
 }
 
 void launch_chol_solve_rows(const double* l, int R, const double* b, std::int64_t rows, double* y, cudaStream_t st) {
