@@ -312,16 +312,19 @@ Context::Context(int dev) : device(dev) {
     CPK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     const char* pe = std::getenv("CPKIT_AUX_PRIORITY");
     CPK_CUDA(cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, (pe && std::atoi(pe) == 0) ? lo : hi));
+    CPK_CUDA(cudaStreamCreateWithFlags(&aux2, cudaStreamNonBlocking));
     for (auto& e : ev) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
 Context::~Context() {
     comm.reset();
     for (auto& e : ev)
         if (e) cudaEventDestroy(e);
+    if (aux2) cudaStreamDestroy(aux2);
     if (aux) cudaStreamDestroy(aux);
     if (stream) cudaStreamDestroy(stream);
 }
 void Context::sync() const {
+    CPK_CUDA(cudaStreamSynchronize(aux2));
     CPK_CUDA(cudaStreamSynchronize(aux));
     CPK_CUDA(cudaStreamSynchronize(stream));
 }
@@ -436,6 +439,12 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
         }
     }
     ws_.resize(std::max<std::size_t>(ws, 1));
+    {
+        KrpDesc kf = krp(0, h_, A_.get(), false);
+        std::size_t wr = 1;
+        for (int n = 0; n < h_; ++n) wr = std::max(wr, reduce_kept_workspace_elems(kf, n, R_));
+        ws_red_.resize(wr);
+    }
     grams_.resize(N * RR);
     pair_.resize(static_cast<std::size_t>(N) * N * RR);
     gam_.resize(N * RR);
@@ -670,16 +679,20 @@ void DeviceProblem::root_front() {
     ++contractions_;
     pb_valid_ = true;
 }
-void DeviceProblem::second_level_back(int mode) {
+void DeviceProblem::second_level_back(int mode, cudaStream_t st, double* ws, std::size_t ws_elems) {
+    if (!st) {
+        st = ctx_.stream;
+        ws = ws_.get();
+        ws_elems = ws_.size();
+    }
     double* out = M_.get() + off_[mode];
     if (h_ == 1) {
         CPK_CUDA(cudaMemcpyAsync(out, PF_.get(), static_cast<std::size_t>(F_) * R_ * sizeof(double),
-                                 cudaMemcpyDeviceToDevice, ctx_.stream));
+                                 cudaMemcpyDeviceToDevice, st));
     } else {
-        launch_reduce_kept(PF_.get(), krp(0, h_, A_.get(), false), mode, R_, out, ws_.get(), ws_.size(),
-                           ctx_.stream);
+        launch_reduce_kept(PF_.get(), krp(0, h_, A_.get(), false), mode, R_, out, ws, ws_elems, st);
     }
-    if (ctx_.comm && !defer_coll_) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, ctx_.stream);
+    if (ctx_.comm && !defer_coll_) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, st);
 }
 void DeviceProblem::second_level_front(int mode) {
     const int N = order();
@@ -829,11 +842,29 @@ void DeviceProblem::compute_all_mttkrp() {
         if (msdt_copies_) {
             // order 3: M^(0), M^(1) from the back root X A_2; M^(2) from the
             // single-mode root X x_1 A_1 (NN GEMM on the permuted copy, then the
-            // i0 contraction) instead of the Khatri-Rao front root
-            mttkrp(0);
-            mttkrp(1);
-            if (pm_mode_ != 1) root_single(1);
-            second_level_pm(2);
+            // i0 contraction) instead of the Khatri-Rao front root. The two
+            // HBM-bound reduces of X A_2 run on a third stream beside the
+            // DMMA-bound second root (own workspace; collectives deferred).
+            if (!pf_valid_) root_back();
+            const bool beside = pm_mode_ != 1 && !std::getenv("CPKIT_NO_REDUCE_OVERLAP");
+            if (beside) {
+                CPK_CUDA(cudaEventRecord(ctx_.ev[2 * kMaxOrder + 2], ctx_.stream));
+                CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[2 * kMaxOrder + 2], 0));
+                const bool dc = defer_coll_;
+                defer_coll_ = true;  // a sharded run reduces every block after the pass anyway
+                second_level_back(0, ctx_.aux2, ws_red_.get(), ws_red_.size());
+                second_level_back(1, ctx_.aux2, ws_red_.get(), ws_red_.size());
+                defer_coll_ = dc;
+                CPK_CUDA(cudaEventRecord(ctx_.ev[2 * kMaxOrder + 3], ctx_.aux2));
+                root_single(1);
+                second_level_pm(2);
+                CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[2 * kMaxOrder + 3], 0));
+            } else {
+                mttkrp(0);
+                mttkrp(1);
+                if (pm_mode_ != 1) root_single(1);
+                second_level_pm(2);
+            }
         } else {
             for (int n = 0; n < N; ++n) mttkrp(n);
         }

@@ -157,7 +157,8 @@ struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // side stream: SPD factorisations overlap the MTTKRP
-    static constexpr int kEvents = 2 * kMaxOrder + 2;
+    cudaStream_t aux2 = nullptr;  // second-level reduces beside the next root GEMM (GN tree pass)
+    static constexpr int kEvents = 2 * kMaxOrder + 4;
     cudaEvent_t ev[kEvents] = {};
     std::unique_ptr<Comm> comm;  // null: single GPU
     explicit Context(int dev);
@@ -378,7 +379,8 @@ private:
     KrpDesc krp(int lo, int hi, const double* base, bool local_last) const;
     void root_back();
     void root_front();
-    void second_level_back(int mode);
+    void second_level_back(int mode, cudaStream_t st = nullptr, double* ws = nullptr, std::size_t ws_elems = 0);
+    DevBuf<double> ws_red_;  // reduce workspace of the reduces run beside a root (aux2)
     void second_level_front(int mode);
     void root_single(int c);          // P_c into PM_ (c in {0, 1})
     void second_level_pm(int mode);   // M^(mode) from PM_
