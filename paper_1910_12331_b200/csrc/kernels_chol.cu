@@ -518,6 +518,7 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
 #pragma unroll
         for (int cb = 0; cb < NB; ++cb) {
             const int iend = min(32, R - 32 * cb);
+#pragma unroll 4
             for (int il = 0; il < iend; ++il) {
                 const int i = 32 * cb + il;
                 const double zi = __shfl_sync(0xffffffffu, v[cb], il) * Linv(i);
@@ -534,6 +535,7 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
 #pragma unroll
         for (int cb = NB - 1; cb >= 0; --cb) {
             const int iend = min(32, R - 32 * cb);
+#pragma unroll 4
             for (int il = iend - 1; il >= 0; --il) {
                 const int i = 32 * cb + il;
                 const double yi = __shfl_sync(0xffffffffu, v[cb], il) * Linv(i);
