@@ -126,8 +126,10 @@ int norm2_parts(std::uint64_t n);
 // grams of modes [lo, hi): factor n at base + offs[n] (device arrays), rows[n];
 // ws holds gram_workspace_elems(hi - lo, R, max rows) doubles.
 std::size_t gram_workspace_elems(int nmodes, int R, std::int64_t smax);
+// sq != null: the first CTA also adds sqrt(sum of sq[0..nsq)) to *sq_acc (ALS step norm)
 void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
-                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st);
+                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st,
+                  const double* sq = nullptr, int nsq = 0, double* sq_acc = nullptr);
 // pair[(n*order+p)] = Hadamard over grams m not in {n,p} ascending (kruskal.cpp:42-65)
 void launch_gamma_pairs(const double* grams, int order, int R, double* pair, cudaStream_t st);
 // gamma_one = Hadamard over grams m != n (als.cpp:34-37)

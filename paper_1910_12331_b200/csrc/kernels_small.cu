@@ -70,8 +70,14 @@ constexpr int kGramChunk = 64;
 __global__ void __launch_bounds__(tile::kThreads)
 gram_tiles_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
                   const long long* __restrict__ rows, int lo, int nmodes, int R, int nsplit,
-                  double* __restrict__ partial) {
+                  double* __restrict__ partial, const double* __restrict__ sq, int nsq, double* sq_acc) {
     __shared__ tile::Smem sm;
+    if (sq && blockIdx.x == 0) {  // the ALS step norm: *sq_acc += sqrt(sum of the row partials)
+        double v = 0.0;
+        for (int i = threadIdx.x; i < nsq; i += blockDim.x) v += sq[i];
+        const double s = block_sum(v);
+        if (threadIdx.x == 0) *sq_acc += sqrt(s);
+    }
     const int tr = (R + tile::kT - 1) / tile::kT;
     const int tri = tr * (tr + 1) / 2;
     const int tasks = nmodes * tri * nsplit;
@@ -400,13 +406,14 @@ std::size_t gram_workspace_elems(int nmodes, int R, std::int64_t smax) {
     return static_cast<std::size_t>(nmodes) * gram_splits(smax) * R * R;
 }
 void launch_grams(const double* base, const std::int64_t* offs, const std::int64_t* rows, int lo,
-                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st) {
+                  int hi, int R, std::int64_t smax, double* ws, double* grams, cudaStream_t st, const double* sq,
+                  int nsq, double* sq_acc) {
     const int nsplit = gram_splits(smax);
     const int tr = (R + tile::kT - 1) / tile::kT;
     const int tasks = (hi - lo) * tr * (tr + 1) / 2 * nsplit;
     gram_tiles_kernel<<<std::min(tasks, 4 * 148), tile::kThreads, 0, st>>>(
         base, reinterpret_cast<const long long*>(offs), reinterpret_cast<const long long*>(rows), lo, hi - lo, R,
-        nsplit, ws); ::cpkit::count_launch(1);
+        nsplit, ws, sq, nsq, sq_acc); ::cpkit::count_launch(1);
     const long long total = static_cast<long long>(hi - lo) * R * R;
     gram_finalize_kernel<<<grid_for(total, 256, 592), 256, 0, st>>>(ws, lo, hi - lo, R, nsplit, grams); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());

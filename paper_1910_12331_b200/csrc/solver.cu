@@ -1149,10 +1149,10 @@ void DeviceProblem::als_sweep_body(double lambda) {
         // A_n <- M_n (Gamma + lambda I)^-1 in place; the step norm from per-row partials
         launch_chol_solve_rows_update(chol_.get() + n * LDR, R_, M_.get() + off_[n], rows, A_.get() + off_[n],
                                       partials_.get(), ctx_.stream);
-        launch_sqrt_add(partials_.get(), static_cast<int>(rows), scal_.get() + kStep, ctx_.stream);
         note_factor_update(n);
+        // Gram of the new factor; its first CTA also folds in this mode's step norm
         launch_grams(A_.get(), offs_dev_.get(), rows_dev_.get(), n, n + 1, R_, smax_, gram_ws_.get(), grams_.get(),
-                     ctx_.stream);
+                     ctx_.stream, partials_.get(), static_cast<int>(rows), scal_.get() + kStep);
     }
     (void)RR;
 }
