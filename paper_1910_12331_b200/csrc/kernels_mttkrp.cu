@@ -827,9 +827,10 @@ BackSplit plan_back(long long M, long long K, int R, int reserve_sms) {
     const GemmPlan& p = b.main;
     if (p.splits != 1 || p.ntiles != 1 || std::getenv("CPKIT_NO_TAIL_LAUNCH")) return b;
     const long long slots = static_cast<long long>(num_sms() - reserve_sms) * p.per_sm;
+    const long long all_slots = static_cast<long long>(num_sms()) * p.per_sm;  // the tail runs after: every SM
     const long long units = p.mtiles;
     const long long rem = units % slots;
-    if (units <= slots || rem == 0 || 2 * rem > slots) return b;
+    if (units <= slots || rem == 0 || 2 * rem > all_slots) return b;
     const long long rows_main = (units - rem) * p.BM();
     GemmPlan tail = plan_gemm(M - rows_main, K, R, false, 0, 3);
     if (tail.splits < 2) return b;
