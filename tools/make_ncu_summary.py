@@ -37,15 +37,16 @@ for r in rows[2:]:
         "grid": d.get("launch__grid_size"),
         "block": d.get("launch__block_size"),
     })
-# one back + one front launch (the capture holds naive mode-0 (back) and mode-h (front) roots)
-seen, pick = set(), []
-for k in kernels:
-    if k["kernel"] not in seen:
-        seen.add(k["kernel"])
-        pick.append(k)
-tr = [k["dram_read_bytes"] + k["dram_write_bytes"] for k in pick]
-summary = {"source": f"ncu --set full --clock-control none, tools/profile_roots.py (C2: 400^3, R=100) {label}",
-           "kernels": pick, "root_gemm_dram_bytes_per_launch": sum(tr) / len(tr)}
+# One root contraction = a main launch plus, when the tiles leave a partial last
+# wave, its split-K tail launch (plan_back). Traffic per contraction = all
+# captured root-kernel DRAM bytes / number of main launches (the long ones).
+longest = max(k["duration_s"] for k in kernels)
+mains = [k for k in kernels if k["duration_s"] >= 0.5 * longest]
+total = sum(k["dram_read_bytes"] + k["dram_write_bytes"] for k in kernels)
+summary = {"source": label or "ncu --set full --clock-control none (root GEMMs)",
+           "kernels": kernels,
+           "root_gemm_dram_bytes_per_launch": total / len(mains),
+           "note": "per root contraction (main launch + its split-K tail launch when present)"}
 with open(out, "w") as f:
     json.dump(summary, f, indent=1)
 print(json.dumps(summary, indent=1))
