@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 #include "tile_gemm.cuh"
@@ -70,7 +71,8 @@ constexpr int kGramChunk = 64;
 __global__ void __launch_bounds__(tile::kThreads)
 gram_tiles_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
                   const long long* __restrict__ rows, int lo, int nmodes, int R, int nsplit,
-                  double* __restrict__ partial, const double* __restrict__ sq, int nsq, double* sq_acc) {
+                  double* __restrict__ partial, const double* __restrict__ sq, int nsq, double* sq_acc,
+                  double* __restrict__ direct) {
     __shared__ tile::Smem sm;
     if (sq && blockIdx.x == 0) {  // the ALS step norm: *sq_acc += sqrt(sum of the row partials)
         double v = 0.0;
@@ -107,6 +109,21 @@ gram_tiles_kernel(const double* __restrict__ base, const long long* __restrict__
         tile::tile_gemm(sm, K, la, lb, acc);
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
         const int g = lane >> 2, t = lane & 3;
+        if (direct) {  // one split: the final symmetric Gram, mirrored bitwise
+            double* out = direct + static_cast<long long>(n) * R * R;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int r = r0 + (warp >> 2) * 16 + g + 8 * h;
+                    const int z = z0 + (warp & 3) * 8 + 2 * t + c;
+                    if (r < R && z < R && r <= z) {
+                        out[r * R + z] = acc[2 * h + c];
+                        out[z * R + r] = acc[2 * h + c];
+                    }
+                }
+            continue;
+        }
         double* out = partial + (static_cast<long long>(n - lo) * nsplit + sp) * R * R;
 #pragma unroll
         for (int h = 0; h < 2; ++h)
@@ -400,6 +417,7 @@ void launch_norm2(const double* x, std::uint64_t n, double* partials, int nparts
 }
 
 int gram_splits(std::int64_t smax) {
+    if (const char* e = std::getenv("CPKIT_GRAM_SPLITS")) return std::max(1, std::atoi(e));  // experiments
     return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(32, (smax + kGramChunk - 1) / kGramChunk)));
 }
 std::size_t gram_workspace_elems(int nmodes, int R, std::int64_t smax) {
@@ -413,9 +431,13 @@ void launch_grams(const double* base, const std::int64_t* offs, const std::int64
     const int tasks = (hi - lo) * tr * (tr + 1) / 2 * nsplit;
     gram_tiles_kernel<<<std::min(tasks, 4 * 148), tile::kThreads, 0, st>>>(
         base, reinterpret_cast<const long long*>(offs), reinterpret_cast<const long long*>(rows), lo, hi - lo, R,
-        nsplit, ws, sq, nsq, sq_acc); ::cpkit::count_launch(1);
-    const long long total = static_cast<long long>(hi - lo) * R * R;
-    gram_finalize_kernel<<<grid_for(total, 256, 592), 256, 0, st>>>(ws, lo, hi - lo, R, nsplit, grams); ::cpkit::count_launch(1);
+        nsplit, ws, sq, nsq, sq_acc, nsplit == 1 ? grams : nullptr);
+    ::cpkit::count_launch(1);
+    if (nsplit > 1) {
+        const long long total = static_cast<long long>(hi - lo) * R * R;
+        gram_finalize_kernel<<<grid_for(total, 256, 592), 256, 0, st>>>(ws, lo, hi - lo, R, nsplit, grams);
+        ::cpkit::count_launch(1);
+    }
     CPK_CUDA(cudaGetLastError());
 }
 
