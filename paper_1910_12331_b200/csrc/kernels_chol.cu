@@ -304,17 +304,27 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
                 for (int m = first + 1; m < src.order; ++m) {
                     if (m == src.excl) continue;
                     const double* sm = src.grams + m * rr;
-                    for (int i = warp; i < R; i += nw) {
-                        double f[4];
+                    // four rows per warp per round: 16 loads in flight per lane
+                    for (int i0 = warp; i0 < R; i0 += 4 * nw) {
+                        double f[4][4];
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            const int k = lane + 32 * c;
-                            f[c] = k <= i ? __ldg(sm + i * R + k) : 1.0;
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = i0 + q * nw;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                const int k = lane + 32 * c;
+                                f[q][c] = (i < R && k <= i) ? __ldg(sm + i * R + k) : 1.0;
+                            }
                         }
 #pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (lane + 32 * c <= i) w[i * LD + lane + 32 * c] *= f[c];
-                        for (int k = lane + 128; k <= i; k += 32) w[i * LD + k] *= __ldg(sm + i * R + k);
+                        for (int q = 0; q < 4; ++q) {
+                            const int i = i0 + q * nw;
+                            if (i >= R) break;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c)
+                                if (lane + 32 * c <= i) w[i * LD + lane + 32 * c] *= f[q][c];
+                            for (int k = lane + 128; k <= i; k += 32) w[i * LD + k] *= __ldg(sm + i * R + k);
+                        }
                     }
                 }
                 __syncthreads();
