@@ -141,6 +141,9 @@ void launch_residual(const double* m_last, const double* a_last, std::int64_t ro
 // G_n = A_n * Gamma(n,n) - M_n  (gauss_newton.cpp:81-94)
 void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
                      double* g, cudaStream_t st);
+// G for every mode in one launch (off: N + 1 stacked offsets, rows: N extents)
+void launch_gradient_all(const double* a, const double* pair, const double* m, const std::int64_t* off,
+                         const std::int64_t* rows, int order, int R, double* g, cudaStream_t st);
 // out = sum_n scale*||X_n||_F (per-block Frobenius norms, summed in block order)
 void launch_block_norm_sum(const double* x, const std::int64_t* offsets, int nblocks,
                            double* partials, double* out, double scale, cudaStream_t st);
@@ -216,6 +219,7 @@ struct CgParams {
     int cap = 0;
     int* result = nullptr;         // [iters, hit_cap, breakdown, nonfinite, final_buffer]
     unsigned long long* trace = nullptr;  // optional: CTA 0 phase timestamps (ns), 8 per iteration
+    bool barrier_zeroed = false;   // the caller guarantees barrier[] is zero (no memset before the launch)
 };
 void run_cg(const CgParams& p, int grid, cudaStream_t st);
 // tile-resident CG (kernels_cg_res.cu); false when the problem does not fit it

@@ -558,7 +558,7 @@ void run_cg(const CgParams& p, int grid, cudaStream_t st) {
     const Layout L0 = make_layout(p, grid);
     grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
     d.L = make_layout(p, grid);
-    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
+    if (!p.barrier_zeroed) CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
     launch_coop(d, grid, st);
 }
 
@@ -574,7 +574,7 @@ void launch_jtj_matvec(const CgParams& p, const double* w, double* u, cudaStream
     const Layout L0 = make_layout(p, grid);
     grid = std::max(1, std::min(grid, std::max(L0.tasksA, L0.tasksBC)));
     d.L = make_layout(p, grid);
-    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
+    if (!p.barrier_zeroed) CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
     launch_coop(d, grid, st);
 }
 

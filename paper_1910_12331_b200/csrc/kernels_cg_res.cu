@@ -687,7 +687,7 @@ bool run_cg_resident(const CgParams& p, cudaStream_t st) {
     d.L = bestL;
     const int grid = bestL.tasks;
     const std::size_t smem = static_cast<std::size_t>(bestL.smem) * sizeof(double);
-    CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
+    if (!p.barrier_zeroed) CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
     switch (kCands[best].mt * 10 + kCands[best].nt) {
         case 11: launch_res<1, 1>(d, grid, smem, st); break;
         case 12: launch_res<1, 2>(d, grid, smem, st); break;

@@ -226,45 +226,74 @@ __global__ void residual_final_kernel(const double* __restrict__ partials, int n
 }
 
 // G = A * Gamma - M   (s x R) (R x R), DMMA tiles with the subtraction in the epilogue
+// G = A Gamma(n,n) - M (gauss_newton.cpp:81-94) for one 32x32 output tile: the
+// A row panel and the Gamma column slice staged with cp.async (one round trip
+// per panel of kPB columns), DMMA tiles
+__device__ __forceinline__ void gradient_tile(const double* __restrict__ a, const double* __restrict__ gnn,
+                                              const double* __restrict__ m, long long rows, int R,
+                                              double* __restrict__ g, long long task, double* gsm) {
+    using namespace tile;
+    const int tr = (R + kT - 1) / kT;
+    double* As = gsm;
+    double* Bs = gsm + kT * (kPB + 4);
+    const long long i0 = (task / tr) * kT;
+    const int c0 = static_cast<int>(task % tr) * kT;
+    const int vr = static_cast<int>(min(static_cast<long long>(kT), rows - i0)), vc = min(kT, R - c0);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int k0 = 0; k0 < R; k0 += kPB) {
+        const int kp = min(kPB, R - k0), kpad = pad8(kp);
+        stage_rows<32>(As, kPB + 4, kT, kpad, kp,
+                       [&](int row) { return row < vr ? a + (i0 + row) * R + k0 : nullptr; });
+        stage_rows<16>(Bs, kKS, kpad, kT, vc,
+                       [&](int k) { return k < kp ? gnn + static_cast<long long>(k0 + k) * R + c0 : nullptr; });
+        cp_async_wait_all();
+        __syncthreads();
+        mma_panel<false>(As, kPB + 4, Bs, kpad, acc);
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gg = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const long long i = i0 + (warp >> 2) * 16 + gg + 8 * h;
+            const int col = c0 + (warp & 3) * 8 + 2 * t + c;
+            if (i < rows && col < R) g[i * R + col] = acc[2 * h + c] - m[i * R + col];
+        }
+}
 __global__ void __launch_bounds__(tile::kThreads)
 gradient_kernel(const double* __restrict__ a, const double* __restrict__ gnn,
                 const double* __restrict__ m, long long rows, int R, double* __restrict__ g) {
-    // G = A Gamma(n,n) - M (gauss_newton.cpp:81-94): 32x32 output tiles, the A row
-    // panel and the Gamma column slice staged with cp.async (one round trip per
-    // panel of kPB columns), DMMA tiles
     extern __shared__ __align__(16) double gsm[];
-    using namespace tile;
-    const int tr = (R + kT - 1) / kT;
-    const long long rt_n = (rows + kT - 1) / kT;
-    const long long tasks = rt_n * tr;
-    double* As = gsm;
-    double* Bs = gsm + kT * (kPB + 4);
-    for (long long task = blockIdx.x; task < tasks; task += gridDim.x) {
-        const long long i0 = (task / tr) * kT;
-        const int c0 = static_cast<int>(task % tr) * kT;
-        const int vr = static_cast<int>(min(static_cast<long long>(kT), rows - i0)), vc = min(kT, R - c0);
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int k0 = 0; k0 < R; k0 += kPB) {
-            const int kp = min(kPB, R - k0), kpad = pad8(kp);
-            stage_rows<32>(As, kPB + 4, kT, kpad, kp,
-                           [&](int row) { return row < vr ? a + (i0 + row) * R + k0 : nullptr; });
-            stage_rows<16>(Bs, kKS, kpad, kT, vc,
-                           [&](int k) { return k < kp ? gnn + static_cast<long long>(k0 + k) * R + c0 : nullptr; });
-            cp_async_wait_all();
-            __syncthreads();
-            mma_panel<false>(As, kPB + 4, Bs, kpad, acc);
-            __syncthreads();
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const long long tasks = ((rows + tile::kT - 1) / tile::kT) * tr;
+    for (long long task = blockIdx.x; task < tasks; task += gridDim.x) gradient_tile(a, gnn, m, rows, R, g, task, gsm);
+}
+// every mode in one launch: tasks of mode n follow those of mode n-1
+struct GradDev {
+    int order;
+    long long off[kMaxOrder + 1];  // stacked block offsets
+    long long rows[kMaxOrder];
+};
+__global__ void __launch_bounds__(tile::kThreads)
+gradient_all_kernel(const GradDev gd, const double* __restrict__ a, const double* __restrict__ pair,
+                    const double* __restrict__ m, int R, double* __restrict__ g) {
+    extern __shared__ __align__(16) double gsm[];
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const long long rr = static_cast<long long>(R) * R;
+    long long total = 0;
+    for (int n = 0; n < gd.order; ++n) total += ((gd.rows[n] + tile::kT - 1) / tile::kT) * tr;
+    for (long long task = blockIdx.x; task < total; task += gridDim.x) {
+        long long t = task;
+        int n = 0;
+        for (; n < gd.order; ++n) {
+            const long long tn = ((gd.rows[n] + tile::kT - 1) / tile::kT) * tr;
+            if (t < tn) break;
+            t -= tn;
         }
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-        const int gg = lane >> 2, t = lane & 3;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const long long i = i0 + (warp >> 2) * 16 + gg + 8 * h;
-                const int col = c0 + (warp & 3) * 8 + 2 * t + c;
-                if (i < rows && col < R) g[i * R + col] = acc[2 * h + c] - m[i * R + col];
-            }
+        gradient_tile(a + gd.off[n], pair + (n * gd.order + n) * rr, m + gd.off[n], gd.rows[n], R, g + gd.off[n], t,
+                      gsm);
     }
 }
 
@@ -466,6 +495,26 @@ void launch_residual(const double* m_last, const double* a_last, std::int64_t ro
     CPK_CUDA(cudaGetLastError());
 }
 
+void launch_gradient_all(const double* a, const double* pair, const double* m, const std::int64_t* off,
+                         const std::int64_t* rows, int order, int R, double* g, cudaStream_t st) {
+    GradDev gd{};
+    gd.order = order;
+    long long tasks = 0;
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    for (int n = 0; n < order; ++n) {
+        gd.off[n] = off[n];
+        gd.rows[n] = rows[n];
+        tasks += ((rows[n] + tile::kT - 1) / tile::kT) * tr;
+    }
+    gd.off[order] = off[order];
+    const std::size_t smem = (tile::kT * (tile::kPB + 4) + tile::kPB * tile::kKS) * sizeof(double);
+    CPK_CUDA(cudaFuncSetAttribute(gradient_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    gradient_all_kernel<<<static_cast<int>(std::min<long long>(tasks, 2 * 148)), tile::kThreads, smem, st>>>(
+        gd, a, pair, m, R, g);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
 void launch_gradient(const double* a, const double* gnn, const double* m, std::int64_t rows, int R,
                      double* g, cudaStream_t st) {
     const long long tasks = ((rows + tile::kT - 1) / tile::kT) * ((R + tile::kT - 1) / tile::kT);

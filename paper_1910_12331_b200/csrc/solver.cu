@@ -818,10 +818,12 @@ void DeviceProblem::note_factor_update(int mode) {
     else pb_valid_ = false;             // front-root key holds modes < h
     if (mode == pm_mode_) pm_mode_ = -1;
     pinv_ready_ = false;
+    res_current_ = false;
     m_all_valid_ = false;
 }
 void DeviceProblem::invalidate_all() {  // factors changed wholesale
     pinv_ready_ = false;
+    res_current_ = false;
     pf_valid_ = pb_valid_ = false;
     pm_mode_ = -1;
     m_all_valid_ = false;
@@ -848,17 +850,17 @@ void DeviceProblem::compute_all_mttkrp() {
             if (!pf_valid_) root_back();
             const bool beside = pm_mode_ != 1 && !std::getenv("CPKIT_NO_REDUCE_OVERLAP");
             if (beside) {
-                CPK_CUDA(cudaEventRecord(ctx_.ev[2 * kMaxOrder + 2], ctx_.stream));
-                CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[2 * kMaxOrder + 2], 0));
+                CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
+                CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
                 const bool dc = defer_coll_;
                 defer_coll_ = true;  // a sharded run reduces every block after the pass anyway
                 second_level_back(0, ctx_.aux2, ws_red_.get(), ws_red_.size());
                 second_level_back(1, ctx_.aux2, ws_red_.get(), ws_red_.size());
                 defer_coll_ = dc;
-                CPK_CUDA(cudaEventRecord(ctx_.ev[2 * kMaxOrder + 3], ctx_.aux2));
+                CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
                 root_single(1);
                 second_level_pm(2);
-                CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[2 * kMaxOrder + 3], 0));
+                CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));
             } else {
                 mttkrp(0);
                 mttkrp(1);
@@ -931,10 +933,8 @@ std::pair<double, double> DeviceProblem::residual_fitness(double xnorm2, int /*l
 }
 void DeviceProblem::gradient() {
     const int N = order();
-    const std::size_t RR = static_cast<std::size_t>(R_) * R_;
-    for (int n = 0; n < N; ++n)
-        launch_gradient(A_.get() + off_[n], pair_.get() + (n * N + n) * RR, M_.get() + off_[n],
-                        static_cast<std::int64_t>(dims_[n]), R_, G_.get() + off_[n], ctx_.stream);
+    std::vector<std::int64_t> rows(dims_.begin(), dims_.end());
+    launch_gradient_all(A_.get(), pair_.get(), M_.get(), off_.data(), rows.data(), N, R_, G_.get(), ctx_.stream);
 }
 double DeviceProblem::norm_sum(const double* dev_stacked) {
     launch_block_norm_sum(dev_stacked, offs_dev_.get(), order(), partials_.get(), scal_.get() + kNormSum, 1.0,
@@ -1027,7 +1027,9 @@ void DeviceProblem::jtj_matvec(const double* dev_w, double* dev_u, double lambda
     p.barrier = barrier_.get();
     p.lambda = lambda;
     p.shape = shape == RegShape::identity ? 0 : 1;
+    cg_barrier_ready();
     launch_jtj_matvec(p, dev_w, dev_u, ctx_.stream);
+    barrier_zero_ = false;  // used: the next solve zeroes it itself
 }
 
 // gauss_newton.cpp:279-349; G must hold the gradient. Result in V.
@@ -1078,7 +1080,9 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gno
         p.trace = trace.get();
     }
     prof_begin(kProfCg);
+    cg_barrier_ready();
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);
+    barrier_zero_ = false;  // used: the next solve zeroes it itself
     prof_end();
     if (want_trace) {
         std::vector<unsigned long long> h(64 * 16 + 1024);
@@ -1310,12 +1314,17 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     }
     pinv_ready_ = false;
     precond_pending_ = false;
-    residual_launch(xnorm2);
+    if (!(res_current_ && res_xnorm_ == xnorm2)) residual_launch(xnorm2);  // else: the last step's residual_after
     gradient();
     launch_block_norm_sum(G_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm, ctx_.stream);
     launch_pack_values(scal_.get() + kNormSum, 1, nullptr, 0, dm + 2, ctx_.stream);
-    als_snapshot_factors();  // pre-step factors (restored when the step must not happen)
+    // pre-step factors (restored when the step must not happen), copied on the
+    // third stream while the CG runs; the update waits for it
+    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
+    CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), off_[N] * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.aux2));
+    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
     // preconditioner inverse ready (its factorisation status is checked at the end)
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
     launch_pack_values(nullptr, 0, status_.get(), N, dm + o_st, ctx_.stream);
@@ -1346,10 +1355,19 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     p.cg_tol = cfg.cg_tol;
     p.cap = cap;
     p.result = cgres_.get();
+    p.barrier_zeroed = barrier_zero_;  // re-zeroed on the third stream after the previous solve
+    cg_barrier_ready();
     prof_begin(kProfCg);
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);  // G = 0: 0 iterations, V = 0 (cp_cg's shortcut)
     prof_end();
+    // zero the grid barrier for the next solve off the critical path
+    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
+    CPK_CUDA(cudaMemsetAsync(barrier_.get(), 0, cg_barrier_words() * sizeof(unsigned int), ctx_.aux2));
+    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvBarrier], ctx_.aux2));
+    barrier_zero_ = true;
     launch_pack_values(nullptr, 0, cgres_.get(), 5, dm + o_cg, ctx_.stream);
+    CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));  // pre-step snapshot taken
     launch_axpy(A_.get(), V_.get(), 1.0, S, ctx_.stream);
     launch_block_norm_sum(V_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
     launch_set_flag_scalar(flag_.get(), 1, scal_.get() + kStep, 0.0, ctx_.stream);
@@ -1369,6 +1387,8 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     side_busy_ = false;
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));  // Grams
     residual_launch(xnorm2);
+    res_current_ = true;
+    res_xnorm_ = xnorm2;
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);
     ctx_.sync_main();
 

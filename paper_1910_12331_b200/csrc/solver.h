@@ -158,7 +158,9 @@ struct Context {
     cudaStream_t stream = nullptr;
     cudaStream_t aux = nullptr;  // side stream: SPD factorisations overlap the MTTKRP
     cudaStream_t aux2 = nullptr;  // second-level reduces beside the next root GEMM (GN tree pass)
-    static constexpr int kEvents = 2 * kMaxOrder + 4;
+    static constexpr int kEvents = 2 * kMaxOrder + 6;
+    static constexpr int kEvAux2A = 2 * kMaxOrder + 2, kEvAux2B = 2 * kMaxOrder + 3,
+                         kEvBarrier = 2 * kMaxOrder + 4;  // third-stream hand-offs
     cudaEvent_t ev[kEvents] = {};
     std::unique_ptr<Comm> comm;  // null: single GPU
     explicit Context(int dev);
@@ -249,6 +251,14 @@ private:
     // ctx_.ev[1]. pinv_ready_ marks a chain launched ahead for (lambda, shape).
     void launch_precond_chain(double lambda, RegShape shape, bool grams_and_gamma);
     bool pinv_ready_ = false;
+    // the residual slots hold the residual of the current factors for res_xnorm_
+    bool res_current_ = false;
+    double res_xnorm_ = 0.0;
+    // the CG grid barrier is being re-zeroed on the third stream (ev[kEvBarrier])
+    bool barrier_zero_ = false;
+    void cg_barrier_ready() {
+        if (barrier_zero_) CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvBarrier], 0));
+    }
     double pinv_lambda_ = 0.0;
     RegShape pinv_shape_ = RegShape::identity;
 
