@@ -1308,7 +1308,9 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     const int o_cg = 3, o_st = 8, o_step = 8 + N, o_after = 10 + N;
     const RegShape shape = cfg.schedule.shape;
     if (!m_all_valid_) compute_all_mttkrp();
-    if (!(pinv_ready_ && pinv_lambda_ == schedule.lambda && pinv_shape_ == shape)) {
+    // ready: launched at the end of the previous step, which waited for it before its residual
+    const bool chain_waited = pinv_ready_ && pinv_lambda_ == schedule.lambda && pinv_shape_ == shape;
+    if (!chain_waited) {
         build_gamma_set();
         launch_precond_chain(schedule.lambda, shape, false);  // side stream, overlaps residual/gradient
     }
@@ -1326,7 +1328,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), off_[N] * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.aux2));
     CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
     // preconditioner inverse ready (its factorisation status is checked at the end)
-    CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
+    if (!chain_waited) CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
     launch_pack_values(nullptr, 0, status_.get(), N, dm + o_st, ctx_.stream);
     CgParams p = base_params(N, R_, dims_, off_);
     int cap = cfg.cg_max_iters;
