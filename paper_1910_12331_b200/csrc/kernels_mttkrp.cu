@@ -627,7 +627,8 @@ long long best_splits(long long base, long long slots, long long K, double* eff_
             best = sp;
         }
     }
-    if (eff_out) *eff_out = best_eff;
+    if (eff_out) *eff_out = best_score;  // split candidates carry their reduce cost into the tile score
+    (void)best_eff;
     return best;
 }
 int resident_per_sm(const GemmPlan& p) {
@@ -662,7 +663,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
     double best_score = -1.0;
     GemmPlan best = p;
     for (int wm = 4; wm <= 10; ++wm) {
-        for (int nw : {8, 12}) {
+        for (int nw : {4, 8, 12}) {
             for (int nt8p = p.nt8; nt8p <= p.nt8 + 4 && nt8p <= 26; ++nt8p) {
                 GemmPlan c = p;
                 c.wm = wm;
@@ -692,9 +693,15 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
                     best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
                                 K, &w_eff, min_chunks);
                 }
+                // four DMMA warps = one per SM sub-partition: ~0.93 of the two-per-SMSP
+                // issue rate (tools/probe/probe_fp64.cu), only worth it to fill a wave
                 const double score = cell_efficiency(wm, nt8p, nw) * (static_cast<double>(p.nt8) / nt8p) * m_eff *
                                      w_eff * (full ? 1.0 : trans ? 0.97 : 0.85) * (1.0 + 0.002 * wm) *
-                                     (c.stages >= 3 ? 1.0 : 0.97);
+                                     (c.stages >= 3 ? 1.0 : 0.97) * (nw == 4 ? 0.93 : 1.0);
+                if (const char* dbg = std::getenv("CPKIT_PLAN_DEBUG"))
+                    if (std::atoi(dbg) >= 2)
+                        std::fprintf(stderr, "  cand M=%lld wm=%d nw=%d nt8=%d maxc=%d full=%d stages=%d per_sm=%d w_eff=%.3f score=%.4f\n",
+                                     M, wm, nw, nt8p, c.maxc, full ? 1 : 0, c.stages, c.per_sm, w_eff, score);
                 if (score > best_score + 1e-12) {
                     best_score = score;
                     best = c;
@@ -833,7 +840,9 @@ BackSplit plan_back(long long M, long long K, int R, int reserve_sms) {
     if (units <= slots || rem == 0 || 2 * rem > all_slots) return b;
     const long long rows_main = (units - rem) * p.BM();
     GemmPlan tail = plan_gemm(M - rows_main, K, R, false, 0, 3);
-    if (tail.splits < 2) return b;
+    // the tail must fill (at most) one wave: smaller tiles or a k split
+    if (static_cast<long long>(tail.ntiles) * tail.mtiles * tail.splits > all_slots) return b;
+    if (tail.splits < 2 && tail.BM() >= p.BM()) return b;  // no smaller tiles and no split: nothing gained
     b.main = plan_gemm(rows_main, K, R, false);
     b.tail = tail;
     b.rows_main = rows_main;
@@ -852,7 +861,8 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
                       const KrpDesc& kb, double* krp, double* pf, double* ws, std::size_t ws_elems,
                       cudaStream_t st, int reserve_sms) {
     const BackSplit bs = plan_back(F, B, R, reserve_sms);
-    if (bs.rows_main < F && ws_elems >= static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R) {
+    if (bs.rows_main < F &&
+        (bs.tail.splits < 2 || ws_elems >= static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R)) {
         const int Rs2 = (R + 1) & ~1;
         const bool direct2 = kb.nmodes == 1 && R % 2 == 0;
         if (!direct2) fill_krp(kb, B, R, krp, st);
@@ -873,6 +883,10 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
                                        : make_map(direct2 ? kb.fac[0] : krp, static_cast<std::uint64_t>(Rs2),
                                                   static_cast<std::uint64_t>(B),
                                                   static_cast<std::uint32_t>(bs.tail.bns), kBK, false);
+        if (bs.tail.splits < 2) {  // smaller tiles fill the wave: straight into the output rows
+            dispatch<false, false>(bs.tail, st, xmap_t, kmap_t, to_dev(kb), mt, B, R, pf + bs.rows_main * R, 0);
+            return;
+        }
         dispatch<false, false>(bs.tail, st, xmap_t, kmap_t, to_dev(kb), mt, B, R, ws, mt * R);
         const long long n = mt * static_cast<long long>(R);
         const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 4LL * num_sms()));
@@ -913,11 +927,12 @@ std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R) {
     std::size_t w = 0;
     for (int reserve = 0; reserve <= 1; ++reserve) {
         const BackSplit bs = plan_back(F, B, R, reserve);
-        if (bs.rows_main < F) w = std::max<std::size_t>(w, static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R);
+        if (bs.rows_main < F && bs.tail.splits > 1)
+            w = std::max<std::size_t>(w, static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R);
     }
     if (w) return w;
     const BackSplit bs = plan_back(F, B, R, 0);
-    if (bs.rows_main < F) return static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R;
+    if (bs.rows_main < F) return bs.tail.splits > 1 ? static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R : 0;
     const GemmPlan& p = bs.main;
     return p.splits > 1 ? static_cast<std::size_t>(p.splits) * F * R : 0;
 }
