@@ -1,6 +1,7 @@
 // Bandwidth/latency-bound kernels of the GN/ALS path (sm_100a, fp64).
 // All reductions are two-pass with a fixed grid and a fixed combine order,
 // so every result is bitwise reproducible run to run.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -134,6 +135,70 @@ gram_tiles_kernel(const double* __restrict__ base, const long long* __restrict__
                 if (r < R && z < R && r <= z) out[r * R + z] = acc[2 * h + c];
             }
     }
+}
+// One thread-block cluster per 32x32 upper-triangle tile of a Gram, one CTA
+// per row split: each CTA leaves its partial tile in shared memory and the
+// cluster sums the partials through distributed shared memory in split order
+// (bitwise the finalize pass's ((0 + p0) + p1) + ...), writing the tile and its
+// mirror. No partial workspace round trip and no finalize launch.
+__global__ void __launch_bounds__(tile::kThreads)
+gram_cluster_kernel(const double* __restrict__ base, const long long* __restrict__ offs,
+                    const long long* __restrict__ rows, int lo, int R, int nsplit, double* __restrict__ grams,
+                    const double* __restrict__ sq, int nsq, double* sq_acc) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ tile::Smem sm;
+    __shared__ double part[tile::kT * tile::kT];
+    if (sq && blockIdx.x == 0) {  // the ALS step norm: *sq_acc += sqrt(sum of the row partials)
+        double v = 0.0;
+        for (int i = threadIdx.x; i < nsq; i += blockDim.x) v += sq[i];
+        const double s = block_sum(v);
+        if (threadIdx.x == 0) *sq_acc += sqrt(s);
+    }
+    const int tr = (R + tile::kT - 1) / tile::kT;
+    const int tri = tr * (tr + 1) / 2;
+    int rem = blockIdx.x;
+    const int sp = rem % nsplit; rem /= nsplit;  // == this CTA's rank in its cluster
+    int tt = rem % tri; rem /= tri;
+    const int n = lo + rem;
+    int rt = 0;
+    while (tt >= tr - rt) { tt -= tr - rt; ++rt; }
+    const int zt = rt + tt;
+    const double* a = base + offs[n];
+    const long long s = rows[n];
+    const long long per = (s + nsplit - 1) / nsplit;
+    const long long i0 = sp * per, i1 = min(s, i0 + per);
+    const int K = static_cast<int>(max(0LL, i1 - i0));
+    const int r0 = rt * tile::kT, z0 = zt * tile::kT;
+    auto la = [&](int row, int k) -> double {
+        const int r = r0 + row;
+        return r < R ? a[(i0 + k) * R + r] : 0.0;
+    };
+    auto lb = [&](int k, int col) -> double {
+        const int z = z0 + col;
+        return z < R ? a[(i0 + k) * R + z] : 0.0;
+    };
+    double acc[4];
+    tile::tile_gemm(sm, K, la, lb, acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            part[((warp >> 2) * 16 + g + 8 * h) * tile::kT + (warp & 3) * 8 + 2 * t + c] = acc[2 * h + c];
+    cluster.sync();
+    double* out = grams + static_cast<long long>(n) * R * R;
+    const int per_cta = (tile::kT * tile::kT + nsplit - 1) / nsplit;
+    for (int e = sp * per_cta + threadIdx.x; e < min(tile::kT * tile::kT, (sp + 1) * per_cta); e += blockDim.x) {
+        const int r = r0 + e / tile::kT, z = z0 + e % tile::kT;
+        if (r >= R || z >= R || r > z) continue;
+        double v = 0.0;
+        for (int q = 0; q < nsplit; ++q) v += cluster.map_shared_rank(part, q)[e];
+        out[r * R + z] = v;
+        out[z * R + r] = v;
+    }
+    cluster.sync();  // partial tiles stay readable until every CTA of the cluster is done
 }
 __global__ void gram_finalize_kernel(const double* __restrict__ partial, int lo, int nmodes, int R,
                                      int nsplit, double* __restrict__ grams) {
@@ -458,6 +523,24 @@ void launch_grams(const double* base, const std::int64_t* offs, const std::int64
     const int nsplit = gram_splits(smax);
     const int tr = (R + tile::kT - 1) / tile::kT;
     const int tasks = (hi - lo) * tr * (tr + 1) / 2 * nsplit;
+    if (nsplit > 1 && nsplit <= 8 && !std::getenv("CPKIT_GRAM_NO_CLUSTER")) {  // portable cluster sizes
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(tasks));
+        cfg.blockDim = dim3(tile::kThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(nsplit);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CPK_CUDA(cudaLaunchKernelEx(&cfg, gram_cluster_kernel, base, reinterpret_cast<const long long*>(offs),
+                                    reinterpret_cast<const long long*>(rows), lo, R, nsplit, grams, sq, nsq, sq_acc));
+        ::cpkit::count_launch(1);
+        return;
+    }
     gram_tiles_kernel<<<std::min(tasks, 4 * 148), tile::kThreads, 0, st>>>(
         base, reinterpret_cast<const long long*>(offs), reinterpret_cast<const long long*>(rows), lo, hi - lo, R,
         nsplit, ws, sq, nsq, sq_acc, nsplit == 1 ? grams : nullptr);
