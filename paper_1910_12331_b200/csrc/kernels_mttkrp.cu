@@ -603,7 +603,8 @@ bool runs_fit(int wm, int nt8, int nw) {
 }
 // Split count with the best wave efficiency (<= 2 waves or the unsplit count),
 // keeping >= 8 k-stages per split; ties go to fewer splits.
-long long best_splits(long long base, long long slots, long long K, double* eff_out, int min_chunks = 8) {
+long long best_splits(long long base, long long slots, long long K, double* eff_out, int min_chunks = 8,
+                      int wave_cap = 0) {
     const long long kchunks = (K + kBK - 1) / kBK;
     long long best = 1;
     double best_eff = -1.0;
@@ -612,7 +613,8 @@ long long best_splits(long long base, long long slots, long long K, double* eff_
     // ~24 sp / K of the GEMM's time) charged against its wave efficiency.
     // Otherwise at most 2 waves (the NN root's partial last wave is handled by
     // a separate tail launch, plan_back).
-    const long long max_waves = base < slots ? 8 : std::max<long long>(2, (base + slots - 1) / slots);
+    long long max_waves = base < slots ? 8 : std::max<long long>(2, (base + slots - 1) / slots);
+    if (wave_cap > 0) max_waves = std::min<long long>(max_waves, wave_cap);
     double best_score = -1.0;
     for (long long sp = 1; sp <= 64; ++sp) {
         if (sp > 1 && kchunks / sp < min_chunks) break;
@@ -646,7 +648,8 @@ bool runs_full(const GemmPlan& p) {
 
 // fixed_kps > 0: batched contraction, split s covers k in [s kps, (s+1) kps)
 // and writes its own output slab (no split search, no reduction).
-GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0, int min_chunks = 8) {
+GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0, int min_chunks = 8,
+                   int wave_cap = 0) {
     GemmPlan p{};
     // rank split: one CTA column covers up to 208 ranks (26 n8 cells)
     p.ntiles = (R + 207) / 208;
@@ -691,7 +694,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
                     w_eff = static_cast<double>(units) / static_cast<double>(((units + slots - 1) / slots) * slots);
                 } else {
                     best_splits(static_cast<long long>(c.ntiles) * mt, static_cast<long long>(num_sms()) * c.per_sm,
-                                K, &w_eff, min_chunks);
+                                K, &w_eff, min_chunks, wave_cap);
                 }
                 // four DMMA warps = one per SM sub-partition: ~0.93 of the two-per-SMSP
                 // issue rate (tools/probe/probe_fp64.cu), only worth it to fill a wave
@@ -751,7 +754,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
     if (fixed_kps > 0) {
         p.kps = fixed_kps;
     } else {
-        const long long sp = best_splits(base, slots, K, nullptr, min_chunks);
+        const long long sp = best_splits(base, slots, K, nullptr, min_chunks, wave_cap);
         const long long kchunks = (K + kBK - 1) / kBK;
         p.kps = ((kchunks + sp - 1) / sp) * kBK;  // multiple of kBK: splits never share a stage
     }
@@ -839,7 +842,7 @@ BackSplit plan_back(long long M, long long K, int R, int reserve_sms) {
     const long long rem = units % slots;
     if (units <= slots || rem == 0 || 2 * rem > all_slots) return b;
     const long long rows_main = (units - rem) * p.BM();
-    GemmPlan tail = plan_gemm(M - rows_main, K, R, false, 0, 3);
+    GemmPlan tail = plan_gemm(M - rows_main, K, R, false, 0, 3, 1);  // one wave at most
     // the tail must fill (at most) one wave: smaller tiles or a k split
     if (static_cast<long long>(tail.ntiles) * tail.mtiles * tail.splits > all_slots) return b;
     if (tail.splits < 2 && tail.BM() >= p.BM()) return b;  // no smaller tiles and no split: nothing gained
