@@ -463,6 +463,23 @@ def test_als_pipelined_driver_equals_sequential(ck, orc, cfg, monkeypatch):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("dims,rank", [([300, 120, 200], 100), ([400, 70, 90], 37), ([130, 257, 64], 200)])
+def test_gram_cluster_bitwise(ck, orc, dims, rank, monkeypatch):
+    """The cluster Gram kernel sums the row-split partial tiles in split order
+    through distributed shared memory: bitwise the split + finalize path."""
+    f = gauss_factors(orc, dims, rank, 41)
+    x = np.zeros(dims)
+    p = make(ck, x, f)
+    g1, pr1 = p.gamma_set()
+    monkeypatch.setenv("CPKIT_GRAM_NO_CLUSTER", "1")
+    q = make(ck, x, f)
+    g2, pr2 = q.gamma_set()
+    assert np.array_equal(g1, g2) and np.array_equal(pr1, pr2)
+    for n, a in enumerate(f):  # and the reference definition S = A^T A, symmetrised
+        s = a.T @ a
+        assert rel_err(g1[n], 0.5 * (s + s.T)) < KTOL
+
+
 # ---------------------------------------------------------------- C ABI end to end
 def test_decompose_through_c_abi(orc, ck):
     # test_capi.cpp:96-126 shape: gaussian [4,4,4] rank 2, GN
