@@ -1362,11 +1362,9 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     prof_begin(kProfCg);
     run_cg(p, cg_max_grid(ctx_.device), ctx_.stream);  // G = 0: 0 iterations, V = 0 (cp_cg's shortcut)
     prof_end();
-    // zero the grid barrier for the next solve off the critical path
-    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
-    CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
-    CPK_CUDA(cudaMemsetAsync(barrier_.get(), 0, cg_barrier_words() * sizeof(unsigned int), ctx_.aux2));
-    CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvBarrier], ctx_.aux2));
+    // zero the grid barrier for the next solve now (in stream order; cheaper
+    // than a cross-stream hand-off in front of the next cooperative launch)
+    CPK_CUDA(cudaMemsetAsync(barrier_.get(), 0, cg_barrier_words() * sizeof(unsigned int), ctx_.stream));
     barrier_zero_ = true;
     launch_pack_values(nullptr, 0, cgres_.get(), 5, dm + o_cg, ctx_.stream);
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));  // pre-step snapshot taken

@@ -254,11 +254,9 @@ private:
     // the residual slots hold the residual of the current factors for res_xnorm_
     bool res_current_ = false;
     double res_xnorm_ = 0.0;
-    // the CG grid barrier is being re-zeroed on the third stream (ev[kEvBarrier])
+    // the CG grid barrier was re-zeroed on the solver stream after the last solve
     bool barrier_zero_ = false;
-    void cg_barrier_ready() {
-        if (barrier_zero_) CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvBarrier], 0));
-    }
+    void cg_barrier_ready() {}
     double pinv_lambda_ = 0.0;
     RegShape pinv_shape_ = RegShape::identity;
 
