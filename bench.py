@@ -340,11 +340,39 @@ def run_b200(args, rank, world, local_rank):
         x_host = x_pinned.reshape(DIMS)
         result["cpu_baseline"] = cpu_baseline_sample(x_host, init)
     p.close()
+    if rank == 0 and world == 1 and not args.no_c5s:
+        result["c5s"] = c5s_slice(cpkit, result["roofline"]["peak"])
     if dist:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
     return 0
+
+
+def c5s_slice(cpkit, peak_tf):
+    """The largest config that fits one GPU (C5s: order 4, s=200, R=200, 12.8 GB,
+    the 1-GPU anchor of the C5 scaling case), generated on device: ALS sweep and
+    GN iteration times, reported beside the headline (not the bench value)."""
+    dims, R = [200] * 4, 200
+    truth = cpkit.random_factors(dims, R, cpkit.problem_seed(0, R, 0))
+    init = cpkit.random_factors(dims, R, cpkit.init_seed(0, R, 0, 0))
+    q = cpkit.DeviceProblem(dims, R)
+    q.generate(truth, 1, 1e-4)
+    q.set_factors(init)
+    q.time_als_sweeps(0.0, 1)  # warm-up (graph capture)
+    als_ms = q.time_als_sweeps(0.0, 3) / 3
+    q.set_factors(init)
+    q.time_gn_steps({}, 1)  # warm-up
+    q.set_factors(init)
+    gn_ms, cg = q.time_gn_steps({}, 2)
+    q.close()
+    root_flops = 4.0 * R * 200 ** 4  # two root contractions per sweep / per GN iteration
+    return {"workload": "C5s: order-4 s=200 R=200 uniform[0,1) + 1e-4 noise (12.8 GB), generated on device",
+            "als_ms_per_sweep": als_ms, "als_sweeps_per_s": 1e3 / als_ms,
+            "als_root_tflops": root_flops / (als_ms * 1e-3) / 1e12,
+            "als_root_frac_of_peak": root_flops / (als_ms * 1e-3) / 1e12 / peak_tf,
+            "gn_ms_per_iter": gn_ms / 2, "gn_cg_iters": cg,
+            "note": "TFLOP/s = the two root contractions' 4 R prod(s) flops over the whole sweep time"}
 
 
 def main():
@@ -355,6 +383,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5s", action="store_true", help="skip the C5s (largest single-GPU config) line item")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
