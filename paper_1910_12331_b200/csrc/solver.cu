@@ -502,6 +502,33 @@ KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) 
 }
 
 void DeviceProblem::upload_tensor(const double* host_local) {
+    if (msdt_copies_ && !std::getenv("CPKIT_UPLOAD_UNCHUNKED")) {
+        // order 3: upload by i0 slabs; each slab's share of both permuted copies is
+        // transposed on the third stream while the next slab crosses PCIe
+        const std::int64_t s0 = local_rows_[0], s1 = local_rows_[1];
+        const std::int64_t chunks = std::min<std::int64_t>(8, s0), step = (s0 + chunks - 1) / chunks;
+        for (std::int64_t a = 0; a < s0; a += step) {
+            const std::int64_t b = std::min(s0, a + step), rows = (b - a) * s1;
+            double* xd = x_.get() + a * s1 * Bs_;
+            const double* xh = host_local + a * s1 * Bl_;
+            if (Bs_ == Bl_)
+                CPK_CUDA(cudaMemcpyAsync(xd, xh, rows * Bl_ * sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
+            else
+                CPK_CUDA(cudaMemcpy2DAsync(xd, Bs_ * sizeof(double), xh, Bl_ * sizeof(double), Bl_ * sizeof(double),
+                                           rows, cudaMemcpyHostToDevice, ctx_.stream));
+            CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
+            CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
+            // X^(0)[i1][i2][i0], columns i0 in [a, b): batch i1, rows i0, cols i2
+            launch_transpose_batched(xd, s1, b - a, Bl_, s1 * Bs_, Bs_, X0_.get() + a, ld0_, Bl_ * ld0_, ctx_.aux2);
+            // X^(1)[i0][i2][i1] for i0 in [a, b): batch i0, rows i1, cols i2
+            launch_transpose_batched(xd, b - a, s1, Bl_, Bs_, s1 * Bs_, X1_.get() + a * Bl_ * ld1_, ld1_,
+                                     Bl_ * ld1_, ctx_.aux2);
+        }
+        CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
+        CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));
+        invalidate_all();
+        return;
+    }
     if (Bs_ == Bl_)
         CPK_CUDA(cudaMemcpyAsync(x_.get(), host_local, local_elems_ * sizeof(double), cudaMemcpyHostToDevice,
                                  ctx_.stream));
