@@ -1330,9 +1330,11 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     if (cfg.armijo || std::getenv("CPKIT_GN_SYNC")) return gn_step_sync(cfg, schedule, xnorm2);
     const int N = order();
     const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
-    double* hm = hmap_ + kGnMapOff;   // [res, fit, gnorm | cg 5 | status N | step, fin | res_after, fit_after]
+    // [res, fit, (step slot), gnorm | status N | cg 5 | step, fin | res_after, fit_after]
+    double* hm = hmap_ + kGnMapOff;
     double* dm = dmap_ + kGnMapOff;
-    const int o_cg = 3, o_st = 8, o_step = 8 + N, o_after = 10 + N;
+    static_assert(kRes + 3 == kNormSum, "residual, fitness, step and gradient-norm slots are adjacent");
+    const int o_gn = 3, o_st = 4, o_cg = 4 + N, o_step = 9 + N, o_after = 11 + N;
     const RegShape shape = cfg.schedule.shape;
     if (!m_all_valid_) compute_all_mttkrp();
     // ready: launched at the end of the previous step, which waited for it before its residual
@@ -1346,8 +1348,6 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     if (!(res_current_ && res_xnorm_ == xnorm2)) residual_launch(xnorm2);  // else: the last step's residual_after
     gradient();
     launch_block_norm_sum(G_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
-    launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm, ctx_.stream);
-    launch_pack_values(scal_.get() + kNormSum, 1, nullptr, 0, dm + 2, ctx_.stream);
     // pre-step factors (restored when the step must not happen), copied on the
     // third stream while the CG runs; the update waits for it
     CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
@@ -1356,7 +1356,8 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
     // preconditioner inverse ready (its factorisation status is checked at the end)
     if (!chain_waited) CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
-    launch_pack_values(nullptr, 0, status_.get(), N, dm + o_st, ctx_.stream);
+    // residual, fitness, gradient norm and the preconditioner status in one launch
+    launch_pack_values(scal_.get() + kRes, 4, status_.get(), N, dm, ctx_.stream);
     CgParams p = base_params(N, R_, dims_, off_);
     int cap = cfg.cg_max_iters;
     if (cap <= 0) {  // default_cg_cap (gauss_newton.cpp:267-275)
@@ -1433,7 +1434,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
         diag.halt = GnStepDiag::Halt::residual;
         return diag;
     }
-    diag.grad_norm = hm[2];
+    diag.grad_norm = hm[o_gn];
     if (diag.grad_norm <= cfg.grad_tol) {
         undo();
         diag.halt = GnStepDiag::Halt::gradient;
