@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "common.h"
 #include "grid_sync.cuh"
@@ -518,12 +519,19 @@ Layout make_layout(const CgParams& p, int grid) {
 }
 
 int occupancy_grid(int device) {
+    // per-device result cached: it sits on the host path in front of every solve
+    static std::mutex mu;
+    static int cached[64] = {};
+    std::lock_guard<std::mutex> lock(mu);
+    if (device >= 0 && device < 64 && cached[device] > 0) return cached[device];
     int sms = 0, per = 0;
     CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     CPK_CUDA(cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kAsyncSmemBytes)));
     CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, kAsyncSmemBytes));
-    return sms * std::max(1, per);
+    const int g = sms * std::max(1, per);
+    if (device >= 0 && device < 64) cached[device] = g;
+    return g;
 }
 
 void launch_coop(const Dev& d, int grid, cudaStream_t st) {

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -631,7 +632,17 @@ bool make_rlayout(const CgParams& p, int mt, int nt, RLayout& L) {
 template <int MT, int NT>
 void launch_res(const RDev& d, int grid, std::size_t smem, cudaStream_t st) {
     auto* fn = cg_res_kernel<MT, NT>;
-    CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    static std::mutex mu;
+    static std::size_t set_to[64] = {};  // per device: the attribute only ever grows
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev < 0 || dev >= 64 || set_to[dev] < smem) {
+            CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            if (dev >= 0 && dev < 64) set_to[dev] = smem;
+        }
+    }
     RDev dd = d;
     void* args[] = {&dd};
     CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(MT * NT * 32), args, smem, st));
@@ -655,8 +666,19 @@ bool run_cg_resident(const CgParams& p, cudaStream_t st) {
     if (std::getenv("CPKIT_CG_STREAMING")) return false;
     int dev = 0, sms = 0, optin = 0;
     CPK_CUDA(cudaGetDevice(&dev));
-    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    CPK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    {  // device attributes, cached per device (host path in front of every solve)
+        static std::mutex mu;
+        static int cache[64][2] = {};
+        std::lock_guard<std::mutex> lock(mu);
+        if (dev >= 0 && dev < 64 && cache[dev][0] > 0) {
+            sms = cache[dev][0];
+            optin = cache[dev][1];
+        } else {
+            CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            CPK_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            if (dev >= 0 && dev < 64) cache[dev][0] = sms, cache[dev][1] = optin;
+        }
+    }
     const int budget = optin - 1024;  // static shared memory headroom
     int best = -1, best_cost = 1 << 30;
     RLayout bestL{};
