@@ -1965,10 +1965,29 @@ cpkit_status cpkit_dev_time_gn_steps(cpkit_dev_problem* p, const char* gn_json, 
         int cg = 0;
         EventPair ev;
         CPK_CUDA(cudaEventRecord(ev.a, p->ctx->stream));
-        for (int i = 0; i < steps; ++i) {
-            cpkit::GnStepDiag d = p->p->gn_step(cfg, s, xn2);
-            cg += d.cg_iters;
-            if (!d.stepped) break;
+        if (!cfg.armijo && !std::getenv("CPKIT_GN_SYNC") && !std::getenv("CPKIT_GN_NO_PIPELINE")) {
+            // gn_optimize's pipelined loop: step k+1 queued before step k is read
+            int slot = 0;
+            p->p->gn_enqueue(cfg, s, xn2, slot);
+            for (int i = 0; i < steps; ++i) {
+                const cpkit::RegSchedule next = cpkit::schedule_next(s);
+                const bool spec = i + 1 < steps;
+                if (spec) p->p->gn_enqueue(cfg, next, xn2, slot ^ 1);
+                const cpkit::GnStepDiag d = p->p->gn_decode(cfg, s.lambda, slot);
+                cg += d.cg_iters;
+                if (!d.stepped) {
+                    if (spec) p->p->ctx().sync();
+                    break;
+                }
+                s = next;
+                slot ^= 1;
+            }
+        } else {
+            for (int i = 0; i < steps; ++i) {
+                cpkit::GnStepDiag d = p->p->gn_step(cfg, s, xn2);
+                cg += d.cg_iters;
+                if (!d.stepped) break;
+            }
         }
         CPK_CUDA(cudaEventRecord(ev.b, p->ctx->stream));
         *ms = ev.ms();

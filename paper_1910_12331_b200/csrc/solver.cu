@@ -350,8 +350,9 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
     if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
     CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hpin_), 16 * sizeof(double), cudaHostAllocDefault));
-    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), (kGnMapOff + kGnMapDoubles) * sizeof(double),
+    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), (kGnMapOff + 2 * kGnMapDoubles) * sizeof(double),
                            cudaHostAllocMapped));
+    for (auto& e : gn_ev_) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CPK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dmap_), hmap_, 0));
     als_graphs_.reserve(kAlsGraphs);  // in-flight sweeps hold pointers to their graphs
     for (auto& e : slot_ev_) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -378,7 +379,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     x_.resize(static_cast<std::size_t>(F_) * static_cast<std::size_t>(Bs_));
     if (Bs_ != Bl_) CPK_CUDA(cudaMemset(x_.get(), 0, x_.size() * sizeof(double)));
     krp_.resize(krp_workspace_elems(std::max<std::int64_t>(std::max(F_, Bl_), N == 3 ? std::max(local_rows_[0], local_rows_[1]) : 0), R_));
-    A_.resize(S); Atrial_.resize(S); M_.resize(S); G_.resize(S); V_.resize(S); Z_.resize(S); Q_.resize(S);
+    A_.resize(S); Atrial_.resize(S); Asnap1_.resize(S); M_.resize(S); G_.resize(S); V_.resize(S); Z_.resize(S); Q_.resize(S);
     for (int i = 0; i < 2; ++i) { Rr_[i].resize(S); W_[i].resize(S); }
     PF_.resize(static_cast<std::size_t>(F_) * R_);
     PB_.resize(static_cast<std::size_t>(Bl_) * R_);
@@ -486,6 +487,8 @@ DeviceProblem::~DeviceProblem() {
     if (hpin_) cudaFreeHost(hpin_);
     if (hmap_) cudaFreeHost(hmap_);
     for (auto& e : slot_ev_)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : gn_ev_)
         if (e) cudaEventDestroy(e);
 }
 
@@ -1197,6 +1200,10 @@ void DeviceProblem::als_snapshot_factors() {
     CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), off_[order()] * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx_.stream));
 }
+void DeviceProblem::restore_factors_from(const double* src) {
+    CPK_CUDA(cudaMemcpyAsync(A_.get(), src, off_[order()] * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.stream));
+    invalidate_all();
+}
 void DeviceProblem::als_restore_factors() {
     CPK_CUDA(cudaMemcpyAsync(A_.get(), Atrial_.get(), off_[order()] * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx_.stream));
@@ -1328,11 +1335,21 @@ AlsSweepDiag DeviceProblem::als_sweep_finish(double* res, double* fit) {
 // phase-by-phase version (`CPKIT_GN_SYNC=1`, used for Armijo).
 GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
     if (cfg.armijo || std::getenv("CPKIT_GN_SYNC")) return gn_step_sync(cfg, schedule, xnorm2);
+    gn_enqueue(cfg, schedule, xnorm2, 0);
+    GnStepDiag diag = gn_decode(cfg, schedule.lambda, 0);
+    if (diag.stepped) schedule = schedule_next(schedule);
+    return diag;
+}
+
+// The whole default step queued on the device. slot selects the diagnostics
+// area, the pre-step snapshot and the completion event, so that two steps can
+// be in flight (gn_optimize queues step k+1 before reading step k).
+void DeviceProblem::gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule, double xnorm2, int slot) {
     const int N = order();
     const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
     // [res, fit, (step slot), gnorm | status N | cg 5 | step, fin | res_after, fit_after]
-    double* hm = hmap_ + kGnMapOff;
-    double* dm = dmap_ + kGnMapOff;
+    double* dm = dmap_ + kGnMapOff + slot * kGnMapDoubles;
+    double* snap = slot == 0 ? Atrial_.get() : Asnap1_.get();
     static_assert(kRes + 3 == kNormSum, "residual, fitness, step and gradient-norm slots are adjacent");
     const int o_gn = 3, o_st = 4, o_cg = 4 + N, o_step = 9 + N, o_after = 11 + N;
     const RegShape shape = cfg.schedule.shape;
@@ -1352,7 +1369,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     // third stream while the CG runs; the update waits for it
     CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
     CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
-    CPK_CUDA(cudaMemcpyAsync(Atrial_.get(), A_.get(), off_[N] * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.aux2));
+    CPK_CUDA(cudaMemcpyAsync(snap, A_.get(), off_[N] * sizeof(double), cudaMemcpyDeviceToDevice, ctx_.aux2));
     CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
     // preconditioner inverse ready (its factorisation status is checked at the end)
     if (!chain_waited) CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));
@@ -1418,15 +1435,21 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     res_current_ = true;
     res_xnorm_ = xnorm2;
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);
-    ctx_.sync_main();
+    CPK_CUDA(cudaEventRecord(gn_ev_[slot], ctx_.stream));
+}
 
+// Decode a queued step: waits for its completion event only.
+GnStepDiag DeviceProblem::gn_decode(const GnConfig& cfg, double lambda, int slot) {
+    const int N = order();
+    double* hm = hmap_ + kGnMapOff + slot * kGnMapDoubles;
+    const int o_gn = 3, o_st = 4, o_cg = 4 + N, o_step = 9 + N, o_after = 11 + N;
+    CPK_CUDA(cudaEventSynchronize(gn_ev_[slot]));
     GnStepDiag diag;
     const double res = hm[0];
     diag.residual_before = res;
     diag.residual_after = res;
     auto undo = [&] {  // the step must not have happened: pre-step factors, caches rebuilt on demand
-        als_restore_factors();
-        pinv_ready_ = false;
+        restore_factors_from(slot == 0 ? Atrial_.get() : Asnap1_.get());
         ctx_.sync();
     };
     if (res < cfg.residual_tol) {
@@ -1440,7 +1463,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
         diag.halt = GnStepDiag::Halt::gradient;
         return diag;
     }
-    diag.lambda = schedule.lambda;
+    diag.lambda = lambda;
     if (diag.grad_norm != 0.0) {
         for (int n = 0; n < N; ++n)
             if (hm[o_st + n] == 2.0) {
@@ -1460,9 +1483,9 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
     if (hm[o_step + 1] == 0.0) throw NumericalFailure("gn_step: non-finite factors after update");
     diag.residual_after = hm[o_after];
     diag.stepped = true;
-    schedule = schedule_next(schedule);
     return diag;
 }
+
 
 GnStepDiag DeviceProblem::gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
     const int N = order();
@@ -1640,6 +1663,57 @@ std::pair<KruskalModel, ConvergenceReport> gn_optimize(DeviceProblem& p, Kruskal
     report.status = TerminalStatus::cap_hit;
     RegSchedule schedule = cfg.schedule;
     const auto t0 = std::chrono::steady_clock::now();
+    // B200 change (default steps, no Armijo): step k+1 is queued before the host
+    // reads step k (the lambda schedule is deterministic), hiding the per-step
+    // host round trip. When step k stops the run, the queued step is undone
+    // from its own pre-step snapshot (or step k from its snapshot when k itself
+    // must not have happened); records and factors are those of the sequential
+    // loop (CPKIT_GN_NO_PIPELINE=1 runs it).
+    const bool pipeline = !cfg.armijo && !std::getenv("CPKIT_GN_SYNC") && !std::getenv("CPKIT_GN_NO_PIPELINE");
+    if (pipeline) {
+        int slot = 0;
+        p.gn_enqueue(cfg, schedule, xnorm2, slot);
+        for (int iter = 1; iter <= cfg.max_iters; ++iter) {
+            const RegSchedule next = schedule_next(schedule);
+            const bool spec = iter < cfg.max_iters;
+            if (spec) p.gn_enqueue(cfg, next, xnorm2, slot ^ 1);
+            GnStepDiag diag;
+            try {
+                diag = p.gn_decode(cfg, schedule.lambda, slot);  // undoes step iter itself when it must
+            } catch (...) {
+                p.ctx().sync();
+                throw;
+            }
+            bool stop = false;
+            if (diag.halt == GnStepDiag::Halt::residual) {
+                report.status = TerminalStatus::converged_residual;
+                stop = true;
+            } else if (diag.halt == GnStepDiag::Halt::gradient) {
+                report.status = TerminalStatus::converged_step;
+                stop = true;
+            } else {
+                const double seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                report.records.push_back({iter, diag.residual_after, 1.0 - diag.residual_after, diag.lambda,
+                                          diag.cg_iters, seconds});
+                if (diag.residual_after < cfg.residual_tol) {
+                    report.status = TerminalStatus::converged_residual;
+                    stop = true;
+                } else if (diag.step_norm < cfg.step_tol) {
+                    report.status = TerminalStatus::converged_step;
+                    stop = true;
+                }
+                if (stop && spec) p.restore_factors_from(p.gn_snapshot(slot ^ 1));  // drop the queued step
+            }
+            if (stop) {
+                p.ctx().sync();
+                break;
+            }
+            schedule = next;
+            slot ^= 1;
+        }
+        p.get_factors(model);
+        return {std::move(model), std::move(report)};
+    }
     for (int iter = 1; iter <= cfg.max_iters; ++iter) {
         GnStepDiag diag = p.gn_step(cfg, schedule, xnorm2);
         if (diag.halt == GnStepDiag::Halt::residual) {

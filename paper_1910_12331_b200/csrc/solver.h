@@ -244,6 +244,13 @@ public:
     GnStepDiag gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);  // :360-449
     // the same step with a host decision after every phase (Armijo needs it)
     GnStepDiag gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);
+    // the default step split for pipelining: queue it (slot 0/1: diagnostics,
+    // pre-step snapshot, completion event), then decode it (a step that must not
+    // have happened is undone from its slot's snapshot)
+    void gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule, double xnorm2, int slot);
+    GnStepDiag gn_decode(const GnConfig& cfg, double lambda, int slot);
+    void restore_factors_from(const double* dev_src);  // factors <- device copy, caches dropped
+    const double* gn_snapshot(int slot) const { return slot == 0 ? Atrial_.get() : Asnap1_.get(); }
 
 private:
     // Side-stream chain for a GN step's preconditioner: [Grams + Gamma set,]
@@ -360,6 +367,8 @@ private:
     bool msdt_copies_ = false;
     std::int64_t ld0_ = 0, ld1_ = 0;
     DevBuf<double> X0_, X1_;
+    DevBuf<double> Asnap1_;     // GN pre-step snapshot of slot 1 (slot 0: Atrial_)
+    cudaEvent_t gn_ev_[2] = {}; // GN step completion per slot
     // Order >= 4: X^T [B_local][F] (row stride ldT_) when memory allows, so the
     // front root P_B = X^T KRP_F runs as the NN GEMM instead of the TN one.
     bool front_copy_ = false;

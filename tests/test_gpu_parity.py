@@ -480,6 +480,32 @@ def test_gram_cluster_bitwise(ck, orc, dims, rank, monkeypatch):
         assert rel_err(g1[n], 0.5 * (s + s.T)) < KTOL
 
 
+@pytest.mark.parametrize("cfg", [{"cg_max_iters": 20}, {"max_iters": 4, "cg_max_iters": 20},
+                                 {"residual_tol": 1e-3, "cg_max_iters": 20},
+                                 {"step_tol": 1e-2, "cg_max_iters": 20},
+                                 {"grad_tol": 1e9, "cg_max_iters": 20}])
+def test_gn_pipelined_driver_equals_sequential(ck, orc, cfg, monkeypatch):
+    """gn_optimize queues step k+1 before reading step k (undoing the queued
+    step, or step k itself, on stop): records and factors are bitwise those of
+    the sequential loop for every stop rule (cap, residual, step norm, gradient halt)."""
+    dims, rank, x, init = _c1(orc)
+    runs = []
+    for flag in ("1", None):
+        if flag:
+            monkeypatch.setenv("CPKIT_GN_NO_PIPELINE", flag)
+        else:
+            monkeypatch.delenv("CPKIT_GN_NO_PIPELINE", raising=False)
+        p = ck.DeviceProblem(dims, rank)
+        p.upload(x)
+        got, rep = p.optimize({"optimizer": "gn", "gn": cfg}, init)
+        j = rep.to_json()
+        runs.append((got, j["status"], [(r["residual"], r["lambda"], r["cg_iters"]) for r in j["records"]]))
+    (f1, s1, r1), (f2, s2, r2) = runs
+    assert s1 == s2 and r1 == r2
+    for a, b in zip(f1, f2):
+        assert np.array_equal(a, b)
+
+
 # ---------------------------------------------------------------- C ABI end to end
 def test_decompose_through_c_abi(orc, ck):
     # test_capi.cpp:96-126 shape: gaussian [4,4,4] rank 2, GN
