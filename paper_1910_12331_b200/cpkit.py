@@ -347,17 +347,34 @@ class DeviceProblem:
         _chk(load().cpkit_dev_slab(self._h, C.byref(lo), C.byref(hi), C.byref(n)))
         return lo.value, hi.value, n.value
 
+    # The cpkit_dev_* entries take bare pointers sized by the problem; every
+    # buffer is checked here so a wrong shape or dtype raises ValueError
+    # instead of reading or writing past the end of a host array.
+    def _factor_stack(self, blocks, what="factors") -> np.ndarray:
+        if len(blocks) != len(self.dims):
+            raise ValueError(f"{what}: expected {len(self.dims)} blocks, got {len(blocks)}")
+        for n, b in enumerate(blocks):
+            if np.shape(b) != (self.dims[n], self.rank):
+                raise ValueError(f"{what}[{n}]: expected shape {(self.dims[n], self.rank)}, got {np.shape(b)}")
+        return stack(blocks)
+
+    def _slab_array(self, x, what) -> np.ndarray:
+        n = self.slab()[2]
+        if np.size(x) != n:
+            raise ValueError(f"{what}: expected {n} elements (the local slab), got {np.size(x)}")
+        return _f64(x)
+
     def upload(self, x_local: np.ndarray):
-        x = _f64(x_local)
+        x = self._slab_array(x_local, "upload")
         _chk(load().cpkit_dev_upload_tensor(self._h, _ptr(x)))
 
     def generate(self, truth: Sequence[np.ndarray], noise_seed: int = 0, noise_rel: float = 0.0):
-        buf = stack(truth)
+        buf = self._factor_stack(truth, "truth")
         _chk(load().cpkit_dev_generate_tensor(self._h, _ptr(buf), _u64(noise_seed),
                                               C.c_double(noise_rel)))
 
     def set_factors(self, factors):
-        buf = stack(factors)
+        buf = self._factor_stack(factors)
         _chk(load().cpkit_dev_set_factors(self._h, _ptr(buf)))
 
     def get_factors(self):
@@ -400,6 +417,9 @@ class DeviceProblem:
         return g, p
 
     def set_gamma_set(self, grams, pair):
+        n, r = len(self.dims), self.rank
+        if np.size(grams) != n * r * r or np.size(pair) != n * n * r * r:
+            raise ValueError("set_gamma_set: expected N*R*R grams and N*N*R*R pairwise blocks")
         g, p = _f64(grams), _f64(pair)
         _chk(load().cpkit_dev_set_gamma_set(self._h, _ptr(g), _ptr(p)))
 
@@ -410,12 +430,12 @@ class DeviceProblem:
 
     def gradient(self, mttkrps=None):
         out = np.empty(self.stacked)
-        m = None if mttkrps is None else stack(mttkrps)
+        m = None if mttkrps is None else self._factor_stack(mttkrps, "mttkrps")
         _chk(load().cpkit_dev_gradient(self._h, _ptr(m), _ptr(out)))
         return unstack(out, self.dims, self.rank)
 
     def jtj_matvec(self, w, lam: float, shape: int = 0):
-        wb = stack(w)
+        wb = self._factor_stack(w, "w")
         out = np.empty(self.stacked)
         _chk(load().cpkit_dev_jtj_matvec(self._h, _ptr(wb), C.c_double(lam), shape, _ptr(out)))
         return unstack(out, self.dims, self.rank)
@@ -426,7 +446,7 @@ class DeviceProblem:
         return out
 
     def cp_cg(self, g, lam: float, gn: Optional[dict] = None):
-        gb = stack(g)
+        gb = self._factor_stack(g, "g")
         out = np.empty(self.stacked)
         it, cap, bd = C.c_int(), C.c_int(), C.c_int()
         _chk(load().cpkit_dev_cp_cg(self._h, _ptr(gb), C.c_double(lam),
@@ -436,6 +456,9 @@ class DeviceProblem:
 
     def spd_solve(self, s, b, lam: float):
         s, b = _f64(s), _f64(b)
+        r = self.rank
+        if s.shape != (r, r) or b.ndim != 2 or b.shape[1] != r:
+            raise ValueError(f"spd_solve: need S ({r}, {r}) and B (rows, {r})")
         out = np.empty_like(b)
         _chk(load().cpkit_dev_spd_solve(self._h, _ptr(s), _ptr(b), _u64(b.shape[0]),
                                         C.c_double(lam), _ptr(out)))
@@ -443,6 +466,8 @@ class DeviceProblem:
 
     def spd_inverse(self, s, lam: float):
         s = _f64(s)
+        if s.shape != (self.rank, self.rank):
+            raise ValueError(f"spd_inverse: need S ({self.rank}, {self.rank})")
         out = np.empty_like(s)
         _chk(load().cpkit_dev_spd_inverse(self._h, _ptr(s), C.c_double(lam), _ptr(out)))
         return out
@@ -462,7 +487,7 @@ class DeviceProblem:
         return dict(zip(keys, d.tolist()))
 
     def optimize(self, config: dict, init=None):
-        ib = None if init is None else stack(init)
+        ib = None if init is None else self._factor_stack(init, "init")
         out = np.empty(self.stacked)
         r = _vp()
         _chk(load().cpkit_dev_optimize(self._h, json.dumps(config).encode(), _ptr(ib), _ptr(out),
@@ -501,6 +526,10 @@ class DeviceProblem:
         return out.reshape(self.dims[:-1] + [hi - lo])
 
     def download_into(self, out: np.ndarray) -> None:
+        n = self.slab()[2]
+        if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.flags.c_contiguous
+                and out.flags.writeable and out.size == n):
+            raise ValueError(f"download_into: need a writable C-contiguous float64 array of {n} elements")
         _chk(load().cpkit_dev_download_tensor(self._h, _ptr(out)))
 
     def time_gn_steps(self, gn: Optional[dict], steps: int):

@@ -77,6 +77,18 @@ private:
 void count_launch(int n);
 std::uint64_t kernel_launches();
 
+// ---- per-device launch attributes, safe for concurrent solves (runtime.cu)
+// SM count of the current device (cached per device).
+int device_sm_count();
+// Raise fn's dynamic shared-memory limit on the current device to at least
+// `bytes`: grow-only per (device, function) under one process-wide mutex, so
+// a solve on another thread can never lower it under this one's launch.
+void ensure_dynamic_smem(const void* fn, std::size_t bytes);
+template <typename F>
+inline void ensure_dynamic_smem(F* fn, std::size_t bytes) {
+    ensure_dynamic_smem(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // ---- device launch helpers (implemented in kernels_*.cu) -------------------
 
 constexpr int kMaxOrder = 16;

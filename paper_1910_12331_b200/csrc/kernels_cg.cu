@@ -526,8 +526,7 @@ int occupancy_grid(int device) {
     if (device >= 0 && device < 64 && cached[device] > 0) return cached[device];
     int sms = 0, per = 0;
     CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    CPK_CUDA(cudaFuncSetAttribute(cg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kAsyncSmemBytes)));
+    ensure_dynamic_smem(cg_kernel, kAsyncSmemBytes);
     CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_kernel, kThreads, kAsyncSmemBytes));
     const int g = sms * std::max(1, per);
     if (device >= 0 && device < 64) cached[device] = g;

@@ -632,17 +632,7 @@ bool make_rlayout(const CgParams& p, int mt, int nt, RLayout& L) {
 template <int MT, int NT>
 void launch_res(const RDev& d, int grid, std::size_t smem, cudaStream_t st) {
     auto* fn = cg_res_kernel<MT, NT>;
-    static std::mutex mu;
-    static std::size_t set_to[64] = {};  // per device: the attribute only ever grows
-    int dev = 0;
-    CPK_CUDA(cudaGetDevice(&dev));
-    {
-        std::lock_guard<std::mutex> lock(mu);
-        if (dev < 0 || dev >= 64 || set_to[dev] < smem) {
-            CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            if (dev >= 0 && dev < 64) set_to[dev] = smem;
-        }
-    }
+    ensure_dynamic_smem(fn, smem);  // grow-only per device, under the process-wide mutex
     RDev dd = d;
     void* args[] = {&dd};
     CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(MT * NT * 32), args, smem, st));

@@ -581,19 +581,18 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
 template <int NB>
 void solve_rows_nb(const double* l, int R, const double* b, long long rows, double* y, long long l_stride, int nmats,
                    long long rows_per_mat, cudaStream_t st, const double* old = nullptr, double* row_sq = nullptr) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = device_sm_count();
     const long long per_mat_ctas = std::max<long long>(
         1, std::min<long long>((rows_per_mat + kSolveWarps - 1) / kSolveWarps, std::max(1, 2 * sms / nmats)));
     const dim3 grid(static_cast<unsigned>(per_mat_ctas), nmats);
     const Layout lay = layout_of(R);
     if (lay == kSquareSmem) {
         auto fn = chol_solve_rows_kernel<NB, SqIdx, true>;
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        ensure_dynamic_smem(fn, sq_bytes(R));
         fn<<<grid, 32 * kSolveWarps, sq_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat, old, row_sq);
     } else if (lay == kPackedSmem) {
         auto fn = chol_solve_rows_kernel<NB, PkIdx, true>;
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
+        ensure_dynamic_smem(fn, pk_bytes(R));
         fn<<<grid, 32 * kSolveWarps, pk_bytes(R), st>>>(l, R, b, rows, y, l_stride, rows_per_mat, old, row_sq);
     } else {
         chol_solve_rows_kernel<NB, SqIdx, false><<<grid, 32 * kSolveWarps, 0, st>>>(l, R, b, rows, y, l_stride,
@@ -685,15 +684,15 @@ void launch_chol_batch_src(double* s, const double* grams, int order, int excl, 
     }
     if (blocked) {
         auto fn = chol_blocked_kernel<16>;
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        ensure_dynamic_smem(fn, sq_bytes(R));
         fn<<<count, 256, sq_bytes(R), st>>>(CholSrc{s, grams, order, excl, s_stride}, R, *lambda, mode, l_out, status);
     } else if (lay == kSquareSmem) {
         auto fn = chol_kernel<SqIdx, true>;
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sq_bytes(R))));
+        ensure_dynamic_smem(fn, sq_bytes(R));
         fn<<<count, 512, sq_bytes(R), st>>>(s, R, *lambda, mode, l_out, status, s_stride);
     } else if (lay == kPackedSmem) {
         auto fn = chol_kernel<PkIdx, true>;
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pk_bytes(R))));
+        ensure_dynamic_smem(fn, pk_bytes(R));
         fn<<<count, 512, pk_bytes(R), st>>>(s, R, *lambda, mode, l_out, status, s_stride);
     } else {
         chol_kernel<SqIdx, false><<<count, 512, 0, st>>>(s, R, *lambda, mode, l_out, status, s_stride);

@@ -544,15 +544,7 @@ KrpDev to_dev(const KrpDesc& d) {
     return k;
 }
 
-int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        CPK_CUDA(cudaGetDevice(&dev));
-        CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return sms;
-}
+int num_sms() { return device_sm_count(); }  // per device (runtime.cu)
 
 // ---- tile planning --------------------------------------------------------
 // CTA tile = (16 WM rows) x (8 NTW WN rank columns); WM x WN DMMA warps + 1
@@ -779,8 +771,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
     case NTV: {                                                                                    \
         auto fn = runs_full(p) ? root_gemm_kernel<NTV, TRANS, GEN, true>                          \
                                : root_gemm_kernel<NTV, TRANS, GEN, false>;                         \
-        CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,              \
-                                      static_cast<int>(smem)));                                    \
+        ensure_dynamic_smem(fn, smem);                                                             \
         if (std::getenv("CPKIT_GRID_OCC")) { /* experiments: grid from the real occupancy */        \
             int occ = 1;                                                                           \
             CPK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, static_cast<int>(block.x), smem)); \

@@ -591,8 +591,7 @@ void launch_gradient_all(const double* a, const double* pair, const double* m, c
     }
     gd.off[order] = off[order];
     const std::size_t smem = (tile::kT * (tile::kPB + 4) + tile::kPB * tile::kKS) * sizeof(double);
-    CPK_CUDA(cudaFuncSetAttribute(gradient_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    ensure_dynamic_smem(gradient_all_kernel, smem);
     gradient_all_kernel<<<static_cast<int>(std::min<long long>(tasks, 2 * 148)), tile::kThreads, smem, st>>>(
         gd, a, pair, m, R, g);
     ::cpkit::count_launch(1);
@@ -602,7 +601,7 @@ void launch_gradient(const double* a, const double* gnn, const double* m, std::i
                      double* g, cudaStream_t st) {
     const long long tasks = ((rows + tile::kT - 1) / tile::kT) * ((R + tile::kT - 1) / tile::kT);
     const std::size_t smem = (tile::kT * (tile::kPB + 4) + tile::kPB * tile::kKS) * sizeof(double);
-    CPK_CUDA(cudaFuncSetAttribute(gradient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_dynamic_smem(gradient_kernel, smem);
     gradient_kernel<<<static_cast<int>(std::min<long long>(tasks, 2 * 148)), tile::kThreads, smem, st>>>(
         a, gnn, m, rows, R, g); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());

@@ -794,7 +794,7 @@ bool tiny_layout(int order, const std::uint64_t* dims, int rank, TinyLayout& L, 
 
 void launch_tiny(const TinyParams& p, cudaStream_t st) {
     const std::size_t smem = static_cast<std::size_t>(p.layout.total) * sizeof(double);
-    CPK_CUDA(cudaFuncSetAttribute(tiny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    ensure_dynamic_smem(tiny_kernel, smem);
     tiny_kernel<<<p.count, p.threads > 0 ? p.threads : kTinyThreads, smem, st>>>(p);
     count_launch(1);
     CPK_CUDA(cudaGetLastError());

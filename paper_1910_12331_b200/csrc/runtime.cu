@@ -5,7 +5,9 @@
 
 #include <atomic>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "solver.h"
 
@@ -17,6 +19,33 @@ std::atomic<std::uint64_t> g_launches{0};
 }
 void count_launch(int n) { g_launches.fetch_add(static_cast<std::uint64_t>(n), std::memory_order_relaxed); }
 std::uint64_t kernel_launches() { return g_launches.load(); }
+
+// ---------------------------------------------------------------- launch attributes
+namespace {
+std::mutex g_attr_mu;
+std::map<int, int> g_sms;                                   // device -> SM count
+std::map<std::pair<int, const void*>, std::size_t> g_smem;  // (device, kernel) -> limit set
+}  // namespace
+int device_sm_count() {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    auto it = g_sms.find(dev);
+    if (it != g_sms.end()) return it->second;
+    int sms = 0;
+    CPK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    g_sms[dev] = sms;
+    return sms;
+}
+void ensure_dynamic_smem(const void* fn, std::size_t bytes) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    std::size_t& cur = g_smem[{dev, fn}];
+    if (cur >= bytes) return;
+    CPK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    cur = bytes;
+}
 
 // ---------------------------------------------------------------- NCCL (dlopen'd)
 // The library links no NCCL at build time; the sharded path resolves the

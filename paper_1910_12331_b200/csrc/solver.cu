@@ -1444,6 +1444,7 @@ GnStepDiag DeviceProblem::gn_decode(const GnConfig& cfg, double lambda, int slot
     double* hm = hmap_ + kGnMapOff + slot * kGnMapDoubles;
     const int o_gn = 3, o_st = 4, o_cg = 4 + N, o_step = 9 + N, o_after = 11 + N;
     CPK_CUDA(cudaEventSynchronize(gn_ev_[slot]));
+    gn_failed_applied_ = false;
     GnStepDiag diag;
     const double res = hm[0];
     diag.residual_before = res;
@@ -1480,7 +1481,10 @@ GnStepDiag DeviceProblem::gn_decode(const GnConfig& cfg, double lambda, int slot
     }
     diag.alpha = 1.0;
     diag.step_norm = hm[o_step];
-    if (hm[o_step + 1] == 0.0) throw NumericalFailure("gn_step: non-finite factors after update");
+    if (hm[o_step + 1] == 0.0) {
+        gn_failed_applied_ = true;  // the step was applied (the reference throws after its update too)
+        throw NumericalFailure("gn_step: non-finite factors after update");
+    }
     diag.residual_after = hm[o_after];
     diag.stepped = true;
     return diag;
@@ -1681,6 +1685,9 @@ std::pair<KruskalModel, ConvergenceReport> gn_optimize(DeviceProblem& p, Kruskal
             try {
                 diag = p.gn_decode(cfg, schedule.lambda, slot);  // undoes step iter itself when it must
             } catch (...) {
+                // step iter applied a non-finite update and step iter+1 ran on top of
+                // it: leave the factors the sequential loop leaves (after step iter)
+                if (spec && p.gn_failed_applied()) p.restore_factors_from(p.gn_snapshot(slot ^ 1));
                 p.ctx().sync();
                 throw;
             }

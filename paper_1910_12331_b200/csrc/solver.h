@@ -250,6 +250,8 @@ public:
     void gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule, double xnorm2, int slot);
     GnStepDiag gn_decode(const GnConfig& cfg, double lambda, int slot);
     void restore_factors_from(const double* dev_src);  // factors <- device copy, caches dropped
+    // the last gn_decode threw after its step had been applied (non-finite update)
+    bool gn_failed_applied() const { return gn_failed_applied_; }
     const double* gn_snapshot(int slot) const { return slot == 0 ? Atrial_.get() : Asnap1_.get(); }
 
 private:
@@ -258,6 +260,7 @@ private:
     // ctx_.ev[1]. pinv_ready_ marks a chain launched ahead for (lambda, shape).
     void launch_precond_chain(double lambda, RegShape shape, bool grams_and_gamma);
     bool pinv_ready_ = false;
+    bool gn_failed_applied_ = false;
     // the residual slots hold the residual of the current factors for res_xnorm_
     bool res_current_ = false;
     double res_xnorm_ = 0.0;
