@@ -20,6 +20,7 @@
 // Build: oracle/Makefile -> oracle/build/libcpkit_oracle.so (C ABI below).
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -484,28 +485,149 @@ GammaSet build_gamma_set(const Model& model) {
 }
 // kruskal.cpp:67-92 (dense evaluation, reference per-entry order)
 std::vector<double> reconstruct(const Model& model) {
+    // kruskal.cpp:76-90 per entry: acc = sum_r (((1 A_0) A_1) ... A_{N-1}), r
+    // ascending, separate multiply and add. The product over modes 0..N-2 is
+    // the same for every last-mode index, so it is formed once per prefix row
+    // (the same roundings); the last-mode loop then runs across j.
     std::uint64_t total = 1;
     for (auto d : model.dims) total *= d;
     const std::size_t order = model.order();
     std::vector<double> t(total);
     const std::uint64_t R = static_cast<std::uint64_t>(model.rank);
-    std::vector<std::uint64_t> stride(order, 1);
-    for (std::size_t m = order - 1; m-- > 0;) stride[m] = stride[m + 1] * model.dims[m + 1];
-    parallel_rows(static_cast<std::int64_t>(total), [&](std::int64_t lo, std::int64_t hi) {
+    const std::uint64_t sl = model.dims[order - 1];
+    const std::uint64_t rows = total / sl;
+    std::vector<double> bt(R * sl);  // last factor transposed: bt[r][j]
+    for (std::uint64_t j = 0; j < sl; ++j)
+        for (std::uint64_t r = 0; r < R; ++r) bt[r * sl + j] = model.factors[order - 1].d[j * R + r];
+    parallel_rows(static_cast<std::int64_t>(rows), [&](std::int64_t lo, std::int64_t hi) {
+        std::vector<double> pre(R), acc(sl);
+        std::vector<std::uint64_t> idx(order, 0);
         for (std::int64_t f = lo; f < hi; ++f) {
-            double acc = 0.0;
+            std::uint64_t q = static_cast<std::uint64_t>(f);
+            for (std::size_t m = order - 1; m-- > 0;) {
+                idx[m] = q % model.dims[m];
+                q /= model.dims[m];
+            }
             for (std::uint64_t r = 0; r < R; ++r) {
                 double prod = 1.0;
-                for (std::size_t n = 0; n < order; ++n) {
-                    const std::uint64_t i = (static_cast<std::uint64_t>(f) / stride[n]) % model.dims[n];
-                    prod *= model.factors[n].d[i * R + r];
-                }
-                acc += prod;
+                for (std::size_t n = 0; n + 1 < order; ++n) prod *= model.factors[n].d[idx[n] * R + r];
+                pre[r] = prod;
             }
-            t[static_cast<std::size_t>(f)] = acc;
+            std::fill(acc.begin(), acc.end(), 0.0);
+            for (std::uint64_t r = 0; r < R; ++r) {
+                const double pr = pre[r];
+                const double* br = bt.data() + r * sl;
+                for (std::uint64_t j = 0; j < sl; ++j) acc[j] += pr * br[j];
+            }
+            std::memcpy(t.data() + static_cast<std::uint64_t>(f) * sl, acc.data(), sl * 8);
         }
     });
     return t;
+}
+
+// ---------------------------------------------------------------- keyed noise
+// Restatement of the product's noise definition (BASELINE configs 2 and 5:
+// Gaussian noise scaled to rel ||X||_F; SURVEY.md §8d stream 0x4E01). The
+// reference generates no noise; the product defines it so that a GPU and this
+// CPU restatement produce the same bits: rng.hpp:40-46's Box-Muller with log
+// and cos evaluated by fixed polynomial programs of correctly rounded
+// +, -, *, /, sqrt (this file is built with -ffp-contract=off), keyed at each
+// entry's global flat index; ||X||^2 and ||E||^2 summed in a fixed
+// column-block order that does not depend on how the last mode is sharded.
+constexpr int kNoiseBlocks = 256;
+double portable_log(double u) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &u, 8);
+    int e = static_cast<int>((bits >> 52) & 0x7FF) - 1022;
+    bits = (bits & 0x000FFFFFFFFFFFFFull) | (static_cast<std::uint64_t>(1022) << 52);
+    double m;
+    std::memcpy(&m, &bits, 8);
+    if (m < 0x1.6a09e667f3bcdp-1) {
+        m *= 2.0;
+        e -= 1;
+    }
+    const double s = (m - 1.0) / (m + 1.0), z = s * s;
+    static const double kl[14] = {0x1.0000000000000p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3,
+                                  0x1.2492492492492p-3, 0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4,
+                                  0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4, 0x1.e1e1e1e1e1e1ep-5,
+                                  0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5,
+                                  0x1.47ae147ae147bp-5, 0x1.2f684bda12f68p-5};
+    double p = kl[13];
+    for (int i = 12; i >= 0; --i) p = p * z + kl[i];
+    const double de = static_cast<double>(e);
+    return de * 0x1.62e42fee00000p-1 + (de * 0x1.a39ef35793c76p-33 + (2.0 * s) * p);
+}
+double portable_cos_2pi(double u) {
+    const double t = u * 4.0;
+    const int k = static_cast<int>(t);
+    const double r = t - static_cast<double>(k);
+    const double th = r * 0x1.921fb54442d18p+0, z = th * th;
+    static const double kc[14] = {0x1.0000000000000p+0,  -0x1.0000000000000p-1, 0x1.5555555555555p-5,
+                                  -0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-16,  -0x1.27e4fb7789f5cp-22,
+                                  0x1.1eed8eff8d898p-29,  -0x1.93974a8c07c9dp-37, 0x1.ae7f3e733b81fp-45,
+                                  -0x1.6827863b97d97p-53, 0x1.e542ba4020225p-62,  -0x1.0ce396db7f853p-70,
+                                  0x1.f2cf01972f578p-80,  -0x1.88e85fc6a4e59p-89};
+    static const double ks[13] = {0x1.0000000000000p+0,  -0x1.5555555555555p-3, 0x1.1111111111111p-7,
+                                  -0x1.a01a01a01a01ap-13, 0x1.71de3a556c734p-19,  -0x1.ae64567f544e4p-26,
+                                  0x1.6124613a86d09p-33,  -0x1.ae7f3e733b81fp-41, 0x1.952c77030ad4ap-49,
+                                  -0x1.2f49b46814157p-57, 0x1.71b8ef6dcf572p-66,  -0x1.761b413163819p-75,
+                                  0x1.3f3ccdd165fa9p-84};
+    double cc = kc[13], ss = ks[12];
+    for (int i = 12; i >= 0; --i) cc = cc * z + kc[i];
+    for (int i = 11; i >= 0; --i) ss = ss * z + ks[i];
+    ss *= th;
+    switch (k & 3) {
+        case 0: return cc;
+        case 1: return -ss;
+        case 2: return -cc;
+        default: return ss;
+    }
+}
+double noise_gaussian(std::uint64_t base, std::uint64_t gidx) {
+    const std::uint64_t h = derive(base, gidx);
+    const double u1 = static_cast<double>((derive(h, 1) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = static_cast<double>(derive(h, 2) >> 11) * 0x1.0p-53;
+    return std::sqrt(-2.0 * portable_log(u1)) * portable_cos_2pi(u2);
+}
+// x (full tensor, last extent sl) += scale E; returns {scale, ||X||^2, ||E||^2}
+std::array<double, 3> add_noise(double* x, const std::vector<std::uint64_t>& dims, std::uint64_t seed, double rel) {
+    std::uint64_t total = 1;
+    for (auto d : dims) total *= d;
+    const std::uint64_t sl = dims.back(), rows = total / sl;
+    const std::uint64_t blk = (rows + kNoiseBlocks - 1) / kNoiseBlocks;
+    const std::uint64_t base = derive(mix64(seed), 0x4E01);
+    std::vector<double> part(2 * kNoiseBlocks * sl, 0.0);  // [X | E][block][column]
+    parallel_rows(kNoiseBlocks, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t b = lo; b < hi; ++b) {
+            double* px = part.data() + static_cast<std::uint64_t>(b) * sl;
+            double* pe = part.data() + (kNoiseBlocks + static_cast<std::uint64_t>(b)) * sl;
+            const std::uint64_t r1 = std::min(rows, (static_cast<std::uint64_t>(b) + 1) * blk);
+            for (std::uint64_t r = static_cast<std::uint64_t>(b) * blk; r < r1; ++r)
+                for (std::uint64_t j = 0; j < sl; ++j) {
+                    const double v = x[r * sl + j];
+                    px[j] += v * v;
+                    const double g = noise_gaussian(base, r * sl + j);
+                    pe[j] += g * g;
+                }
+        }
+    });
+    double nx = 0.0, ne = 0.0;
+    for (std::uint64_t j = 0; j < sl; ++j) {
+        double cx = 0.0, ce = 0.0;
+        for (int b = 0; b < kNoiseBlocks; ++b) {
+            cx += part[static_cast<std::uint64_t>(b) * sl + j];
+            ce += part[(kNoiseBlocks + static_cast<std::uint64_t>(b)) * sl + j];
+        }
+        nx += cx;
+        ne += ce;
+    }
+    // (columns in ascending j: the GPU sums rank blocks in rank order, i.e. the same order)
+    const double scale = rel * std::sqrt(nx) / std::sqrt(ne);
+    parallel_rows(static_cast<std::int64_t>(rows), [&](std::int64_t lo, std::int64_t hi) {
+        for (std::uint64_t e = static_cast<std::uint64_t>(lo) * sl; e < static_cast<std::uint64_t>(hi) * sl; ++e)
+            x[e] += scale * noise_gaussian(base, e);
+    });
+    return {scale, nx, ne};
 }
 // kruskal.cpp:94-118
 std::pair<double, double> residual_fitness(const Model& model, const Tensor& x, double xnorm2,
@@ -1069,6 +1191,15 @@ int orc_get_threads(void) { return orc::g_threads; }
 uint64_t orc_mix64(uint64_t x) { return orc::mix64(x); }
 uint64_t orc_keyed(uint64_t s, uint64_t st, uint64_t i, uint64_t salt) { return orc::keyed(s, st, i, salt); }
 double orc_uniform(uint64_t s, uint64_t st, uint64_t i, double a, double b) { return orc::uniform(s, st, i, a, b); }
+double orc_noise_gaussian(uint64_t seed, uint64_t gidx) {
+    return orc::noise_gaussian(orc::derive(orc::mix64(seed), 0x4E01), gidx);
+}
+int orc_add_noise(const uint64_t* dims, int order, double* x, uint64_t seed, double rel, double* out3) {
+    return guarded([&] {
+        auto r = orc::add_noise(x, std::vector<std::uint64_t>(dims, dims + order), seed, rel);
+        if (out3) std::memcpy(out3, r.data(), 3 * 8);
+    });
+}
 double orc_gaussian(uint64_t s, uint64_t st, uint64_t i) { return orc::gaussian(s, st, i); }
 uint64_t orc_problem_seed(uint64_t m, int r, int p) { return orc::problem_seed(m, r, p); }
 uint64_t orc_init_seed(uint64_t m, int r, int p, int i) { return orc::init_seed(m, r, p, i); }

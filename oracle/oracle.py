@@ -99,6 +99,9 @@ def lib():
         L.orc_init_seed.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int]
         L.orc_norm2.restype = C.c_double
         L.orc_norm2.argtypes = [_u64p, C.c_int, _dp]
+        L.orc_noise_gaussian.restype = C.c_double
+        L.orc_noise_gaussian.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_add_noise.argtypes = [_u64p, C.c_int, _dp, C.c_uint64, C.c_double, _dp]
         _lib = L
     return _lib
 
@@ -153,6 +156,20 @@ def uniform(seed, stream, index, a=0.0, b=1.0) -> float:
 
 def gaussian(seed, stream, index) -> float:
     return lib().orc_gaussian(seed, stream, index)
+
+
+def noise_gaussian(seed: int, gidx: int) -> float:
+    """The keyed noise draw (stream 0x4E01, portable log/cos) at global flat index gidx."""
+    return lib().orc_noise_gaussian(seed, gidx)
+
+
+def add_noise(x: np.ndarray, seed: int, rel: float):
+    """x += scale * E in place (C-contiguous float64 tensor); returns (scale, ||X||^2, ||E||^2)."""
+    if not (x.dtype == np.float64 and x.flags.c_contiguous):
+        raise ValueError("add_noise: need a C-contiguous float64 tensor")
+    out = np.empty(3)
+    _chk(lib().orc_add_noise(_dims(x.shape), x.ndim, _dptr(x), seed, rel, _dptr(out)))
+    return float(out[0]), float(out[1]), float(out[2])
 
 
 def problem_seed(master: int, rank: int, problem: int) -> int:

@@ -84,6 +84,11 @@ int device_sm_count();
 // `bytes`: grow-only per (device, function) under one process-wide mutex, so
 // a solve on another thread can never lower it under this one's launch.
 void ensure_dynamic_smem(const void* fn, std::size_t bytes);
+// Cooperative (grid-barrier) kernels of different streams must not run at the
+// same time on one device: two partially resident grids could wait on each
+// other's SMs. Every cooperative launch goes through this: the stream waits for
+// the device's previous cooperative launch, launches, and becomes the new tail.
+void launch_cooperative(const void* fn, dim3 grid, dim3 block, void** args, std::size_t smem, cudaStream_t st);
 template <typename F>
 inline void ensure_dynamic_smem(F* fn, std::size_t bytes) {
     ensure_dynamic_smem(reinterpret_cast<const void*>(fn), bytes);
@@ -177,11 +182,19 @@ void launch_pack_sweep(const double* scal, int kstep, int kres, const int* flag,
 // Dense evaluation of a Kruskal model + keyed-RNG noise (generators / reconstruct)
 void launch_reconstruct(const KrpDesc& all, int R, double* out, std::uint64_t offset, std::uint64_t n,
                         cudaStream_t st);
-void launch_gaussian_fill(std::uint64_t seed, std::uint64_t stream, double* out, std::uint64_t n,
-                          std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
-                          cudaStream_t st);
-void launch_scaled_add(double* y, const double* x, const double* scale_num, const double* scale_den,
-                       double factor, std::uint64_t n, cudaStream_t st);
+// Keyed noise (keyed_noise.cuh), bit-identical to the CPU restatement and
+// independent of the GPU count. Slab view: rows (all modes but the last) x
+// slab columns (this rank's last-mode indices, global offset slab_lo).
+std::size_t noise_workspace_elems(std::int64_t slab);
+// colsq[0..slab) = per-column sum of X^2, colsq[slab..2 slab) = of E^2 (ws: noise_workspace_elems)
+void launch_noise_colsq(const double* x, std::int64_t rows, std::int64_t slab, std::uint64_t seed,
+                        std::uint64_t s_last, std::uint64_t slab_lo, double* ws, double* colsq, cudaStream_t st);
+// out3 = [rel ||X|| / ||E||, ||X||^2, ||E||^2] from every rank's [X cols | E cols] block (rank-major)
+void launch_noise_scale(const double* colsq_all, int world, std::int64_t slab, double rel, double* out3,
+                        cudaStream_t st);
+// x += scale[0] * E (no fused multiply-add)
+void launch_noise_add(double* x, std::uint64_t n, std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
+                      std::uint64_t seed, const double* scale, cudaStream_t st);
 
 // Cholesky-based SPD kernels (kernels_chol.cu); status: 0 ok, 1 ok after jitter, 2 singular
 // chol_factor_elems(count, R) doubles hold the factors (row stride R + 1).

@@ -536,8 +536,8 @@ int occupancy_grid(int device) {
 void launch_coop(const Dev& d, int grid, cudaStream_t st) {
     Dev dd = d;
     void* args[] = {&dd};
-    CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_kernel), dim3(grid),
-                                         dim3(kThreads), args, kAsyncSmemBytes, st));
+    launch_cooperative(reinterpret_cast<const void*>(cg_kernel), dim3(grid), dim3(kThreads), args, kAsyncSmemBytes,
+                       st);
     count_launch(1);
 }
 

@@ -635,7 +635,7 @@ void launch_res(const RDev& d, int grid, std::size_t smem, cudaStream_t st) {
     ensure_dynamic_smem(fn, smem);  // grow-only per device, under the process-wide mutex
     RDev dd = d;
     void* args[] = {&dd};
-    CPK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(fn), dim3(grid), dim3(MT * NT * 32), args, smem, st));
+    launch_cooperative(reinterpret_cast<const void*>(fn), dim3(grid), dim3(MT * NT * 32), args, smem, st);
     count_launch(1);
 }
 

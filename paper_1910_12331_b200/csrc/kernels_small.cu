@@ -8,6 +8,7 @@
 #include <cstdlib>
 
 #include "common.h"
+#include "keyed_noise.cuh"
 #include "tile_gemm.cuh"
 
 namespace cpkit {
@@ -468,29 +469,59 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
 __device__ __forceinline__ unsigned long long derive(unsigned long long h, unsigned long long v) {
     return mix64(h ^ (v * 0xD6E8FEB86659FD93ull + 0xA0761D6478BD642Full));
 }
-// Noise entry e of a (possibly last-mode-sharded) slab uses the keyed index of
-// its GLOBAL flat position so the noise is independent of the GPU count.
-__global__ void gaussian_fill_kernel(unsigned long long seed, unsigned long long stream,
-                                     double* __restrict__ out, unsigned long long n,
-                                     unsigned long long slab, unsigned long long s_last,
-                                     unsigned long long slab_lo) {
-    const unsigned long long base = derive(mix64(seed), stream);
-    for (unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
-         e < n; e += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
-        const unsigned long long gidx = (e / slab) * s_last + slab_lo + (e % slab);
-        const unsigned long long h = derive(base, gidx);
-        const double u1 = static_cast<double>((derive(h, 1) >> 11) + 1) * 0x1.0p-53;
-        const double u2 = static_cast<double>(derive(h, 2) >> 11) * 0x1.0p-53;
-        out[e] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+// ---- keyed noise (keyed_noise.cuh): entry (f', j) of a last-mode slab has the
+// keyed index of its GLOBAL flat position f' s_last + slab_lo + j.
+// Column-block sums of X^2 and E^2: thread (b, j) sums rows [b blk, (b+1) blk)
+// of column j sequentially (adjacent threads read adjacent columns).
+__global__ void noise_colsq_part_kernel(const double* __restrict__ x, long long rows, long long slab,
+                                        long long blk, unsigned long long base, unsigned long long s_last,
+                                        unsigned long long slab_lo, double* __restrict__ part) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(noise::kNoiseBlocks) * slab) return;
+    const long long b = t / slab, j = t % slab;
+    const long long r0 = b * blk, r1 = min(rows, r0 + blk);
+    double ax = 0.0, ae = 0.0;
+    for (long long r = r0; r < r1; ++r) {
+        const double v = x[r * slab + j];
+        ax = __dadd_rn(ax, __dmul_rn(v, v));
+        const double g = noise::keyed_gaussian(base, static_cast<unsigned long long>(r) * s_last + slab_lo +
+                                                         static_cast<unsigned long long>(j));
+        ae = __dadd_rn(ae, __dmul_rn(g, g));
     }
+    part[b * slab + j] = ax;
+    part[(noise::kNoiseBlocks + b) * slab + j] = ae;
 }
-__global__ void scaled_add_kernel(double* __restrict__ y, const double* __restrict__ x,
-                                  const double* num, const double* den, double factor,
-                                  unsigned long long n) {
-    const double s = factor * sqrt(*num) / sqrt(*den);
-    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x;
-         i < n; i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
-        y[i] += s * x[i];
+// colsq[j] (X) and colsq[slab + j] (E): the block partials of column j in block order
+__global__ void noise_colsq_final_kernel(const double* __restrict__ part, long long slab, double* __restrict__ colsq) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= 2 * slab) return;
+    const long long which = t / slab, j = t % slab;
+    double a = 0.0;
+    for (int b = 0; b < noise::kNoiseBlocks; ++b) a = __dadd_rn(a, part[(which * noise::kNoiseBlocks + b) * slab + j]);
+    colsq[t] = a;
+}
+// scale = rel ||X|| / ||E|| from the gathered per-rank [X cols | E cols] blocks, columns in global order
+__global__ void noise_scale_kernel(const double* __restrict__ colsq, int world, long long slab, double rel,
+                                   double* __restrict__ out) {
+    double nx = 0.0, ne = 0.0;
+    for (int g = 0; g < world; ++g)
+        for (long long j = 0; j < slab; ++j) {
+            nx = __dadd_rn(nx, colsq[g * 2 * slab + j]);
+            ne = __dadd_rn(ne, colsq[g * 2 * slab + slab + j]);
+        }
+    out[0] = __ddiv_rn(__dmul_rn(rel, __dsqrt_rn(nx)), __dsqrt_rn(ne));
+    out[1] = nx;
+    out[2] = ne;
+}
+__global__ void noise_add_kernel(double* __restrict__ x, unsigned long long n, unsigned long long slab,
+                                 unsigned long long s_last, unsigned long long slab_lo, unsigned long long base,
+                                 const double* __restrict__ scale) {
+    const double s = scale[0];
+    for (unsigned long long e = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        const unsigned long long gidx = (e / slab) * s_last + slab_lo + (e % slab);
+        x[e] = __dadd_rn(x[e], __dmul_rn(s, noise::keyed_gaussian(base, gidx)));
+    }
 }
 
 int grid_for(unsigned long long n, int threads, int cap = kRedBlocksMax) {
@@ -714,17 +745,31 @@ void launch_reconstruct(const KrpDesc& all, int R, double* out, std::uint64_t of
     CPK_CUDA(cudaGetLastError());
 }
 
-void launch_gaussian_fill(std::uint64_t seed, std::uint64_t stream, double* out, std::uint64_t n,
-                          std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
-                          cudaStream_t st) {
-    gaussian_fill_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(seed, stream, out, n, slab, s_last,
-                                                                      slab_lo); ::cpkit::count_launch(1);
+std::size_t noise_workspace_elems(std::int64_t slab) {
+    return static_cast<std::size_t>(2 * noise::kNoiseBlocks + 2) * static_cast<std::size_t>(slab);
+}
+void launch_noise_colsq(const double* x, std::int64_t rows, std::int64_t slab, std::uint64_t seed,
+                        std::uint64_t s_last, std::uint64_t slab_lo, double* ws, double* colsq, cudaStream_t st) {
+    const long long blk = (rows + noise::kNoiseBlocks - 1) / noise::kNoiseBlocks;
+    const unsigned long long base = noise::nz_derive(noise::nz_mix64(seed), noise::kNoiseStream);
+    const long long threads = static_cast<long long>(noise::kNoiseBlocks) * slab;
+    noise_colsq_part_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, st>>>(x, rows, slab, blk, base,
+                                                                                          s_last, slab_lo, ws);
+    noise_colsq_final_kernel<<<static_cast<unsigned>((2 * slab + 127) / 128), 128, 0, st>>>(ws, slab, colsq);
+    ::cpkit::count_launch(2);
     CPK_CUDA(cudaGetLastError());
 }
-
-void launch_scaled_add(double* y, const double* x, const double* num, const double* den,
-                       double factor, std::uint64_t n, cudaStream_t st) {
-    scaled_add_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(y, x, num, den, factor, n); ::cpkit::count_launch(1);
+void launch_noise_scale(const double* colsq_all, int world, std::int64_t slab, double rel, double* out3,
+                        cudaStream_t st) {
+    noise_scale_kernel<<<1, 1, 0, st>>>(colsq_all, world, slab, rel, out3);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
+void launch_noise_add(double* x, std::uint64_t n, std::uint64_t slab, std::uint64_t s_last, std::uint64_t slab_lo,
+                      std::uint64_t seed, const double* scale, cudaStream_t st) {
+    const unsigned long long base = noise::nz_derive(noise::nz_mix64(seed), noise::kNoiseStream);
+    noise_add_kernel<<<grid_for(n, 256, 148 * 16), 256, 0, st>>>(x, n, slab, s_last, slab_lo, base, scale);
+    ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
 

@@ -37,6 +37,20 @@ int device_sm_count() {
     g_sms[dev] = sms;
     return sms;
 }
+namespace {
+std::mutex g_coop_mu;
+std::map<int, cudaEvent_t> g_coop_tail;  // device -> completion of its last cooperative launch
+}  // namespace
+void launch_cooperative(const void* fn, dim3 grid, dim3 block, void** args, std::size_t smem, cudaStream_t st) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_coop_mu);
+    cudaEvent_t& tail = g_coop_tail[dev];
+    if (!tail) CPK_CUDA(cudaEventCreateWithFlags(&tail, cudaEventDisableTiming));
+    else CPK_CUDA(cudaStreamWaitEvent(st, tail, 0));  // no-op when the last one was on this stream
+    CPK_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, st));
+    CPK_CUDA(cudaEventRecord(tail, st));
+}
 void ensure_dynamic_smem(const void* fn, std::size_t bytes) {
     int dev = 0;
     CPK_CUDA(cudaGetDevice(&dev));

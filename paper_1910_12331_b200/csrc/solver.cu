@@ -563,7 +563,8 @@ void DeviceProblem::download_tensor(double* host_local) {
 
 // Device-side low-rank (+ noise) generation: the reference's reconstruct
 // order per entry (kruskal.cpp:76-90) with non-fused multiply/add, so the
-// noiseless tensor is bitwise equal to the CPU generator's.
+// noiseless tensor is bitwise equal to the CPU generator's; the keyed noise
+// (keyed_noise.cuh) is bitwise equal to the CPU restatement's too.
 void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel) {
     set_factors(truth);
     const int N = order();
@@ -578,16 +579,22 @@ void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noi
     }
     launch_reconstruct(all, R_, xd, 0, local_elems_, ctx_.stream);
     if (noise_rel > 0.0) {
-        // noise E ~ N(0,1) (keyed, stream 0x4E01), scaled to noise_rel * ||X|| / ||E||
-        DevBuf<double> e(local_elems_);
-        launch_gaussian_fill(noise_seed, 0x4E01, e.get(), local_elems_, slab_hi_ - slab_lo_, dims_[N - 1], slab_lo_,
-                             ctx_.stream);
-        const int parts = norm2_parts(local_elems_);
-        launch_norm2(xd, local_elems_, partials_.get(), parts, scal_.get() + 8, ctx_.stream);
-        launch_norm2(e.get(), local_elems_, partials_.get() + parts, parts, scal_.get() + 9, ctx_.stream);
-        if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + 8, 2, ctx_.stream);
-        launch_scaled_add(xd, e.get(), scal_.get() + 8, scal_.get() + 9, noise_rel, local_elems_,
-                          ctx_.stream);
+        // keyed noise E (stream 0x4E01) scaled to noise_rel ||X|| / ||E||, with no
+        // tensor-sized buffer: pass 1 sums X^2 and E^2 per last-mode column (E
+        // recomputed from its key), the columns are gathered and summed in global
+        // order (the same bits for every GPU count), pass 2 adds scale * E
+        const std::int64_t slab = local_rows_[N - 1];
+        const std::int64_t rows = static_cast<std::int64_t>(local_elems_) / slab;
+        const int world = ctx_.world();
+        const std::size_t wse = noise_workspace_elems(slab);
+        DevBuf<double> nws(wse + 2 * static_cast<std::size_t>(slab) * world);
+        double* cs = nws.get() + wse - 2 * slab;  // this rank's [X cols | E cols]
+        double* all = nws.get() + wse;
+        launch_noise_colsq(xd, rows, slab, noise_seed, dims_[N - 1], slab_lo_, nws.get(), cs, ctx_.stream);
+        if (ctx_.comm) ctx_.comm->allgather(cs, all, 2 * static_cast<std::size_t>(slab), ctx_.stream);
+        launch_noise_scale(ctx_.comm ? all : cs, world, slab, noise_rel, scal_.get() + 8, ctx_.stream);
+        launch_noise_add(xd, local_elems_, static_cast<std::uint64_t>(slab), dims_[N - 1], slab_lo_, noise_seed,
+                         scal_.get() + 8, ctx_.stream);
     }
     if (Bs_ != Bl_)
         CPK_CUDA(cudaMemcpy2DAsync(x_.get(), Bs_ * sizeof(double), xd, Bl_ * sizeof(double), Bl_ * sizeof(double),
