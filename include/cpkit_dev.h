@@ -34,6 +34,14 @@ CPKIT_API cpkit_status cpkit_dev_problem_create_sharded(int device, const uint64
                                                         uint64_t rank, int shard, int world,
                                                         const void* nccl_id128,
                                                         cpkit_dev_problem** out);
+/* TEST ONLY: `world` last-mode shards of one problem on ONE device, joined by
+ * an in-process loopback group instead of NCCL (collectives become device
+ * copies and a fixed rank-order sum; ranks meet on the host). Fills out[0..world).
+ * Each shard must be driven by its own host thread, issuing the same call
+ * sequence on every shard, exactly as NCCL ranks would. Lets one GPU run the
+ * sharded code path of a multi-GPU job. */
+CPKIT_API cpkit_status cpkit_dev_problem_create_loopback(int device, const uint64_t* dims, uint64_t order,
+                                                         uint64_t rank, int world, cpkit_dev_problem** out);
 CPKIT_API void cpkit_dev_problem_destroy(cpkit_dev_problem* p);
 /* [lo, hi) rows of the last mode owned by this problem, and its element count. */
 CPKIT_API cpkit_status cpkit_dev_slab(const cpkit_dev_problem* p, uint64_t* lo, uint64_t* hi,

@@ -48,6 +48,7 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
     "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
     "cpkit_dev_init_seed", "cpkit_dev_download_tensor", "cpkit_dev_shard_range",
+    "cpkit_dev_problem_create_loopback",
 )
 
 
@@ -333,6 +334,24 @@ class DeviceProblem:
                                                     _u64(self.rank), shard, world, buf, C.byref(h)))
         self._h = h
         self.stacked = sum(self.dims) * self.rank
+
+    @classmethod
+    def loopback(cls, dims: Sequence[int], rank: int, world: int, device: int = 0) -> List["DeviceProblem"]:
+        """TEST ONLY: `world` last-mode shards on one GPU joined by the in-process
+        loopback group (cpkit_dev_problem_create_loopback). Drive each shard from
+        its own thread with the same call sequence."""
+        hs = (_vp * world)()
+        _chk(load().cpkit_dev_problem_create_loopback(device, _dims(dims), _u64(len(dims)), _u64(rank), world,
+                                                      hs))
+        out = []
+        for r in range(world):
+            p = cls.__new__(cls)
+            p.dims = [int(d) for d in dims]
+            p.rank = int(rank)
+            p._h = _vp(hs[r])
+            p.stacked = sum(p.dims) * p.rank
+            out.append(p)
+        return out
 
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:

@@ -1631,6 +1631,25 @@ cpkit_status cpkit_dev_problem_create_sharded(int device, const uint64_t* dims, 
         *out = h.release();
     });
 }
+cpkit_status cpkit_dev_problem_create_loopback(int device, const uint64_t* dims, uint64_t order, uint64_t rank,
+                                               int world, cpkit_dev_problem** out) {
+    if (auto st = require(dims && out && order > 0 && rank > 0 && world >= 1,
+                          "cpkit_dev_problem_create_loopback: bad argument"))
+        return st;
+    return guarded([&] {
+        auto comms = cpkit::make_loopback_comms(world);
+        std::vector<std::unique_ptr<cpkit_dev_problem>> hs;
+        for (int r = 0; r < world; ++r) {
+            auto h = std::make_unique<cpkit_dev_problem>();
+            h->ctx = std::make_unique<cpkit::Context>(device);
+            h->ctx->comm = std::move(comms[r]);
+            h->p = std::make_unique<cpkit::DeviceProblem>(*h->ctx, std::vector<std::uint64_t>(dims, dims + order),
+                                                          static_cast<int>(rank));
+            hs.push_back(std::move(h));
+        }
+        for (int r = 0; r < world; ++r) out[r] = hs[r].release();
+    });
+}
 void cpkit_dev_problem_destroy(cpkit_dev_problem* p) {
     if (!p) return;
     try {

@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -139,6 +142,124 @@ void nccl_unique_id(void* out128) {
     NcclUniqueId uid;
     nccl_check(nccl().GetUniqueId(&uid), "GetUniqueId");
     std::memcpy(out128, uid.internal, sizeof uid.internal);
+}
+
+// ---------------------------------------------------------------- loopback group
+// Test-only collectives for `world` last-mode shards on ONE device, each shard
+// driven by its own host thread: the NCCL call sequence of the sharded path
+// runs unchanged, with the data movement done as device copies and a
+// fixed-order (rank 0, 1, ...) sum. Every rank posts its buffer and an event
+// on its stream, meets the others on the host, rank 0's thread enqueues the
+// exchange behind all the events, and every stream waits for its completion.
+namespace {
+constexpr int kLoopMax = 16;
+struct RankPtrs {
+    const double* p[kLoopMax];
+};
+__global__ void loopback_sum_kernel(RankPtrs src, int world, double* __restrict__ dst, unsigned long long n) {
+    for (unsigned long long i = blockIdx.x * static_cast<unsigned long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<unsigned long long>(gridDim.x) * blockDim.x) {
+        double a = src.p[0][i];
+        for (int q = 1; q < world; ++q) a = __dadd_rn(a, src.p[q][i]);
+        dst[i] = a;
+    }
+}
+
+class LoopbackGroup {
+public:
+    explicit LoopbackGroup(int world) : world_(world), in_(world), out_(world), ready_(world) {
+        if (world < 1 || world > kLoopMax) throw InvalidArgument("loopback group: 1..16 shards");
+        for (auto& e : ready_) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CPK_CUDA(cudaEventCreateWithFlags(&done_, cudaEventDisableTiming));
+    }
+    ~LoopbackGroup() {
+        for (auto& e : ready_) cudaEventDestroy(e);
+        cudaEventDestroy(done_);
+    }
+    int world() const { return world_; }
+    // kind 0: in-place sum of `count` doubles; kind 1: gather `count` doubles per rank
+    void collective(int rank, int kind, const double* in, double* out, std::size_t count, cudaStream_t st) {
+        CPK_CUDA(cudaEventRecord(ready_[rank], st));
+        in_[rank] = in;
+        out_[rank] = out;
+        meet();  // every rank has posted its buffers and its ready event
+        if (rank == 0) {
+            for (int q = 0; q < world_; ++q) CPK_CUDA(cudaStreamWaitEvent(st, ready_[q], 0));
+            if (kind == 0) {
+                tmp_.ensure(count);
+                RankPtrs src{};
+                for (int q = 0; q < world_; ++q) src.p[q] = in_[q];
+                const unsigned blocks = static_cast<unsigned>(std::min<std::size_t>((count + 255) / 256, 1184));
+                if (count) {
+                    loopback_sum_kernel<<<blocks, 256, 0, st>>>(src, world_, tmp_.get(), count);
+                    count_launch(1);
+                    CPK_CUDA(cudaGetLastError());
+                }
+                for (int q = 0; q < world_; ++q)
+                    CPK_CUDA(cudaMemcpyAsync(out_[q], tmp_.get(), count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            } else {
+                for (int d = 0; d < world_; ++d)
+                    for (int q = 0; q < world_; ++q) {
+                        double* dst = out_[d] + static_cast<std::size_t>(q) * count;
+                        if (dst != in_[q])
+                            CPK_CUDA(cudaMemcpyAsync(dst, in_[q], count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                    }
+            }
+            CPK_CUDA(cudaEventRecord(done_, st));
+        }
+        meet();  // the exchange is enqueued
+        if (rank != 0) CPK_CUDA(cudaStreamWaitEvent(st, done_, 0));
+        meet();  // everyone waits on this round's done event before the next round re-records it
+    }
+
+private:
+    void meet() {
+        std::unique_lock<std::mutex> lock(mu_);
+        const unsigned gen = gen_;
+        if (++arrived_ == world_) {
+            arrived_ = 0;
+            ++gen_;
+            cv_.notify_all();
+            return;
+        }
+        if (!cv_.wait_for(lock, std::chrono::seconds(300), [&] { return gen_ != gen; }))
+            throw DeviceError("loopback collective: a shard did not arrive within 300 s");
+    }
+    int world_;
+    std::vector<const double*> in_;
+    std::vector<double*> out_;
+    std::vector<cudaEvent_t> ready_;
+    cudaEvent_t done_ = nullptr;
+    DevBuf<double> tmp_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int arrived_ = 0;
+    unsigned gen_ = 0;
+};
+
+class LoopbackComm final : public Comm {
+public:
+    LoopbackComm(std::shared_ptr<LoopbackGroup> g, int rank) : g_(std::move(g)), rank_(rank) {}
+    int rank() const override { return rank_; }
+    int world() const override { return g_->world(); }
+    void allreduce_sum(double* dev, std::size_t count, cudaStream_t st) override {
+        g_->collective(rank_, 0, dev, dev, count, st);
+    }
+    void allgather(const double* in, double* out, std::size_t per, cudaStream_t st) override {
+        g_->collective(rank_, 1, in, out, per, st);
+    }
+
+private:
+    std::shared_ptr<LoopbackGroup> g_;
+    int rank_;
+};
+}  // namespace
+
+std::vector<std::unique_ptr<Comm>> make_loopback_comms(int world) {
+    auto g = std::make_shared<LoopbackGroup>(world);
+    std::vector<std::unique_ptr<Comm>> out;
+    for (int r = 0; r < world; ++r) out.push_back(std::make_unique<LoopbackComm>(g, r));
+    return out;
 }
 
 // ---------------------------------------------------------------- DMMA peak probe

@@ -151,6 +151,9 @@ public:
                            cudaStream_t st) = 0;
 };
 std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int world);
+// Test-only: `world` communicators of one in-process group on one device; each
+// rank must be driven by its own host thread (runtime.cu, LoopbackGroup).
+std::vector<std::unique_ptr<Comm>> make_loopback_comms(int world);
 void nccl_unique_id(void* out128);
 
 struct Context {
