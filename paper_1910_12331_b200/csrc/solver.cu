@@ -340,6 +340,11 @@ void shard_range(std::uint64_t extent, int rank, int world, std::uint64_t* lo, s
 
 // ================================================================ DeviceProblem
 namespace {
+// Layout copies of the tensor (order-3 permuted copies, order >= 4 X^T) are
+// made when they take at most this share of the HBM still free after X is
+// allocated; the rest covers the root partials and workspaces. C5 per GPU:
+// P=1 (C5s) and P>=4 copy, P=2 (102 GB slab) runs the TN front root on X.
+constexpr double kLayoutCopyShare = 0.7;
 enum Scal { kXnorm = 0, kRes = 1, kFit = 2, kStep = 3, kNormSum = 4, kDot = 5, kNScal = 16 };
 }
 
@@ -384,7 +389,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     PF_.resize(static_cast<std::size_t>(F_) * R_);
     PB_.resize(static_cast<std::size_t>(Bl_) * R_);
     if (N == 3 && !std::getenv("CPKIT_ALS_TREE")) {
-        // the permuted copies need 2 more tensors; keep half of the free memory spare
+        // the permuted copies need 2 more tensors (X itself is already allocated)
         std::size_t free_b = 0, total_b = 0;
         CPK_CUDA(cudaMemGetInfo(&free_b, &total_b));
         ld0_ = (local_rows_[0] + 1) & ~1LL;
@@ -392,7 +397,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
         const double copy_b = 8.0 * static_cast<double>(Bl_) *
                               static_cast<double>(local_rows_[1] * ld0_ + local_rows_[0] * ld1_);
         const char* ce = std::getenv("CPKIT_MSDT_COPIES");
-        msdt_copies_ = ce ? std::atoi(ce) != 0 : copy_b + 8.0 * static_cast<double>(local_elems_) < 0.5 * free_b;
+        msdt_copies_ = ce ? std::atoi(ce) != 0 : copy_b < kLayoutCopyShare * static_cast<double>(free_b);
         // without copies the single-mode roots are TN GEMMs with the factor as the B operand
         msdt_ = msdt_copies_ || (R_ % 2 == 0 && Bs_ == Bl_);
     }
@@ -402,7 +407,7 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
         ldT_ = (F_ + 1) & ~1LL;
         const double copy_b = 8.0 * static_cast<double>(Bl_) * static_cast<double>(ldT_);
         const char* ce = std::getenv("CPKIT_FRONT_COPY");
-        front_copy_ = ce ? std::atoi(ce) != 0 : copy_b + 8.0 * static_cast<double>(local_elems_) < 0.5 * free_b;
+        front_copy_ = ce ? std::atoi(ce) != 0 : copy_b < kLayoutCopyShare * static_cast<double>(free_b);
         if (front_copy_) {
             XT_.resize(static_cast<std::size_t>(Bl_ * ldT_));
             CPK_CUDA(cudaMemset(XT_.get(), 0, XT_.size() * sizeof(double)));  // stride padding stays zero
