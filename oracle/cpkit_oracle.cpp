@@ -140,16 +140,28 @@ struct Mat {
 
 // C (m x n) = A (m x k) * B (k x n); each entry summed in ascending k.
 // Row loop is threaded; per-entry summation order is thread-independent.
-void gemm_nn(const double* a, const double* b, double* c, std::int64_t m, std::int64_t n,
-             std::int64_t k) {
-    parallel_rows(m, [&](std::int64_t lo, std::int64_t hi) {
-        for (std::int64_t i = lo; i < hi; ++i) {
-            double* ci = c + i * n;
-            for (std::int64_t j = 0; j < n; ++j) ci[j] = 0.0;
-            for (std::int64_t kk = 0; kk < k; ++kk) {
-                const double aik = a[i * k + kk];
-                const double* bk = b + kk * n;
-                for (std::int64_t j = 0; j < n; ++j) ci[j] += aik * bk[j];
+// Cache blocking only regroups independent entries: 8 rows share each row of
+// B and a 256-column strip of C stays in L1; every entry still accumulates
+// a(i,0) b(0,j), a(i,1) b(1,j), ... in that order from 0.0.
+void gemm_nn(const double* __restrict a, const double* __restrict b, double* __restrict c, std::int64_t m,
+             std::int64_t n, std::int64_t k) {
+    constexpr std::int64_t kRows = 8, kCols = 256;
+    const std::int64_t blocks = (m + kRows - 1) / kRows;
+    parallel_rows(blocks, [&](std::int64_t lo, std::int64_t hi) {
+        for (std::int64_t blk = lo; blk < hi; ++blk) {
+            const std::int64_t i0 = blk * kRows, i1 = std::min(m, i0 + kRows);
+            for (std::int64_t j0 = 0; j0 < n; j0 += kCols) {
+                const std::int64_t j1 = std::min(n, j0 + kCols);
+                for (std::int64_t i = i0; i < i1; ++i)
+                    for (std::int64_t j = j0; j < j1; ++j) c[i * n + j] = 0.0;
+                for (std::int64_t kk = 0; kk < k; ++kk) {
+                    const double* bk = b + kk * n;
+                    for (std::int64_t i = i0; i < i1; ++i) {
+                        const double aik = a[i * k + kk];
+                        double* ci = c + i * n;
+                        for (std::int64_t j = j0; j < j1; ++j) ci[j] += aik * bk[j];
+                    }
+                }
             }
         }
     });

@@ -1,0 +1,156 @@
+"""BASELINE.json configs at their FULL sizes against the CPU oracle.
+
+North star: the same GN/ALS iteration counts, final fitness within 1e-8 and
+per-kernel outputs within 1e-11 (gauss_newton.cpp:451-494, als.cpp:54-94,
+mttkrp.cpp:160-189). Inputs follow SURVEY.md §8d: factors from the keyed RNG
+at problem_seed(0, R, 0), the start at init_seed(0, R, 0, 0), noise on stream
+0x4E01. Tensors are generated on the device (bit-identical to the oracle's
+reconstruct + keyed noise, tests/test_gpu_noise.py) and downloaded for the
+oracle.
+
+Where a trajectory is roundoff-determined (the
+sqrt(eps) residual floor, capped CG solves on an ill-conditioned swamp), the
+records are compared exactly up to that point and the run's terminal status
+and final fitness after it.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers import rel_err, swamp_factors, vec_rel_err
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def ck():
+    from paper_1910_12331_b200 import cpkit
+    cpkit.load()
+    return cpkit
+
+
+@pytest.fixture(scope="module", autouse=True)
+def all_cores(orc):
+    orc.set_threads(os.cpu_count() or 1)
+
+
+def generated(ck, dims, R, noise_rel, truth=None):
+    if truth is None:
+        truth = ck.random_factors(dims, R, ck.problem_seed(0, R, 0))
+    p = ck.DeviceProblem(dims, R)
+    p.generate(truth, noise_seed=1, noise_rel=noise_rel)
+    return p, p.download()
+
+
+def trace(orc, p, x, init, optimizer, dev_cfg, orc_cfg):
+    f_dev, rep = p.optimize(dict(dev_cfg, optimizer=optimizer), init)
+    j = rep.to_json()
+    if optimizer == "gn":
+        f_ref, recs, st = orc.gn_optimize(x, init, orc_cfg)
+    else:
+        f_ref, recs, st = orc.als_optimize(x, init, orc_cfg)
+    j["factors"] = f_dev
+    return j, recs, st, f_ref
+
+
+def assert_same_trace(j, recs, st, tol=1e-8):
+    assert j["status"] == st, (j["status"], st)
+    assert len(j["records"]) == len(recs), (len(j["records"]), len(recs))
+    for a, b in zip(j["records"], recs):
+        assert a["cg_iters"] == b["cg_iters"], (a, b)
+        assert a["lambda"] == b["lambda"], (a, b)
+        assert abs(a["residual"] - b["residual"]) < tol, (a, b)
+
+
+FIXED = [  # (name, dims, R, noise) - configs 2 and 4
+    ("C2", [400, 400, 400], 100, 1e-6),
+    ("C4", [100, 100, 100, 100], 50, 0.0),
+]
+
+
+@pytest.mark.parametrize("name,dims,R,noise", FIXED)
+@pytest.mark.parametrize("tree", [False, True])
+def test_full_als_five_sweeps(orc, ck, monkeypatch, name, dims, R, noise, tree):
+    if tree:
+        if len(dims) != 3:
+            pytest.skip("orders >= 4 always run the reference tree")
+        monkeypatch.setenv("CPKIT_ALS_TREE", "1")  # read when the problem is created
+    p, x = generated(ck, dims, R, noise)
+    init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
+    cfg = {"als": {"max_sweeps": 5, "residual_tol": 0.0, "step_tol": 0.0}}
+    j, recs, st, f_ref = trace(orc, p, x, init, "als", cfg, orc.AlsConfig(max_sweeps=5, residual_tol=0.0,
+                                                                          step_tol=0.0))
+    assert_same_trace(j, recs, st)
+    assert vec_rel_err(j["factors"], f_ref) < 1e-10
+
+
+@pytest.mark.parametrize("name,dims,R,noise", FIXED)
+def test_full_gn_five_iterations(orc, ck, name, dims, R, noise):
+    p, x = generated(ck, dims, R, noise)
+    init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
+    j, recs, st, f_ref = trace(orc, p, x, init, "gn", {"gn": {"max_iters": 5}}, orc.GnConfig(max_iters=5))
+    assert_same_trace(j, recs, st)
+
+
+def _converge_prefix(j, recs, cap):
+    """Records agree exactly (CG count, lambda) and to 1e-8 in residual up to the
+    first record below the 1e-8 floor or the first capped CG solve."""
+    n = 0
+    for a, b in zip(j["records"], recs):
+        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (n, a, b)
+        assert abs(a["residual"] - b["residual"]) < 1e-8, (n, a, b)
+        n += 1
+        if b["residual"] < 1e-8 or max(a["cg_iters"], b["cg_iters"]) >= cap:
+            break
+    return n
+
+
+def test_full_c3_swamp_to_convergence(orc, ck):
+    """Config 3: s=200, R=20, collinear (c=0.9) columns, residual_tol 1e-10."""
+    dims, R = [200, 200, 200], 20
+    truth = swamp_factors(orc, dims, R, 0)
+    p, x = generated(ck, dims, R, 0.0, truth=truth)
+    init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
+    cap = min(sum(dims) * R, 10 * R)
+    j, recs, st, _ = trace(orc, p, x, init, "gn", {"gn": {"max_iters": 200, "residual_tol": 1e-10}},
+                           orc.GnConfig(max_iters=200, residual_tol=1e-10))
+    n = _converge_prefix(j, recs, cap)
+    assert n >= 3
+    assert j["status"] == st
+    assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
+    if n == len(recs):  # no capped solve before the floor: the whole run matches
+        assert len(j["records"]) == len(recs)
+    j, recs, st, _ = trace(orc, p, x, init, "als", {"als": {"max_sweeps": 400, "residual_tol": 1e-10}},
+                           orc.AlsConfig(max_sweeps=400, residual_tol=1e-10))
+    n = _converge_prefix(j, recs, 1 << 30)
+    assert j["status"] == st
+    assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
+    if all(r["residual"] >= 1e-8 for r in recs):  # the floor was never reached: every sweep matches
+        assert len(j["records"]) == len(recs) == n
+
+
+def test_full_c5s_every_mode_and_one_sweep(orc, ck):
+    """The 1-GPU slice of config 5 (order 4, s=200, R=200, noise 1e-4, 12.8 GB):
+    every mode's MTTKRP vs the oracle tree, then one ALS sweep and one GN step."""
+    dims, R = [200, 200, 200, 200], 200
+    p, x = generated(ck, dims, R, 1e-4)
+    init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
+    p.set_factors(init)
+    ref, cnt = orc.mttkrp_tree_all(x, init)
+    for n in range(4):
+        assert rel_err(p.mttkrp(n), ref[n]) < 1e-11, n
+    assert p.full_contractions == cnt == 2
+    del ref
+    p.set_factors(init)
+    step, _ = p.als_sweep(0.0)
+    f_ref, step_ref, _, _ = orc.als_sweep(x, init, 0.0)
+    assert abs(step - step_ref) <= 1e-10 * step_ref
+    assert vec_rel_err(p.get_factors(), f_ref) < 1e-10
+    xn2 = orc.norm2(x)
+    p.set_factors(init)
+    d = p.gn_step({}, xn2)
+    f_ref, d_ref = orc.gn_step(x, init, orc.GnConfig(), xn2)
+    assert d["cg_iters"] == d_ref["cg_iters"], (d, d_ref)
+    assert abs(d["residual_after"] - d_ref["residual_after"]) < 1e-10
+    assert vec_rel_err(p.get_factors(), f_ref) < 1e-9
