@@ -93,21 +93,33 @@ def test_full_gn_five_iterations(orc, ck, name, dims, R, noise):
     assert_same_trace(j, recs, st)
 
 
-def _converge_prefix(j, recs, cap):
-    """Records agree exactly (CG count, lambda) and to 1e-8 in residual up to the
-    first record below the 1e-8 floor or the first capped CG solve."""
+def _converge_prefix(j, recs, cap, rtol):
+    """Records agree exactly in CG count and lambda, and to rtol (relative) in
+    residual, up to the first near-capped CG solve or the first record below
+    the 1e-8 residual floor."""
     n = 0
     for a, b in zip(j["records"], recs):
-        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (n, a, b)
-        assert abs(a["residual"] - b["residual"]) < 1e-8, (n, a, b)
-        n += 1
-        if b["residual"] < 1e-8 or max(a["cg_iters"], b["cg_iters"]) >= cap:
+        if b["residual"] < 1e-8 or max(a["cg_iters"], b["cg_iters"]) >= 0.8 * cap:
             break
+        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (n, a, b)
+        assert abs(a["residual"] - b["residual"]) <= rtol * b["residual"], (n, a, b)
+        n += 1
     return n
 
 
 def test_full_c3_swamp_to_convergence(orc, ck):
-    """Config 3: s=200, R=20, collinear (c=0.9) columns, residual_tol 1e-10."""
+    """Config 3: s=200, R=20, collinear (c=0.9) columns, residual_tol 1e-10.
+
+    Measured (tools/c3_trace.py, profiles/r02_c3_trace.txt): GN records agree
+    in CG count and lambda for the first 24 iterations (residuals to <= 1e-6
+    relative while the swamp amplifies last-bit differences); from iteration
+    25 the inner solves run near their cap of 200 and the counts drift by a
+    few. Both runs stop after the same number of iterations; the residual then
+    sits at each side's sqrt(eps) floor of the fast residual formula
+    (kruskal.cpp:94-118: the oracle's sequential ||X||^2 sum floors at 3.6e-7,
+    the device's tree sums below 1e-8, where the clamp gives 0), so the status
+    label (converged_residual / converged_step) and the last fitness digits
+    are roundoff-determined, as SURVEY.md Appendix A.1 predicts."""
     dims, R = [200, 200, 200], 20
     truth = swamp_factors(orc, dims, R, 0)
     p, x = generated(ck, dims, R, 0.0, truth=truth)
@@ -115,19 +127,17 @@ def test_full_c3_swamp_to_convergence(orc, ck):
     cap = min(sum(dims) * R, 10 * R)
     j, recs, st, _ = trace(orc, p, x, init, "gn", {"gn": {"max_iters": 200, "residual_tol": 1e-10}},
                            orc.GnConfig(max_iters=200, residual_tol=1e-10))
-    n = _converge_prefix(j, recs, cap)
-    assert n >= 3
-    assert j["status"] == st
-    assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
-    if n == len(recs):  # no capped solve before the floor: the whole run matches
-        assert len(j["records"]) == len(recs)
+    n = _converge_prefix(j, recs, cap, 1e-6)
+    assert n >= 20, n
+    assert j["status"] in ("converged_residual", "converged_step") and st in ("converged_residual", "converged_step")
+    assert abs(len(j["records"]) - len(recs)) <= 2, (len(j["records"]), len(recs))
+    assert j["records"][-1]["residual"] < 1e-6 and recs[-1]["residual"] < 1e-6
+    # ALS: 400 sweeps (capped), every record within 1e-9 of the oracle's
     j, recs, st, _ = trace(orc, p, x, init, "als", {"als": {"max_sweeps": 400, "residual_tol": 1e-10}},
                            orc.AlsConfig(max_sweeps=400, residual_tol=1e-10))
-    n = _converge_prefix(j, recs, 1 << 30)
-    assert j["status"] == st
-    assert abs(j["records"][-1]["fitness"] - recs[-1]["fitness"]) < 1e-8
-    if all(r["residual"] >= 1e-8 for r in recs):  # the floor was never reached: every sweep matches
-        assert len(j["records"]) == len(recs) == n
+    assert j["status"] == st == "cap_hit" and len(j["records"]) == len(recs) == 400
+    for a, b in zip(j["records"], recs):
+        assert abs(a["residual"] - b["residual"]) < 1e-9, (a, b)
 
 
 def test_full_c5s_every_mode_and_one_sweep(orc, ck):
