@@ -49,6 +49,12 @@ CPKIT_API cpkit_status cpkit_dev_slab(const cpkit_dev_problem* p, uint64_t* lo, 
 
 /* Tensor in: host copy of the local slab (tensor.hpp:16-48 layout). */
 CPKIT_API cpkit_status cpkit_dev_upload_tensor(cpkit_dev_problem* p, const double* host_local);
+/* Tensor in from a CPKT1 file (tensor.cpp:197-239), streamed: chunks of whole
+ * last-mode rows are read into two pinned staging buffers while the previous
+ * chunk is copied to HBM (only this shard's slab columns); the finiteness
+ * check of the reference's read_tensor runs on the device. No host copy of
+ * the tensor is made. */
+CPKIT_API cpkit_status cpkit_dev_load_tensor(cpkit_dev_problem* p, const char* path);
 /* Tensor generated on device: reconstruct(truth) (kruskal.cpp:67-92, bitwise)
  * plus keyed-RNG Gaussian noise scaled to noise_rel * ||X||_F. */
 CPKIT_API cpkit_status cpkit_dev_generate_tensor(cpkit_dev_problem* p, const double* truth_factors,

@@ -48,7 +48,7 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
     "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
     "cpkit_dev_init_seed", "cpkit_dev_download_tensor", "cpkit_dev_shard_range",
-    "cpkit_dev_problem_create_loopback",
+    "cpkit_dev_problem_create_loopback", "cpkit_dev_load_tensor",
 )
 
 
@@ -386,6 +386,10 @@ class DeviceProblem:
     def upload(self, x_local: np.ndarray):
         x = self._slab_array(x_local, "upload")
         _chk(load().cpkit_dev_upload_tensor(self._h, _ptr(x)))
+
+    def load_file(self, path: str):
+        """CPKT1 file -> this shard's slab on the device, streamed (cpkit_dev_load_tensor)."""
+        _chk(load().cpkit_dev_load_tensor(self._h, path.encode()))
 
     def generate(self, truth: Sequence[np.ndarray], noise_seed: int = 0, noise_rel: float = 0.0):
         buf = self._factor_stack(truth, "truth")

@@ -1677,6 +1677,10 @@ cpkit_status cpkit_dev_upload_tensor(cpkit_dev_problem* p, const double* host) {
         p->ctx->sync();
     });
 }
+cpkit_status cpkit_dev_load_tensor(cpkit_dev_problem* p, const char* path) {
+    DEV_REQ(p && path);
+    return guarded([&] { p->p->load_tensor_file(path); });
+}
 cpkit_status cpkit_dev_generate_tensor(cpkit_dev_problem* p, const double* truth, uint64_t noise_seed,
                                        double noise_rel) {
     DEV_REQ(p && truth);

@@ -17,6 +17,8 @@
 #include <cstring>
 #include <fstream>
 #include <limits>
+#include <atomic>
+#include <thread>
 
 #include "solver.h"
 
@@ -45,25 +47,97 @@ std::uint64_t product_of_dims(const std::vector<std::uint64_t>& dims) {  // tens
     return n;
 }
 
+// ---- host tensor storage
+HostArray::HostArray(std::size_t n) : n_(n) {
+    if (n == 0) return;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, n * sizeof(double), cudaHostAllocPortable) == cudaSuccess) {
+        pinned_ = true;
+    } else {
+        cudaGetLastError();  // no device / pinning refused: ordinary heap memory
+        p = std::malloc(n * sizeof(double));
+        if (!p) throw std::bad_alloc();
+    }
+    p_ = static_cast<double*>(p);
+}
+HostArray::~HostArray() {
+    if (!p_) return;
+    if (pinned_) cudaFreeHost(p_);
+    else std::free(p_);
+}
+HostArray& HostArray::operator=(HostArray&& o) noexcept {
+    if (this != &o) {
+        this->~HostArray();
+        p_ = o.p_;
+        n_ = o.n_;
+        pinned_ = o.pinned_;
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    return *this;
+}
+
+namespace {
+// fn(lo, hi) over [0, n) on up to hardware_concurrency threads (large host passes only)
+template <typename F>
+void host_parallel(std::uint64_t n, F&& fn) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const std::uint64_t t = n < (1ull << 24) ? 1 : std::min<std::uint64_t>(hw, 16);
+    if (t <= 1) {
+        fn(std::uint64_t{0}, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const std::uint64_t chunk = (n + t - 1) / t;
+    for (std::uint64_t i = 0; i < t; ++i) {
+        const std::uint64_t lo = i * chunk, hi = std::min(n, lo + chunk);
+        if (lo < hi) pool.emplace_back([&, lo, hi] { fn(lo, hi); });
+    }
+    for (auto& th : pool) th.join();
+}
+}  // namespace
+
 DenseTensor::DenseTensor(std::vector<std::uint64_t> dims) : dims_(std::move(dims)) {
     if (dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
-    data_.assign(product_of_dims(dims_), 0.0);
+    data_ = HostArray(product_of_dims(dims_));
+    double* d = data_.data();
+    host_parallel(data_.size(), [&](std::uint64_t lo, std::uint64_t hi) { std::fill(d + lo, d + hi, 0.0); });
 }
 DenseTensor DenseTensor::from_data(std::vector<std::uint64_t> dims, std::vector<double> data) {
+    if (dims.empty()) throw InvalidArgument("tensor order must be at least 1");
+    if (product_of_dims(dims) != data.size()) throw InvalidArgument("tensor data length does not match extents");
+    return copy_of(std::move(dims), data.data());
+}
+DenseTensor DenseTensor::copy_of(std::vector<std::uint64_t> dims, const double* src) {
+    if (dims.empty()) throw InvalidArgument("tensor order must be at least 1");
+    HostArray a(product_of_dims(dims));
+    double* d = a.data();
+    host_parallel(a.size(), [&](std::uint64_t lo, std::uint64_t hi) {
+        std::memcpy(d + lo, src + lo, (hi - lo) * sizeof(double));
+    });
+    return adopt(std::move(dims), std::move(a));
+}
+DenseTensor DenseTensor::adopt(std::vector<std::uint64_t> dims, HostArray data) {
     DenseTensor t;
     t.dims_ = std::move(dims);
     t.data_ = std::move(data);
     if (t.dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
-    if (product_of_dims(t.dims_) != t.data_.size())
-        throw InvalidArgument("tensor data length does not match extents");
+    if (product_of_dims(t.dims_) != t.data_.size()) throw InvalidArgument("tensor data length does not match extents");
     return t;
 }
 void DenseTensor::validate() const {  // tensor.cpp:71-83
     if (dims_.empty()) throw InvalidArgument("tensor order must be at least 1");
-    if (product_of_dims(dims_) != data_.size())
-        throw InvalidArgument("tensor data length does not match extents");
-    for (double v : data_)
-        if (!std::isfinite(v)) throw InvalidArgument("tensor contains non-finite entries");
+    if (product_of_dims(dims_) != data_.size()) throw InvalidArgument("tensor data length does not match extents");
+    std::atomic<bool> bad{false};
+    const double* d = data_.data();
+    host_parallel(data_.size(), [&](std::uint64_t lo, std::uint64_t hi) {
+        for (std::uint64_t i = lo; i < hi; ++i)
+            if (!std::isfinite(d[i])) {
+                bad = true;
+                return;
+            }
+    });
+    if (bad) throw InvalidArgument("tensor contains non-finite entries");
 }
 
 void KruskalModel::validate() const {  // kruskal.cpp:27-40
@@ -107,7 +181,7 @@ void write_tensor(const DenseTensor& t, const std::string& path) {  // tensor.cp
     put_f64s(os, t.data(), t.size());
     if (!os) throw IoError("write failed: " + path);
 }
-DenseTensor read_tensor(const std::string& path) {  // tensor.cpp:278-306
+std::vector<std::uint64_t> read_tensor_header(const std::string& path, std::uint64_t* data_offset) {
     std::ifstream is(path, std::ios::binary);
     if (!is) throw IoError("cannot open for reading: " + path);
     char magic[5];
@@ -118,11 +192,19 @@ DenseTensor read_tensor(const std::string& path) {  // tensor.cpp:278-306
     std::vector<std::uint64_t> dims(order);
     for (auto& d : dims) d = get_u64(is);
     if (!is) throw ParseError("truncated tensor header: " + path);
-    const std::uint64_t total = product_of_dims(dims);
-    std::vector<double> data(total);
-    get_f64s(is, data.data(), total);
+    product_of_dims(dims);  // extents > 0, no overflow
+    if (data_offset) *data_offset = 5 + 8 * (1 + order);
+    return dims;
+}
+DenseTensor read_tensor(const std::string& path) {  // tensor.cpp:278-306
+    std::uint64_t off = 0;
+    std::vector<std::uint64_t> dims = read_tensor_header(path, &off);
+    std::ifstream is(path, std::ios::binary);
+    is.seekg(static_cast<std::streamoff>(off));
+    HostArray data(product_of_dims(dims));  // read straight into (pinned) tensor storage
+    get_f64s(is, data.data(), data.size());
     if (!is) throw ParseError("truncated tensor data: " + path);
-    DenseTensor t = DenseTensor::from_data(std::move(dims), std::move(data));
+    DenseTensor t = DenseTensor::adopt(std::move(dims), std::move(data));
     t.validate();
     return t;
 }
@@ -545,6 +627,67 @@ void DeviceProblem::upload_tensor(const double* host_local) {
                                    Bl_ * sizeof(double), F_, cudaMemcpyHostToDevice, ctx_.stream));
     build_msdt_copies();
     invalidate_all();
+}
+void DeviceProblem::load_tensor_file(const std::string& path) {
+    std::uint64_t off = 0;
+    if (read_tensor_header(path, &off) != dims_) throw InvalidArgument("tensor file extents do not match the problem");
+    const int N = order();
+    const std::uint64_t sl = dims_[N - 1], slab = slab_hi_ - slab_lo_, rows = local_elems_ / slab;
+    std::ifstream is(path, std::ios::binary);
+    is.seekg(static_cast<std::streamoff>(off));
+    auto read_rows = [&](double* dst, std::uint64_t nr) {
+        get_f64s(is, dst, nr * sl);
+        if (!is) throw ParseError("truncated tensor data: " + path);
+    };
+    if (Bs_ != Bl_) {  // padded row stride (odd back extent): gather the slab, then the ordinary upload
+        HostArray h(local_elems_), row(sl);
+        for (std::uint64_t r = 0; r < rows; ++r) {
+            read_rows(row.data(), 1);
+            std::memcpy(h.data() + r * slab, row.data() + slab_lo_, slab * sizeof(double));
+        }
+        upload_tensor(h.data());
+    } else {
+        // whole last-mode rows per chunk; two pinned staging buffers: chunk k is
+        // read while chunk k-1 crosses to HBM (2-D copy of the slab columns if sharded)
+        const std::uint64_t per = std::max<std::uint64_t>(1, (64ull << 20) / (sl * sizeof(double)));
+        HostArray stage[2] = {HostArray(per * sl), HostArray(per * sl)};
+        cudaEvent_t ev[2];
+        for (auto& e : ev) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        try {
+            std::uint64_t k = 0;
+            for (std::uint64_t r0 = 0; r0 < rows; r0 += per, ++k) {
+                const std::uint64_t nr = std::min(per, rows - r0);
+                const int b = static_cast<int>(k & 1);
+                if (k >= 2) CPK_CUDA(cudaEventSynchronize(ev[b]));  // its previous copy has landed
+                read_rows(stage[b].data(), nr);
+                double* dst = x_.get() + r0 * slab;
+                if (slab == sl)
+                    CPK_CUDA(cudaMemcpyAsync(dst, stage[b].data(), nr * sl * sizeof(double), cudaMemcpyHostToDevice,
+                                             ctx_.stream));
+                else
+                    CPK_CUDA(cudaMemcpy2DAsync(dst, slab * sizeof(double), stage[b].data() + slab_lo_,
+                                               sl * sizeof(double), slab * sizeof(double), nr, cudaMemcpyHostToDevice,
+                                               ctx_.stream));
+                CPK_CUDA(cudaEventRecord(ev[b], ctx_.stream));
+            }
+            ctx_.sync_main();
+        } catch (...) {
+            cudaStreamSynchronize(ctx_.stream);
+            for (auto& e : ev) cudaEventDestroy(e);
+            throw;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        build_msdt_copies();
+        invalidate_all();
+    }
+    // tensor.cpp:71-83 (validate on load), checked on the device
+    launch_set_flag_scalar(flag_.get(), 1, scal_.get() + 11, 0.0, ctx_.stream);
+    launch_all_finite(x_.get(), static_cast<std::uint64_t>(F_) * static_cast<std::uint64_t>(Bs_), flag_.get(),
+                      ctx_.stream);
+    int ok = 0;
+    CPK_CUDA(cudaMemcpyAsync(&ok, flag_.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync_main();
+    if (!ok) throw InvalidArgument("tensor contains non-finite entries");
 }
 void DeviceProblem::build_msdt_copies() {
     if (front_copy_)  // X^T [B_local][F]

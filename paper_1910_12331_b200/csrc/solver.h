@@ -32,23 +32,51 @@ inline constexpr std::uint64_t kDefaultElementCap = 100'000'000ull;  // tensor.h
 
 std::uint64_t product_of_dims(const std::vector<std::uint64_t>& dims);
 
+// Host storage of a dense tensor: page-locked (cudaHostAlloc) when a CUDA
+// device is present, so an upload is one direct DMA at full link bandwidth with
+// no driver staging copy; ordinary heap memory otherwise (e.g. CPU-only hosts).
+// Not initialised on allocation.
+class HostArray {
+public:
+    HostArray() = default;
+    explicit HostArray(std::size_t n);
+    ~HostArray();
+    HostArray(const HostArray&) = delete;
+    HostArray& operator=(const HostArray&) = delete;
+    HostArray(HostArray&& o) noexcept : p_(o.p_), n_(o.n_), pinned_(o.pinned_) { o.p_ = nullptr; o.n_ = 0; }
+    HostArray& operator=(HostArray&& o) noexcept;
+    double* data() { return p_; }
+    const double* data() const { return p_; }
+    std::size_t size() const { return n_; }
+    bool pinned() const { return pinned_; }
+
+private:
+    double* p_ = nullptr;
+    std::size_t n_ = 0;
+    bool pinned_ = false;
+};
+
 // tensor.hpp:16-48 (host copy; the device copy lives in DeviceProblem)
 class DenseTensor {
 public:
     DenseTensor() = default;
-    explicit DenseTensor(std::vector<std::uint64_t> dims);
+    explicit DenseTensor(std::vector<std::uint64_t> dims);  // zero-filled
     static DenseTensor from_data(std::vector<std::uint64_t> dims, std::vector<double> data);
+    // copies n = prod(dims) doubles from src (threaded for large tensors)
+    static DenseTensor copy_of(std::vector<std::uint64_t> dims, const double* src);
+    static DenseTensor adopt(std::vector<std::uint64_t> dims, HostArray data);
     std::size_t order() const { return dims_.size(); }
     std::uint64_t extent(std::size_t m) const { return dims_[m]; }
     const std::vector<std::uint64_t>& dims() const { return dims_; }
     std::uint64_t size() const { return data_.size(); }
     double* data() { return data_.data(); }
     const double* data() const { return data_.data(); }
+    bool pinned() const { return data_.pinned(); }
     void validate() const;
 
 private:
     std::vector<std::uint64_t> dims_;
-    std::vector<double> data_;
+    HostArray data_;
 };
 
 // kruskal.hpp:15-26
@@ -63,6 +91,8 @@ struct KruskalModel {
 // CPKT1 / CPKM1 binary formats (tensor.cpp:197-239, kruskal.cpp:143-203)
 void write_tensor(const DenseTensor& t, const std::string& path);
 DenseTensor read_tensor(const std::string& path);
+// CPKT1 header: extents (and the byte offset of the data)
+std::vector<std::uint64_t> read_tensor_header(const std::string& path, std::uint64_t* data_offset);
 void write_model(const KruskalModel& m, const std::string& path);
 KruskalModel read_model(const std::string& path);
 
@@ -186,6 +216,10 @@ public:
     DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int rank);
     ~DeviceProblem();
     void upload_tensor(const double* host_local);          // H2D copy of the local slab
+    // CPKT1 file -> device, streamed: chunks of whole last-mode rows are read into
+    // two pinned staging buffers while the previous chunk crosses to HBM (this
+    // rank's slab columns only); finiteness checked on the device (tensor.cpp:71-83)
+    void load_tensor_file(const std::string& path);
     void generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel);
     double* tensor_device() { return x_.get(); }
     void download_tensor(double* host_local);
