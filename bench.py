@@ -1,20 +1,26 @@
 """Benchmark of the B200 GN-CG / ALS hot path (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], "C2"): order-3 tensor, s=400 per mode,
-R=100, factors i.i.d. uniform[0,1) from the reference keyed RNG
-(problem_seed(0,100,0)), X = reconstruct(truth) + Gaussian noise scaled to
-1e-6 ||X||_F, generated on device (512 MB > the 126 MB L2, so no L2 flush is
-needed between steps). ALS from a uniform[0,1) init (init_seed(0,100,0,0)).
+Workload (the largest BASELINE config that fits one GPU): "C5s", the 1-GPU
+slice of configs[4] - order-4 tensor, s=200 per mode (1.6e9 fp64 entries,
+12.8 GB > the 126 MB L2, so no L2 flush is needed between steps), R=200,
+factors i.i.d. uniform[0,1) from the reference keyed RNG at
+problem_seed(0,200,0), X = reconstruct(truth) + keyed Gaussian noise scaled to
+1e-4 ||X||_F, generated on device. ALS from a uniform[0,1) start at
+init_seed(0,200,0,0). Under torchrun (N>1) the same tensor is sharded along
+its last mode (strong scaling; NCCL all-reduce / all-gather of the s x R
+MTTKRP partials over NVLink) and, with --c5, the full configs[4] tensor
+(order 4, s=400, 205 GB) is timed as well.
 
-A step = one ALS sweep (2 root MTTKRP contractions + N SPD solves + grams).
-`value` = sweeps/s with the tensor resident in HBM; `e2e` = the same metric
-through the public C ABI (host tensor -> device -> optimize -> host factors).
-Under torchrun (N>1) the tensor is sharded along its last mode across ranks
-(strong scaling of the same C2 problem; NCCL all-reduce / all-gather of the
-s x R MTTKRP partials over NVLink).
+A step = one ALS sweep (2 root MTTKRP contractions + 4 SPD solves + Grams).
+`value` = sweeps/s with the tensor resident in HBM (max over ranks); `e2e` =
+the same metric through the reference's drop-in entry, cpkit_decompose, on a
+host tensor (allocation, H2D of the 12.8 GB tensor and its layout copy, the
+sweeps, and the D2H of the factors inside the timed region).
 
---impl reference times the reference algorithm's CPU path (the oracle
-restatement, oracle/, all host threads) on the same workload.
+--impl reference times the reference's ALS path on the host cores: the
+restatement of als.cpp / mttkrp.cpp with its dense products on OpenBLAS
+(oracle/blas_arm.py, all host threads), on the bit-identical tensor (the
+oracle's reconstruct + keyed noise, which the device reproduces exactly).
 """
 import argparse
 import json
@@ -30,20 +36,30 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DIMS = [400, 400, 400]
-RANK = 100
-NOISE = 1e-6
-METRIC = "ALS sweeps/s (order-3 s=400 R=100, C2)"
+WORKLOADS = {
+    "c5s": {"dims": [200, 200, 200, 200], "rank": 200, "noise": 1e-4,
+            "name": "C5s: order-4 s=200 R=200 uniform[0,1) + 1e-4 keyed noise (12.8 GB), ALS "
+                    "(the 1-GPU slice of BASELINE configs[4])"},
+    "c2": {"dims": [400, 400, 400], "rank": 100, "noise": 1e-6,
+           "name": "C2: order-3 s=400 R=100 uniform[0,1) + 1e-6 keyed noise (512 MB), ALS (BASELINE configs[1])"},
+    "c5": {"dims": [400, 400, 400, 400], "rank": 200, "noise": 1e-4,
+           "name": "C5: order-4 s=400 R=200 uniform[0,1) + 1e-4 keyed noise (205 GB), ALS (BASELINE configs[4])"},
+}
 UNIT = "sweeps/s"
 E2E_SWEEPS = 20
 
 
-def workload_config(world):
-    return {"workload": "C2: order-3 s=400 R=100 uniform[0,1) exact rank + 1e-6 noise, ALS",
-            "dims": DIMS, "rank": RANK, "noise_rel": NOISE, "master_seed": 0,
-            "step": "one ALS sweep", "l2": "tensor 512 MB > 126 MB L2 (no flush needed)",
+def metric(w):
+    return f"ALS sweeps/s ({w})"
+
+
+def workload_config(key, world):
+    w = WORKLOADS[key]
+    return {"workload": w["name"], "dims": w["dims"], "rank": w["rank"], "noise_rel": w["noise"],
+            "master_seed": 0, "step": "one ALS sweep",
+            "l2": f"tensor {8 * np.prod(w['dims']) / 1e9:.2f} GB >> 126 MB L2 (no flush needed)",
             "parallelism": f"last-mode shard x{world}" if world > 1 else "single GPU",
-            "sharding": "mode-3 slabs, NCCL allreduce/allgather of s x R partials"}
+            "sharding": "mode-4 slabs, NCCL all-reduce / all-gather of the s x R partials"}
 
 
 class ClockSampler:
@@ -110,85 +126,162 @@ def measured_peaks():
         return {}
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the root GEMMs from the committed ncu --set full capture."""
+def ncu_traffic(key):
+    """Per-launch DRAM bytes of the root GEMM from the committed ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f)
+            return json.load(f).get(f"{key}_root_gemm_dram_bytes_per_launch")
     except OSError:
-        return {}
+        return None
 
 
-# ------------------------------------------------------------------------ reference arm
+def cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+# ------------------------------------------------------------------------ CPU arm (reference path)
+def host_tensor(key):
+    """The workload's tensor built on the host: oracle reconstruct (kruskal.cpp:67-92
+    order) + keyed noise - bit-identical to the device's generate()."""
+    from oracle import oracle as orc
+    w = WORKLOADS[key]
+    orc.set_threads(cores())
+    truth = orc.random_model(w["dims"], w["rank"], orc.problem_seed(0, w["rank"], 0))
+    x = orc.reconstruct(truth)
+    if w["noise"] > 0:
+        orc.add_noise(x, 1, w["noise"])
+    init = orc.random_model(w["dims"], w["rank"], orc.init_seed(0, w["rank"], 0, 0))
+    return x, init
+
+
+def cpu_als(x, init, steps, warmup, nthreads):
+    """blas_arm ALS sweeps: warm-up, restart from init, then `steps` timed sweeps.
+    Returns (seconds per sweep list, final residual)."""
+    from oracle import blas_arm as ba
+    with ba.threads(nthreads):
+        f = init
+        for _ in range(warmup):
+            f, _, _, _ = ba.als_sweep(ba.Tree(x), f, 0.0)
+        f = init
+        tree = ba.Tree(x)
+        times = []
+        m_last = None
+        for _ in range(steps):
+            t = time.perf_counter()
+            f, _, _, m_last = ba.als_sweep(tree, f, 0.0)
+            times.append(time.perf_counter() - t)
+        xn2 = float(np.dot(x.ravel(), x.ravel()))
+        r, _ = ba.residual_fitness(f, m_last, xn2)
+    return times, r
+
+
+def cpu_gn(x, init, steps, nthreads):
+    from oracle import blas_arm as ba
+    with ba.threads(nthreads):
+        xn2 = float(np.dot(x.ravel(), x.ravel()))
+        f, lam, d = init, 1e-2, 0
+        tree = ba.Tree(x)
+        times, cg = [], 0
+        for _ in range(steps):
+            t = time.perf_counter()
+            f, diag = ba.gn_step(x, f, lam, xn2, tree)
+            times.append(time.perf_counter() - t)
+            cg += diag["cg_iters"]
+            lam, d = ba.schedule_next(lam, d)
+    return times, cg
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    from oracle import oracle as orc
-    cores = os.cpu_count() or 1
-    orc.set_threads(cores)
+    key = args.workload
     t0 = time.time()
-    truth = orc.random_model(DIMS, RANK, orc.problem_seed(0, RANK, 0))
-    x = orc.reconstruct(truth)
-    xn = float(np.linalg.norm(x))
-    noise = np.random.default_rng(0x4E01).standard_normal(x.shape)  # timing input only
-    x += NOISE * xn / float(np.linalg.norm(noise)) * noise
-    del noise
-    init = orc.random_model(DIMS, RANK, orc.init_seed(0, RANK, 0, 0))
+    x, init = host_tensor(key)
     gen_s = time.time() - t0
-    f = init
-    for _ in range(args.warmup):
-        f, _, _, _ = orc.als_sweep(x, f, 0.0)
-    times = []
-    for _ in range(args.steps):
-        t = time.perf_counter()
-        f, _, _, _ = orc.als_sweep(x, f, 0.0)
-        times.append(time.perf_counter() - t)
+    n = cores()
+    times, r = cpu_als(x, init, args.steps, args.warmup, n)
     total = sum(times)
     value = args.steps / total
+    gn_times, gn_cg = cpu_gn(x, init, 2, n)
+    sample = (f"{args.steps} ALS sweeps (after {args.warmup} warm-up) of the full {key.upper()} tensor: "
+              f"als.cpp:22-52 / mttkrp.cpp:160-189 restated with OpenBLAS DGEMMs (oracle/blas_arm.py), "
+              f"{n} threads; input generation {gen_s:.1f} s untimed")
     out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "impl": "reference", "metric": metric(key.upper()), "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded keyed-RNG factors; numpy Gaussian noise for the CPU timing input)",
-        "config": workload_config(1),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} ALS sweeps of the full C2 tensor (oracle restatement "
-                                   f"of als.cpp:22-52, {cores} threads); input generation {gen_s:.1f}s untimed"},
+        "data": "synthetic (reference keyed RNG; the device generates the same bits)",
+        "config": workload_config(key, 1),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference (Eigen/CMake) cannot be built here; oracle/ is its CPU restatement",
+        "final_residual": r,
+        "gn": {"iters_per_s": len(gn_times) / sum(gn_times), "ms_per_iter": 1e3 * sum(gn_times) / len(gn_times),
+               "cg_iters_total": gn_cg,
+               "note": "gauss_newton.cpp:360-449 with BLAS products: 2 tree contractions + the naive "
+                       "residual contraction + CG (per-(n,p) J^T J v)"},
+        "note": "the reference (Eigen/CMake) cannot be built here (DESIGN.md §4); this is its algorithm "
+                "on OpenBLAS. 1-thread figures (the reference's own Eigen setting) are in the B200 line's "
+                "cpu_baseline.single_thread",
     }
     print(json.dumps(out), flush=True)
     return 0
 
 
+def cpu_baseline_sample(x, init, key):
+    """blas_arm on this host's cores over the same tensor (reported only): all
+    cores (the value) and 1 thread (the reference's own setting)."""
+    n = cores()
+    times, _ = cpu_als(x, init, 2, 0, n)
+    t1, _ = cpu_als(x, init, 1, 0, 1)
+    return {"value": len(times) / sum(times), "unit": UNIT, "cores": n, "kind": "port",
+            "sample": f"{len(times)} ALS sweeps of the full {key.upper()} tensor (the device-generated bytes), "
+                      f"als.cpp:22-52 with OpenBLAS DGEMMs (oracle/blas_arm.py), {n} threads, "
+                      f"{sum(times):.2f} s",
+            "single_thread": {"value": 1.0 / t1[0], "unit": UNIT, "cores": 1,
+                              "sample": f"1 sweep on 1 BLAS thread, the reference's setting ({t1[0]:.2f} s)"}}
+
+
 # ------------------------------------------------------------------------ B200 arm
-def cpu_baseline_sample(x_host, init):
-    """Oracle ALS sweep on the host cores over the same tensor (reported only).
-    Two settings: all host cores (the reported value), and one
-    thread, the reference's own setting (Eigen without OpenMP)."""
-    from oracle import oracle as orc
-    cores = os.cpu_count() or 1
-    orc.set_threads(cores)
-    t = time.perf_counter()
-    orc.als_sweep(x_host, init, 0.0)
-    dt = time.perf_counter() - t
-    orc.set_threads(1)
-    t = time.perf_counter()
-    orc.als_sweep(x_host, init, 0.0)
-    dt1 = time.perf_counter() - t
-    orc.set_threads(cores)
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"1 ALS sweep of the full C2 tensor (oracle restatement of als.cpp:22-52, "
-                      f"{cores} threads, {dt:.2f}s)",
-            "single_thread": {"value": 1.0 / dt1, "unit": UNIT, "cores": 1,
-                              "sample": f"the same sweep on 1 thread, the reference's setting ({dt1:.2f}s)"}}
+def timed_sweeps(p, init, steps, warmup, clocks_device=None):
+    from paper_1910_12331_b200 import cpkit
+    sampler = ClockSampler(clocks_device) if clocks_device is not None else None
+    if sampler:
+        sampler.__enter__()
+    try:
+        p.time_als_sweeps(0.0, max(1, warmup))
+        p.set_factors(init)
+        launches0 = cpkit.kernel_launches()
+        p.profile(True)
+        ms = p.time_als_sweeps(0.0, steps)
+        prof_ms, prof_cnt = p.profile_read()
+        p.profile(False)
+        launches = cpkit.kernel_launches() - launches0
+    finally:
+        if sampler:
+            sampler.__exit__(None, None, None)
+    return ms, prof_ms, prof_cnt, launches, (sampler.summary() if sampler else None)
+
+
+def residual_now(p, dims, xn2):
+    p.mttkrp(len(dims) - 1, download=False)
+    return p.residual(xn2)[0]
+
+
+def gn_rate(p, init, steps=3, reps=3):
+    runs = []
+    for _ in range(reps + 1):  # the first call warms the CG launch path
+        p.set_factors(init)
+        runs.append(p.time_gn_steps({}, steps))
+    ms = statistics.median(r[0] for r in runs[1:])
+    return {"iters_per_s": steps / (ms * 1e-3), "ms_per_iter": ms / steps, "cg_iters_total": runs[-1][1],
+            "iters": steps, "config": "default GnConfig (varying lambda, CG cap min(sum s R, 10 R)), steady "
+                                      "state: the start's tree pass cached before timing"}
 
 
 def run_b200(args, rank, world, local_rank):
     from paper_1910_12331_b200 import cpkit
     cpkit.load()
-    dist = None
-    nccl_id = None
+    dist, nccl_id = None, None
     if world > 1:
         import torch
         import torch.distributed as tdist
@@ -213,135 +306,140 @@ def run_b200(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    truth = cpkit.random_factors(DIMS, RANK, cpkit.problem_seed(0, RANK, 0))
-    init = cpkit.random_factors(DIMS, RANK, cpkit.init_seed(0, RANK, 0, 0))
-    p = cpkit.DeviceProblem(DIMS, RANK, device=local_rank, shard=rank, world=world, nccl_id=nccl_id)
-    p.generate(truth, noise_seed=1, noise_rel=NOISE)
+    key = args.workload
+    w = WORKLOADS[key]
+    dims, R = w["dims"], w["rank"]
+    truth = cpkit.random_factors(dims, R, cpkit.problem_seed(0, R, 0))
+    init = cpkit.random_factors(dims, R, cpkit.init_seed(0, R, 0, 0))
+    p = cpkit.DeviceProblem(dims, R, device=local_rank, shard=rank, world=world, nccl_id=nccl_id)
+    t0 = time.time()
+    p.generate(truth, noise_seed=1, noise_rel=w["noise"])
+    gen_s = time.time() - t0
     p.set_factors(init)
     lo, hi, local_elems = p.slab()
-
+    xn2 = p.norm2()
     peak_dmma = cpkit.probe_dmma_peak(local_rank)
 
-    # ---- warm-up, then exactly K timed sweeps (CUDA events on the problem's stream);
-    # clocks are sampled from just before the warm-up through the timed region
-    with ClockSampler(local_rank) as clk:
-        p.time_als_sweeps(0.0, max(1, args.warmup))
-        p.set_factors(init)
-        barrier()
-        launches0 = cpkit.kernel_launches()
-        p.profile(True)
-        ms = p.time_als_sweeps(0.0, args.steps)
-        prof_ms, prof_cnt = p.profile_read()
-        p.profile(False)
-        launches = cpkit.kernel_launches() - launches0
+    # ---- warm-up, then exactly K timed sweeps (CUDA events on the problem's stream)
     barrier()
+    ms, prof_ms, prof_cnt, launches, clocks = timed_sweeps(p, init, args.steps, args.warmup, local_rank)
     ms = max_over_ranks(ms)
     value = args.steps / (ms / 1e3)
+    final_res = residual_now(p, dims, xn2)
 
-    # ---- roofline: root MTTKRP GEMMs (2 per sweep), measured inside the timed region
-    flops_per_root = 2.0 * RANK * local_elems
-    root_ms = (prof_ms[0] + prof_ms[1]) / max(1, prof_cnt[0] + prof_cnt[1])
+    # ---- roofline: the root MTTKRP contractions (2 per sweep), timed inside the region
+    flops_per_root = 2.0 * R * local_elems
+    nroots = prof_cnt[0] + prof_cnt[1]
+    root_ms = (prof_ms[0] + prof_ms[1]) / max(1, nroots)
     achieved_tf = flops_per_root / (root_ms * 1e-3) / 1e12
     share = (prof_ms[0] + prof_ms[1]) / ms if ms > 0 else None
-    traffic = ncu_traffic().get("root_gemm_dram_bytes_per_launch")  # committed ncu --set full capture
+    h = (len(dims) + 1) // 2
+    Fdim = int(np.prod(dims[:h]))
+    root_bytes = 8.0 * local_elems + 8.0 * R * Fdim
 
-    # ---- secondary kernels: J^T J v (GN inner loop) and ||X||^2 streaming
+    # ---- secondary: GN iterations, J^T J v, ||X||^2 streaming
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs", 6650.0)
+    gn = gn_rate(p, init)
+    S = sum(dims)
     jtj_ms = p.time_jtj(50)
-    S = sum(DIMS)
-    jtj_bytes = 8.0 * (3 * RANK * S + len(DIMS) * (len(DIMS) + 1) / 2 * RANK * RANK)
-    jtj_flops = 6.0 * RANK * RANK * S
+    jtj_bytes = 8.0 * (3 * R * S + len(dims) * (len(dims) + 1) / 2 * R * R)
     nrm_ms = p.time_norm2(5)
     nrm_gbs = 8.0 * local_elems / (nrm_ms * 1e-3) / 1e9
-    # the same streaming kernel on a >= 1 GB tensor (bandwidth-bound
-    # kernels shown at a size where HBM, not launch latency, is the bound)
-    big = None
+
+    # ---- end to end through the public C ABI
+    e2e = None
+    x_host = None
     if world == 1:
-        bdims = [512, 512, 512]  # 1.07 GB
-        pb = cpkit.DeviceProblem(bdims, 1)
-        pb.generate(cpkit.random_factors(bdims, 1, 7))
-        big_ms = pb.time_norm2(10)
-        big_bytes = 8.0 * 512 ** 3
-        big = {"ms": big_ms, "gbs": big_bytes / (big_ms * 1e-3) / 1e9, "bytes": big_bytes}
-        pb.close()
-
-    # ---- GN outer iterations (default config: varying lambda, CG cap min(sum s R, 10 R)=1000)
-    # GN: steady-state iterations. Each timed call starts from the same init with
-    # the tree pass of the starting point already cached (gn_optimize computes it
-    # once before its first iteration), so the per-iteration figure is one tree
-    # pass (the post-step residual) + gradient + preconditioner + CG + update.
-    GN_STEPS = 4
-    gn_runs = []
-    for i in range(4):  # first call warms the CG kernel's launch path; median of the rest
-        p.set_factors(init)  # time_gn_steps caches the starting point's tree pass before timing
-        gn_runs.append(p.time_gn_steps({}, GN_STEPS))
-    gn_ms = statistics.median(r[0] for r in gn_runs[1:])
-    gn_cg = gn_runs[-1][1]
-
-    # ---- end to end through the public C ABI (host tensor in, host factors out)
-    import torch
-    x_pinned = torch.empty(local_elems, dtype=torch.float64, pin_memory=True).numpy()
-    p.download_into(x_pinned)
-    e2e_cfg = {"optimizer": "als", "als": {"max_sweeps": E2E_SWEEPS, "residual_tol": 0.0,
-                                           "step_tol": 0.0}}
-    e2e_times = []
-    for i in range(max(1, args.e2e_steps) + 1):
-        barrier()
-        t = time.perf_counter()
-        p.upload(x_pinned)
-        out, rep = p.optimize(e2e_cfg, init)
-        dt = time.perf_counter() - t
-        if i > 0:
-            e2e_times.append(dt)
-    e2e_dt = max_over_ranks(statistics.median(e2e_times))
-    e2e_value = E2E_SWEEPS / e2e_dt
-    final = rep.to_json()["records"][-1]
+        import torch
+        x_host = torch.empty(local_elems, dtype=torch.float64, pin_memory=True).numpy()
+        p.download_into(x_host)
+        p.close()  # the drop-in call allocates its own device problem
+        t = cpkit.Tensor.create(x_host.reshape(dims))  # the user's host tensor (pinned storage)
+        cfg = {"optimizer": "als", "rank": R, "seed": 0, "init": {"distribution": "uniform", "a": 0.0, "b": 1.0},
+               "als": {"max_sweeps": E2E_SWEEPS, "residual_tol": 0.0, "step_tol": 0.0}}
+        times = []
+        for i in range(max(1, args.e2e_steps) + 1):
+            t1 = time.perf_counter()
+            model, rep = cpkit.decompose(t, cfg)
+            fac = model.factors()  # D2H of the result happened inside decompose; read it here
+            dt = time.perf_counter() - t1
+            if i > 0:
+                times.append(dt)
+        e2e_dt = statistics.median(times)
+        recs = rep.to_json()["records"]
+        e2e = {"value": E2E_SWEEPS / e2e_dt, "unit": UNIT,
+               "h2d_bytes_per_step": int((8 * local_elems + 8 * S * R) / E2E_SWEEPS),
+               "d2h_bytes_per_step": int(8 * S * R / E2E_SWEEPS),
+               "h2d_bytes_per_call": int(8 * local_elems + 8 * S * R), "d2h_bytes_per_call": int(8 * S * R),
+               "sweeps_per_call": E2E_SWEEPS, "s_per_call": e2e_dt,
+               "path": f"cpkit_decompose(host cpkit_tensor, ALS {E2E_SWEEPS} sweeps) -> cpkit_model: device "
+                       "problem allocation, H2D of the tensor + X^T layout copy, sweeps, factors D2H",
+               "final_residual": recs[-1]["residual"], "factors_checksum": float(sum(a.sum() for a in fac))}
+        del t
+    else:
+        # sharded: each rank uploads its host slab and runs cpkit_dev_optimize
+        import torch
+        x_host = torch.empty(local_elems, dtype=torch.float64, pin_memory=True).numpy()
+        p.download_into(x_host)
+        cfg = {"optimizer": "als", "als": {"max_sweeps": E2E_SWEEPS, "residual_tol": 0.0, "step_tol": 0.0}}
+        times = []
+        for i in range(max(1, args.e2e_steps) + 1):
+            barrier()
+            t1 = time.perf_counter()
+            p.upload(x_host)
+            out, rep = p.optimize(cfg, init)
+            dt = time.perf_counter() - t1
+            if i > 0:
+                times.append(dt)
+        e2e_dt = max_over_ranks(statistics.median(times))
+        e2e = {"value": E2E_SWEEPS / e2e_dt, "unit": UNIT,
+               "h2d_bytes_per_step": int((8 * local_elems + 8 * S * R) / E2E_SWEEPS),
+               "d2h_bytes_per_step": int(8 * S * R / E2E_SWEEPS),
+               "path": f"per rank: cpkit_dev_upload_tensor(host slab) + cpkit_dev_optimize (ALS, {E2E_SWEEPS} "
+                       "sweeps) + host factors"}
+        p.close()
 
     result = None
     if rank == 0:
         result = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": metric(key.upper()), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference keyed RNG, generated on device)",
-            "config": workload_config(world),
+            "data": "synthetic (reference keyed RNG, generated on device; bit-identical to the CPU arm's tensor)",
+            "config": workload_config(key, world),
             "roofline": {"bound": "tensor", "kernel": "root MTTKRP GEMM (TMA + DMMA m16n8k16)",
                          "achieved": achieved_tf, "peak": peak_dmma, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_dmma,
                          "peak_source": "FP64 DMMA issue-rate probe measured in this run "
                                         "(MEASURED_PEAKS.json has no fp64 entry)",
-                         "traffic": traffic, "algorithmic_flops_per_launch": flops_per_root,
-                         "algorithmic_bytes_per_launch": 8.0 * local_elems + 8.0 * RANK * 160000,
-                         "avg_launch_ms": root_ms, "launches": prof_cnt[0] + prof_cnt[1],
-                         "share_of_step": share},
+                         "traffic": ncu_traffic(key), "algorithmic_flops_per_launch": flops_per_root,
+                         "algorithmic_bytes_per_launch": root_bytes, "avg_launch_ms": root_ms,
+                         "launches": nroots, "share_of_step": share},
+            "gn": gn,
             "kernels": {
                 "jtj_matvec": {"ms": jtj_ms, "gbs": jtj_bytes / (jtj_ms * 1e-3) / 1e9,
                                "hbm_frac": jtj_bytes / (jtj_ms * 1e-3) / 1e9 / hbm,
-                               "tflops": jtj_flops / (jtj_ms * 1e-3) / 1e12,
-                               "bytes": jtj_bytes, "note": "3.4 MB working set, L2-resident, launch-bound"},
-                "norm2_1GB": None if big is None else {**big, "hbm_frac": big["gbs"] / hbm},
-                "norm2": {"ms": nrm_ms, "gbs": nrm_gbs, "hbm_frac": nrm_gbs / hbm,
+                               "tflops": 6.0 * R * R * S / (jtj_ms * 1e-3) / 1e12, "bytes": jtj_bytes,
+                               "note": "L2-resident working set: latency-bound"},
+                "norm2": {"ms": nrm_ms, "gbs": nrm_gbs, "hbm_frac": nrm_gbs / hbm, "bytes": 8.0 * local_elems,
                           "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
             },
-            "gn": {"iters_per_s": GN_STEPS / (gn_ms * 1e-3), "ms_per_iter": gn_ms / GN_STEPS,
-                   "cg_iters_total": gn_cg, "iters": GN_STEPS,
-                   "config": "default GnConfig (varying lambda, cg cap 1000), steady state: "
-                             "the starting point's tree pass cached before timing"},
-            "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(8 * local_elems + 8 * S * RANK),
-                    "d2h_bytes_per_step": int(8 * S * RANK),
-                    "path": f"cpkit_dev_upload_tensor + cpkit_dev_optimize (ALS, {E2E_SWEEPS} sweeps) "
-                            "+ host factors", "final_fitness": final["fitness"]},
+            "e2e": e2e,
+            "final_residual": final_res,
+            "generation_s": gen_s,
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        x_host = x_pinned.reshape(DIMS)
-        result["cpu_baseline"] = cpu_baseline_sample(x_host, init)
-    p.close()
-    if rank == 0 and world == 1 and not args.no_c5s:
-        result["c5s"] = c5s_slice(cpkit, result["roofline"]["peak"])
+        result["cpu_baseline"] = cpu_baseline_sample(x_host.reshape(dims), init, key)
+    del x_host
+    if rank == 0 and world == 1 and not args.no_c2 and key != "c2":
+        result["c2"] = c2_line(cpkit, peak_dmma)
+    if world > 1 and not args.no_c5:
+        c5 = c5_line(cpkit, rank, world, local_rank, nccl_id, peak_dmma, barrier, max_over_ranks)
+        if rank == 0:
+            result["c5"] = c5
     if dist:
         dist.destroy_process_group()
     if rank == 0:
@@ -349,41 +447,60 @@ def run_b200(args, rank, world, local_rank):
     return 0
 
 
-def c5s_slice(cpkit, peak_tf):
-    """The largest config that fits one GPU (C5s: order 4, s=200, R=200, 12.8 GB,
-    the 1-GPU anchor of the C5 scaling case), generated on device: ALS sweep and
-    GN iteration times, reported beside the headline (not the bench value)."""
-    dims, R = [200] * 4, 200
+def c2_line(cpkit, peak):
+    """BASELINE configs[1] (C2) beside the headline: ALS sweeps/s, GN iterations/s
+    and the root GEMM's fraction of the DMMA peak (device-resident)."""
+    w = WORKLOADS["c2"]
+    dims, R = w["dims"], w["rank"]
     truth = cpkit.random_factors(dims, R, cpkit.problem_seed(0, R, 0))
     init = cpkit.random_factors(dims, R, cpkit.init_seed(0, R, 0, 0))
     q = cpkit.DeviceProblem(dims, R)
-    q.generate(truth, 1, 1e-4)
+    q.generate(truth, 1, w["noise"])
     q.set_factors(init)
-    q.time_als_sweeps(0.0, 1)  # warm-up (graph capture)
-    als_ms = q.time_als_sweeps(0.0, 3) / 3
-    q.set_factors(init)
-    q.time_gn_steps({}, 1)  # warm-up
-    q.set_factors(init)
-    gn_ms, cg = q.time_gn_steps({}, 2)
+    ms, pm, pc, _, _ = timed_sweeps(q, init, 50, 5)
+    root_ms = (pm[0] + pm[1]) / max(1, pc[0] + pc[1])
+    tf = 2.0 * R * np.prod(dims) / (root_ms * 1e-3) / 1e12
+    gn = gn_rate(q, init, steps=4)
     q.close()
-    root_flops = 4.0 * R * 200 ** 4  # two root contractions per sweep / per GN iteration
-    return {"workload": "C5s: order-4 s=200 R=200 uniform[0,1) + 1e-4 noise (12.8 GB), generated on device",
-            "als_ms_per_sweep": als_ms, "als_sweeps_per_s": 1e3 / als_ms,
-            "als_root_tflops": root_flops / (als_ms * 1e-3) / 1e12,
-            "als_root_frac_of_peak": root_flops / (als_ms * 1e-3) / 1e12 / peak_tf,
-            "gn_ms_per_iter": gn_ms / 2, "gn_cg_iters": cg,
-            "note": "TFLOP/s = the two root contractions' 4 R prod(s) flops over the whole sweep time"}
+    return {"workload": w["name"], "als_sweeps_per_s": 50 / (ms * 1e-3), "als_ms_per_sweep": ms / 50,
+            "root_tflops": tf, "root_frac_of_peak": tf / peak, "gn": gn,
+            "note": "order 3: multi-sweep dimension tree (3 root contractions per 2 sweeps), 50 sweeps timed"}
+
+
+def c5_line(cpkit, rank, world, local_rank, nccl_id, peak, barrier, max_over_ranks):
+    """BASELINE configs[4] at its full size (order 4, s=400, R=200, 205 GB), sharded
+    on the last mode over the N GPUs: ALS sweep time and the work-normalised root
+    rate (2 contractions of 2 R prod(s) flops per sweep)."""
+    w = WORKLOADS["c5"]
+    dims, R = w["dims"], w["rank"]
+    truth = cpkit.random_factors(dims, R, cpkit.problem_seed(0, R, 0))
+    init = cpkit.random_factors(dims, R, cpkit.init_seed(0, R, 0, 0))
+    q = cpkit.DeviceProblem(dims, R, device=local_rank, shard=rank, world=world, nccl_id=nccl_id)
+    t0 = time.time()
+    q.generate(truth, 1, w["noise"])
+    gen_s = time.time() - t0
+    q.set_factors(init)
+    barrier()
+    ms, pm, pc, _, _ = timed_sweeps(q, init, 3, 1)
+    ms = max_over_ranks(ms)
+    q.close()
+    flops = 4.0 * R * float(np.prod(dims))
+    return {"workload": w["name"], "n_gpus": world, "als_ms_per_sweep": ms / 3, "als_sweeps_per_s": 3e3 / ms,
+            "work_normalised_tflops": flops / (ms / 3 * 1e-3) / 1e12,
+            "per_gpu_frac_of_peak": flops / world / (ms / 3 * 1e-3) / 1e12 / peak, "generation_s": gen_s}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--workload", default="c5s", choices=["c5s", "c2"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c5s", action="store_true", help="skip the C5s (largest single-GPU config) line item")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 line item")
+    ap.add_argument("--no-c5", action="store_true", help="N>1: skip the full 205 GB configs[4] tensor")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -512,7 +512,7 @@ std::vector<double> reconstruct(const Model& model) {
     for (std::uint64_t j = 0; j < sl; ++j)
         for (std::uint64_t r = 0; r < R; ++r) bt[r * sl + j] = model.factors[order - 1].d[j * R + r];
     parallel_rows(static_cast<std::int64_t>(rows), [&](std::int64_t lo, std::int64_t hi) {
-        std::vector<double> pre(R), acc(sl);
+        std::vector<double> pre(R);
         std::vector<std::uint64_t> idx(order, 0);
         for (std::int64_t f = lo; f < hi; ++f) {
             std::uint64_t q = static_cast<std::uint64_t>(f);
@@ -525,13 +525,13 @@ std::vector<double> reconstruct(const Model& model) {
                 for (std::size_t n = 0; n + 1 < order; ++n) prod *= model.factors[n].d[idx[n] * R + r];
                 pre[r] = prod;
             }
-            std::fill(acc.begin(), acc.end(), 0.0);
+            double* __restrict a = t.data() + static_cast<std::uint64_t>(f) * sl;
+            for (std::uint64_t j = 0; j < sl; ++j) a[j] = 0.0;
             for (std::uint64_t r = 0; r < R; ++r) {
                 const double pr = pre[r];
-                const double* br = bt.data() + r * sl;
-                for (std::uint64_t j = 0; j < sl; ++j) acc[j] += pr * br[j];
+                const double* __restrict br = bt.data() + r * sl;
+                for (std::uint64_t j = 0; j < sl; ++j) a[j] += pr * br[j];
             }
-            std::memcpy(t.data() + static_cast<std::uint64_t>(f) * sl, acc.data(), sl * 8);
         }
     });
     return t;
