@@ -201,6 +201,10 @@ cpkit::GnConfig gn_from_block(const Json& g) {
     if (beta == "standard") c.cg_beta = cpkit::CgBetaVariant::standard;
     else if (beta == "stale_denominator") c.cg_beta = cpkit::CgBetaVariant::stale_denominator;
     else throw cpkit::ParseError("unknown cg_beta variant: " + beta);
+    // B200 extension: "naive" = the reference's third contraction for residual_after
+    const std::string ra = g.value("residual_after", "tree");
+    if (ra == "naive") c.residual_naive = true;
+    else if (ra != "tree") throw cpkit::ParseError("unknown residual_after mode: " + ra);
     return c;
 }
 cpkit::GnConfig gn_from_json(const Json& j) {
@@ -323,6 +327,7 @@ Json gn_to_json(const cpkit::GnConfig& c) {
     }
     g["armijo"] = a;
     g["cg_beta"] = c.cg_beta == cpkit::CgBetaVariant::standard ? "standard" : "stale_denominator";
+    if (c.residual_naive) g["residual_after"] = "naive";  // only when set: the reference schema otherwise
     return g;
 }
 Json init_to_json(const InitDist& d) {

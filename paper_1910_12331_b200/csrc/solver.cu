@@ -1488,6 +1488,10 @@ AlsSweepDiag DeviceProblem::als_sweep_finish(double* res, double* fit) {
 // values packed into mapped pinned memory; a step that must not have happened
 // is undone from the device copy of the pre-step factors. Same results as the
 // phase-by-phase version (`CPKIT_GN_SYNC=1`, used for Armijo).
+bool DeviceProblem::ref_residual(const GnConfig& cfg) {
+    static const bool env = std::getenv("CPKIT_GN_REF_RESIDUAL") != nullptr;
+    return cfg.residual_naive || env;
+}
 GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
     if (cfg.armijo || std::getenv("CPKIT_GN_SYNC")) return gn_step_sync(cfg, schedule, xnorm2);
     gn_enqueue(cfg, schedule, xnorm2, 0);
@@ -1581,13 +1585,19 @@ void DeviceProblem::gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule,
     pinv_ready_ = true;
     pinv_lambda_ = next.lambda;
     pinv_shape_ = shape;
-    // residual_after from the next iteration's tree pass (cached for the next step)
     side_busy_ = true;
-    compute_all_mttkrp();
+    if (ref_residual(cfg)) {
+        // reference semantics: an uncached contraction of the stepped factors;
+        // the next step recomputes its tree pass and residual_before
+        mttkrp_naive(N - 1);
+    } else {
+        // residual_after from the next iteration's tree pass (cached for the next step)
+        compute_all_mttkrp();
+    }
     side_busy_ = false;
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[1], 0));  // Grams
     residual_launch(xnorm2);
-    res_current_ = true;
+    res_current_ = !ref_residual(cfg);
     res_xnorm_ = xnorm2;
     launch_pack_values(scal_.get() + kRes, 2, nullptr, 0, dm + o_after, ctx_.stream);
     CPK_CUDA(cudaEventRecord(gn_ev_[slot], ctx_.stream));
@@ -1731,7 +1741,8 @@ GnStepDiag DeviceProblem::gn_step_sync(const GnConfig& cfg, RegSchedule& schedul
     diag.step_norm = hpin_[3];
     if (!*fin_pin) throw NumericalFailure("gn_step: non-finite factors after update");
     if (residual_after < 0.0) {
-        compute_all_mttkrp();
+        if (ref_residual(cfg)) mttkrp_naive(N - 1);
+        else compute_all_mttkrp();
         grams_all();
         residual_after = residual_fitness(xnorm2, N - 1).first;
     }

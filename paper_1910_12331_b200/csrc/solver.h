@@ -125,6 +125,11 @@ struct GnConfig {  // gauss_newton.hpp:50-62
     RegSchedule schedule = RegSchedule::varying();
     std::optional<ArmijoParams> armijo;
     CgBetaVariant cg_beta = CgBetaVariant::standard;
+    // residual_after from a third, uncached contraction of the stepped factors
+    // (the reference's semantics, gauss_newton.cpp:442-444) instead of the next
+    // iteration's tree pass. JSON gn.residual_after = "naive" | "tree" (default),
+    // or CPKIT_GN_REF_RESIDUAL=1.
+    bool residual_naive = false;
     void validate() const;
 };
 struct AlsConfig {  // als.hpp:11-22
@@ -281,6 +286,7 @@ public:
     GnStepDiag gn_step(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);  // :360-449
     // the same step with a host decision after every phase (Armijo needs it)
     GnStepDiag gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2);
+    static bool ref_residual(const GnConfig& cfg);  // GnConfig::residual_naive or CPKIT_GN_REF_RESIDUAL
     // the default step split for pipelining: queue it (slot 0/1: diagnostics,
     // pre-step snapshot, completion event), then decode it (a step that must not
     // have happened is undone from its slot's snapshot)

@@ -145,3 +145,34 @@ def test_full_size_properties(ck, name, dims, R):
         prev = r
     # order 3: multi-sweep dimension tree (3 roots per 2 sweeps); else the reference tree (2 per sweep)
     assert counts == ([2, 1, 2] if len(dims) == 3 else [2, 2, 2])
+
+
+@pytest.mark.parametrize("dims,R", [([14, 12, 11], 5), ([9, 8, 7, 6], 4)])
+def test_gn_reference_residual_semantics(orc, ck, dims, R):
+    """gn.residual_after = "naive": residual_after from a third, uncached
+    contraction of the stepped factors, as gauss_newton.cpp:442-444 does (the
+    default reuses the next iteration's tree pass). Same trace as the oracle
+    (which follows the reference), and exactly one extra front-root contraction
+    per stepped iteration."""
+    truth = orc.random_model(dims, R, orc.problem_seed(3, R, 0))
+    x = orc.reconstruct(truth) + 1e-3 * orc.random_model([int(np.prod(dims))], 1, 77, kind="gaussian")[0].reshape(dims)
+    init = orc.random_model(dims, R, orc.init_seed(3, R, 0, 0))
+    _, recs, st = orc.gn_optimize(x, init, orc.GnConfig(max_iters=8))
+    counts = {}
+    for mode in ("tree", "naive"):
+        p = ck.DeviceProblem(dims, R)
+        p.upload(x)
+        p.profile(True)
+        _, rep = p.optimize({"optimizer": "gn", "gn": {"max_iters": 8, "residual_after": mode}}, init)
+        _, cnt = p.profile_read()
+        j = rep.to_json()
+        assert j["status"] == st and len(j["records"]) == len(recs) == 8
+        for a, b in zip(j["records"], recs):
+            assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (mode, a, b)
+            assert abs(a["residual"] - b["residual"]) <= 1e-10 * b["residual"], (mode, a, b)
+        assert j["config"]["gn"].get("residual_after", "tree") == mode
+        counts[mode] = cnt
+    # profile counters [back roots, front/single-mode roots, CG solves]: a tree
+    # pass is one of each; the naive mode adds one front root per stepped iteration
+    assert counts["tree"][1] == counts["tree"][0], counts
+    assert counts["naive"][1] - counts["naive"][0] == len(recs), counts
