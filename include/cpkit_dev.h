@@ -153,6 +153,12 @@ CPKIT_API cpkit_status cpkit_dev_shard_range(uint64_t extent, int shard, int wor
 CPKIT_API cpkit_status cpkit_dev_download_tensor(cpkit_dev_problem* p, double* host_local);
 /* Number of kernels this library launched since load (for the bench). */
 CPKIT_API uint64_t cpkit_dev_kernel_launches(void);
+/* Guarded allocation mode (env CPKIT_GUARD=1, the pool has no compute-sanitizer):
+ * device buffers released so far whose 64 KB red zones were overwritten. */
+CPKIT_API uint64_t cpkit_dev_guard_violations(void);
+/* Positive control of the guard mode: out-of-bounds writes past both ends of
+ * fresh buffers are detected (*detected = 1). INVALID_ARGUMENT without CPKIT_GUARD. */
+CPKIT_API cpkit_status cpkit_dev_guard_selftest(int* detected);
 
 #ifdef __cplusplus
 }

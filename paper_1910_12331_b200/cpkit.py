@@ -46,6 +46,7 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_time_als_sweeps", "cpkit_dev_time_roots", "cpkit_dev_profile",
     "cpkit_dev_profile_read", "cpkit_dev_time_jtj",
     "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
+    "cpkit_dev_guard_violations", "cpkit_dev_guard_selftest",
     "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
     "cpkit_dev_init_seed", "cpkit_dev_download_tensor", "cpkit_dev_shard_range",
     "cpkit_dev_problem_create_loopback", "cpkit_dev_load_tensor",
@@ -96,6 +97,7 @@ def load():
     L.cpkit_dev_reset_contraction_counter.argtypes = [_vp]
     L.cpkit_dev_reset_contraction_counter.restype = None
     L.cpkit_dev_kernel_launches.restype = _u64
+    L.cpkit_dev_guard_violations.restype = _u64
     L.cpkit_report_ok.argtypes = [_vp]
     L.cpkit_dev_problem_seed.restype = _u64
     L.cpkit_dev_problem_seed.argtypes = [_u64, C.c_int, C.c_int]
@@ -605,3 +607,15 @@ def init_seed(master: int, rank: int, problem: int, init: int) -> int:
 
 def kernel_launches() -> int:
     return int(load().cpkit_dev_kernel_launches())
+
+
+def guard_violations() -> int:
+    """Released device buffers whose red zones were overwritten (CPKIT_GUARD=1 mode)."""
+    return int(load().cpkit_dev_guard_violations())
+
+
+def guard_selftest() -> bool:
+    """Positive control of the guard mode (needs CPKIT_GUARD=1 in the environment)."""
+    d = C.c_int()
+    _chk(load().cpkit_dev_guard_selftest(C.byref(d)))
+    return bool(d.value)

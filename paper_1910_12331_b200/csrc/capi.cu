@@ -1973,6 +1973,11 @@ cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops) {
     return guarded([&] { *tflops = cpkit::probe_dmma_peak(device); });
 }
 uint64_t cpkit_dev_kernel_launches(void) { return cpkit::kernel_launches(); }
+uint64_t cpkit_dev_guard_violations(void) { return cpkit::guard_violations(); }
+cpkit_status cpkit_dev_guard_selftest(int* detected) {
+    if (!detected) return fail(CPKIT_ERR_INVALID_ARGUMENT, "null argument");
+    return guarded([&] { *detected = cpkit::guard_selftest() ? 1 : 0; });
+}
 
 cpkit_status cpkit_dev_random_factors(const uint64_t* dims, uint64_t order, uint64_t rank, uint64_t seed,
                                       int kind, double a, double b, double* out) {

@@ -39,6 +39,21 @@ class DeviceError : public Error { public: using Error::Error; };
                                        " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
     } while (0)
 
+// ---- guarded allocation mode (CPKIT_GUARD=1; runtime.cu). compute-sanitizer
+// is not available on the GPU pool, so out-of-bounds WRITES are caught here:
+// every DevBuf sits between two kGuardBytes red zones filled with kGuardByte,
+// and each red zone is checked when the buffer is released (after a device
+// synchronisation); a changed byte is reported on stderr and counted
+// (cpkit_dev_guard_violations). Out-of-bounds READS return the pattern, which
+// the parity tests then see as wrong results.
+constexpr std::size_t kGuardBytes = 64 * 1024;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_enabled();
+void* guard_alloc(std::size_t bytes);                 // returns the user pointer
+void guard_free(void* user, std::size_t bytes);       // checks both red zones, frees
+std::uint64_t guard_violations();
+bool guard_selftest();  // positive control (CPKIT_GUARD=1 only)
+
 // ---- owning device buffer
 template <typename T>
 class DevBuf {
@@ -48,20 +63,34 @@ public:
     ~DevBuf() { release(); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), guarded_(o.guarded_) { o.p_ = nullptr; o.n_ = 0; }
     DevBuf& operator=(DevBuf&& o) noexcept {
-        if (this != &o) { release(); p_ = o.p_; n_ = o.n_; o.p_ = nullptr; o.n_ = 0; }
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            guarded_ = o.guarded_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
         return *this;
     }
     void resize(std::size_t n) {
         if (n == n_) return;
         release();
-        if (n) CPK_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        if (n) {
+            guarded_ = guard_enabled();
+            if (guarded_) p_ = static_cast<T*>(guard_alloc(n * sizeof(T)));
+            else CPK_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        }
         n_ = n;
     }
     void ensure(std::size_t n) { if (n > n_) resize(n); }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) {
+            if (guarded_) guard_free(p_, n_ * sizeof(T));
+            else cudaFree(p_);
+        }
         p_ = nullptr;
         n_ = 0;
     }
@@ -71,6 +100,7 @@ public:
 private:
     T* p_ = nullptr;
     std::size_t n_ = 0;
+    bool guarded_ = false;
 };
 
 // ---- kernel launch accounting (runtime.cu)

@@ -7,10 +7,13 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 #include "solver.h"
 
@@ -20,6 +23,74 @@ namespace cpkit {
 namespace {
 std::atomic<std::uint64_t> g_launches{0};
 }
+// ---- guarded allocation mode (common.h)
+namespace {
+std::atomic<std::uint64_t> g_guard_violations{0};
+bool guard_zone_ok(const unsigned char* dev, const char* which, std::size_t bytes) {
+    std::vector<unsigned char> h(kGuardBytes);
+    if (cudaMemcpy(h.data(), dev, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) return true;  // sticky fault: reported elsewhere
+    for (std::size_t i = 0; i < kGuardBytes; ++i)
+        if (h[i] != kGuardByte) {
+            std::fprintf(stderr, "cpkit guard: %s red zone of a %zu-byte buffer changed at byte %zu\n", which, bytes, i);
+            return false;
+        }
+    return true;
+}
+}  // namespace
+bool guard_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("CPKIT_GUARD");
+        return e && e[0] && e[0] != '0';
+    }();
+    return on;
+}
+void* guard_alloc(std::size_t bytes) {
+    const std::size_t body = (bytes + 255) & ~static_cast<std::size_t>(255);  // keep 256-B alignment of the tail zone
+    unsigned char* base = nullptr;
+    CPK_CUDA(cudaMalloc(&base, body + 2 * kGuardBytes));
+    CPK_CUDA(cudaMemset(base, kGuardByte, kGuardBytes));
+    CPK_CUDA(cudaMemset(base + kGuardBytes + bytes, kGuardByte, body - bytes + kGuardBytes));
+    return base + kGuardBytes;
+}
+void guard_free(void* user, std::size_t bytes) {
+    unsigned char* u = static_cast<unsigned char*>(user);
+    unsigned char* base = u - kGuardBytes;
+    cudaDeviceSynchronize();  // every stream's writes landed
+    const bool ok_front = guard_zone_ok(base, "front", bytes);
+    const bool ok_back = guard_zone_ok(u + bytes, "back", bytes);
+    if (!ok_front || !ok_back) g_guard_violations.fetch_add(1);
+    cudaFree(base);
+}
+std::uint64_t guard_violations() { return g_guard_violations.load(); }
+namespace {
+__global__ void guard_poke_kernel(double* p, long long i) { p[i] = 1.0; }
+}  // namespace
+// Positive control: write one element past the end of a guarded buffer and
+// one before its start; both must be counted.
+bool guard_selftest() {
+    if (!guard_enabled()) throw InvalidArgument("guard self-test needs CPKIT_GUARD=1");
+    const std::uint64_t before = guard_violations();
+    {
+        DevBuf<double> b(1000);
+        guard_poke_kernel<<<1, 1>>>(b.get(), 1000);
+        CPK_CUDA(cudaGetLastError());
+        count_launch(1);
+    }
+    {
+        DevBuf<double> b(7);
+        guard_poke_kernel<<<1, 1>>>(b.get(), -1);
+        CPK_CUDA(cudaGetLastError());
+        count_launch(1);
+    }
+    {
+        DevBuf<double> b(1000);  // in bounds: no report
+        guard_poke_kernel<<<1, 1>>>(b.get(), 999);
+        CPK_CUDA(cudaGetLastError());
+        count_launch(1);
+    }
+    return guard_violations() - before == 2;
+}
+
 void count_launch(int n) { g_launches.fetch_add(static_cast<std::uint64_t>(n), std::memory_order_relaxed); }
 std::uint64_t kernel_launches() { return g_launches.load(); }
 

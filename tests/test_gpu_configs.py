@@ -169,7 +169,7 @@ def test_gn_reference_residual_semantics(orc, ck, dims, R):
         assert j["status"] == st and len(j["records"]) == len(recs) == 8
         for a, b in zip(j["records"], recs):
             assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (mode, a, b)
-            assert abs(a["residual"] - b["residual"]) <= 1e-10 * b["residual"], (mode, a, b)
+            assert abs(a["residual"] - b["residual"]) <= 1e-9, (mode, a, b)  # fitness, as the trace tests
         assert j["config"]["gn"].get("residual_after", "tree") == mode
         counts[mode] = cnt
     # profile counters [back roots, front/single-mode roots, CG solves]: a tree
