@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,6 +54,9 @@ void* guard_alloc(std::size_t bytes);                 // returns the user pointe
 void guard_free(void* user, std::size_t bytes);       // checks both red zones, frees
 std::uint64_t guard_violations();
 bool guard_selftest();  // positive control (CPKIT_GUARD=1 only)
+// The red-zone check synchronises the device, which would invalidate another
+// thread's CUDA-graph capture: in guard mode captures and checks take this lock.
+std::recursive_mutex& guard_capture_mutex();
 
 // ---- owning device buffer
 template <typename T>
@@ -119,6 +123,12 @@ void ensure_dynamic_smem(const void* fn, std::size_t bytes);
 // other's SMs. Every cooperative launch goes through this: the stream waits for
 // the device's previous cooperative launch, launches, and becomes the new tail.
 void launch_cooperative(const void* fn, dim3 grid, dim3 block, void** args, std::size_t smem, cudaStream_t st);
+// Cooperative launch in clusters of cluster_x CTAs (cudaLaunchKernelEx with the
+// cooperative and cluster-dimension attributes), serialised like launch_cooperative.
+void launch_cooperative_cluster(const void* fn, dim3 grid, dim3 block, unsigned cluster_x, void** args,
+                                std::size_t smem, cudaStream_t st);
+// Clusters of cluster_x CTAs of fn that can be resident at once (cached per device).
+int max_active_clusters(const void* fn, dim3 block, unsigned cluster_x, std::size_t smem);
 template <typename F>
 inline void ensure_dynamic_smem(F* fn, std::size_t bytes) {
     ensure_dynamic_smem(reinterpret_cast<const void*>(fn), bytes);

@@ -23,6 +23,10 @@
 // in the same order (bitwise identical across CTAs; deterministic run to run).
 // Used when every tile fits one CTA (tasks <= #SMs) and the resident set fits
 // shared memory; kernels_cg.cu's streaming kernel covers the rest.
+// Cluster mode (CLU, the default when R needs 2..8 column tiles): the column
+// tiles of one row block form a thread-block cluster; W' and R' reach the
+// siblings by DSMEM bulk copies (push_own) instead of global stores + L2
+// gathers, bitwise the same arithmetic (tests/test_gpu_cg_cluster.py).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -64,6 +68,7 @@ struct RLayout {
     long long bp_off[kMaxOrder];                  // partial slabs of mode p (rowtiles[p] x R x R)
     int a2g, a2lg;                                // A2 lane-group size (pow2 >= order) and its log2
     long long dt_off;                             // D_n^T blocks (order x R x R)
+    int bs;                                       // CLU: row stride of a column block of Rb (tn + 4)
 };
 
 struct RDev {
@@ -252,7 +257,79 @@ __device__ __forceinline__ void r_stamp(const RDev& d, int vb, int it, int k) {
     }
 }
 
-template <int MT, int NT>
+// ---- thread-block cluster mode (CLU): the nct column tiles of one row block
+// form a cluster, so a row's sibling columns (W' in phase B, R' in phase C)
+// arrive by bulk copies into this CTA's shared memory (DSMEM pushes from the
+// siblings) instead of being published to global memory and gathered back
+// through L2. Measured at C2: 23.9 -> 22.0-22.6 us per CG iteration; pulling
+// the columns with ld.shared::cluster instead was slower than the L2 gather
+// (28 us), and a cluster-hierarchical grid barrier cost 2.5 us more.
+__device__ __forceinline__ void clu_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void clu_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ unsigned clu_map(unsigned addr, unsigned rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+// CLU row buffer: Rb is stored as nct column blocks [block][tm rows][bs],
+// so this CTA's own block (its tile of the vector, all tm rows) is one
+// contiguous run. push_own sends it to the same place in every sibling's Rb
+// with one shared::cta -> shared::cluster bulk copy per sibling, completing
+// on the sibling's exchange mbarrier. Every thread fences its own-block
+// stores to the async proxy first; thread 0 arms the local barrier with the
+// bytes the siblings push here.
+__device__ __forceinline__ void push_own(double* Rb, int tm, int bs, int nct, int me, unsigned long long* xbar) {
+    tile::fence_async_shared();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned bytes = static_cast<unsigned>(tm * bs * 8);
+        const unsigned bar_local = tile::su32(xbar);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_local),
+                     "r"(bytes * static_cast<unsigned>(nct - 1))
+                     : "memory");
+        const unsigned src = tile::su32(Rb + static_cast<long long>(me) * tm * bs);
+        for (int k = 0; k < nct; ++k) {
+            if (k == me) continue;
+            const unsigned dst = clu_map(src, static_cast<unsigned>(k));
+            const unsigned bar = clu_map(bar_local, static_cast<unsigned>(k));
+            asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(dst), "r"(src), "r"(bytes), "r"(bar)
+                         : "memory");
+        }
+    }
+}
+
+// acc += Rb[16 rows from am][kpad] * B[kpad][8 cols from bn] with Rb in the
+// CLU column-block layout (a k16 step never straddles a block: tn % 16 == 0).
+__device__ __forceinline__ void warp_mma_blk(const double* A, int tm, int bs, int tn, int am, const double* B, int ldb,
+                                             int bn, int kpad, double acc[4]) {
+    if (kAblate & 4) return;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    int k = 0;
+    for (; k + 16 <= kpad; k += 16) {
+        const int blk = k / tn;
+        const double* Ab = A + static_cast<long long>(blk) * tm * bs + (k - blk * tn);
+        double a[8], b[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = Ab[(am + g + 8 * (i & 1)) * bs + t + 4 * (i >> 1)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) b[i] = B[(k + t + 4 * i) * ldb + bn + g];
+        dmma16816(acc, a, b);
+    }
+    if (k < kpad) {
+        const int blk = k / tn;
+        const double* Ab = A + static_cast<long long>(blk) * tm * bs + (k - blk * tn);
+        double a[4], b[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = Ab[(am + g + 8 * (i & 1)) * bs + t + 4 * (i >> 1)];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) b[i] = B[(k + t + 4 * i) * ldb + bn + g];
+        dmma1688(acc, a, b);
+    }
+}
+
+template <int MT, int NT, bool CLU>
 __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_constant__ RDev d) {
     constexpr int WARPS = MT * NT, THREADS = WARPS * 32;
     extern __shared__ __align__(16) double sm[];
@@ -262,8 +339,12 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
     const int R = L.R, N = L.order;
     const long long RR = static_cast<long long>(R) * R;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-    const int vb = cta_rank(p.barrier);
+    // CLU: block order = task order (a cluster is the nct column tiles of one row block)
+    const int vb = CLU ? static_cast<int>(blockIdx.x) : cta_rank(p.barrier);
     const unsigned nb = gridDim.x;
+    auto gbar = [&](unsigned int& rnd) {
+        grid_barrier(p.barrier, nb, rnd);
+    };
     unsigned int round = 0;
 
     // ---- this CTA's tile
@@ -315,6 +396,16 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         copy_rows<WARPS>(Ps, ks, R, p.pinv + n * RR + c0, R, vc, 0, 0);
     }
     cp_async_wait_all();
+    __shared__ unsigned long long xbar;  // CLU: sibling blocks of the row buffer
+    unsigned xphase = 0;
+    if (CLU) {
+        if (tid == 0) {
+            tile::bar_init(&xbar);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        clu_arrive();  // every sibling's barrier exists before the first push
+        clu_wait();
+    }
     __syncthreads();
 
     // Row buffer Rb[0:vr, 0:R] = own tile (registers) | sibling columns formed
@@ -354,7 +445,8 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
     auto phase_c_tail = [&]() {
         // Z = Rb Pinv_n (rows x cols); partials of <R, Z>, ||R||^2, finiteness
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        warp_mma<false>(Rb, ld, wm, Ps, ks, wn, L.rk, acc);
+        if (CLU) warp_mma_blk(Rb, L.tm, L.bs, L.tn, wm, Ps, ks, wn, L.rk, acc);
+        else warp_mma<false>(Rb, ld, wm, Ps, ks, wn, L.rk, acc);
         double rz = 0.0, nrm = 0.0, bad = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -395,15 +487,33 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                 }
         }
     };
-    if (has) {
+    // CLU: own tile into the own columns of Rb, pushed to the siblings (DSMEM
+    // bulk copies); their blocks arrive on xbar
+    auto push_rows = [&](const double own[4]) {
+        double* blk = Rb + static_cast<long long>(ct) * L.tm * L.bs;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            if (fv[k]) p.Rr[rc][fe[k]] = Rg[k];
-        form_rows(p.G, nullptr, -1.0, Rg, nullptr, nullptr);
+            if (fv[k]) blk[fi[k] * L.bs + fc[k]] = own[k];
+        push_own(Rb, L.tm, L.bs, L.nct, ct, &xbar);
+    };
+    auto wait_rows = [&]() {
+        tile::bar_wait(&xbar, xphase);
+        xphase ^= 1u;
+    };
+    if (has) {
+        if (CLU) {
+            push_rows(Rg);
+            wait_rows();
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (fv[k]) p.Rr[rc][fe[k]] = Rg[k];
+            form_rows(p.G, nullptr, -1.0, Rg, nullptr, nullptr);
+        }
         phase_c_tail();
         z_partial();
     }
-    grid_barrier(p.barrier, nb, round);
+    gbar(round);
 
     double gnorm, unused0, unused1;
     top_sums<WARPS>(d, red, unused0, gnorm, unused1);  // ||R|| = ||G|| at init
@@ -445,8 +555,9 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 Wg[k] = first ? Zg[k] : __fma_rn(beta, Wg[k], Zg[k]);
-                if (fv[k]) p.W[0][fe[k]] = Wg[k];
+                if (!CLU && fv[k]) p.W[0][fe[k]] = Wg[k];
             }
+            if (CLU) push_rows(Wg);  // waited for in phase B
         }
         r_stamp(d, vb, it, 1);
         r_stamp(d, vb, it, 2);
@@ -502,19 +613,26 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             }
         }
         r_stamp(d, vb, it, 8);
-        grid_barrier(p.barrier, nb, round);
+        gbar(round);
         r_stamp(d, vb, it, 3);
         // ---- B: Q = [W' | A_n] [Gamma_nn ; D_n^T] + lambda Reg(W'); <W', Q> partial
         if (has) {
-            copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
+            if (CLU) {
+                copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
+                wait_rows();  // the siblings' W' blocks (pushed in phase A)
+                r_stamp(d, vb, it, 13);
+            } else {
+                copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (fv[k]) Rb[fi[k] * ld + c0 + fc[k]] = Wg[k];
-            copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
+                for (int k = 0; k < 4; ++k)
+                    if (fv[k]) Rb[fi[k] * ld + c0 + fc[k]] = Wg[k];
+                copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
+            }
             cp_async_wait_all();  // sibling W' columns and the D slice
             __syncthreads();
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
+            if (CLU) warp_mma_blk(Rb, L.tm, L.bs, L.tn, wm, Gs, ks, wn, L.rk, acc);
+            else warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
             warp_mma<false>(An, ld, wm, Ds, ks, wn, L.rk, acc);
             double part = 0.0;
 #pragma unroll
@@ -524,7 +642,7 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                     const double reg = (p.shape == 0) ? p.lambda * w
                                                       : w * (p.lambda * Gs[(c0 + fc[k]) * ks + fc[k]]);
                     Qg[k] = acc[k] + reg;
-                    p.Q[fe[k]] = Qg[k];
+                    if (!CLU) p.Q[fe[k]] = Qg[k];
                     part += w * Qg[k];
                 } else {
                     Qg[k] = 0.0;
@@ -534,7 +652,7 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             if (tid == 0) r_slot_wq(d)[vb] = tot;
         }
         r_stamp(d, vb, it, 4);
-        grid_barrier(p.barrier, nb, round);
+        gbar(round);
         r_stamp(d, vb, it, 5);
         // ---- C: alpha; V += alpha W'; R' = R - alpha Q; Z = R' Pinv
         wq = (kAblate & 8) ? 1.0 : warp0_sum_slots<WARPS>(r_slot_wq(d), L.tasks, red);
@@ -551,10 +669,15 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                 if (fv[k]) {
                     Vg[k] = __fma_rn(alpha, Wg[k], Vg[k]);
                     Rg[k] = __fma_rn(-alpha, Qg[k], Rg[k]);
-                    p.Rr[rc ^ 1][fe[k]] = Rg[k];
+                    if (!CLU) p.Rr[rc ^ 1][fe[k]] = Rg[k];
                 }
             }
-            form_rows(p.Rr[rc], p.Q, -alpha, Rg, nullptr, nullptr);
+            if (CLU) {
+                push_rows(Rg);
+                wait_rows();
+            } else {
+                form_rows(p.Rr[rc], p.Q, -alpha, Rg, nullptr, nullptr);
+            }
             r_stamp(d, vb, it, 10);
             phase_c_tail();
             r_stamp(d, vb, it, 11);
@@ -563,7 +686,7 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         }
         rc ^= 1;
         r_stamp(d, vb, it, 6);
-        grid_barrier(p.barrier, nb, round);
+        gbar(round);
         r_stamp(d, vb, it, 7);
         ++it;
         first = false;
@@ -572,6 +695,10 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
 #pragma unroll
         for (int k = 0; k < 4; ++k)
             if (fv[k]) p.V[fe[k]] = Vg[k];
+    }
+    if (CLU) {  // no CTA leaves while a sibling could still read its shared memory
+        clu_arrive();
+        clu_wait();
     }
     if (vb == 0 && tid == 0) {
         p.result[0] = it;
@@ -588,7 +715,7 @@ struct Cand {
 };
 constexpr Cand kCands[] = {{1, 1}, {1, 2}, {1, 3}, {1, 4}, {2, 1}, {2, 2}, {2, 3}, {2, 4}, {3, 1}, {3, 2}, {3, 3}, {3, 4}};
 
-bool make_rlayout(const CgParams& p, int mt, int nt, RLayout& L) {
+bool make_rlayout(const CgParams& p, int mt, int nt, RLayout& L, bool clu = false) {
     L = RLayout{};
     L.order = p.order;
     L.R = p.R;
@@ -620,23 +747,45 @@ bool make_rlayout(const CgParams& p, int mt, int nt, RLayout& L) {
     L.ks = L.tn + 4;
     const int rowbuf = L.tm * L.ld;
     const int kslice = L.rk * L.ks;
+    L.bs = L.tn + 4;
+    while (L.bs % 16 != 4) ++L.bs;
     L.o_gnn = rowbuf;
     L.o_pinv = L.o_gnn + kslice;
     L.o_row = L.o_pinv + kslice;
-    L.o_aux = L.o_row + rowbuf;
-    L.o_ds = L.o_aux + std::max(rowbuf, L.tm * L.ks);
+    if (clu) {  // Rb as nct column blocks; Ax only stages Z for z_partial (no sibling rebuild)
+        L.o_aux = L.o_row + L.nct * L.tm * L.bs;
+        L.o_ds = L.o_aux + L.tm * L.ks;
+    } else {
+        L.o_aux = L.o_row + rowbuf;
+        L.o_ds = L.o_aux + std::max(rowbuf, L.tm * L.ks);
+    }
     L.smem = L.o_ds + kslice;
     return true;
 }
 
 template <int MT, int NT>
 void launch_res(const RDev& d, int grid, std::size_t smem, cudaStream_t st) {
-    auto* fn = cg_res_kernel<MT, NT>;
+    auto* fn = cg_res_kernel<MT, NT, false>;
     ensure_dynamic_smem(fn, smem);  // grow-only per device, under the process-wide mutex
     RDev dd = d;
     void* args[] = {&dd};
     launch_cooperative(reinterpret_cast<const void*>(fn), dim3(grid), dim3(MT * NT * 32), args, smem, st);
     count_launch(1);
+}
+// Cluster mode (clusters of nct column tiles); false when the device cannot
+// hold every cluster at once (the caller then launches the plain kernel).
+template <int MT>
+bool launch_res_clu(const RDev& d, int grid, std::size_t smem, cudaStream_t st) {
+    auto* fn = cg_res_kernel<MT, 4, true>;
+    ensure_dynamic_smem(fn, smem);
+    const unsigned cx = static_cast<unsigned>(d.L.nct);
+    if (max_active_clusters(reinterpret_cast<const void*>(fn), dim3(MT * 4 * 32), cx, smem) < grid / d.L.nct)
+        return false;
+    RDev dd = d;
+    void* args[] = {&dd};
+    launch_cooperative_cluster(reinterpret_cast<const void*>(fn), dim3(grid), dim3(MT * 4 * 32), cx, args, smem, st);
+    count_launch(1);
+    return true;
 }
 
 }  // namespace
@@ -700,6 +849,23 @@ bool run_cg_resident(const CgParams& p, cudaStream_t st) {
     const int grid = bestL.tasks;
     const std::size_t smem = static_cast<std::size_t>(bestL.smem) * sizeof(double);
     if (!p.barrier_zeroed) CPK_CUDA(cudaMemsetAsync(p.barrier, 0, cg_barrier_words() * sizeof(unsigned int), st));
+    // the nct column tiles of a row block as one thread-block cluster (sibling
+    // columns through DSMEM); CPKIT_CG_NO_CLUSTER=1 keeps the L2 gathers
+    // (R even: every row block is a whole number of 16-byte units, as the bulk copies need)
+    if (kCands[best].nt == 4 && bestL.nct >= 2 && bestL.nct <= 8 && !std::getenv("CPKIT_CG_NO_CLUSTER")) {
+        RDev dc = d;
+        make_rlayout(p, kCands[best].mt, kCands[best].nt, dc.L, true);
+        const std::size_t smem_c = static_cast<std::size_t>(dc.L.smem) * sizeof(double);
+        bool done = false;
+        if (static_cast<long long>(dc.L.smem) * 8 <= budget) {
+            switch (kCands[best].mt) {
+                case 1: done = launch_res_clu<1>(dc, grid, smem_c, st); break;
+                case 2: done = launch_res_clu<2>(dc, grid, smem_c, st); break;
+                default: done = launch_res_clu<3>(dc, grid, smem_c, st); break;
+            }
+        }
+        if (done) return true;
+    }
     switch (kCands[best].mt * 10 + kCands[best].nt) {
         case 11: launch_res<1, 1>(d, grid, smem, st); break;
         case 12: launch_res<1, 2>(d, grid, smem, st); break;

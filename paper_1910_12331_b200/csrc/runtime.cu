@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -52,9 +53,14 @@ void* guard_alloc(std::size_t bytes) {
     CPK_CUDA(cudaMemset(base + kGuardBytes + bytes, kGuardByte, body - bytes + kGuardBytes));
     return base + kGuardBytes;
 }
+std::recursive_mutex& guard_capture_mutex() {
+    static std::recursive_mutex mu;
+    return mu;
+}
 void guard_free(void* user, std::size_t bytes) {
     unsigned char* u = static_cast<unsigned char*>(user);
     unsigned char* base = u - kGuardBytes;
+    std::lock_guard<std::recursive_mutex> lock(guard_capture_mutex());  // no graph capture in progress anywhere
     cudaDeviceSynchronize();  // every stream's writes landed
     const bool ok_front = guard_zone_ok(base, "front", bytes);
     const bool ok_back = guard_zone_ok(u + bytes, "back", bytes);
@@ -124,6 +130,59 @@ void launch_cooperative(const void* fn, dim3 grid, dim3 block, void** args, std:
     else CPK_CUDA(cudaStreamWaitEvent(st, tail, 0));  // no-op when the last one was on this stream
     CPK_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, st));
     CPK_CUDA(cudaEventRecord(tail, st));
+}
+void launch_cooperative_cluster(const void* fn, dim3 grid, dim3 block, unsigned cluster_x, void** args,
+                                std::size_t smem, cudaStream_t st) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_coop_mu);
+    cudaEvent_t& tail = g_coop_tail[dev];
+    if (!tail) CPK_CUDA(cudaEventCreateWithFlags(&tail, cudaEventDisableTiming));
+    else CPK_CUDA(cudaStreamWaitEvent(st, tail, 0));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster_x;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    CPK_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    CPK_CUDA(cudaEventRecord(tail, st));
+}
+int max_active_clusters(const void* fn, dim3 block, unsigned cluster_x, std::size_t smem) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, unsigned, unsigned, std::size_t>, int> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const auto key = std::make_tuple(dev, fn, block.x, cluster_x, smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cluster_x * 148);
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster_x;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    cache[key] = n;
+    return n;
 }
 void ensure_dynamic_smem(const void* fn, std::size_t bytes) {
     int dev = 0;

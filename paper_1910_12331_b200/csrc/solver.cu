@@ -1287,6 +1287,8 @@ CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gno
                              dt(it, 10, 11), dt(it, 11, 12));
             if (h[it * 16 + 8])
                 std::fprintf(stderr, " | A2 work %5.2f", dt(it, 2, 8));
+            if (h[it * 16 + 13])
+                std::fprintf(stderr, " | B pull %5.2f", dt(it, 3, 13));
             std::fprintf(stderr, " us\n");
         }
     }
@@ -1401,6 +1403,8 @@ void DeviceProblem::als_sweep_launch(double lambda, bool with_residual) {
         }
         const std::size_t prof0 = prof_.size();
         const long long k0 = static_cast<long long>(kernel_launches());
+        std::unique_lock<std::recursive_mutex> guard_lock(guard_capture_mutex(), std::defer_lock);
+        if (guard_enabled()) guard_lock.lock();  // CPKIT_GUARD: red-zone checks synchronise the device
         CPK_CUDA(cudaStreamBeginCapture(ctx_.stream, cudaStreamCaptureModeThreadLocal));
         try {
             als_sweep_body(lambda);
