@@ -260,3 +260,27 @@ def schedule_next(lam, direction, mu=2.0, lower=1e-6, upper=1e-2):  # gauss_newt
         if lam > upper:
             direction = 0
     return lam, direction
+
+
+def als_optimize(x, factors, max_sweeps=10000, residual_tol=5e-5, step_tol=1e-7, lambda0=0.0,
+                 decay_factor=2.0, decay_every=None):  # als.cpp:54-94
+    """Outer ALS loop: lambda_k = lambda0 / decay^floor((k-1)/every), a record
+    per sweep from the residual of the sweep's own last-mode MTTKRP, stop on
+    residual_tol (converged_residual) or step_tol (converged_step), else cap_hit."""
+    xnorm2 = float(np.dot(x.ravel(), x.ravel()))
+    if not xnorm2 > 0.0:
+        raise ValueError("als_optimize: tensor norm must be positive")
+    tree = Tree(x)
+    records, status = [], "cap_hit"
+    for sweep in range(1, max_sweeps + 1):
+        lam = lambda0 / decay_factor ** ((sweep - 1) // decay_every) if decay_every else lambda0
+        factors, step, _, m_last = als_sweep(tree, factors, lam)
+        r, f = residual_fitness(factors, m_last, xnorm2)
+        records.append({"iter": sweep, "residual": r, "fitness": f, "lambda": lam, "cg_iters": 0})
+        if r < residual_tol:
+            status = "converged_residual"
+            break
+        if step < step_tol:
+            status = "converged_step"
+            break
+    return factors, records, status

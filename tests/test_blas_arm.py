@@ -33,3 +33,16 @@ def test_als_and_gn_steps(orc, dims, rank):
     assert d["cg_iters"] == d_ref["cg_iters"]
     assert abs(d["residual_after"] - d_ref["residual_after"]) < 1e-10
     assert vec_rel_err(f, f_ref) < 1e-9
+
+
+def test_als_optimize_matches_oracle(orc):
+    dims, rank = [8, 7, 6], 3
+    truth = orc.random_model(dims, rank, 11)
+    x = orc.reconstruct(truth)
+    init = orc.random_model(dims, rank, 12)
+    f_ref, recs, st = orc.als_optimize(x, init, orc.AlsConfig(max_sweeps=60, lambda0=1e-3, decay_every=5))
+    f, recs2, st2 = ba.als_optimize(x, init, max_sweeps=60, lambda0=1e-3, decay_every=5)
+    assert st2 == st and len(recs2) == len(recs)
+    for a, b in zip(recs2, recs):
+        assert a["lambda"] == b["lambda"] and abs(a["residual"] - b["residual"]) < 1e-9
+    assert vec_rel_err(f, f_ref) < 1e-8
