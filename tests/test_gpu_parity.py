@@ -567,3 +567,47 @@ def test_als_graph_replay_bitwise_and_lambda_decay(orc, monkeypatch):
     for a, b in zip(ja["records"], recs):
         assert a["lambda"] == b["lambda"]
         assert abs(a["residual"] - b["residual"]) < 1e-10
+
+
+def _pair_with_offdiag(N, R, c):
+    grams = np.stack([np.eye(R)] * N)
+    pair = np.zeros((N, N, R, R))
+    for n in range(N):
+        for q in range(N):
+            pair[n, q] = np.eye(R) if n == q else c * np.ones((R, R))
+    return grams, pair
+
+
+@pytest.mark.parametrize("c", [1.0, 5.0])
+def test_cg_breakdown_matches_oracle(orc, ck, c):
+    """gauss_newton.cpp:318-324: <W, Q> <= 0 stops the solve with the current
+    iterate (breakdown). An SPD preconditioner (Gamma(n,n) = I) with strongly
+    negative off-diagonal Gamma blocks makes J^T J indefinite."""
+    dims, R = [5, 4, 6], 3
+    f = orc.random_model(dims, R, 3)
+    g = orc.random_model(dims, R, 4, kind="gaussian")
+    grams, pair = _pair_with_offdiag(3, R, -c)
+    v_ref, it_ref, cap_ref, bd_ref = orc.cp_cg(f, grams, pair, g, 0.0, orc.GnConfig(cg_max_iters=50))
+    assert bd_ref
+    p = make(ck, np.zeros(dims), f)
+    p.set_gamma_set(grams, pair)
+    v, it, cap, bd = p.cp_cg(g, 0.0, {"cg_max_iters": 50})
+    assert (it, cap, bd) == (it_ref, cap_ref, bd_ref)
+    assert vec_rel_err(v, v_ref) < 1e-12
+
+
+@pytest.mark.parametrize("c", [1e307, 1.7e308])
+def test_cg_nonfinite_iterate_is_numerical_failure(orc, ck, c):
+    """gauss_newton.cpp:341-343: a non-finite V or R after an iteration throws
+    NumericalFailure, which the C ABI maps to CPKIT_ERR_NUMERICAL (5)."""
+    dims, R = [5, 4, 6], 3
+    f = orc.random_model(dims, R, 3)
+    g = [np.abs(x) for x in orc.random_model(dims, R, 4, kind="gaussian")]
+    grams, pair = _pair_with_offdiag(3, R, c)
+    with pytest.raises(Exception, match="non-finite"):
+        orc.cp_cg(f, grams, pair, g, 0.0, orc.GnConfig(cg_max_iters=50))
+    p = make(ck, np.zeros(dims), f)
+    p.set_gamma_set(grams, pair)
+    with pytest.raises(ck.CpkitError) as ei:
+        p.cp_cg(g, 0.0, {"cg_max_iters": 50})
+    assert ei.value.code == 5 and "non-finite" in str(ei.value)
