@@ -185,15 +185,15 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
     return __fma_rn(y * e, __fma_rn(0.375, e, 0.5), y);
 }
 
-template <int kNB>
-__device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int kb) {
+template <int kNB, class Idx>
+__device__ __noinline__ bool diag_factor(double* w, const Idx ix, int k0, int kb) {
     static_assert(kNB % 2 == 0 && kNB <= 32, "diagonal block: even width, one warp");
     __shared__ __align__(16) double colb[32];  // column j of L, broadcast to the warp
     __syncwarp();
     const int i = threadIdx.x & 31;
     double r[kNB];
 #pragma unroll
-    for (int m = 0; m < kNB; ++m) r[m] = (i < kb && m <= i) ? w[(k0 + i) * LD + k0 + m] : 0.0;
+    for (int m = 0; m < kNB; ++m) r[m] = (i < kb && m <= i) ? w[ix.at(k0 + i, k0 + m)] : 0.0;
     bool failed = false;
     // The pivot of the next column is computed by its own lane from its own row
     // (the same fma as the row update, so bitwise the same value) and shuffled
@@ -210,7 +210,7 @@ __device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int k
         const double inv = rsqrt_pos(x > 0.0 ? x : 1.0), l = x * inv;  // L_jj = x / sqrt(x)
         const double lij = i > j ? r[j] * inv : (i == j ? l : r[j]);
         if (j + 1 < kNB) x = __shfl_sync(0xffffffffu, __fma_rn(-lij, lij, r[j + 1]), j + 1);
-        if (i == j && j < kb && !failed) w[(k0 + j) * LD + R] = inv;
+        if (i == j && j < kb && !failed) w[ix.inv(k0 + j)] = inv;
         r[j] = lij;
         if (j + 1 < kNB) {
             colb[i] = lij;
@@ -227,7 +227,7 @@ __device__ __noinline__ bool diag_factor(double* w, int LD, int R, int k0, int k
     if (CPKIT_CHOL_TRACE && k0 == 0 && blockIdx.x == 0 && i == 0) g_chol_trace[24 + kNB] = clock64();
 #pragma unroll
     for (int m = 0; m < kNB; ++m)
-        if (i < kb && m <= i) w[(k0 + i) * LD + k0 + m] = r[m];
+        if (i < kb && m <= i) w[ix.at(k0 + i, k0 + m)] = r[m];
     return failed;
 }
 
@@ -249,12 +249,17 @@ __device__ __forceinline__ double chol_src_at(const CholSrc& src, const double* 
     return g;
 }
 
-template <int kNB>
+// Idx = SqIdx: the square R x (R+1) layout in shared memory (R <= ~165), the
+// factor leaves in one bulk copy; Idx = PkIdx: the packed lower triangle (R up
+// to ~233), rows contiguous, so the panel and DMMA trailing update address it
+// the same way; the factor leaves row by row into the square global layout.
+template <int kNB, class Idx>
 __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, int R, double lambda,
                                                            int mode, double* __restrict__ l_all,
                                                            int* __restrict__ status) {
-    extern __shared__ double w[];
+    extern __shared__ __align__(16) double w[];
     const int LD = R + 1;
+    const Idx ix{LD, R};
     const int mat = blockIdx.x;
     const long long rr = static_cast<long long>(R) * R;
     const double* s = src.s + static_cast<long long>(mat) * src.s_stride;
@@ -293,10 +298,10 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
             const double* s0 = src.grams ? (first >= 0 ? src.grams + first * rr : nullptr) : s;
             if (s0) {
                 for (int i = warp; i < R; i += nw)
-                    for (int k = lane; k <= i; k += 32) tile::cp_async8(w + i * LD + k, s0 + i * R + k);
+                    for (int k = lane; k <= i; k += 32) tile::cp_async8(w + ix.at(i, k), s0 + i * R + k);
             } else {  // order 1 (no other mode): Gamma = Ones
                 for (int i = warp; i < R; i += nw)
-                    for (int k = lane; k <= i; k += 32) w[i * LD + k] = 1.0;
+                    for (int k = lane; k <= i; k += 32) w[ix.at(i, k)] = 1.0;
             }
             tile::cp_async_wait_all();
             __syncthreads();
@@ -322,19 +327,19 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
                             if (i >= R) break;
 #pragma unroll
                             for (int c = 0; c < 4; ++c)
-                                if (lane + 32 * c <= i) w[i * LD + lane + 32 * c] *= f[q][c];
-                            for (int k = lane + 128; k <= i; k += 32) w[i * LD + k] *= __ldg(sm + i * R + k);
+                                if (lane + 32 * c <= i) w[ix.at(i, lane + 32 * c)] *= f[q][c];
+                            for (int k = lane + 128; k <= i; k += 32) w[ix.at(i, k)] *= __ldg(sm + i * R + k);
                         }
                     }
                 }
                 __syncthreads();
             }
             for (int i = tid; i < R; i += blockDim.x) {  // the diagonal: shape, lambda, jitter
-                double x = w[i * LD + i];
+                double x = w[ix.at(i, i)];
                 if (mode == 1) x *= (1.0 + lambda);
                 x += add;
                 if (attempt == 1) x += jitter;
-                w[i * LD + i] = x;
+                w[ix.at(i, i)] = x;
             }
         }
         if (tid == 0) fail_sh = 0;
@@ -344,21 +349,21 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
             const int kb = min(kNB, R - k0);
             // 1. diagonal block (warp 0): lane i holds row i in registers; per column
             //    the pivot and every L_mj travel by shuffle (no shared-memory round trips)
-            if (!(kCholAblate & 1) && warp == 0 && diag_factor<kNB>(w, LD, R, k0, kb)) fail_sh = 1;
+            if (!(kCholAblate & 1) && warp == 0 && diag_factor<kNB>(w, ix, k0, kb)) fail_sh = 1;
             __syncthreads();
             chol_stamp(2 + 3 * (k0 / kNB));
             if (fail_sh) break;
             // 2. panel: L[i][k0+j] = (A[i][k0+j] - sum_{m<j} L[i][k0+m] L[k0+j][k0+m]) / L_jj,
             //    one thread per row, the row in registers, two partial sums per dot
             for (int i = k0 + kb + tid; i < R && !(kCholAblate & 2); i += blockDim.x) {
-                double* row = w + i * LD + k0;
+                double* row = w + ix.at(i, k0);
                 double x[kNB];
 #pragma unroll
                 for (int m = 0; m < kNB; ++m) x[m] = (m < kb) ? row[m] : 0.0;
 #pragma unroll
                 for (int j = 0; j < kNB; ++j) {
                     if (j < kb) {
-                        const double* lj = w + (k0 + j) * LD + k0;
+                        const double* lj = w + ix.at(k0 + j, k0);
                         double s0 = 0.0, s1 = 0.0;
 #pragma unroll
                         for (int m = 0; m + 1 < j; m += 2) {
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
                             s1 += x[m + 1] * lj[m + 1];
                         }
                         if (j & 1) s0 += x[j - 1] * lj[j - 1];
-                        x[j] = (x[j] - (s0 + s1)) * w[(k0 + j) * LD + R];
+                        x[j] = (x[j] - (s0 + s1)) * w[ix.inv(k0 + j)];
                     }
                 }
 #pragma unroll
@@ -392,12 +397,12 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const int row = r0 + g + 8 * (q & 1), col = t + 4 * (q >> 1);
-                            a[q] = row < R ? w[row * LD + k0 + col] : 0.0;
+                            a[q] = row < R ? w[ix.at(row, k0 + col)] : 0.0;
                         }
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const int nn = c0 + g, kk = t + 4 * q;
-                            b[q] = nn < R ? w[nn * LD + k0 + kk] : 0.0;
+                            b[q] = nn < R ? w[ix.at(nn, k0 + kk)] : 0.0;
                         }
                         asm volatile(
                             "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3},"
@@ -410,17 +415,17 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
 #pragma unroll
                             for (int c = 0; c < 2; ++c) {
                                 const int row = r0 + g + 8 * h, col = c0 + 2 * t + c;
-                                if (row < R && col <= row) w[row * LD + col] -= acc[2 * h + c];
+                                if (row < R && col <= row) w[ix.at(row, col)] -= acc[2 * h + c];
                             }
                     }
                 } else {
                     for (int i = t0 + warp; i < R; i += nw) {
-                        const double* li = w + i * LD + k0;
+                        const double* li = w + ix.at(i, k0);
                         for (int m = t0 + lane; m <= i; m += 32) {
-                            const double* lm = w + m * LD + k0;
-                            double acc = w[i * LD + m];
+                            const double* lm = w + ix.at(m, k0);
+                            double acc = w[ix.at(i, m)];
                             for (int j = 0; j < kb; ++j) acc -= li[j] * lm[j];
-                            w[i * LD + m] = acc;
+                            w[ix.at(i, m)] = acc;
                         }
                     }
                 }
@@ -434,8 +439,18 @@ __global__ void __launch_bounds__(256) chol_blocked_kernel(const CholSrc src, in
         }
         __syncthreads();
     }
-    // the factor (same R x (R+1) layout as in shared memory) in one bulk copy
     __syncthreads();
+    if (!std::is_same<Idx, SqIdx>::value) {
+        // packed: row i's lower triangle and 1 / L_ii into the square layout
+        for (int i = warp; i < R; i += nw) {
+            for (int k = lane; k <= i; k += 32) out[i * LD + k] = w[ix.at(i, k)];
+            if (lane == 0) out[i * LD + R] = w[ix.inv(i)];
+        }
+        if (tid == 0) status[mat] = st;
+        chol_stamp(63);
+        return;
+    }
+    // the factor (same R x (R+1) layout as in shared memory) in one bulk copy
     if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out),
@@ -677,15 +692,19 @@ void launch_chol_batch_src(double* s, const double* grams, int order, int excl, 
     if (R > 512) throw LimitExceeded("rank exceeds the device SPD solver limit (512)");
     if (s_stride <= 0) s_stride = static_cast<long long>(R) * R;
     const Layout lay = layout_of(R);
-    const bool blocked = lay == kSquareSmem && !std::getenv("CPKIT_CHOL_UNBLOCKED");
+    const bool blocked = (lay == kSquareSmem || lay == kPackedSmem) && !std::getenv("CPKIT_CHOL_UNBLOCKED");
     if (grams && !blocked) {
         launch_gamma_excl(grams, order, R, excl, s, st);
         grams = nullptr;
     }
-    if (blocked) {
-        auto fn = chol_blocked_kernel<16>;
+    if (blocked && lay == kSquareSmem) {
+        auto fn = chol_blocked_kernel<16, SqIdx>;
         ensure_dynamic_smem(fn, sq_bytes(R));
         fn<<<count, 256, sq_bytes(R), st>>>(CholSrc{s, grams, order, excl, s_stride}, R, *lambda, mode, l_out, status);
+    } else if (blocked) {
+        auto fn = chol_blocked_kernel<16, PkIdx>;
+        ensure_dynamic_smem(fn, pk_bytes(R));
+        fn<<<count, 256, pk_bytes(R), st>>>(CholSrc{s, grams, order, excl, s_stride}, R, *lambda, mode, l_out, status);
     } else if (lay == kSquareSmem) {
         auto fn = chol_kernel<SqIdx, true>;
         ensure_dynamic_smem(fn, sq_bytes(R));

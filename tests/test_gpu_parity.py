@@ -235,7 +235,9 @@ def test_jtj_vs_explicit_and_identity(orc, ck):
 
 # ---------------------------------------------------------------- SPD / preconditioner
 def test_spd_solve_and_inverse(orc, ck):
-    for R in (2, 5, 33, 100, 200):
+    # 166 .. 233: the blocked factorisation on the packed lower triangle (the
+    # square R x (R+1) layout no longer fits shared memory), incl. a ragged tail block
+    for R in (2, 5, 33, 100, 165, 166, 180, 200, 233):
         a = gauss_factors(orc, [R + 7], R, R)[0]
         s = orc.gram(a)
         b = gauss_factors(orc, [37], R, R + 1)[0]
@@ -249,6 +251,13 @@ def test_spd_solve_and_inverse(orc, ck):
     with pytest.raises(ck.CpkitError) as e:
         p.spd_solve(np.zeros((2, 2)), np.eye(2), 0.0)
     assert e.value.status == "singular_system"
+    for R in (100, 200):  # jitter retry and SingularSystem on the square and the packed blocked kernels
+        p = ck.DeviceProblem([3, 3], R)
+        y = p.spd_solve(np.ones((R, R)), np.ones((3, R)), 0.0)
+        assert np.isfinite(y).all()
+        with pytest.raises(ck.CpkitError) as e:
+            p.spd_solve(np.zeros((R, R)), np.eye(R)[:4], 0.0)
+        assert e.value.status == "singular_system"
 
 
 @pytest.mark.parametrize("shape", [0, 1])
