@@ -6,12 +6,14 @@ import torch
 from torch.profiler import profile, ProfilerActivity
 from paper_1910_12331_b200 import cpkit
 
-dims, R = [400, 400, 400], 100
 mode = sys.argv[1] if len(sys.argv) > 1 else "als"
+dims, R, noise = [400, 400, 400], 100, 1e-6
+if len(sys.argv) > 2 and sys.argv[2] == "c5s":
+    dims, R, noise = [200, 200, 200, 200], 200, 1e-4
 truth = cpkit.random_factors(dims, R, cpkit.problem_seed(0, R, 0))
 init = cpkit.random_factors(dims, R, cpkit.init_seed(0, R, 0, 0))
 p = cpkit.DeviceProblem(dims, R)
-p.generate(truth, 1, 1e-6)
+p.generate(truth, 1, noise)
 p.set_factors(init)
 torch.cuda.init()
 for _ in range(6):
@@ -25,9 +27,9 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
     if mode == "gn":
         p.time_gn_steps({}, 2)
     else:
-        p.time_als_sweeps(float(os.environ.get("LAM", "0")), 4)  # the bench's pipelined loop
+        p.time_als_sweeps(float(os.environ.get("LAM", "0")), 4 if R < 200 else 2)  # the bench's pipelined loop
     torch.cuda.synchronize()
-out = os.path.join(os.environ.get("OUT", "gpurun_out"), f"timeline_{mode}.json")
+out = os.path.join(os.environ.get("OUT", "gpurun_out"), f"timeline_{mode}{'_c5s' if R == 200 else ''}.json")
 prof.export_chrome_trace(out)
 ev = [e for e in json.load(open(out))["traceEvents"] if e.get("cat") == "kernel"]
 ev.sort(key=lambda e: e["ts"])
