@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -986,13 +987,29 @@ cpkit_status cpkit_decompose(const cpkit_tensor* t, const char* config_json, con
         cfg["optimizer"] = optimizer;
         report->config = cfg;
 
-        cpkit::Context ctx(current_device());
-        cpkit::DeviceProblem p(ctx, t->t.dims(), static_cast<int>(start.rank));
-        p.upload_tensor(t->t.data());
-        cpkit::KruskalModel result;
-        run_optimizer(p, optimizer, spec, std::move(start), result, *report);
-        if (out_model) *out_model = new cpkit_model{std::move(result)};
-        if (out_report) *out_report = report.release();
+        static const bool phase_trace = std::getenv("CPKIT_PHASE_TRACE") != nullptr;  // timing experiments
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t0 = now();
+        auto t1 = t0, t2 = t0, t3 = t0;
+        {
+            cpkit::Context ctx(current_device());
+            cpkit::DeviceProblem p(ctx, t->t.dims(), static_cast<int>(start.rank));
+            p.upload_tensor(t->t.data());
+            if (phase_trace) {
+                ctx.sync();
+                t1 = now();
+            }
+            cpkit::KruskalModel result;
+            run_optimizer(p, optimizer, spec, std::move(start), result, *report);
+            t2 = now();
+            if (out_model) *out_model = new cpkit_model{std::move(result)};
+            if (out_report) *out_report = report.release();
+        }
+        t3 = now();
+        if (phase_trace)
+            std::fprintf(stderr, "cpkit_decompose: setup+upload %.1f ms, optimize %.1f ms, teardown %.1f ms\n",
+                         ms(t0, t1), ms(t1, t2), ms(t2, t3));
     });
 }
 

@@ -53,6 +53,29 @@ bool guard_enabled();
 void* guard_alloc(std::size_t bytes);                 // returns the user pointer
 void guard_free(void* user, std::size_t bytes);       // checks both red zones, frees
 std::uint64_t guard_violations();
+// Plain device allocations of DevBuf (runtime.cu). cudaMalloc / cudaFree each
+// cost milliseconds on the B200 boxes (a device problem holds ~50 buffers),
+// so buffers released inside an OwnerSyncedRelease scope - their owner has
+// synchronised every stream that used them - go to a per-device cache keyed
+// by size and are handed out again without a driver call; every other release
+// is a cudaFree (which orders itself after in-flight work). An allocation that
+// fails empties the device's cache and retries. CPKIT_NO_ALLOC_CACHE=1 turns
+// the cache off; CPKIT_ALLOC_TRACE=1 reports driver calls slower than 2 ms.
+void* dev_alloc(std::size_t bytes);
+void dev_free(void* p, std::size_t bytes);
+void dev_cache_empty();  // every device: cached blocks back to the driver
+// Small pinned host blocks (diagnostic slots, mapped flags) from a process-wide
+// free list: cudaFreeHost was measured taking up to 0.7 s on the B200 hosts
+// (page unpinning), so the blocks are allocated once (portable, and mapped
+// when asked) and recycled, never returned to the driver.
+void* pinned_small_alloc(std::size_t bytes, bool mapped);
+void pinned_small_free(void* p, std::size_t bytes, bool mapped);
+struct OwnerSyncedRelease {  // thread-local scope flag read by dev_free
+    OwnerSyncedRelease();
+    ~OwnerSyncedRelease();
+    OwnerSyncedRelease(const OwnerSyncedRelease&) = delete;
+    OwnerSyncedRelease& operator=(const OwnerSyncedRelease&) = delete;
+};
 bool guard_selftest();  // positive control (CPKIT_GUARD=1 only)
 // The red-zone check synchronises the device, which would invalidate another
 // thread's CUDA-graph capture: in guard mode captures and checks take this lock.
@@ -85,7 +108,7 @@ public:
         if (n) {
             guarded_ = guard_enabled();
             if (guarded_) p_ = static_cast<T*>(guard_alloc(n * sizeof(T)));
-            else CPK_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+            else p_ = static_cast<T*>(dev_alloc(n * sizeof(T)));
         }
         n_ = n;
     }
@@ -93,7 +116,7 @@ public:
     void release() {
         if (p_) {
             if (guarded_) guard_free(p_, n_ * sizeof(T));
-            else cudaFree(p_);
+            else dev_free(p_, n_ * sizeof(T));
         }
         p_ = nullptr;
         n_ = 0;

@@ -69,6 +69,106 @@ void guard_free(void* user, std::size_t bytes) {
 }
 std::uint64_t guard_violations() { return g_guard_violations.load(); }
 namespace {
+bool alloc_trace() {
+    static const bool on = std::getenv("CPKIT_ALLOC_TRACE") != nullptr;
+    return on;
+}
+bool alloc_cache_on() {
+    static const bool on = std::getenv("CPKIT_NO_ALLOC_CACHE") == nullptr;
+    return on;
+}
+thread_local int t_owner_synced = 0;
+std::mutex g_cache_mu;
+std::map<int, std::multimap<std::size_t, void*>> g_cache;  // device -> (bytes, block)
+void traced(const char* what, std::size_t bytes, std::chrono::steady_clock::time_point t0) {
+    if (!alloc_trace()) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 2.0) std::fprintf(stderr, "cpkit %s %zu bytes: %.1f ms\n", what, bytes, ms);
+}
+void cache_empty_device(int dev) {  // caller holds g_cache_mu
+    auto it = g_cache.find(dev);
+    if (it == g_cache.end()) return;
+    for (auto& kv : it->second) cudaFree(kv.second);
+    it->second.clear();
+}
+}  // namespace
+OwnerSyncedRelease::OwnerSyncedRelease() { ++t_owner_synced; }
+OwnerSyncedRelease::~OwnerSyncedRelease() { --t_owner_synced; }
+void* dev_alloc(std::size_t bytes) {
+    int dev = 0;
+    CPK_CUDA(cudaGetDevice(&dev));
+    if (alloc_cache_on()) {
+        std::lock_guard<std::mutex> lock(g_cache_mu);
+        auto& c = g_cache[dev];
+        auto it = c.find(bytes);
+        if (it != c.end()) {
+            void* p = it->second;
+            c.erase(it);
+            return p;
+        }
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();  // not sticky: give the cached blocks back and retry once
+        {
+            std::lock_guard<std::mutex> lock(g_cache_mu);
+            cache_empty_device(dev);
+        }
+        e = cudaMalloc(&p, bytes);
+    }
+    CPK_CUDA(e);
+    traced("alloc", bytes, t0);
+    return p;
+}
+void dev_free(void* p, std::size_t bytes) {
+    if (t_owner_synced > 0 && alloc_cache_on()) {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) {
+            std::lock_guard<std::mutex> lock(g_cache_mu);
+            g_cache[dev].emplace(bytes, p);
+            return;
+        }
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaFree(p);
+    traced("free", bytes, t0);
+}
+namespace {
+std::mutex g_pin_mu;
+std::multimap<std::pair<std::size_t, bool>, void*> g_pin_free;
+}  // namespace
+void* pinned_small_alloc(std::size_t bytes, bool mapped) {
+    {
+        std::lock_guard<std::mutex> lock(g_pin_mu);
+        auto it = g_pin_free.find({bytes, mapped});
+        if (it != g_pin_free.end()) {
+            void* p = it->second;
+            g_pin_free.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CPK_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable | (mapped ? cudaHostAllocMapped : 0u)));
+    return p;
+}
+void pinned_small_free(void* p, std::size_t bytes, bool mapped) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lock(g_pin_mu);
+    g_pin_free.emplace(std::make_pair(bytes, mapped), p);
+}
+void dev_cache_empty() {
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto& kv : g_cache) {
+        cudaSetDevice(kv.first);
+        cache_empty_device(kv.first);
+    }
+    cudaSetDevice(cur);
+}
+namespace {
 __global__ void guard_poke_kernel(double* p, long long i) { p[i] = 1.0; }
 }  // namespace
 // Positive control: write one element past the end of a guarded buffer and

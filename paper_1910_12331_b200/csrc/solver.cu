@@ -436,9 +436,10 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N < 2) throw InvalidArgument("mttkrp: tensor order must be at least 2");
     if (N > kMaxOrder) throw LimitExceeded("tensor order exceeds 16");
     if (R_ < 1) throw InvalidArgument("model needs order >= 1 and rank >= 1");
-    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hpin_), 16 * sizeof(double), cudaHostAllocDefault));
-    CPK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hmap_), (kGnMapOff + 2 * kGnMapDoubles) * sizeof(double),
-                           cudaHostAllocMapped));
+    hpin_ = static_cast<double*>(pinned_small_alloc(kPinBytes, false));
+    hmap_ = static_cast<double*>(pinned_small_alloc(kMapBytes, true));
+    std::memset(hpin_, 0, kPinBytes);  // recycled blocks: no stale diagnostics
+    std::memset(hmap_, 0, kMapBytes);
     for (auto& e : gn_ev_) CPK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CPK_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dmap_), hmap_, 0));
     als_graphs_.reserve(kAlsGraphs);  // in-flight sweeps hold pointers to their graphs
@@ -566,17 +567,33 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
 }
 
 DeviceProblem::~DeviceProblem() {
-    if (!pending_.empty()) cudaStreamSynchronize(ctx_.stream);
+    // every stream idle (no throw from a destructor): the buffers can be reused
+    const bool idle = cudaStreamSynchronize(ctx_.aux2) == cudaSuccess &&
+                      cudaStreamSynchronize(ctx_.aux) == cudaSuccess &&
+                      cudaStreamSynchronize(ctx_.stream) == cudaSuccess;
+    if (idle) release_scope_.emplace();
+    static const bool trace = std::getenv("CPKIT_PHASE_TRACE") != nullptr;  // timing experiments
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!trace) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        const double ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        if (ms > 1.0) std::fprintf(stderr, "  ~DeviceProblem %s %.1f ms\n", what, ms);
+        t0 = t1;
+    };
     pending_.clear();
     done_.clear();
     drop_als_graph();
+    lap("graphs");
     profile_enable(false);
-    if (hpin_) cudaFreeHost(hpin_);
-    if (hmap_) cudaFreeHost(hmap_);
+    pinned_small_free(hpin_, kPinBytes, false);
+    pinned_small_free(hmap_, kMapBytes, true);
+    lap("pinned");
     for (auto& e : slot_ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : gn_ev_)
         if (e) cudaEventDestroy(e);
+    lap("events");
 }
 
 KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) const {

@@ -378,6 +378,8 @@ private:
     int next_slot_ = 0;
     double* hmap_ = nullptr;  // mapped pinned slots (kSweepSlots x kSlotDoubles), then the GN step's area
     static constexpr int kGnMapOff = kSweepSlots * kSlotDoubles, kGnMapDoubles = 16 + 2 * kMaxOrder;
+    static constexpr std::size_t kPinBytes = 16 * sizeof(double);
+    static constexpr std::size_t kMapBytes = (kGnMapOff + 2 * kGnMapDoubles) * sizeof(double);
     double* dmap_ = nullptr;  // their device alias
     cudaEvent_t slot_ev_[kSweepSlots] = {};
     SweepSig sweep_sig() const { return {pf_valid_, pb_valid_, m_all_valid_, profile_, grams_valid_, pm_mode_}; }
@@ -394,6 +396,9 @@ private:
     std::uint64_t slab_lo_ = 0, slab_hi_ = 0, local_elems_ = 0;
     std::int64_t F_ = 0, Bl_ = 0, Bs_ = 0;           // local matrix view F x B_local, row stride Bs
     std::vector<std::int64_t> off_;                  // stacked offsets (elements)
+    // armed by the destructor once every stream is idle: the DevBuf members
+    // below (destroyed before it) then go back to the allocation cache
+    std::optional<OwnerSyncedRelease> release_scope_;
     DevBuf<double> x_;
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
     DevBuf<double> PF_, PB_, ws_, krp_;
