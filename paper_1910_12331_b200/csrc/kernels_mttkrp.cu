@@ -728,6 +728,7 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
     env("NW", p.nw);
     env("NT8", p.nt8);
     if (p.wm != wm0 || p.nw != nw0 || p.nt8 != nt0) {
+        p.ntiles = (R + 8 * p.nt8 - 1) / (8 * p.nt8);  // narrower rank tiles: several CTA columns
         p.maxc = round_maxc((p.wm * p.nt8 + p.nw - 1) / p.nw);
         if (p.maxc < 0 || !runs_fit(p.wm, p.nt8, p.nw) || 32 * (p.nw + 1) > root_max_threads(p.maxc))
             throw DeviceError("CPKIT tile override: bad warp count");
