@@ -1,12 +1,13 @@
-"""Small workload for compute-sanitizer (tools/sanitize.sh): every device kernel
+"""Small workload for the guarded allocation mode (CPKIT_GUARD=1,
+tests/test_gpu_guard.py; compute-sanitizer itself is closed on the GPU pool):
+every device kernel
 family of the product on shapes that take the same code paths as the BASELINE
 configs (TMA + mbarrier root GEMM with its tail launch, split-K TN root,
 cluster Gram, blocked Cholesky, cooperative tile-resident and streaming CG with
 the software grid barrier, pipelined GN/ALS drivers with CUDA graphs, batched
-tiny instances), sized so memcheck/racecheck finish in minutes.
+tiny instances), sized to finish in seconds.
 
-Checks results loosely against numpy so a sanitizer-perturbed run that still
-"passes" also computed the right thing. Not a test: tests/ holds the parity
+Checks the MTTKRPs against numpy so a run whose buffers were corrupted fails. Not a test: tests/ holds the parity
 suite."""
 import os
 import sys
