@@ -177,3 +177,53 @@ def test_sharded_optimize_trace(orc, ck, optimizer):
         for a, b in zip(rr, recs):
             assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"]
             assert abs(a["residual"] - b["residual"]) < 1e-8
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_c5s_matches_unsharded(ck, world):
+    """bench.py's multi-GPU configuration itself: the C5s tensor (order 4, s=200,
+    R=200, noise 1e-4) generated per shard and sharded on mode 4 over `world`
+    shards (the tile plans of the short local slabs, split-K front roots, the
+    collectives), against the unsharded device run: every mode's MTTKRP at
+    1e-11, one ALS sweep and one GN step at the trajectory tolerances."""
+    dims, R = [200, 200, 200, 200], 200
+    truth = ck.random_factors(dims, R, ck.problem_seed(0, R, 0))
+    init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
+    ref = ck.DeviceProblem(dims, R)
+    ref.generate(truth, noise_seed=1, noise_rel=1e-4)
+    ref.set_factors(init)
+    m_ref = [ref.mttkrp(n) for n in range(4)]
+    xn2 = ref.norm2()
+    step_ref, _ = ref.als_sweep(0.0)
+    f_als = ref.get_factors()
+    ref.set_factors(init)
+    d_ref = ref.gn_step({}, xn2)
+    f_gn = ref.get_factors()
+    ref.close()
+    probs = ck.DeviceProblem.loopback(dims, R, world)
+
+    def run(r, p):
+        p.generate(truth, noise_seed=1, noise_rel=1e-4)
+        p.set_factors(init)
+        m = [p.mttkrp(n) for n in range(4)]
+        n2 = p.norm2()
+        step, _ = p.als_sweep(0.0)
+        fa = p.get_factors()
+        p.set_factors(init)
+        d = p.gn_step({}, n2)
+        return m, n2, step, fa, d, p.get_factors()
+
+    got = on_ranks(probs, run)
+    for p in probs:
+        p.close()
+    for r in range(world):
+        m, n2, step, fa, d, fg = got[r]
+        for n in range(4):
+            assert rel_err(m[n], m_ref[n]) < 1e-11, (r, n)
+        assert abs(n2 - xn2) <= 1e-13 * xn2
+        assert abs(step - step_ref) <= 1e-10 * step_ref
+        assert vec_rel_err(fa, f_als) < 1e-10
+        assert int(d["cg_iters"]) == int(d_ref["cg_iters"])
+        assert abs(d["residual_after"] - d_ref["residual_after"]) < 1e-10
+        assert vec_rel_err(fg, f_gn) < 1e-9
