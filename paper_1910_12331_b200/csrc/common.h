@@ -240,6 +240,11 @@ void launch_axpby(double* out, const double* a, double alpha, const double* x, s
 void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st);
 void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_t st);
 void launch_pack_values(const double* d, int nd, const int* iv, int ni, double* out_mapped, cudaStream_t st);
+// GN update A += V with the step norm (sum of per-mode norms), the finiteness
+// flag and the packed CG result / step diagnostics, in one launch.
+void launch_gn_apply(double* a, const double* v, const std::int64_t* offsets, int nblocks, double* partials,
+                     int* bad_part, unsigned int* counter, const int* cgres, int ncg, double* out_cg,
+                     double* step_out, double* step_slot_zero, int* flag, double* out_step, cudaStream_t st);
 void launch_pack_sweep(const double* scal, int kstep, int kres, const int* flag, const int* status, int n,
                        double* out_mapped, cudaStream_t st);
 // Dense evaluation of a Kruskal model + keyed-RNG noise (generators / reconstruct)

@@ -728,6 +728,71 @@ void launch_set_flag_scalar(int* flag, int fv, double* d, double dv, cudaStream_
     ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());
 }
+namespace {
+// The GN update in one launch (gauss_newton.cpp:428-441 and the step norm,
+// :435): A += V, per-(mode, chunk) partial sums of ||V||^2 (the same chunks
+// and block sums as block_sq_partial_kernel, so the step norm is bitwise
+// launch_block_norm_sum's), finiteness of the new A; the last block to finish
+// sums the partials in fixed order, stores the step norm and the flag, and
+// packs the CG result and both values into the mapped diagnostics.
+__global__ void gn_apply_kernel(double* __restrict__ a, const double* __restrict__ v,
+                                const long long* __restrict__ off, int nblocks, int chunks,
+                                double* __restrict__ partials, int* __restrict__ bad_part,
+                                unsigned int* __restrict__ counter, const int* __restrict__ cgres, int ncg,
+                                double* out_cg, double* step_out, double* step_slot_zero, int* flag,
+                                double* out_step) {
+    const int b = blockIdx.x / chunks, c = blockIdx.x % chunks;
+    const long long lo = off[b], hi = off[b + 1];
+    double acc = 0.0;
+    bool bad = false;
+    for (long long i = lo + c * static_cast<long long>(blockDim.x) + threadIdx.x; i < hi;
+         i += static_cast<long long>(chunks) * blockDim.x) {
+        const double x = v[i];
+        const double y = a[i] + 1.0 * x;
+        a[i] = y;
+        acc += x * x;
+        bad |= !isfinite(y);
+    }
+    const double sum = block_sum(acc);
+    const int anybad = __syncthreads_or(bad);
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = sum;
+        bad_part[blockIdx.x] = anybad;
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    double total = 0.0;
+    int fin = 1;
+    for (int q = 0; q < nblocks; ++q) {
+        double sq = 0.0;
+        for (int k = 0; k < chunks; ++k) sq += __ldcg(partials + q * chunks + k);
+        total += 1.0 * sqrt(sq);
+    }
+    for (int q = 0; q < nblocks * chunks; ++q)
+        if (__ldcg(bad_part + q)) fin = 0;
+    *step_out = total;
+    *step_slot_zero = 0.0;
+    *flag = fin;
+    for (int i = 0; i < ncg; ++i) out_cg[i] = static_cast<double>(cgres[i]);
+    out_step[0] = total;
+    out_step[1] = static_cast<double>(fin);
+    *counter = 0u;  // ready for the next launch (stream order)
+}
+}  // namespace
+void launch_gn_apply(double* a, const double* v, const std::int64_t* offsets, int nblocks, double* partials,
+                     int* bad_part, unsigned int* counter, const int* cgres, int ncg, double* out_cg,
+                     double* step_out, double* step_slot_zero, int* flag, double* out_step, cudaStream_t st) {
+    const int chunks = 16;
+    gn_apply_kernel<<<nblocks * chunks, kRedThreads, 0, st>>>(a, v, reinterpret_cast<const long long*>(offsets),
+                                                             nblocks, chunks, partials, bad_part, counter, cgres,
+                                                             ncg, out_cg, step_out, step_slot_zero, flag, out_step);
+    ::cpkit::count_launch(1);
+    CPK_CUDA(cudaGetLastError());
+}
 void launch_all_finite(const double* x, std::uint64_t n, int* flag, cudaStream_t st) {
     all_finite_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(x, n, flag); ::cpkit::count_launch(1);
     CPK_CUDA(cudaGetLastError());

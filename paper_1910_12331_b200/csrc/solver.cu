@@ -549,6 +549,9 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     partials_.resize(std::max<std::size_t>(std::max(4096, 2 * norm2_parts(static_cast<std::uint64_t>(F_) * Bs_) + 8),
                                            static_cast<std::size_t>(smax)));  // >= one slot per factor row
     status_.resize(std::max(N, 1));
+    apply_bad_.resize(static_cast<std::size_t>(N) * 16);
+    apply_cnt_.resize(1);
+    CPK_CUDA(cudaMemset(apply_cnt_.get(), 0, sizeof(unsigned int)));
     cgres_.resize(8);
     flag_.resize(4);
     barrier_.resize(cg_barrier_words());
@@ -1591,13 +1594,11 @@ void DeviceProblem::gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule,
     // than a cross-stream hand-off in front of the next cooperative launch)
     CPK_CUDA(cudaMemsetAsync(barrier_.get(), 0, cg_barrier_words() * sizeof(unsigned int), ctx_.stream));
     barrier_zero_ = true;
-    launch_pack_values(nullptr, 0, cgres_.get(), 5, dm + o_cg, ctx_.stream);
     CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));  // pre-step snapshot taken
-    launch_axpy(A_.get(), V_.get(), 1.0, S, ctx_.stream);
-    launch_block_norm_sum(V_.get(), offs_dev_.get(), N, partials_.get(), scal_.get() + kNormSum, 1.0, ctx_.stream);
-    launch_set_flag_scalar(flag_.get(), 1, scal_.get() + kStep, 0.0, ctx_.stream);
-    launch_all_finite(A_.get(), S, flag_.get(), ctx_.stream);
-    launch_pack_values(scal_.get() + kNormSum, 1, flag_.get(), 1, dm + o_step, ctx_.stream);
+    // A += V, step norm, finiteness, CG result and step diagnostics: one launch
+    launch_gn_apply(A_.get(), V_.get(), offs_dev_.get(), N, partials_.get(), apply_bad_.get(), apply_cnt_.get(),
+                    cgres_.get(), 5, dm + o_cg, scal_.get() + kNormSum, scal_.get() + kStep, flag_.get(),
+                    dm + o_step, ctx_.stream);
     invalidate_all();
     // the next step's Grams, Gamma set and preconditioner (lambda of the next
     // schedule state) on the side stream, hidden behind the tree pass

@@ -434,6 +434,8 @@ private:
     std::int64_t smax_ = 1;
     DevBuf<double> scal_, partials_, slots_;
     DevBuf<int> status_, cgres_, flag_;
+    DevBuf<int> apply_bad_;            // gn_apply: per-block finiteness
+    DevBuf<unsigned int> apply_cnt_;   // gn_apply: last-block counter (self-resetting)
     DevBuf<unsigned int> barrier_;
     DevBuf<std::int64_t> offs_dev_, rows_dev_;
     DevBuf<const double*> facptr_dev_;
