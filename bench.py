@@ -242,6 +242,17 @@ def cpu_baseline_sample(x, init, key):
 
 
 # ------------------------------------------------------------------------ B200 arm
+REJECT_REASONS = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def throttled(clocks):
+    if not clocks or not clocks.get("sm_mhz") or not clocks.get("sm_max_mhz"):
+        return False
+    if REJECT_REASONS & set(clocks.get("reasons", [])):
+        return True
+    return clocks["sm_mhz"] < 0.9 * clocks["sm_max_mhz"] and not clocks.get("reasons")
+
+
 def timed_sweeps(p, init, steps, warmup, clocks_device=None):
     from paper_1910_12331_b200 import cpkit
     sampler = ClockSampler(clocks_device) if clocks_device is not None else None
@@ -323,6 +334,13 @@ def run_b200(args, rank, world, local_rank):
     # ---- warm-up, then exactly K timed sweeps (CUDA events on the problem's stream)
     barrier()
     ms, prof_ms, prof_cnt, launches, clocks = timed_sweeps(p, init, args.steps, args.warmup, local_rank)
+    # a run that saw a hardware / thermal slowdown, or SM clocks stuck well below
+    # max with no reason (a leftover lock), is measured once more (all ranks)
+    if max_over_ranks(1.0 if throttled(clocks) else 0.0) > 0.0:
+        first = clocks
+        barrier()
+        ms, prof_ms, prof_cnt, launches, clocks = timed_sweeps(p, init, args.steps, args.warmup, local_rank)
+        clocks = dict(clocks, remeasured=True, first_attempt=first)
     ms = max_over_ranks(ms)
     value = args.steps / (ms / 1e3)
     final_res = residual_now(p, dims, xn2)
