@@ -284,3 +284,31 @@ def als_optimize(x, factors, max_sweeps=10000, residual_tol=5e-5, step_tol=1e-7,
             status = "converged_step"
             break
     return factors, records, status
+
+
+def gn_optimize(x, factors, max_iters=500, residual_tol=5e-5, step_tol=1e-7, upper=1e-2, lower=1e-6, mu=2.0):
+    """Outer GN loop with the default varying schedule (gauss_newton.cpp:451-494,
+    :10-59): lambda starts at `upper`, a record per stepped iteration
+    {iter, residual_after, 1 - r, lambda, cg_iters}, stop on residual_tol
+    (converged_residual) or step_tol (converged_step), else cap_hit."""
+    xnorm2 = float(np.dot(x.ravel(), x.ravel()))
+    if not xnorm2 > 0.0:
+        raise ValueError("gn_optimize: tensor norm must be positive")
+    tree = Tree(x)
+    lam, direction = upper, 0
+    records, status = [], "cap_hit"
+    for it in range(1, max_iters + 1):
+        factors, d = gn_step(x, factors, lam, xnorm2, tree, residual_tol)
+        if not d["stepped"]:
+            status = "converged_residual"
+            break
+        r = d["residual_after"]
+        records.append({"iter": it, "residual": r, "fitness": 1.0 - r, "lambda": lam, "cg_iters": d["cg_iters"]})
+        if r < residual_tol:
+            status = "converged_residual"
+            break
+        if d["step_norm"] < step_tol:
+            status = "converged_step"
+            break
+        lam, direction = schedule_next(lam, direction, mu, lower, upper)
+    return factors, records, status

@@ -46,3 +46,18 @@ def test_als_optimize_matches_oracle(orc):
     for a, b in zip(recs2, recs):
         assert a["lambda"] == b["lambda"] and abs(a["residual"] - b["residual"]) < 1e-9
     assert vec_rel_err(f, f_ref) < 1e-8
+
+
+def test_gn_optimize_matches_oracle(orc):
+    dims, rank = [8, 7, 6], 3
+    truth = orc.random_model(dims, rank, 21)
+    x = orc.reconstruct(truth)
+    orc.add_noise(x, 3, 1e-4)
+    init = orc.random_model(dims, rank, 22)
+    f_ref, recs, st = orc.gn_optimize(x, init, orc.GnConfig(max_iters=15))
+    f, recs2, st2 = ba.gn_optimize(x, init, max_iters=15)
+    assert st2 == st and len(recs2) == len(recs)
+    for a, b in zip(recs2, recs):
+        assert a["lambda"] == b["lambda"] and a["cg_iters"] == b["cg_iters"]
+        assert abs(a["residual"] - b["residual"]) < 1e-9
+    assert vec_rel_err(f, f_ref) < 1e-7

@@ -182,10 +182,11 @@ def test_full_c3_swamp_to_convergence(orc, ck):
         assert abs(a["residual"] - b["residual"]) < 1e-9, (a, b)
 
 
-def test_full_c5s_every_mode_and_one_sweep(orc, ck):
-    """The 1-GPU slice of config 5 (order 4, s=200, R=200, noise 1e-4, 12.8 GB):
-    every mode's MTTKRP vs the oracle tree, then one ALS sweep and one GN step
-    (default GnConfig) vs the BLAS restatement."""
+def test_full_c5s_every_mode_and_traces(orc, ck):
+    """The 1-GPU slice of config 5 (order 4, s=200, R=200, noise 1e-4, 12.8 GB),
+    the bench's workload: every mode's MTTKRP vs the oracle tree, then 4 ALS
+    sweeps and 6 GN iterations (default GnConfig) record by record vs the BLAS
+    restatement."""
     dims, R = [200, 200, 200, 200], 200
     p, x = generated(ck, dims, R, 1e-4)
     init = ck.random_factors(dims, R, ck.init_seed(0, R, 0, 0))
@@ -195,21 +196,24 @@ def test_full_c5s_every_mode_and_one_sweep(orc, ck):
         assert rel_err(p.mttkrp(n), ref[n]) < 1e-11, n
     assert p.full_contractions == cnt == 2
     del ref
-    # the sweep and the GN step against the BLAS restatement (pinned to the
-    # oracle by tests/test_blas_arm.py): the fixed-order oracle needs minutes
-    # per C5s contraction
+    # ALS and GN traces against the BLAS restatement (pinned to the oracle by
+    # tests/test_blas_arm.py): the fixed-order oracle needs minutes per C5s contraction
     from oracle import blas_arm as ba
-    p.set_factors(init)
-    step, _ = p.als_sweep(0.0)
+    f_dev, rep = p.optimize({"optimizer": "als", "als": {"max_sweeps": 4, "residual_tol": 0.0, "step_tol": 0.0}},
+                            init)
+    j = rep.to_json()
     with ba.threads(os.cpu_count() or 1):
-        f_ref, step_ref, _, _ = ba.als_sweep(ba.Tree(x), init, 0.0)
-    assert abs(step - step_ref) <= 1e-10 * step_ref
-    assert vec_rel_err(p.get_factors(), f_ref) < 1e-10
-    xn2 = orc.norm2(x)
-    p.set_factors(init)
-    d = p.gn_step({}, xn2)
+        f_ref, recs, st = ba.als_optimize(x, init, max_sweeps=4, residual_tol=0.0, step_tol=0.0)
+    assert j["status"] == st == "cap_hit" and len(j["records"]) == len(recs) == 4
+    for a, b in zip(j["records"], recs):
+        assert abs(a["residual"] - b["residual"]) < 1e-10, (a, b)
+    assert vec_rel_err(f_dev, f_ref) < 1e-10
+    f_dev, rep = p.optimize({"optimizer": "gn", "gn": {"max_iters": 6}}, init)
+    j = rep.to_json()
     with ba.threads(os.cpu_count() or 1):
-        f_ref, d_ref = ba.gn_step(x, init, 1e-2, xn2)  # the default schedule starts at lambda = upper = 1e-2
-    assert d["cg_iters"] == d_ref["cg_iters"], (d, d_ref)
-    assert abs(d["residual_after"] - d_ref["residual_after"]) < 1e-10
-    assert vec_rel_err(p.get_factors(), f_ref) < 1e-9
+        f_ref, recs, st = ba.gn_optimize(x, init, max_iters=6)
+    assert j["status"] == st and len(j["records"]) == len(recs) == 6
+    for a, b in zip(j["records"], recs):
+        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"], (a, b)
+        assert abs(a["residual"] - b["residual"]) < 1e-9, (a, b)
+    assert vec_rel_err(f_dev, f_ref) < 1e-8
