@@ -15,6 +15,8 @@ double ref_uniform(std::uint64_t seed, std::uint64_t stream, std::uint64_t index
 double ref_gaussian(std::uint64_t seed, std::uint64_t stream, std::uint64_t index) {
     return cpkit::rng::gaussian(seed, stream, index);
 }
+std::uint64_t ref_mix64(std::uint64_t x) { return cpkit::rng::mix64(x); }
+std::uint64_t ref_derive(std::uint64_t h, std::uint64_t v) { return cpkit::rng::derive(h, v); }
 std::uint64_t ref_keyed(std::uint64_t seed, std::uint64_t stream, std::uint64_t index, std::uint64_t salt) {
     return cpkit::rng::keyed(seed, stream, index, salt);
 }

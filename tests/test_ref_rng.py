@@ -46,3 +46,31 @@ def test_oracle_matches_reference_rng_sampled(orc):
         assert orc.uniform(s, st, i, 0.0, 1.0) == L.ref_uniform(s, st, i, 0.0, 1.0)
         g1, g2 = orc.gaussian(s, st, i), L.ref_gaussian(s, st, i)
         assert hx(g1) == hx(g2), (s, st, i, g1, g2)
+
+
+REF_HARNESS = "/root/reference/proj/src/core/harness.cpp"
+
+
+@pytest.mark.skipif(not (os.path.exists(REFLIB) and os.path.exists(REF_HARNESS)),
+                    reason="reference source tree not present (GPU box)")
+def test_seed_derivation_matches_reference(orc):
+    """harness.cpp:378-391 problem_seed / init_seed: the reference's derive /
+    mix64 chain (from rng.hpp, via the shim) with the tag constants read from
+    the reference source, against the oracle's derivation."""
+    import re
+    src = open(REF_HARNESS).read()
+    tags = {k: int(v, 0) for k, v in re.findall(r"(kProblemTag|kInitTag)\s*=\s*(0x[0-9A-Fa-f]+)", src)}
+    assert set(tags) == {"kProblemTag", "kInitTag"}
+    L = C.CDLL(REFLIB)
+    for f in ("ref_mix64", "ref_derive"):
+        getattr(L, f).restype = C.c_uint64
+    L.ref_mix64.argtypes = [C.c_uint64]
+    L.ref_derive.argtypes = [C.c_uint64, C.c_uint64]
+    for master in (0, 1, 7, 2**40 + 3):
+        for rank in (1, 5, 100, 200):
+            for prob in (0, 1, 29):
+                ps = L.ref_derive(L.ref_derive(L.ref_derive(L.ref_mix64(master), tags["kProblemTag"]), rank), prob)
+                assert orc.problem_seed(master, rank, prob) == ps
+                for init in (0, 4):
+                    h = L.ref_derive(L.ref_derive(L.ref_derive(L.ref_mix64(master), tags["kInitTag"]), rank), prob)
+                    assert orc.init_seed(master, rank, prob, init) == L.ref_derive(h, init)
