@@ -506,25 +506,15 @@ chol_solve_rows_kernel(const double* __restrict__ l_all, int R, const double* __
             if (ok) break;
         }
     } else if (kSmem) {
-        // batch the global loads (8 in flight per thread) before the shared stores
-        const int total = R * LD;
-        for (int e0 = threadIdx.x; e0 < total; e0 += 8 * blockDim.x) {
-            double v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = e0 + u * blockDim.x;
-                v[u] = (e < total) ? __ldg(Lg + e) : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int e = e0 + u * blockDim.x;
-                if (e < total) {
-                    const int i = e / LD, k = e - i * LD;
-                    if (k <= i) lsh[ix.at(i, k)] = v[u];
-                    else if (k == R) lsh[ix.inv(i)] = v[u];
-                }
-            }
+        // packed: one warp per row, 8-byte async copies of its lower part and 1 / L_ii
+        // (no index division; rows of the square global layout start at odd offsets)
+        for (int i = warp; i < R; i += kSolveWarps) {
+            const double* src = Lg + static_cast<long long>(i) * LD;
+            double* dst = lsh + ix.at(i, 0);
+            for (int k = lane; k <= i; k += 32) tile::cp_async8(dst + k, src + k);
+            if (lane == 0) tile::cp_async8(lsh + ix.inv(i), src + R);
         }
+        tile::cp_async_wait_all();
         __syncthreads();
     }
     auto Lat = [&](int i, int k) -> double { return kSmem ? lsh[ix.at(i, k)] : Lg[i * LD + k]; };
