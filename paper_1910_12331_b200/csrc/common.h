@@ -64,6 +64,7 @@ std::uint64_t guard_violations();
 void* dev_alloc(std::size_t bytes);
 void dev_free(void* p, std::size_t bytes);
 void dev_cache_empty();  // every device: cached blocks back to the driver
+std::size_t dev_cache_bytes();  // bytes cached for the current device
 // Small pinned host blocks (diagnostic slots, mapped flags) from a process-wide
 // free list: cudaFreeHost was measured taking up to 0.7 s on the B200 hosts
 // (page unpinning), so the blocks are allocated once (portable, and mapped

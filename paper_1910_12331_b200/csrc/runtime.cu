@@ -158,6 +158,16 @@ void pinned_small_free(void* p, std::size_t bytes, bool mapped) {
     std::lock_guard<std::mutex> lock(g_pin_mu);
     g_pin_free.emplace(std::make_pair(bytes, mapped), p);
 }
+std::size_t dev_cache_bytes() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    std::size_t b = 0;
+    auto it = g_cache.find(dev);
+    if (it != g_cache.end())
+        for (auto& kv : it->second) b += kv.first;
+    return b;
+}
 void dev_cache_empty() {
     std::lock_guard<std::mutex> lock(g_cache_mu);
     int cur = 0;

@@ -487,13 +487,15 @@ DeviceProblem::DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int 
     if (N >= 4) {
         std::size_t free_b = 0, total_b = 0;
         CPK_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        free_b += dev_cache_bytes();  // recycled blocks are free for this problem
         ldT_ = (F_ + 1) & ~1LL;
         const double copy_b = 8.0 * static_cast<double>(Bl_) * static_cast<double>(ldT_);
         const char* ce = std::getenv("CPKIT_FRONT_COPY");
         front_copy_ = ce ? std::atoi(ce) != 0 : copy_b < kLayoutCopyShare * static_cast<double>(free_b);
         if (front_copy_) {
             XT_.resize(static_cast<std::size_t>(Bl_ * ldT_));
-            CPK_CUDA(cudaMemset(XT_.get(), 0, XT_.size() * sizeof(double)));  // stride padding stays zero
+            if (ldT_ != F_)  // the stride padding column stays zero
+                CPK_CUDA(cudaMemset2D(XT_.get() + F_, ldT_ * sizeof(double), 0, sizeof(double), Bl_));
         }
     }
     if (msdt_)
@@ -633,6 +635,28 @@ void DeviceProblem::upload_tensor(const double* host_local) {
             // X^(1)[i0][i2][i1] for i0 in [a, b): batch i0, rows i1, cols i2
             launch_transpose_batched(xd, b - a, s1, Bl_, Bs_, s1 * Bs_, X1_.get() + a * Bl_ * ld1_, ld1_,
                                      Bl_ * ld1_, ctx_.aux2);
+        }
+        CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
+        CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));
+        invalidate_all();
+        return;
+    }
+    if (front_copy_ && !std::getenv("CPKIT_UPLOAD_UNCHUNKED")) {
+        // orders >= 4: upload by row slabs; each slab's columns of X^T are
+        // transposed on the third stream while the next slab crosses PCIe
+        const std::int64_t chunks = std::min<std::int64_t>(8, F_), step = (F_ + chunks - 1) / chunks;
+        for (std::int64_t a = 0; a < F_; a += step) {
+            const std::int64_t rows = std::min(F_, a + step) - a;
+            double* xd = x_.get() + a * Bs_;
+            if (Bs_ == Bl_)
+                CPK_CUDA(cudaMemcpyAsync(xd, host_local + a * Bl_, rows * Bl_ * sizeof(double), cudaMemcpyHostToDevice,
+                                         ctx_.stream));
+            else
+                CPK_CUDA(cudaMemcpy2DAsync(xd, Bs_ * sizeof(double), host_local + a * Bl_, Bl_ * sizeof(double),
+                                           Bl_ * sizeof(double), rows, cudaMemcpyHostToDevice, ctx_.stream));
+            CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.stream));
+            CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
+            launch_transpose_batched(xd, 1, rows, Bl_, Bs_, 0, XT_.get() + a, ldT_, 0, ctx_.aux2);
         }
         CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
         CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));
