@@ -995,7 +995,7 @@ cpkit_status cpkit_decompose(const cpkit_tensor* t, const char* config_json, con
         {
             cpkit::Context ctx(current_device());
             cpkit::DeviceProblem p(ctx, t->t.dims(), static_cast<int>(start.rank));
-            p.upload_tensor(t->t.data());
+            p.upload_tensor(t->t.data(), &start);  // the first back root beside the upload (orders >= 4)
             if (phase_trace) {
                 ctx.sync();
                 t1 = now();

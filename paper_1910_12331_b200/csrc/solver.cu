@@ -613,7 +613,42 @@ KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) 
     return d;
 }
 
-void DeviceProblem::upload_tensor(const double* host_local) {
+void DeviceProblem::upload_tensor(const double* host_local, const KruskalModel* start) {
+    const int N = order();
+    if (start && front_copy_ && !ctx_.comm && h_ >= 1 && !std::getenv("CPKIT_UPLOAD_UNCHUNKED") &&
+        !std::getenv("CPKIT_UPLOAD_NO_ROOT")) {
+        // orders >= 4: H2D by row slabs on the side stream; per slab, the back
+        // root's rows on the solver stream and the slab's X^T columns on the
+        // third stream, both beside the next slab's copy
+        set_factors(*start);
+        const std::int64_t chunks = std::max<std::int64_t>(1, std::min<std::int64_t>(8, F_ / 10000));
+        const std::int64_t step = (F_ + chunks - 1) / chunks;
+        for (std::int64_t a = 0; a < F_; a += step) {
+            const std::int64_t rows = std::min(F_, a + step) - a;
+            double* xd = x_.get() + a * Bs_;
+            if (Bs_ == Bl_)
+                CPK_CUDA(cudaMemcpyAsync(xd, host_local + a * Bl_, rows * Bl_ * sizeof(double), cudaMemcpyHostToDevice,
+                                         ctx_.aux));
+            else
+                CPK_CUDA(cudaMemcpy2DAsync(xd, Bs_ * sizeof(double), host_local + a * Bl_, Bl_ * sizeof(double),
+                                           Bl_ * sizeof(double), rows, cudaMemcpyHostToDevice, ctx_.aux));
+            CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2A], ctx_.aux));
+            CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2A], 0));
+            CPK_CUDA(cudaStreamWaitEvent(ctx_.aux2, ctx_.ev[Context::kEvAux2A], 0));
+            launch_transpose_batched(xd, 1, rows, Bl_, Bs_, 0, XT_.get() + a, ldT_, 0, ctx_.aux2);
+            launch_root_back(xd, rows, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get() + a * R_,
+                             ws_.get(), ws_.size(), ctx_.stream, 0);
+        }
+        CPK_CUDA(cudaEventRecord(ctx_.ev[Context::kEvAux2B], ctx_.aux2));
+        CPK_CUDA(cudaStreamWaitEvent(ctx_.stream, ctx_.ev[Context::kEvAux2B], 0));
+        invalidate_all();
+        pf_valid_ = true;  // the back root of the start factors
+        ++contractions_;
+        preset_.clear();
+        for (const auto& f : start->factors) preset_.insert(preset_.end(), f.data.begin(), f.data.end());
+        preset_valid_ = true;
+        return;
+    }
     if (msdt_copies_ && !std::getenv("CPKIT_UPLOAD_UNCHUNKED")) {
         // order 3: upload by i0 slabs; each slab's share of both permuted copies is
         // transposed on the third stream while the next slab crosses PCIe
@@ -797,6 +832,7 @@ void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noi
 }
 
 void DeviceProblem::set_factors(const std::vector<const double*>& host) {
+    preset_valid_ = false;
     for (int n = 0; n < order(); ++n)
         CPK_CUDA(cudaMemcpyAsync(A_.get() + off_[n], host[n], (off_[n + 1] - off_[n]) * sizeof(double),
                                  cudaMemcpyHostToDevice, ctx_.stream));
@@ -810,6 +846,20 @@ void DeviceProblem::get_factors(std::vector<double*>& host) {
 }
 void DeviceProblem::set_factors(const KruskalModel& m) {
     if (m.dims != dims_ || m.rank != R_) throw InvalidArgument("model extents/rank do not match the problem");
+    if (preset_valid_) {  // the factors the upload contracted: keep them and their back root
+        bool same = true;
+        std::size_t at = 0;
+        for (const auto& a : m.factors) {
+            if (at + a.data.size() > preset_.size() ||
+                std::memcmp(a.data.data(), preset_.data() + at, a.data.size() * sizeof(double)) != 0) {
+                same = false;
+                break;
+            }
+            at += a.data.size();
+        }
+        preset_valid_ = false;
+        if (same && at == preset_.size()) return;
+    }
     std::vector<const double*> p;
     for (const auto& a : m.factors) p.push_back(a.data.data());
     set_factors(p);
@@ -1051,6 +1101,7 @@ void DeviceProblem::note_factor_update(int mode) {
     m_all_valid_ = false;
 }
 void DeviceProblem::invalidate_all() {  // factors changed wholesale
+    preset_valid_ = false;
     pinv_ready_ = false;
     res_current_ = false;
     pf_valid_ = pb_valid_ = false;

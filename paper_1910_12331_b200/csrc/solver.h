@@ -220,7 +220,10 @@ public:
     // dims with the last extent replaced by the slab size); host or device.
     DeviceProblem(Context& ctx, std::vector<std::uint64_t> dims, int rank);
     ~DeviceProblem();
-    void upload_tensor(const double* host_local);          // H2D copy of the local slab
+    // H2D copy of the local slab. start (orders >= 4, single GPU): those
+    // factors are set first and the back root contraction runs slab by slab
+    // while the tensor crosses PCIe; a later set_factors(start) keeps it.
+    void upload_tensor(const double* host_local, const KruskalModel* start = nullptr);
     // CPKT1 file -> device, streamed: chunks of whole last-mode rows are read into
     // two pinned staging buffers while the previous chunk crosses to HBM (this
     // rank's slab columns only); finiteness checked on the device (tensor.cpp:71-83)
@@ -399,6 +402,8 @@ private:
     // armed by the destructor once every stream is idle: the DevBuf members
     // below (destroyed before it) then go back to the allocation cache
     std::optional<OwnerSyncedRelease> release_scope_;
+    std::vector<double> preset_;  // factors the upload already contracted (upload_tensor with start)
+    bool preset_valid_ = false;
     DevBuf<double> x_;
     DevBuf<double> A_, Atrial_, M_, G_, V_, Z_, Q_, Rr_[2], W_[2];
     DevBuf<double> PF_, PB_, ws_, krp_;

@@ -620,3 +620,37 @@ def test_cg_nonfinite_iterate_is_numerical_failure(orc, ck, c):
     with pytest.raises(ck.CpkitError) as ei:
         p.cp_cg(g, 0.0, {"cg_max_iters": 50})
     assert ei.value.code == 5 and "non-finite" in str(ei.value)
+
+
+@pytest.mark.parametrize("dims", [[24, 22, 20, 18], [150, 150, 20, 10]])
+@pytest.mark.parametrize("optimizer", ["als", "gn"])
+def test_decompose_overlapped_first_root(ck, dims, optimizer):
+    """cpkit_decompose on an order-4 tensor runs the start factors' back root
+    slab by slab while the tensor crosses PCIe (solver.cu upload_tensor with
+    start); the trace must equal the device path that uploads first and
+    contracts after (cpkit_dev_optimize): bitwise with one slab, within
+    roundoff with several (each slab's rows get their own tile plan)."""
+    R = 6
+    truth = ck.random_factors(dims, R, ck.problem_seed(2, R, 0))
+    p0 = ck.DeviceProblem(dims, R)
+    p0.generate(truth, noise_seed=3, noise_rel=1e-3)
+    x = p0.download()
+    p0.close()
+    cfg = {"optimizer": optimizer, "rank": R, "seed": 4, "init": {"distribution": "uniform", "a": 0.0, "b": 1.0},
+           "als": {"max_sweeps": 6, "residual_tol": 0.0, "step_tol": 0.0}, "gn": {"max_iters": 4}}
+    m, rep = ck.decompose(ck.Tensor.create(x), cfg)
+    j = rep.to_json()
+    init = ck.random_factors(dims, R, ck.init_seed(4, R, 0, 0))
+    p = ck.DeviceProblem(dims, R)
+    p.upload(x)
+    f, rep2 = p.optimize(cfg, init)
+    j2 = rep2.to_json()
+    assert len(j["records"]) == len(j2["records"]) > 0
+    one_slab = dims[0] * dims[1] < 20000
+    for a, b in zip(j["records"], j2["records"]):
+        assert a["cg_iters"] == b["cg_iters"] and a["lambda"] == b["lambda"]
+        if one_slab:
+            assert a["residual"] == b["residual"], (a, b)
+        else:
+            assert abs(a["residual"] - b["residual"]) < 1e-10, (a, b)
+    assert vec_rel_err(m.factors(), f) < (1e-15 if one_slab else 1e-9)
