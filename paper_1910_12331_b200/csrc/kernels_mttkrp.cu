@@ -524,6 +524,115 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     }
 }
 
+// NN root with m8n8k4 DMMA tiles, for ranks that are a multiple of 8 with an
+// odd number NC of n8 cells (R = 200: 25 cells). The m16n8k16 kernel above
+// needs every warp's run inside one m16 row with the cells split evenly over
+// the warps, so it pads 25 cells to 26 (4 % of the DMMA work on zero columns).
+// Here the 64-row CTA tile is 8 m8 strips, one per DMMA warp, each strip with
+// ALL NC cells: no padding, equal work on the four SM sub-partitions. Per k4
+// step a warp loads one A value and NC B values per lane (the B tile is shared
+// by the warps) and issues NC DMMA.8x8x4. Same producer, ring, persistent unit
+// loop and split-K contract as root_gemm_kernel<.., TRANS=false, GEN=false>.
+constexpr int kM8Warps = 8;
+template <int NC>
+__global__ void __launch_bounds__(32 * (kM8Warps + 1), 1)
+root_gemm_m8_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
+                    long long M, long long K, int R, int BNS, int stages, long long k_per_split, int splits,
+                    double* __restrict__ out, long long out_split_stride) {
+    extern __shared__ __align__(1024) char smem_raw[];
+    const std::uint32_t raw = smem_u32(smem_raw);
+    const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);
+    char* const smem = smem_raw + (base - raw);
+    constexpr int W = kM8Warps, BM = 8 * W;
+    const int x_bytes = BM * kBK * 8;
+    const int b_bytes = kBK * BNS * 8;
+    const int stage_bytes = x_bytes + b_bytes;
+    std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + stages * stage_bytes);
+    std::uint64_t* empty = full + stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long mtiles = (M + BM - 1) / BM;
+    const long long units = mtiles * splits;
+    auto unit_geom = [&](long long u, long long& m0, long long& kbeg, int& nk) {
+        m0 = (u % mtiles) * BM;
+        kbeg = (u / mtiles) * k_per_split;
+        const long long kend = min(K, kbeg + k_per_split);
+        nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], W);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == W) {  // ---------------- producer (one lane)
+        if (lane != 0) return;
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&xmap)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
+        long long it = 0;
+        for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+            long long m0, kbeg;
+            int nk;
+            unit_geom(u, m0, kbeg, nk);
+            for (int kt = 0; kt < nk; ++kt, ++it) {
+                const int s = static_cast<int>(it % stages);
+                if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+                const long long kk = kbeg + static_cast<long long>(kt) * kBK;
+                char* xs = smem + s * stage_bytes;
+                mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
+                for (int b = 0; b < kBK / 16; ++b)
+                    tma_load_2d(&xmap, &full[s], xs + b * BM * 128, static_cast<int>(kk + 16 * b), static_cast<int>(m0));
+                tma_load_2d(&kmap, &full[s], xs + x_bytes, 0, static_cast<int>(kk));
+            }
+        }
+        return;
+    }
+    // ---------------- DMMA consumers: warp w owns rows 8w..8w+7 of the tile, all NC cells
+    const int g = lane >> 2, t = lane & 3;
+    const int arow = 8 * warp + g;
+    long long it = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        long long m0, kbeg;
+        int nk;
+        unit_geom(u, m0, kbeg, nk);
+        double acc[NC][2];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = 0.0;
+        for (int kt = 0; kt < nk; ++kt, ++it) {
+            const int s = static_cast<int>(it % stages);
+            mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
+            const char* xs = smem + s * stage_bytes;
+            const double* bs = reinterpret_cast<const double*>(xs + x_bytes);
+            const bool half_stage =
+                kt == nk - 1 && min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
+#pragma unroll
+            for (int ks = 0; ks < kBK / 4; ++ks) {
+                if (ks == kBK / 8 && half_stage) break;
+                const int kr = 4 * ks + t;  // this lane's k inside the stage
+                const double a = *reinterpret_cast<const double*>(xs + (kr >> 4) * BM * 128 + swz(arow, kr & 15));
+                const double* brow = bs + kr * BNS + g;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const double b = brow[8 * c];
+                    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                        : "+d"(acc[c][0]), "+d"(acc[c][1])
+                        : "d"(a), "d"(b));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        double* o = out + (u / mtiles) * out_split_stride;
+        const long long row = m0 + arow;
+        if (row < M) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+                *reinterpret_cast<double2*>(o + row * R + 8 * c + 2 * t) = make_double2(acc[c][0], acc[c][1]);
+        }
+    }
+}
+
 __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, long long n,
                                      double* __restrict__ out) {
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
@@ -558,6 +667,7 @@ int round_maxc(int need) {
 struct GemmPlan {
     int maxc, nw, wm, nt8, ntiles, bns, stages, mtiles, splits, per_sm;
     long long kps;
+    bool m8;  // root_gemm_m8_kernel (wm = 4: 64-row tiles, 8 warps, all nt8 cells per warp)
     int BM() const { return 16 * wm; }
     int BN() const { return 8 * nt8; }
 };
@@ -640,6 +750,13 @@ bool runs_full(const GemmPlan& p) {
 
 // fixed_kps > 0: batched contraction, split s covers k in [s kps, (s+1) kps)
 // and writes its own output slab (no split search, no reduction).
+bool m8_enabled() {  // CPKIT_NN_M8=0: always the m16n8k16 kernel
+    static const int v = [] {
+        const char* e = std::getenv("CPKIT_NN_M8");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
 GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_kps = 0, int min_chunks = 8,
                    int wave_cap = 0) {
     GemmPlan p{};
@@ -740,6 +857,25 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
         }
     }
     env("STAGES", p.stages);
+    p.m8 = false;
+    // m8n8k4 variant (root_gemm_m8_kernel) when the m16n8k16 plan pads the rank:
+    // an odd number of n8 cells, no padding (C5s, R = 200: roots 18.90 -> 18.68 ms)
+    const int nc = R / 8;
+    if (!trans && fixed_kps == 0 && p.ntiles == 1 && R % 8 == 0 && (nc & 1) && nc >= 13 && nc <= 31 &&
+        8 * p.nt8 > R && m8_enabled()) {
+        p.m8 = true;
+        p.nw = kM8Warps;
+        p.wm = kM8Warps / 2;  // BM = 8 nw
+        p.nt8 = nc;
+        p.maxc = nc;
+        p.bns = bns_for(8 * nc, false);
+        p.stages = 2;
+        for (int st = 6; st >= 2; --st) {
+            p.stages = st;
+            if (smem_bytes(p) <= 225 * 1024) break;
+        }
+        env("STAGES", p.stages);
+    }
     p.per_sm = resident_per_sm(p);
     p.mtiles = static_cast<int>((M + p.BM() - 1) / p.BM());
     const long long base = static_cast<long long>(p.ntiles) * p.mtiles;
@@ -768,6 +904,25 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
     if (max_ctas > 0) cap = std::min(cap, max_ctas);
     dim3 grid(static_cast<unsigned>(std::min<long long>(units, cap)));
     const dim3 block(32 * (p.nw + 1));
+    if (!TRANS && !GEN && p.m8) {
+#define CPK_M8(NCV)                                                                                     \
+    case NCV: {                                                                                         \
+        auto fn = root_gemm_m8_kernel<NCV>;                                                             \
+        ensure_dynamic_smem(fn, smem);                                                                  \
+        fn<<<grid, dim3(32 * (kM8Warps + 1)), smem, st>>>(xmap, kmap, M, K, R, p.bns, p.stages, p.kps,  \
+                                                          p.splits, out, oss);                          \
+        break;                                                                                          \
+    }
+        switch (p.nt8) {
+            CPK_M8(13) CPK_M8(15) CPK_M8(17) CPK_M8(19) CPK_M8(21) CPK_M8(23) CPK_M8(25) CPK_M8(27) CPK_M8(29)
+            CPK_M8(31)
+            default: throw DeviceError("unsupported m8 rank tile");
+        }
+#undef CPK_M8
+        count_launch(1);
+        CPK_CUDA(cudaGetLastError());
+        return;
+    }
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
         auto fn = runs_full(p) ? root_gemm_kernel<NTV, TRANS, GEN, true>                          \
