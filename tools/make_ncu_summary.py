@@ -25,7 +25,7 @@ def val(d, k):
 kernels = []
 for r in rows[2:]:
     d = dict(zip(hdr, r))
-    if "root_gemm_kernel" not in d.get("Kernel Name", ""):
+    if "root_gemm_" not in d.get("Kernel Name", ""):
         continue
     kernels.append({
         "kernel": d["Kernel Name"][:90],
