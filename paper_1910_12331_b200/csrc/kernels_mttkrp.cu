@@ -242,7 +242,12 @@ __host__ __device__ constexpr int root_max_threads(int maxc) { return maxc >= 9 
 
 // FULL: every warp's run is exactly MAXC cells inside one m16 row (no per-cell
 // predicates; the common case of a rank tile that the warps split evenly).
-template <int MAXC, bool TRANS, bool GEN, bool FULL>
+// RS (row split, NN only, 8 warps over 4 m16 rows): an odd number NT8 = 2 MAXC
+// - 1 of n8 cells per m16 row is split between the row's two warps as MAXC +
+// (MAXC - 1) cells, the longer run alternating so that each SM sub-partition
+// (warps w and w + 4) carries exactly NT8 cells: no rank padding and no run
+// crossing an m16 row (R = 200: 13 + 12 of 25 cells).
+template <int MAXC, bool TRANS, bool GEN, bool FULL, bool RS = false>
 __global__ void __launch_bounds__(root_max_threads(MAXC), 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int BN, int W,
@@ -397,10 +402,14 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     const int NT8 = BN / 8;
     const int cells = (BM / 16) * NT8;
     const int cbase = cells / W, cextra = cells % W;
-    const int cnt = FULL ? MAXC : cbase + (warp < cextra ? 1 : 0);
-    const int cs = warp * cbase + min(warp, cextra);
+    // RS: warp w takes part w % 2 of m16 row w / 2; the long part (MAXC cells)
+    // is the first one when (w / 4) is even, else the second
+    const bool rs_long_first = ((warp >> 2) & 1) == 0;
+    const int rs_first = rs_long_first ? MAXC : NT8 - MAXC;
+    const int cnt = RS ? ((warp & 1) ? NT8 - rs_first : rs_first) : FULL ? MAXC : cbase + (warp < cextra ? 1 : 0);
+    const int cs = RS ? (warp >> 1) * NT8 + ((warp & 1) ? rs_first : 0) : warp * cbase + min(warp, cextra);
     const int r0 = cs / NT8, c0 = cs - r0 * NT8;
-    const int n1 = FULL ? MAXC : min(cnt, NT8 - c0);
+    const int n1 = (FULL || RS) ? cnt : min(cnt, NT8 - c0);
     // byte offset of cell j's n8 column in a KRP k-row: 64 j + (j < n1 ? ofs_a : ofs_b)
     const std::uint32_t ofs_a = static_cast<std::uint32_t>(c0 * 64), ofs_b = static_cast<std::uint32_t>(-n1 * 64);
     const std::uint32_t rowstep = TRANS ? kBK * 128 : 16 * 128;  // next m16 row of the X tile
@@ -512,6 +521,9 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     using No = std::integral_constant<bool, false>;
     if (FULL) {
         mainloop(CFull{}, No{});
+    } else if (RS) {  // runs never cross an m16 row
+        if (cnt == MAXC) mainloop(CFull{}, No{});
+        else mainloop(CLess{}, No{});
     } else {
         const bool span = n1 < cnt;
         if (cnt == MAXC) {
@@ -668,6 +680,7 @@ struct GemmPlan {
     int maxc, nw, wm, nt8, ntiles, bns, stages, mtiles, splits, per_sm;
     long long kps;
     bool m8;  // root_gemm_m8_kernel (wm = 4: 64-row tiles, 8 warps, all nt8 cells per warp)
+    bool rs;  // root_gemm_kernel<.., RS>: wm = 4, nw = 8, odd nt8 split per row as maxc + (maxc - 1)
     int BM() const { return 16 * wm; }
     int BN() const { return 8 * nt8; }
 };
@@ -750,6 +763,13 @@ bool runs_full(const GemmPlan& p) {
 
 // fixed_kps > 0: batched contraction, split s covers k in [s kps, (s+1) kps)
 // and writes its own output slab (no split search, no reduction).
+bool rs_enabled() {  // CPKIT_NN_RS=0: no row-split dealing (then the m8 variant, or padding)
+    static const int v = [] {
+        const char* e = std::getenv("CPKIT_NN_RS");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v != 0;
+}
 bool m8_enabled() {  // CPKIT_NN_M8=0: always the m16n8k16 kernel
     static const int v = [] {
         const char* e = std::getenv("CPKIT_NN_M8");
@@ -858,10 +878,31 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
     }
     env("STAGES", p.stages);
     p.m8 = false;
+    p.rs = false;
+    // row-split m16 dealing when the plan pads the rank to an even split of an
+    // odd cell count (R = 8 NC, NC odd): NC cells per m16 row as MAXC + (MAXC-1)
+    {
+        const int nc = R / 8, mx = (nc + 1) / 2;
+        if (!trans && fixed_kps == 0 && p.ntiles == 1 && R % 8 == 0 && (nc & 1) && nc >= 3 && round_maxc(mx) == mx &&
+            8 * p.nt8 > R && rs_enabled()) {
+            p.rs = true;
+            p.wm = 4;
+            p.nw = 8;
+            p.nt8 = nc;
+            p.maxc = mx;
+            p.bns = bns_for(8 * nc, false);
+            p.stages = 2;
+            for (int st = 6; st >= 2; --st) {
+                p.stages = st;
+                if (smem_bytes(p) <= 225 * 1024) break;
+            }
+            env("STAGES", p.stages);
+        }
+    }
     // m8n8k4 variant (root_gemm_m8_kernel) when the m16n8k16 plan pads the rank:
     // an odd number of n8 cells, no padding (C5s, R = 200: roots 18.90 -> 18.68 ms)
     const int nc = R / 8;
-    if (!trans && fixed_kps == 0 && p.ntiles == 1 && R % 8 == 0 && (nc & 1) && nc >= 13 && nc <= 31 &&
+    if (!p.rs && !trans && fixed_kps == 0 && p.ntiles == 1 && R % 8 == 0 && (nc & 1) && nc >= 13 && nc <= 31 &&
         8 * p.nt8 > R && m8_enabled()) {
         p.m8 = true;
         p.nw = kM8Warps;
@@ -925,8 +966,9 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
     }
 #define CPK_CASE(NTV)                                                                              \
     case NTV: {                                                                                    \
-        auto fn = runs_full(p) ? root_gemm_kernel<NTV, TRANS, GEN, true>                          \
-                               : root_gemm_kernel<NTV, TRANS, GEN, false>;                         \
+        auto fn = (!TRANS && !GEN && p.rs) ? root_gemm_kernel<NTV, TRANS, GEN, false, !TRANS && !GEN> \
+                  : runs_full(p)           ? root_gemm_kernel<NTV, TRANS, GEN, true>              \
+                                           : root_gemm_kernel<NTV, TRANS, GEN, false>;             \
         ensure_dynamic_smem(fn, smem);                                                             \
         if (std::getenv("CPKIT_GRID_OCC")) { /* experiments: grid from the real occupancy */        \
             int occ = 1;                                                                           \

@@ -663,23 +663,26 @@ M8_CASES = [([30, 28, 26, 24], 200), ([40, 36, 34], 120), ([400, 50, 40], 200)]
 
 
 @pytest.mark.parametrize("dims,R", M8_CASES)
-def test_m8_root_kernel(orc, ck, dims, R, tmp_path):
-    """Ranks with an odd number of n8 cells (R = 200: 25) run the NN roots as
-    m8n8k4 DMMA strips without rank padding (root_gemm_m8_kernel). Every mode's
-    MTTKRP against the oracle, and against the m16n8k16 kernel (CPKIT_NN_M8=0,
-    read once per process: run in a subprocess)."""
+def test_odd_cell_root_kernels(orc, ck, dims, R, tmp_path):
+    """Ranks with an odd number of n8 cells (R = 200: 25) run the NN roots
+    without rank padding: by default the m16n8k16 kernel with the row-split
+    dealing (RS: 13 + 12 cells per m16 row), with CPKIT_NN_RS=0 the m8n8k4
+    strip kernel, with CPKIT_NN_M8=0 as well the padded m16 plan. Every mode's
+    MTTKRP against the oracle, and the three variants against each other (the
+    env switches are read once per process: subprocesses)."""
     import subprocess
     import sys
     f = gauss_factors(orc, dims, R, 61)
     x = np.random.default_rng(5).standard_normal(dims)
     p = make(ck, x, f)
-    got = [p.mttkrp(n) for n in range(len(dims))]
+    got = np.concatenate([p.mttkrp(n).ravel() for n in range(len(dims))])
     ref, _ = orc.mttkrp_tree_all(x, f)
     for n in range(len(dims)):
-        assert rel_err(got[n], ref[n]) < 1e-11, n
+        assert rel_err(p.mttkrp(n), ref[n]) < 1e-11, n
     np.save(tmp_path / "x.npy", x)
     np.save(tmp_path / "f.npy", np.concatenate([a.ravel() for a in f]))
-    code = f"""
+    for tag, env_add in (("m8", {"CPKIT_NN_RS": "0"}), ("pad", {"CPKIT_NN_RS": "0", "CPKIT_NN_M8": "0"})):
+        code = f"""
 import sys, numpy as np
 sys.path.insert(0, {repr(str(ROOT))})
 from paper_1910_12331_b200 import cpkit
@@ -689,10 +692,9 @@ f, at = [], 0
 for d in dims:
     f.append(flat[at:at + d * R].reshape(d, R)); at += d * R
 p = cpkit.DeviceProblem(dims, R); p.upload(x); p.set_factors(f)
-np.save({repr(str(tmp_path / 'm16.npy'))}, np.concatenate([p.mttkrp(n).ravel() for n in range(len(dims))]))
+np.save({repr(str(tmp_path / 'v.npy'))}, np.concatenate([p.mttkrp(n).ravel() for n in range(len(dims))]))
 """
-    env = dict(os.environ, CPKIT_NN_M8="0")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
-    assert r.returncode == 0, r.stderr[-2000:]
-    m16 = np.load(tmp_path / "m16.npy")
-    assert rel_err(np.concatenate([g.ravel() for g in got]), m16) < 1e-13
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env_add), capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert rel_err(got, np.load(tmp_path / "v.npy")) < 1e-13, tag
