@@ -41,14 +41,24 @@
 
 #ifndef CPKIT_CG_ABLATE
 #define CPKIT_CG_ABLATE 0  // timing experiments only: 1 A2 work, 2 gathers, 4 GEMMs, 8 slot sums, 16 phase-A publish
+                           // 32: no overlap (A2 loads after the loop-top sums, W' Gamma_nn after the barrier; same bits)
 #endif
 
 namespace cpkit {
 namespace {
 constexpr int kAblate = CPKIT_CG_ABLATE;
+#ifdef CPKIT_CG_NO_PF
+constexpr int kPrefetchWarps = 1 << 30;
+#else
+// Measured (us per iteration, prefetch on/off): C2 (12 warps) 21.5 / 22.0; C4 (4 warps) 16.5 / 16.3;
+// C3 (3 warps) 15.3 / 15.0 - it pays only where the loop-top block sums are long.
+constexpr int kPrefetchWarps = 8;
+#endif
 
 using gsync::cta_rank;
+using gsync::grid_arrive;
 using gsync::grid_barrier;
+using gsync::grid_wait;
 using tile::cp_async16;
 using tile::cp_async8;
 using tile::cp_async_wait_all;
@@ -521,7 +531,30 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
     int it = 0, hit_cap = 0, breakdown = 0, nonfinite = 0;
     double rz = 0.0, wq = 0.0;
     bool first = true;
+    // A2 item of this thread's first pass (element e of mode q's B_q; the G
+    // lanes of a group hold the modes of one element)
+    const int a2G = L.a2g, a2lg = L.a2lg;
+    const int a2items = static_cast<int>(RR) * a2G;
+    const int a2stride = static_cast<int>(nb) * WARPS * 32;
+    const int a2base0 = (vb * WARPS + warp) * 32;
+    constexpr bool kOverlap = !(kAblate & 32);
+    constexpr int kPF = 10;  // slab partials held in registers across the loop-top sums
     for (;;) {
+        // The slab partials of the first A2
+        // pass are requested before the loop-top sums, so both L2 round trips
+        // (per-tile slots, slabs) overlap instead of following each other.
+        double pf_part[kPF];
+        const bool pf_on = WARPS >= kPrefetchWarps && kOverlap && !(kAblate & 1) && a2base0 < a2items;
+        if (pf_on) {
+            const int w = a2base0 + lane;
+            const bool ok = w < a2items;
+            const int q = w & (a2G - 1);
+            const bool act = ok && q < N;
+            const double* src = r_bpart(d, act ? q : 0) + (ok ? (w >> a2lg) : 0);
+            const int nt = act ? L.rowtiles[q] : 0;
+#pragma unroll
+            for (int u = 0; u < kPF; ++u) pf_part[u] = (u < nt) ? __ldcg(src + u * RR) : 0.0;
+        }
         double rz_new, nsum, bad;
         if (kAblate & 8) {
             rz_new = 1.0;
@@ -567,15 +600,16 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
         // slabs (all loads in flight), the group exchanges the B_p by shuffles and
         // lane q forms D_q.
         if (!(kAblate & 1)) {
-            const int G = L.a2g, lg = L.a2lg;
-            const int items = static_cast<int>(RR) * G;
-            const int wstride = static_cast<int>(nb) * WARPS * 32;
-            for (int base = (vb * WARPS + warp) * 32; base < items; base += wstride) {
+            const int G = a2G, lg = a2lg;
+            const int items = a2items;
+            const int wstride = a2stride;
+            for (int base = a2base0; base < items; base += wstride) {
                 const int w = base + lane;
                 const bool ok = w < items;
                 const int e = ok ? (w >> lg) : 0;
                 const int q = w & (G - 1);
                 const bool act = ok && q < N;
+                const bool pre = pf_on && base == a2base0;  // this pass was requested at the loop top
                 double pr[kMaxOrder];
 #pragma unroll
                 for (int m = 0; m < kMaxOrder; ++m)
@@ -587,7 +621,8 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
                     for (int k0 = 0; k0 < nt; k0 += 16) {
                         double part[16];
 #pragma unroll
-                        for (int u = 0; u < 16; ++u) part[u] = (k0 + u < nt) ? __ldcg(src + (k0 + u) * RR) : 0.0;
+                        for (int u = 0; u < 16; ++u)
+                            part[u] = (pre && k0 == 0 && u < kPF) ? pf_part[u < kPF ? u : 0] : (k0 + u < nt) ? __ldcg(src + (k0 + u) * RR) : 0.0;
 #pragma unroll
                         for (int u = 0; u < 16; ++u)
                             if (k0 + u < nt) b += part[u];
@@ -613,13 +648,28 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             }
         }
         r_stamp(d, vb, it, 8);
-        gbar(round);
+        // CLU: W' Gamma_nn needs no other CTA's global data (the siblings' W'
+        // blocks come through DSMEM), so it runs between this barrier's arrive
+        // and wait; the accumulation order (Gamma_nn part, then the D part) is
+        // the one of the plain sequence.
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        const bool early = CLU && kOverlap;
+        if (early) {
+            grid_arrive(p.barrier, round);
+            if (has) {
+                wait_rows();  // the siblings' W' blocks (pushed in phase A)
+                warp_mma_blk(Rb, L.tm, L.bs, L.tn, wm, Gs, ks, wn, L.rk, acc);
+            }
+            grid_wait(p.barrier, nb, round);
+        } else {
+            gbar(round);
+        }
         r_stamp(d, vb, it, 3);
         // ---- B: Q = [W' | A_n] [Gamma_nn ; D_n^T] + lambda Reg(W'); <W', Q> partial
         if (has) {
             if (CLU) {
                 copy_rows<WARPS>(Ds, ks, R, r_dt(d) + n * RR + c0, R, vc, 0, 0);
-                wait_rows();  // the siblings' W' blocks (pushed in phase A)
+                if (!early) wait_rows();
                 r_stamp(d, vb, it, 13);
             } else {
                 copy_rows<WARPS>(Rb, ld, vr, p.W[0] + rowbase, R, R, c0, c0 + L.tn);
@@ -630,9 +680,11 @@ __global__ void __launch_bounds__(MT * NT * 32, 1) cg_res_kernel(const __grid_co
             }
             cp_async_wait_all();  // sibling W' columns and the D slice
             __syncthreads();
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
-            if (CLU) warp_mma_blk(Rb, L.tm, L.bs, L.tn, wm, Gs, ks, wn, L.rk, acc);
-            else warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
+            if (CLU) {
+                if (!early) warp_mma_blk(Rb, L.tm, L.bs, L.tn, wm, Gs, ks, wn, L.rk, acc);
+            } else {
+                warp_mma<false>(Rb, ld, wm, Gs, ks, wn, L.rk, acc);
+            }
             warp_mma<false>(An, ld, wm, Ds, ks, wn, L.rk, acc);
             double part = 0.0;
 #pragma unroll
