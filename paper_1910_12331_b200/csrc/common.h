@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <mutex>
@@ -39,6 +40,18 @@ class DeviceError : public Error { public: using Error::Error; };
             throw ::cpkit::DeviceError(std::string("CUDA error ") + cudaGetErrorString(e_) + \
                                        " at " + __FILE__ + ":" + std::to_string(__LINE__)); \
     } while (0)
+
+// ---- NVTX ranges around the host-side phases (upload, generation, root
+// contractions, the CG solve, ALS sweeps, GN steps): the reference's only
+// instrumentation is steady_clock around a sweep (als.cpp:67-81); here a
+// profiler (ncu --nvtx --nvtx-include "cpkit:root_back/") can select a phase
+// by name. Header-only NVTX v3: one pointer test per call with no tool attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- guarded allocation mode (CPKIT_GUARD=1; runtime.cu). compute-sanitizer
 // is not available on the GPU pool, so out-of-bounds WRITES are caught here:

@@ -239,6 +239,10 @@ __device__ __forceinline__ double lds64(std::uint32_t addr) {
 // Block-size bound per run length: long runs (many accumulators) get fewer
 // warps and more registers each.
 __host__ __device__ constexpr int root_max_threads(int maxc) { return maxc >= 9 ? 32 * 9 : maxc >= 6 ? 32 * 11 : 32 * 13; }
+// (The register cap ptxas derives from these bounds is per SM sub-partition:
+// 9 warps put 3 on one sub-partition of 16 K registers, so 168 per thread is
+// the real limit for the 288-thread variants, not 65536 / 288 = 224 - a
+// __maxnreg__(224) build fails to launch.)
 
 // FULL: every warp's run is exactly MAXC cells inside one m16 row (no per-cell
 // predicates; the common case of a rank tile that the warps split evenly).
@@ -344,13 +348,20 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
             if (lane == 0) mbar_arrive(&full[s]);  // releases the warp's shared stores
         };
         long long it = 0;  // global stage counter
+        // ring slot and lap parity kept incrementally: a runtime `it % stages`
+        // is an integer division per stage (I2F/MUFU/IMAD.HI chain; 3 % of the
+        // C2 root's stall samples sat on it)
+        int ring = -1;
+        unsigned lap = 1;  // parity of (it / stages)
         for (long long u = blockIdx.x; u < units; u += gridDim.x) {
             int n0, nk, split;
             long long m0, kbeg;
             unit_geom(u, n0, m0, kbeg, nk, split);
             for (int kt = 0; kt < nk; ++kt, ++it) {
-                const int s = static_cast<int>(it % stages);
-                if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+                if (++ring == stages) ring = 0;
+                if (ring == 0) lap ^= 1u;
+                const int s = ring;
+                if (it >= stages) mbar_wait(&empty[s], lap ^ 1u);
                 const long long kk = kbeg + static_cast<long long>(kt) * kBK;
                 char* xs = smem + s * stage_bytes;
                 if (lane == 0) {
@@ -441,7 +452,8 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     auto mainloop = [&](auto c_tag, auto span_tag) {
         constexpr int C = decltype(c_tag)::value;
         constexpr bool SPAN = decltype(span_tag)::value;
-        long long it = 0;
+        int ring = -1;      // ring slot of the current stage and the parity of its lap,
+        unsigned lap = 1;   // kept incrementally (no per-stage integer division)
         for (long long u = blockIdx.x; u < units; u += gridDim.x) {
             int n0, nk, split;
             long long m0, kbeg;
@@ -449,10 +461,14 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
             double acc[C][4];
 #pragma unroll
             for (int j = 0; j < C; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+            // the unit's last stage holds only 16 valid k (see half_stage below)
+            const bool last_half = min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(nk - 1) * kBK) <= 16;
 
-            for (int kt = 0; kt < nk; ++kt, ++it) {
-                const int s = static_cast<int>(it % stages);
-                mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
+            for (int kt = 0; kt < nk; ++kt) {
+                if (++ring == stages) ring = 0;
+                if (ring == 0) lap ^= 1u;
+                const int s = ring;
+                mbar_wait(&full[s], lap);
                 // plain shared loads (ordered after the full-barrier wait by its
                 // memory clobber, otherwise free for the scheduler to hoist)
                 const char* xs = smem + s * stage_bytes;
@@ -462,8 +478,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
                 // a unit's last stage may hold only 16 valid k (its B rows beyond
                 // the unit's k range are zero): skip the empty half instead of
                 // multiplying zeros
-                const bool half_stage =
-                    kt == nk - 1 && min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
+                const bool half_stage = kt == nk - 1 && last_half;
 #pragma unroll
                 for (int ks = 0; ks < kBK / 16; ++ks) {
                     if (ks == 1 && half_stage) break;
@@ -583,13 +598,17 @@ root_gemm_m8_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&xmap)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(&kmap)) : "memory");
         long long it = 0;
+        int ring = -1;
+        unsigned lap = 1;
         for (long long u = blockIdx.x; u < units; u += gridDim.x) {
             long long m0, kbeg;
             int nk;
             unit_geom(u, m0, kbeg, nk);
             for (int kt = 0; kt < nk; ++kt, ++it) {
-                const int s = static_cast<int>(it % stages);
-                if (it >= stages) mbar_wait(&empty[s], static_cast<unsigned>(((it / stages) - 1) & 1));
+                if (++ring == stages) ring = 0;
+                if (ring == 0) lap ^= 1u;
+                const int s = ring;
+                if (it >= stages) mbar_wait(&empty[s], lap ^ 1u);
                 const long long kk = kbeg + static_cast<long long>(kt) * kBK;
                 char* xs = smem + s * stage_bytes;
                 mbar_expect_tx(&full[s], static_cast<unsigned>(stage_bytes));
@@ -603,7 +622,8 @@ root_gemm_m8_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     // ---------------- DMMA consumers: warp w owns rows 8w..8w+7 of the tile, all NC cells
     const int g = lane >> 2, t = lane & 3;
     const int arow = 8 * warp + g;
-    long long it = 0;
+    int ring = -1;
+    unsigned lap = 1;
     for (long long u = blockIdx.x; u < units; u += gridDim.x) {
         long long m0, kbeg;
         int nk;
@@ -611,13 +631,15 @@ root_gemm_m8_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         double acc[NC][2];
 #pragma unroll
         for (int c = 0; c < NC; ++c) acc[c][0] = acc[c][1] = 0.0;
-        for (int kt = 0; kt < nk; ++kt, ++it) {
-            const int s = static_cast<int>(it % stages);
-            mbar_wait(&full[s], static_cast<unsigned>((it / stages) & 1));
+        const bool last_half = min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(nk - 1) * kBK) <= 16;
+        for (int kt = 0; kt < nk; ++kt) {
+            if (++ring == stages) ring = 0;
+            if (ring == 0) lap ^= 1u;
+            const int s = ring;
+            mbar_wait(&full[s], lap);
             const char* xs = smem + s * stage_bytes;
             const double* bs = reinterpret_cast<const double*>(xs + x_bytes);
-            const bool half_stage =
-                kt == nk - 1 && min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(kt) * kBK) <= 16;
+            const bool half_stage = kt == nk - 1 && last_half;
 #pragma unroll
             for (int ks = 0; ks < kBK / 4; ++ks) {
                 if (ks == kBK / 8 && half_stage) break;

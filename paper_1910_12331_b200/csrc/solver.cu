@@ -614,6 +614,7 @@ KrpDesc DeviceProblem::krp(int lo, int hi, const double* base, bool local_last) 
 }
 
 void DeviceProblem::upload_tensor(const double* host_local, const KruskalModel* start) {
+    NvtxRange nvtx_range("cpkit:upload_tensor");
     const int N = order();
     if (start && front_copy_ && !ctx_.comm && h_ >= 1 && !std::getenv("CPKIT_UPLOAD_UNCHUNKED") &&
         !std::getenv("CPKIT_UPLOAD_NO_ROOT")) {
@@ -708,6 +709,7 @@ void DeviceProblem::upload_tensor(const double* host_local, const KruskalModel* 
     invalidate_all();
 }
 void DeviceProblem::load_tensor_file(const std::string& path) {
+    NvtxRange nvtx_range("cpkit:load_tensor_file");
     std::uint64_t off = 0;
     if (read_tensor_header(path, &off) != dims_) throw InvalidArgument("tensor file extents do not match the problem");
     const int N = order();
@@ -793,6 +795,7 @@ void DeviceProblem::download_tensor(double* host_local) {
 // noiseless tensor is bitwise equal to the CPU generator's; the keyed noise
 // (keyed_noise.cuh) is bitwise equal to the CPU restatement's too.
 void DeviceProblem::generate_tensor(const KruskalModel& truth, std::uint64_t noise_seed, double noise_rel) {
+    NvtxRange nvtx_range("cpkit:generate_tensor");
     set_factors(truth);
     const int N = order();
     KrpDesc all = krp(0, N, A_.get(), true);
@@ -938,6 +941,7 @@ void DeviceProblem::profile_read(double* ms, int* count) {
 
 // ---- dimension tree (mttkrp.cpp:160-189) -----------------------------------
 void DeviceProblem::root_back() {
+    NvtxRange nvtx_range("cpkit:root_back");
     const int N = order();
     prof_begin(kProfBack);
     launch_root_back(x_.get(), F_, Bl_, Bs_, R_, krp(h_, N, A_.get(), true), krp_.get(), PF_.get(), ws_.get(),
@@ -947,6 +951,7 @@ void DeviceProblem::root_back() {
     pf_valid_ = true;
 }
 void DeviceProblem::root_front() {
+    NvtxRange nvtx_range("cpkit:root_front");
     prof_begin(kProfFront);
     if (front_copy_)  // P_B = X^T KRP_F on the transposed copy: the back root's NN GEMM
         launch_root_back(XT_.get(), Bl_, F_, ldT_, R_, krp(0, h_, A_.get(), false), krp_.get(), PB_.get(), ws_.get(),
@@ -1006,6 +1011,7 @@ void DeviceProblem::second_level_front(int mode) {
 // Khatri-Rao operand. Each M^(n) is the same sum as the reference tree's, in
 // a different association order (roundoff-level differences).
 void DeviceProblem::root_single(int c) {
+    NvtxRange nvtx_range("cpkit:root_single");
     prof_begin(kProfFront);
     if (msdt_copies_) {
         // P_c = X^(c) A_c: rows (other kept index pairs), the back root's NN GEMM
@@ -1276,6 +1282,7 @@ void DeviceProblem::launch_precond_chain(double lambda, RegShape shape, bool gra
     CPK_CUDA(cudaEventRecord(ctx_.ev[1], ctx_.aux));
 }
 void DeviceProblem::build_preconditioner(double lambda, RegShape shape) {
+    NvtxRange nvtx_range("cpkit:build_preconditioner");
     if (lambda < 0) throw InvalidArgument("build_preconditioner: lambda must be nonnegative");
     if (!precond_pending_ || precond_lambda_ != lambda || precond_shape_ != shape)
         launch_preconditioner_factor(lambda, shape);
@@ -1298,6 +1305,7 @@ CgParams base_params(int N, int R, const std::vector<std::uint64_t>& dims, const
 }  // namespace
 
 void DeviceProblem::jtj_matvec(const double* dev_w, double* dev_u, double lambda, RegShape shape) {
+    NvtxRange nvtx_range("cpkit:jtj_matvec");
     CgParams p = base_params(order(), R_, dims_, off_);
     p.A = A_.get();
     p.pair = pair_.get();
@@ -1314,6 +1322,7 @@ void DeviceProblem::jtj_matvec(const double* dev_w, double* dev_u, double lambda
 
 // gauss_newton.cpp:279-349; G must hold the gradient. Result in V.
 CgResultInfo DeviceProblem::cp_cg(double lambda, const GnConfig& cfg, double gnorm_in) {
+    NvtxRange nvtx_range("cpkit:cp_cg");
     const int N = order();
     const RegShape shape = cfg.schedule.shape;
     int cap = cfg.cg_max_iters;
@@ -1463,6 +1472,7 @@ void DeviceProblem::als_restore_factors() {
 }
 
 void DeviceProblem::als_sweep_launch(double lambda, bool with_residual) {
+    NvtxRange nvtx_range("cpkit:als_sweep");
     const int N = order();
     while (static_cast<int>(pending_.size()) >= kSweepSlots - 1) done_.push_back(complete_oldest());
     // CUDA graph: one capture per (lambda, cache state, profiling); replays skip
@@ -1603,6 +1613,7 @@ GnStepDiag DeviceProblem::gn_step(const GnConfig& cfg, RegSchedule& schedule, do
 // area, the pre-step snapshot and the completion event, so that two steps can
 // be in flight (gn_optimize queues step k+1 before reading step k).
 void DeviceProblem::gn_enqueue(const GnConfig& cfg, const RegSchedule& schedule, double xnorm2, int slot) {
+    NvtxRange nvtx_range("cpkit:gn_step");
     const int N = order();
     const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
     // [res, fit, (step slot), gnorm | status N | cg 5 | step, fin | res_after, fit_after]
@@ -1754,6 +1765,7 @@ GnStepDiag DeviceProblem::gn_decode(const GnConfig& cfg, double lambda, int slot
 
 
 GnStepDiag DeviceProblem::gn_step_sync(const GnConfig& cfg, RegSchedule& schedule, double xnorm2) {
+    NvtxRange nvtx_range("cpkit:gn_step_sync");
     const int N = order();
     const std::uint64_t S = static_cast<std::uint64_t>(off_[N]);
     GnStepDiag diag;
