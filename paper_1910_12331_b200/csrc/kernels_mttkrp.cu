@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(root_max_threads(MAXC), 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int BN, int W,
                  int BNS, int stages, long long k_per_split, int splits, double* __restrict__ out,
-                 long long out_split_stride, int brel) {
+                 long long out_split_stride, int brel, int sk, double* __restrict__ sk_ws) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
@@ -285,6 +285,50 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         const long long kend = min(K, kbeg + k_per_split);
         nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
     };
+
+    // Stream-K mode (sk; one rank tile, no k split): the (row tile, k block)
+    // space, tile-major, is cut into gridDim.x equal contiguous ranges, so
+    // every CTA does the same number of k blocks whatever the tile count (no
+    // partial last wave, no separate tail launch). A CTA's range is a run of
+    // segments, one per tile it touches: a segment covering a whole tile goes
+    // straight to the output; a tile shared by two or more CTAs leaves partial
+    // tiles in sk_ws (slot 2 c for the segment of CTA c that starts inside a
+    // tile, 2 c + 1 for the one that starts a tile and ends inside it), summed
+    // in CTA (= k) order by streamk_fixup_kernel: deterministic.
+    const long long kblocks = (K + kBK - 1) / kBK;
+    const long long sk_total = mtiles * kblocks;
+    const long long sk_lo = sk ? sk_total * blockIdx.x / gridDim.x : 0;
+    const long long sk_hi = sk ? sk_total * (blockIdx.x + 1) / gridDim.x : 0;
+    struct Unit {
+        int n0, nk;
+        long long m0, kbeg, kend;
+        double* o;
+    };
+    auto next_unit = [&](long long& cur, Unit& un) -> bool {
+        if (!sk) {
+            if (cur >= units) return false;
+            int split;
+            unit_geom(cur, un.n0, un.m0, un.kbeg, un.nk, split);
+            un.kend = min(K, un.kbeg + k_per_split);
+            un.o = out + split * out_split_stride;
+            cur += gridDim.x;
+            return true;
+        }
+        if (cur >= sk_hi) return false;
+        const long long tile = cur / kblocks, kb0 = cur - tile * kblocks;
+        const long long len = min(kblocks - kb0, sk_hi - cur);
+        un.n0 = 0;
+        un.m0 = tile * BM;
+        un.kbeg = kb0 * kBK;
+        un.kend = min(K, (kb0 + len) * kBK);
+        un.nk = static_cast<int>(len);
+        un.o = (kb0 == 0 && len == kblocks)
+                   ? out
+                   : sk_ws + (2 * static_cast<long long>(blockIdx.x) + (kb0 != 0 ? 0 : 1)) * BM * R - un.m0 * R;
+        cur += len;
+        return true;
+    };
+    const long long cur0 = sk ? sk_lo : static_cast<long long>(blockIdx.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -353,10 +397,11 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         // C2 root's stall samples sat on it)
         int ring = -1;
         unsigned lap = 1;  // parity of (it / stages)
-        for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-            int n0, nk, split;
-            long long m0, kbeg;
-            unit_geom(u, n0, m0, kbeg, nk, split);
+        long long cur = cur0;
+        Unit un;
+        while (next_unit(cur, un)) {
+            const int n0 = un.n0, nk = un.nk;
+            const long long m0 = un.m0, kbeg = un.kbeg;
             for (int kt = 0; kt < nk; ++kt, ++it) {
                 if (++ring == stages) ring = 0;
                 if (ring == 0) lap ^= 1u;
@@ -454,15 +499,16 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         constexpr bool SPAN = decltype(span_tag)::value;
         int ring = -1;      // ring slot of the current stage and the parity of its lap,
         unsigned lap = 1;   // kept incrementally (no per-stage integer division)
-        for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-            int n0, nk, split;
-            long long m0, kbeg;
-            unit_geom(u, n0, m0, kbeg, nk, split);
+        long long cur = cur0;
+        Unit un;
+        while (next_unit(cur, un)) {
+            const int n0 = un.n0, nk = un.nk;
+            const long long m0 = un.m0, kbeg = un.kbeg;
             double acc[C][4];
 #pragma unroll
             for (int j = 0; j < C; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
             // the unit's last stage holds only 16 valid k (see half_stage below)
-            const bool last_half = min(K, kbeg + k_per_split) - (kbeg + static_cast<long long>(nk - 1) * kBK) <= 16;
+            const bool last_half = un.kend - (kbeg + static_cast<long long>(nk - 1) * kBK) <= 16;
 
             for (int kt = 0; kt < nk; ++kt) {
                 if (++ring == stages) ring = 0;
@@ -508,7 +554,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
 
             // epilogue (overlaps the producer's loads for the next unit):
             // rows m0+16(r0 | r0+1)+g(+8), cols n0+8(cell column)+2t(+1); 16-byte stores when aligned
-            double* o = out + split * out_split_stride;
+            double* o = un.o;
 #pragma unroll
             for (int j = 0; j < C; ++j) {
                 const bool first_row = !SPAN || j < n1;
@@ -674,6 +720,43 @@ __global__ void splitk_reduce_kernel(const double* __restrict__ ws, int splits, 
         double s = 0.0;
         for (int k = 0; k < splits; ++k) s += ws[k * n + i];  // fixed order: deterministic
         out[i] = s;
+    }
+}
+
+// A tile is shared by at most ctas / mtiles + 2 CTAs (plan_streamk checks the bound).
+constexpr int kStreamKMaxPieces = 192;
+// Stream-K fix-up (root_gemm_kernel, sk mode): block c - 1 looks at the range
+// boundary between CTAs c - 1 and c. When it falls inside a row tile and is the
+// first boundary inside that tile, the block sums the tile's partial slots in
+// CTA (= k) order and writes the tile's output rows.
+__global__ void __launch_bounds__(256) streamk_fixup_kernel(const double* __restrict__ ws, double* __restrict__ out,
+                                                            long long M, int R, int BM, long long mtiles,
+                                                            long long kblocks, int G) {
+    const long long T = mtiles * kblocks;
+    const int c = static_cast<int>(blockIdx.x) + 1;
+    const long long b = T * c / G;
+    if (b % kblocks == 0) return;
+    const long long t = b / kblocks, t_lo = t * kblocks, t_hi = t_lo + kblocks;
+    if (T * (c - 1) / G > t_lo) return;  // an earlier boundary is inside the same tile: that block sums it
+    __shared__ int slots[kStreamKMaxPieces];
+    __shared__ int nslots;
+    if (threadIdx.x == 0) {
+        int n = 0;
+        for (int j = c - 1; j < G && n < kStreamKMaxPieces; ++j) {
+            const long long lo = T * j / G;
+            if (lo >= t_hi) break;
+            slots[n++] = 2 * j + (lo > t_lo ? 0 : 1);
+        }
+        nslots = n;
+    }
+    __syncthreads();
+    const long long rows = min(static_cast<long long>(BM), M - t * BM);
+    const long long n = rows * R, slab = static_cast<long long>(BM) * R;
+    double* o = out + t * BM * R;
+    for (long long e = threadIdx.x; e < n; e += blockDim.x) {
+        double v = 0.0;
+        for (int q = 0; q < nslots; ++q) v += ws[slots[q] * slab + e];
+        o[e] = v;
     }
 }
 
@@ -960,12 +1043,14 @@ GemmPlan plan_gemm(long long M, long long K, int R, bool trans, long long fixed_
 
 template <bool TRANS, bool GEN>
 void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const CUtensorMap& kmap, const KrpDev& kd,
-              long long M, long long K, int R, double* out, long long oss, int brel = 0, long long max_ctas = 0) {
+              long long M, long long K, int R, double* out, long long oss, int brel = 0, long long max_ctas = 0,
+              double* sk_ws = nullptr) {
     const std::size_t smem = smem_bytes(p);
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
     long long cap = static_cast<long long>(num_sms()) * p.per_sm;
     if (max_ctas > 0) cap = std::min(cap, max_ctas);
-    dim3 grid(static_cast<unsigned>(std::min<long long>(units, cap)));
+    const int sk = sk_ws != nullptr ? 1 : 0;  // stream-K: exactly max_ctas CTAs share the k blocks
+    dim3 grid(static_cast<unsigned>(sk ? cap : std::min<long long>(units, cap)));
     const dim3 block(32 * (p.nw + 1));
     if (!TRANS && !GEN && p.m8) {
 #define CPK_M8(NCV)                                                                                     \
@@ -998,7 +1083,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
             grid.x = static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * std::max(occ, 1))); \
         }                                                                                          \
         fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.BN(), p.nw, p.bns, p.stages, p.kps,  \
-                                      p.splits, out, oss, brel);                                   \
+                                      p.splits, out, oss, brel, sk, sk_ws);                        \
         break;                                                                                     \
     }
     switch (p.maxc) {
@@ -1064,8 +1149,51 @@ BackSplit plan_back(long long M, long long K, int R, int reserve_sms) {
     return b;
 }
 
+// Stream-K plan for an NN root (launch_root_back): the unsplit plan's tile on
+// exactly (SMs - reserve) CTAs. Used when the row tiles do not fill one wave
+// (the case that otherwise needs a k split into full-size slabs);
+// CPKIT_NO_STREAMK=1 keeps that.
+struct StreamK {
+    bool on = false;
+    GemmPlan plan{};
+    int ctas = 0;
+    std::size_t ws_elems = 0;
+};
+StreamK plan_streamk(long long M, long long K, int R, int reserve_sms) {
+    StreamK sk;
+    static const bool off = std::getenv("CPKIT_NO_STREAMK") != nullptr;
+    if (off) return sk;
+    GemmPlan p = plan_gemm(M, K, R, false);
+    if (p.m8 || p.ntiles != 1 || p.per_sm != 1) return sk;
+    const int ctas = num_sms() - reserve_sms;
+    const long long kblocks = (K + kBK - 1) / kBK;
+    if (ctas < 2) return sk;
+    // Measured: it pays where the unsplit plan has fewer row tiles than CTAs and
+    // would otherwise split k into full-size slabs (C4: 79 tiles, ALS sweep
+    // 0.860 -> 0.845 ms). With several waves of tiles the tail launch stays: at
+    // C5s the root alone gains (18.15 -> 17.97 ms) but inside a sweep, where one
+    // SM is left to the side-stream factorisation during the whole launch
+    // instead of only during the full waves, the sweep loses (36.53 -> 36.64 ms);
+    // short contractions lose outright (C2, 13 k blocks per tile: nearly every
+    // CTA ends inside a tile, back root 457 vs 408 us).
+    if (p.splits < 2 || kblocks < 128) return sk;
+    if (p.mtiles * kblocks < 8LL * ctas) return sk;               // under 8 k blocks per CTA: too little to cut
+    if (ctas / p.mtiles + 2 > kStreamKMaxPieces) return sk;        // the fix-up's piece list
+    p.splits = 1;
+    p.kps = kblocks * kBK;
+    sk.on = true;
+    sk.plan = p;
+    sk.ctas = ctas;
+    sk.ws_elems = 2ull * static_cast<std::size_t>(num_sms()) * p.BM() * R;
+    if (std::getenv("CPKIT_PLAN_DEBUG"))
+        std::fprintf(stderr, "plan stream-K NN M=%lld K=%lld R=%d: %d row tiles x %lld k blocks over %d CTAs\n", M, K, R,
+                     p.mtiles, kblocks, ctas);
+    return sk;
+}
+
 }  // namespace
 
+std::size_t root_back_workspace_elems_classic(std::int64_t F, std::int64_t B, int R);
 std::size_t krp_workspace_elems(std::int64_t rows, int R) {
     return static_cast<std::size_t>(rows) * ((R + 1) & ~1);
 }
@@ -1074,6 +1202,25 @@ std::size_t krp_workspace_elems(std::int64_t rows, int R) {
 void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int64_t Bs, int R,
                       const KrpDesc& kb, double* krp, double* pf, double* ws, std::size_t ws_elems,
                       cudaStream_t st, int reserve_sms) {
+    {  // stream-K: one launch, every CTA the same number of k blocks
+        StreamK sk = plan_streamk(F, B, R, reserve_sms);
+        if (sk.on && ws_elems >= sk.ws_elems) {
+            const int Rs = (R + 1) & ~1;
+            const bool direct = kb.nmodes == 1 && R % 2 == 0;
+            if (!direct) fill_krp(kb, B, R, krp, st);
+            const CUtensorMap xmap = make_map(x, static_cast<std::uint64_t>(Bs), static_cast<std::uint64_t>(F), 16,
+                                              static_cast<std::uint32_t>(sk.plan.BM()), true);
+            const CUtensorMap kmap = make_map(direct ? kb.fac[0] : krp, static_cast<std::uint64_t>(Rs),
+                                              static_cast<std::uint64_t>(B), static_cast<std::uint32_t>(sk.plan.bns),
+                                              kBK, false);
+            dispatch<false, false>(sk.plan, st, xmap, kmap, to_dev(kb), F, B, R, pf, 0, 0, sk.ctas, ws);
+            streamk_fixup_kernel<<<sk.ctas - 1, 256, 0, st>>>(ws, pf, F, R, sk.plan.BM(), sk.plan.mtiles,
+                                                              (B + kBK - 1) / kBK, sk.ctas);
+            count_launch(1);
+            CPK_CUDA(cudaGetLastError());
+            return;
+        }
+    }
     const BackSplit bs = plan_back(F, B, R, reserve_sms);
     if (bs.rows_main < F &&
         (bs.tail.splits < 2 || ws_elems >= static_cast<std::size_t>(bs.tail.splits) * (F - bs.rows_main) * R)) {
@@ -1138,6 +1285,9 @@ void launch_root_back(const double* x, std::int64_t F, std::int64_t B, std::int6
 }
 
 std::size_t root_back_workspace_elems(std::int64_t F, std::int64_t B, int R) {
+    return std::max(root_back_workspace_elems_classic(F, B, R), plan_streamk(F, B, R, 0).ws_elems);
+}
+std::size_t root_back_workspace_elems_classic(std::int64_t F, std::int64_t B, int R) {
     std::size_t w = 0;
     for (int reserve = 0; reserve <= 1; ++reserve) {
         const BackSplit bs = plan_back(F, B, R, reserve);

@@ -659,6 +659,47 @@ def test_decompose_overlapped_first_root(ck, dims, optimizer):
 
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# Back roots with fewer row tiles than SMs and a long contraction run as one
+# stream-K launch (every CTA an equal run of k blocks; tiles shared by several
+# CTAs summed in fixed k order by the fix-up kernel) instead of a k split into
+# full-size slabs. Against the oracle, bitwise repeatable, and against the
+# classic split-K path (CPKIT_NO_STREAMK=1; env read once per process).
+@pytest.mark.parametrize("dims,rank", [([30, 40, 70, 64], 24), ([1000, 5000], 50), ([30, 31, 4500], 77)])
+def test_root_stream_k(orc, ck, dims, rank, tmp_path):
+    import subprocess
+    import sys
+    x = np.random.default_rng(rank + 1).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 23)
+    ref, _ = orc.mttkrp_tree_all(x, f)
+    np.save(tmp_path / "x.npy", x)
+    np.save(tmp_path / "f.npy", np.concatenate([a.ravel() for a in f]))
+    code = f"""
+import sys, numpy as np
+sys.path.insert(0, {repr(str(ROOT))})
+from paper_1910_12331_b200 import cpkit
+x = np.load({repr(str(tmp_path / 'x.npy'))}); flat = np.load({repr(str(tmp_path / 'f.npy'))})
+dims, R = {dims!r}, {rank}
+f, at = [], 0
+for d in dims:
+    f.append(flat[at:at + d * R].reshape(d, R)); at += d * R
+p = cpkit.DeviceProblem(dims, R); p.upload(x); p.set_factors(f)
+a = p.mttkrp_naive(0)
+assert np.array_equal(a, p.mttkrp_naive(0))
+np.save(sys.argv[1], a)
+"""
+    outs = {}
+    for tag, env_add in (("sk", {"CPKIT_PLAN_DEBUG": "1"}), ("classic", {"CPKIT_PLAN_DEBUG": "1", "CPKIT_NO_STREAMK": "1"})):
+        r = subprocess.run([sys.executable, "-c", code, str(tmp_path / f"{tag}.npy")], env=dict(os.environ, **env_add),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert ("plan stream-K" in r.stderr) == (tag == "sk"), r.stderr[-2000:]
+        outs[tag] = np.load(tmp_path / f"{tag}.npy")
+    assert rel_err(outs["sk"], ref[0]) < KTOL
+    assert rel_err(outs["sk"], outs["classic"]) < 1e-13
+
+
 M8_CASES = [([30, 28, 26, 24], 200), ([40, 36, 34], 120), ([400, 50, 40], 200)]
 
 
