@@ -251,12 +251,12 @@ __host__ __device__ constexpr int root_max_threads(int maxc) { return maxc >= 9 
 // (MAXC - 1) cells, the longer run alternating so that each SM sub-partition
 // (warps w and w + 4) carries exactly NT8 cells: no rank padding and no run
 // crossing an m16 row (R = 200: 13 + 12 of 25 cells).
-template <int MAXC, bool TRANS, bool GEN, bool FULL, bool RS = false>
+template <int MAXC, bool TRANS, bool GEN, bool FULL, bool RS = false, bool SK = false>
 __global__ void __launch_bounds__(root_max_threads(MAXC), 1)
 root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap kmap,
                  const __grid_constant__ KrpDev kd, long long M, long long K, int R, int BM, int BN, int W,
                  int BNS, int stages, long long k_per_split, int splits, double* __restrict__ out,
-                 long long out_split_stride, int brel, int sk, double* __restrict__ sk_ws) {
+                 long long out_split_stride, int brel, double* __restrict__ sk_ws) {
     extern __shared__ __align__(1024) char smem_raw[];
     const std::uint32_t raw = smem_u32(smem_raw);
     const std::uint32_t base = raw + ((1024u - (raw & 1023u)) & 1023u);  // 1024-B aligned (swizzle atom)
@@ -286,7 +286,8 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
     };
 
-    // Stream-K mode (sk; one rank tile, no k split): the (row tile, k block)
+    // Stream-K mode (template SK: a separate instantiation, so the classic
+    // kernels carry none of this; one rank tile, no k split): the (row tile, k block)
     // space, tile-major, is cut into gridDim.x equal contiguous ranges, so
     // every CTA does the same number of k blocks whatever the tile count (no
     // partial last wave, no separate tail launch). A CTA's range is a run of
@@ -297,15 +298,15 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     // in CTA (= k) order by streamk_fixup_kernel: deterministic.
     const long long kblocks = (K + kBK - 1) / kBK;
     const long long sk_total = mtiles * kblocks;
-    const long long sk_lo = sk ? sk_total * blockIdx.x / gridDim.x : 0;
-    const long long sk_hi = sk ? sk_total * (blockIdx.x + 1) / gridDim.x : 0;
+    const long long sk_lo = SK ? sk_total * blockIdx.x / gridDim.x : 0;
+    const long long sk_hi = SK ? sk_total * (blockIdx.x + 1) / gridDim.x : 0;
     struct Unit {
         int n0, nk;
         long long m0, kbeg, kend;
         double* o;
     };
     auto next_unit = [&](long long& cur, Unit& un) -> bool {
-        if (!sk) {
+        if (!SK) {
             if (cur >= units) return false;
             int split;
             unit_geom(cur, un.n0, un.m0, un.kbeg, un.nk, split);
@@ -328,7 +329,7 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
         cur += len;
         return true;
     };
-    const long long cur0 = sk ? sk_lo : static_cast<long long>(blockIdx.x);
+    const long long cur0 = SK ? sk_lo : static_cast<long long>(blockIdx.x);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -1076,6 +1077,9 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
         auto fn = (!TRANS && !GEN && p.rs) ? root_gemm_kernel<NTV, TRANS, GEN, false, !TRANS && !GEN> \
                   : runs_full(p)           ? root_gemm_kernel<NTV, TRANS, GEN, true>              \
                                            : root_gemm_kernel<NTV, TRANS, GEN, false>;             \
+        if (sk) /* stream-K instantiations exist for the NN kernel without RS only (plan_streamk) */ \
+            fn = runs_full(p) ? root_gemm_kernel<NTV, TRANS, GEN, true, false, !TRANS && !GEN>     \
+                              : root_gemm_kernel<NTV, TRANS, GEN, false, false, !TRANS && !GEN>;   \
         ensure_dynamic_smem(fn, smem);                                                             \
         if (std::getenv("CPKIT_GRID_OCC")) { /* experiments: grid from the real occupancy */        \
             int occ = 1;                                                                           \
@@ -1083,7 +1087,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
             grid.x = static_cast<unsigned>(std::min<long long>(units, static_cast<long long>(num_sms()) * std::max(occ, 1))); \
         }                                                                                          \
         fn<<<grid, block, smem, st>>>(xmap, kmap, kd, M, K, R, p.BM(), p.BN(), p.nw, p.bns, p.stages, p.kps,  \
-                                      p.splits, out, oss, brel, sk, sk_ws);                        \
+                                      p.splits, out, oss, brel, sk_ws);                            \
         break;                                                                                     \
     }
     switch (p.maxc) {
@@ -1164,7 +1168,7 @@ StreamK plan_streamk(long long M, long long K, int R, int reserve_sms) {
     static const bool off = std::getenv("CPKIT_NO_STREAMK") != nullptr;
     if (off) return sk;
     GemmPlan p = plan_gemm(M, K, R, false);
-    if (p.m8 || p.ntiles != 1 || p.per_sm != 1) return sk;
+    if (p.m8 || p.rs || p.ntiles != 1 || p.per_sm != 1) return sk;
     const int ctas = num_sms() - reserve_sms;
     const long long kblocks = (K + kBK - 1) / kBK;
     if (ctas < 2) return sk;
