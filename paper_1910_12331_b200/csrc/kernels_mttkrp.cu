@@ -276,11 +276,16 @@ root_gemm_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     const int ntiles = (R + BN - 1) / BN;
     const long long mtiles = (M + BM - 1) / BM;
     const long long units = static_cast<long long>(ntiles) * mtiles * splits;
+    // (32-bit divisions: a 64-bit division by a runtime value is a long
+    // subroutine, paid per unit by every warp; the host keeps units < 2^31)
+    const unsigned mtiles32 = static_cast<unsigned>(mtiles), ntiles32 = static_cast<unsigned>(ntiles);
     auto unit_geom = [&](long long u, int& n0, long long& m0, long long& kbeg, int& nk, int& split) {
-        n0 = static_cast<int>(u % ntiles) * BN;
-        const long long rest = u / ntiles;
-        m0 = (rest % mtiles) * BM;
-        split = static_cast<int>(rest / mtiles);
+        const unsigned uu = static_cast<unsigned>(u);
+        const unsigned rest = ntiles32 == 1 ? uu : uu / ntiles32;
+        n0 = ntiles32 == 1 ? 0 : static_cast<int>(uu - rest * ntiles32) * BN;
+        const unsigned sp = rest / mtiles32;
+        m0 = static_cast<long long>(rest - sp * mtiles32) * BM;
+        split = static_cast<int>(sp);
         kbeg = static_cast<long long>(split) * k_per_split;
         const long long kend = min(K, kbeg + k_per_split);
         nk = static_cast<int>((kend - kbeg + kBK - 1) / kBK);
@@ -1050,6 +1055,7 @@ void dispatch(const GemmPlan& p, cudaStream_t st, const CUtensorMap& xmap, const
     const long long units = static_cast<long long>(p.ntiles) * p.mtiles * p.splits;
     long long cap = static_cast<long long>(num_sms()) * p.per_sm;
     if (max_ctas > 0) cap = std::min(cap, max_ctas);
+    if (units >= (1LL << 31)) throw DeviceError("root GEMM: too many tile units");  // 32-bit unit indices in the kernel
     const int sk = sk_ws != nullptr ? 1 : 0;  // stream-K: exactly max_ctas CTAs share the k blocks
     dim3 grid(static_cast<unsigned>(sk ? cap : std::min<long long>(units, cap)));
     const dim3 block(32 * (p.nw + 1));
