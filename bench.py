@@ -426,7 +426,7 @@ def run_b200(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference keyed RNG, generated on device; bit-identical to the CPU arm's tensor)",
             "config": workload_config(key, world),
-            "roofline": {"bound": "tensor", "kernel": "root MTTKRP GEMM (TMA + FP64 DMMA: m16n8k16 runs, or m8n8k4 strips when the rank has an odd n8-cell count, e.g. R=200)",
+            "roofline": {"bound": "tensor", "kernel": "root MTTKRP GEMM root_gemm_kernel (TMA-staged tiles + FP64 DMMA m16n8k16; R=200: row-split dealing of 25 n8 cells as 13 + 12, no rank padding; main launch + k-split tail launch)",
                          "achieved": achieved_tf, "peak": peak_dmma, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_dmma,
                          "peak_source": "FP64 DMMA issue-rate probe measured in this run "
