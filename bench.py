@@ -289,6 +289,16 @@ def gn_rate(p, init, steps=3, reps=3):
                                       "state: the start's tree pass cached before timing"}
 
 
+def second_level_line(p, hbm):
+    """The second dimension-tree level (mttkrp.cpp:63-75) on the cached back-root partial: an
+    HBM-bound pass over 8 |P| bytes when the partial exceeds the L2."""
+    ms, nbytes = p.time_second_level(20)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"ms": ms, "gbs": gbs, "hbm_frac": gbs / hbm, "bytes": nbytes,
+            "note": "reduce of the root partial into M^(0)" +
+                    ("" if nbytes > 126e6 else "; the partial fits the 126 MB L2 (not an HBM measurement)")}
+
+
 def run_b200(args, rank, world, local_rank):
     from paper_1910_12331_b200 import cpkit
     cpkit.load()
@@ -361,6 +371,7 @@ def run_b200(args, rank, world, local_rank):
     gn = gn_rate(p, init)
     S = sum(dims)
     jtj_ms = p.time_jtj(50)
+    second_level = second_level_line(p, hbm) if world == 1 else None
     jtj_bytes = 8.0 * (3 * R * S + len(dims) * (len(dims) + 1) / 2 * R * R)
     nrm_ms = p.time_norm2(5)
     nrm_gbs = 8.0 * local_elems / (nrm_ms * 1e-3) / 1e9
@@ -442,6 +453,7 @@ def run_b200(args, rank, world, local_rank):
                                "note": "L2-resident working set: latency-bound"},
                 "norm2": {"ms": nrm_ms, "gbs": nrm_gbs, "hbm_frac": nrm_gbs / hbm, "bytes": 8.0 * local_elems,
                           "peak_gbs": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                "second_level": second_level,
             },
             "e2e": e2e,
             "final_residual": final_res,
@@ -453,7 +465,7 @@ def run_b200(args, rank, world, local_rank):
         result["cpu_baseline"] = cpu_baseline_sample(x_host.reshape(dims), init, key)
     del x_host
     if rank == 0 and world == 1 and not args.no_c2 and key != "c2":
-        result["c2"] = c2_line(cpkit, peak_dmma)
+        result["c2"] = c2_line(cpkit, peak_dmma, hbm)
     if world > 1 and not args.no_c5:
         c5 = c5_line(cpkit, rank, world, local_rank, nccl_id, peak_dmma, barrier, max_over_ranks)
         if rank == 0:
@@ -465,7 +477,7 @@ def run_b200(args, rank, world, local_rank):
     return 0
 
 
-def c2_line(cpkit, peak):
+def c2_line(cpkit, peak, hbm):
     """BASELINE configs[1] (C2) beside the headline: ALS sweeps/s, GN iterations/s
     and the root GEMM's fraction of the DMMA peak (device-resident)."""
     w = WORKLOADS["c2"]
@@ -479,9 +491,10 @@ def c2_line(cpkit, peak):
     root_ms = (pm[0] + pm[1]) / max(1, pc[0] + pc[1])
     tf = 2.0 * R * np.prod(dims) / (root_ms * 1e-3) / 1e12
     gn = gn_rate(q, init, steps=4)
+    second = second_level_line(q, hbm)
     q.close()
     return {"workload": w["name"], "als_sweeps_per_s": 50 / (ms * 1e-3), "als_ms_per_sweep": ms / 50,
-            "root_tflops": tf, "root_frac_of_peak": tf / peak, "gn": gn,
+            "root_tflops": tf, "root_frac_of_peak": tf / peak, "gn": gn, "second_level": second,
             "note": "order 3: multi-sweep dimension tree (3 root contractions per 2 sweeps), 50 sweeps timed"}
 
 

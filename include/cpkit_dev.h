@@ -132,6 +132,9 @@ CPKIT_API cpkit_status cpkit_dev_profile_read(cpkit_dev_problem* p, double* ms3,
 CPKIT_API cpkit_status cpkit_dev_time_jtj(cpkit_dev_problem* p, int reps, double* ms);
 /* reps x ||X||^2 streaming pass; average ms. */
 CPKIT_API cpkit_status cpkit_dev_time_norm2(cpkit_dev_problem* p, int reps, double* ms);
+/* reps x the second dimension-tree level (mttkrp.cpp:63-75: M^(0) from the cached
+ * back-root partial, an HBM-bound pass); average ms and the partial's bytes. */
+CPKIT_API cpkit_status cpkit_dev_time_second_level(cpkit_dev_problem* p, int reps, double* ms, double* bytes);
 /* FP64 DMMA issue-rate probe on `device`, TFLOP/s (roofline denominator). */
 CPKIT_API cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops);
 /* `steps` gn_step calls (one schedule from the config); total ms and the

@@ -45,7 +45,7 @@ CPKIT_DEV_SYMBOLS = (
     "cpkit_dev_spd_inverse", "cpkit_dev_als_sweep", "cpkit_dev_gn_step", "cpkit_dev_optimize",
     "cpkit_dev_time_als_sweeps", "cpkit_dev_time_roots", "cpkit_dev_profile",
     "cpkit_dev_profile_read", "cpkit_dev_time_jtj",
-    "cpkit_dev_time_norm2", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
+    "cpkit_dev_time_norm2", "cpkit_dev_time_second_level", "cpkit_dev_probe_dmma_peak", "cpkit_dev_kernel_launches",
     "cpkit_dev_guard_violations", "cpkit_dev_guard_selftest",
     "cpkit_dev_time_gn_steps", "cpkit_dev_random_factors", "cpkit_dev_problem_seed",
     "cpkit_dev_init_seed", "cpkit_dev_download_tensor", "cpkit_dev_shard_range",
@@ -567,6 +567,13 @@ class DeviceProblem:
         ms = C.c_double()
         _chk(load().cpkit_dev_time_norm2(self._h, reps, C.byref(ms)))
         return ms.value
+
+
+    def time_second_level(self, reps: int):
+        """(ms per pass, bytes of the back-root partial) of the second tree level, mode 0."""
+        ms, nbytes = C.c_double(), C.c_double()
+        _chk(load().cpkit_dev_time_second_level(self._h, reps, C.byref(ms), C.byref(nbytes)))
+        return ms.value, nbytes.value
 
 
 def nccl_unique_id() -> bytes:

@@ -1985,6 +1985,10 @@ cpkit_status cpkit_dev_time_norm2(cpkit_dev_problem* p, int reps, double* ms) {
         *ms = ev.ms() / reps;
     });
 }
+cpkit_status cpkit_dev_time_second_level(cpkit_dev_problem* p, int reps, double* ms, double* bytes) {
+    DEV_REQ(p && ms && bytes && reps > 0);
+    return guarded([&] { *ms = p->p->time_second_level(reps, bytes); });
+}
 cpkit_status cpkit_dev_probe_dmma_peak(int device, double* tflops) {
     DEV_REQ(tflops);
     return guarded([&] { *tflops = cpkit::probe_dmma_peak(device); });

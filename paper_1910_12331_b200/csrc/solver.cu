@@ -978,6 +978,24 @@ void DeviceProblem::second_level_back(int mode, cudaStream_t st, double* ws, std
     }
     if (ctx_.comm && !defer_coll_) ctx_.comm->allreduce_sum(out, static_cast<std::size_t>(dims_[mode]) * R_, st);
 }
+double DeviceProblem::time_second_level(int reps, double* bytes) {
+    if (!pf_valid_) root_back();
+    second_level_back(0);  // warm-up
+    cudaEvent_t a, b;
+    CPK_CUDA(cudaEventCreate(&a));
+    CPK_CUDA(cudaEventCreate(&b));
+    CPK_CUDA(cudaEventRecord(a, ctx_.stream));
+    for (int i = 0; i < reps; ++i) second_level_back(0);
+    CPK_CUDA(cudaEventRecord(b, ctx_.stream));
+    CPK_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CPK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    m_all_valid_ = false;  // M^(0) was rewritten outside the cache bookkeeping
+    if (bytes) *bytes = 8.0 * static_cast<double>(F_) * R_;
+    return static_cast<double>(ms) / reps;
+}
 void DeviceProblem::second_level_front(int mode) {
     const int N = order();
     const bool last = (mode == N - 1);

@@ -248,6 +248,9 @@ public:
 
     // ---- reference seams
     double norm2();                                   // ||X||^2 (tensor.cpp:61-67)
+    // reps x the second tree level (mttkrp.cpp:63-75) on the cached back-root partial, mode 0:
+    // average ms per pass; *bytes = the partial's size (the pass's compulsory HBM traffic)
+    double time_second_level(int reps, double* bytes);
     void mttkrp(int mode);                            // tree, into M block (mttkrp.cpp:160-189)
     void mttkrp_naive(int mode);                      // uncached, same kernels
     void note_factor_update(int mode);                // mttkrp.cpp:136-145
