@@ -253,7 +253,7 @@ def throttled(clocks):
     return clocks["sm_mhz"] < 0.9 * clocks["sm_max_mhz"] and not clocks.get("reasons")
 
 
-def timed_sweeps(p, init, steps, warmup, clocks_device=None):
+def timed_sweeps(p, init, steps, warmup, clocks_device=None, profile=True):
     from paper_1910_12331_b200 import cpkit
     sampler = ClockSampler(clocks_device) if clocks_device is not None else None
     if sampler:
@@ -262,10 +262,12 @@ def timed_sweeps(p, init, steps, warmup, clocks_device=None):
         p.time_als_sweeps(0.0, max(1, warmup))
         p.set_factors(init)
         launches0 = cpkit.kernel_launches()
-        p.profile(True)
+        if profile:
+            p.profile(True)
         ms = p.time_als_sweeps(0.0, steps)
-        prof_ms, prof_cnt = p.profile_read()
-        p.profile(False)
+        prof_ms, prof_cnt = p.profile_read() if profile else ([0.0] * 3, [0] * 3)
+        if profile:
+            p.profile(False)
         launches = cpkit.kernel_launches() - launches0
     finally:
         if sampler:
@@ -487,7 +489,10 @@ def c2_line(cpkit, peak, hbm):
     q = cpkit.DeviceProblem(dims, R)
     q.generate(truth, 1, w["noise"])
     q.set_factors(init)
-    ms, pm, pc, _, _ = timed_sweeps(q, init, 50, 5)
+    # two passes: the per-root event pairs cost ~4 % of a 0.8 ms sweep, so the
+    # sweep rate is timed without them and the root time with them
+    _, pm, pc, _, _ = timed_sweeps(q, init, 50, 5)
+    ms, _, _, _, _ = timed_sweeps(q, init, 50, 5, profile=False)
     root_ms = (pm[0] + pm[1]) / max(1, pc[0] + pc[1])
     tf = 2.0 * R * np.prod(dims) / (root_ms * 1e-3) / 1e12
     gn = gn_rate(q, init, steps=4)
@@ -495,7 +500,8 @@ def c2_line(cpkit, peak, hbm):
     q.close()
     return {"workload": w["name"], "als_sweeps_per_s": 50 / (ms * 1e-3), "als_ms_per_sweep": ms / 50,
             "root_tflops": tf, "root_frac_of_peak": tf / peak, "gn": gn, "second_level": second,
-            "note": "order 3: multi-sweep dimension tree (3 root contractions per 2 sweeps), 50 sweeps timed"}
+            "note": "order 3: multi-sweep dimension tree (3 root contractions per 2 sweeps), 50 sweeps timed "
+                    "(root events recorded in a separate pass)"}
 
 
 def c5_line(cpkit, rank, world, local_rank, nccl_id, peak, barrier, max_over_ranks):

@@ -658,6 +658,20 @@ def test_decompose_overlapped_first_root(ck, dims, optimizer):
     assert vec_rel_err(m.factors(), f) < (1e-15 if one_slab else 1e-9)
 
 
+def test_second_level_timing_seam_leaves_results_intact(orc, ck):
+    """cpkit_dev_time_second_level (bench.py's HBM line item) repeats the second tree level on
+    the cached back-root partial; the MTTKRPs afterwards still match the oracle."""
+    dims, rank = [24, 18, 20, 16], 12
+    x = np.random.default_rng(7).standard_normal(dims)
+    f = gauss_factors(orc, dims, rank, 41)
+    ref, _ = orc.mttkrp_tree_all(x, f)
+    p = make(ck, x, f)
+    ms, nbytes = p.time_second_level(3)
+    assert ms > 0.0 and nbytes == 8.0 * dims[0] * dims[1] * rank
+    for n in range(len(dims)):
+        assert rel_err(p.mttkrp(n), ref[n]) < KTOL, n
+
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
