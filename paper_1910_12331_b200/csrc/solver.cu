@@ -891,7 +891,8 @@ double DeviceProblem::norm2() {
     const std::uint64_t stored = static_cast<std::uint64_t>(F_) * static_cast<std::uint64_t>(Bs_);  // pad is zero
     launch_norm2(x_.get(), stored, partials_.get(), norm2_parts(stored), scal_.get() + kXnorm, ctx_.stream);
     if (ctx_.comm) ctx_.comm->allreduce_sum(scal_.get() + kXnorm, 1, ctx_.stream);
-    return read_scalar(kXnorm);
+    xnorm_dev_ = read_scalar(kXnorm);
+    return xnorm_dev_;
 }
 
 // ---- launch profiling ----------------------------------------------------------
@@ -1216,8 +1217,12 @@ void DeviceProblem::upload_gammas(const double* grams, const double* pair) {
 void DeviceProblem::residual_launch(double xnorm2) {
     if (!(xnorm2 > 0.0)) throw InvalidArgument("residual_fitness: tensor norm must be positive");
     const int N = order();
-    hpin_[8] = xnorm2;  // pinned upload slot (reused only after a later synchronisation)
-    CPK_CUDA(cudaMemcpyAsync(scal_.get() + kXnorm, hpin_ + 8, sizeof(double), cudaMemcpyHostToDevice, ctx_.stream));
+    if (xnorm_dev_ != xnorm2) {  // the slot keeps its value between calls: no copy-engine hop per GN step
+        hpin_[8] = xnorm2;       // pinned upload slot (reused only after a later synchronisation)
+        CPK_CUDA(cudaMemcpyAsync(scal_.get() + kXnorm, hpin_ + 8, sizeof(double), cudaMemcpyHostToDevice,
+                                 ctx_.stream));
+        xnorm_dev_ = xnorm2;
+    }
     launch_residual(M_.get() + off_[N - 1], A_.get() + off_[N - 1], static_cast<std::int64_t>(dims_[N - 1]),
                     grams_.get(), N, R_, scal_.get() + kXnorm, partials_.get(), scal_.get() + kRes,
                     ctx_.stream);

@@ -441,6 +441,7 @@ private:
     DevBuf<double> grams_, pair_, gam_, pinv_, chol_, chol_tmp_, anew_, gram_ws_;
     std::int64_t smax_ = 1;
     DevBuf<double> scal_, partials_, slots_;
+    double xnorm_dev_ = -1.0;  // the ||X||^2 value the device slot holds (-1: unknown), so an unchanged value is not re-uploaded
     DevBuf<int> status_, cgres_, flag_;
     DevBuf<int> apply_bad_;            // gn_apply: per-block finiteness
     DevBuf<unsigned int> apply_cnt_;   // gn_apply: last-block counter (self-resetting)
